@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""bench.py — best-shift tabu core of CHAP (arxiv 2605.05086) on B200.
+
+A "step" is one tabu iteration of every walker on the GPU: the exact best shift of every
+variable (Algorithm 1, all column classes), the global select, and the apply / weight bump /
+incumbent check — the whole hot path of SURVEY.md §8(a). Default workload: config G
+(BASELINE.json configs[2]: 200k rows x 1M vars, ~10.4M nnz, 100 long columns), one walker per
+GPU; N>1 GPUs run independent walker replicas (weak scaling, no collective in the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config G|S|P] [--impl chap|reference]
+
+Prints ONE JSON line (rank 0). --impl reference times the plain fp64 CPU oracle (oracle/) on
+the same workload on the host cores (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "best-shift move evaluations/sec and tabu iterations/sec; % of HBM roofline"
+UNIT = "move_evals/s"
+
+CONFIGS = {
+    "G": dict(desc="G: synthetic mixed general-integer MIP 200k rows x 1M vars, ~10.4M nnz, 100 long columns "
+                   "(BASELINE.json configs[2])", walkers=1),
+    "S": dict(desc="S: synthetic set cover 10k rows x 50k binaries, ~500k nnz (BASELINE.json configs[1])", walkers=1),
+    "P": dict(desc="P: packing MIP 20k rows x 100k binaries, ~1M nnz, 64 walkers (BASELINE.json configs[3])",
+              walkers=64),
+}
+
+
+def make_instance(cfg: str):
+    if cfg == "G":
+        return synth.mixed()
+    if cfg == "S":
+        return synth.setcover()
+    if cfg == "P":
+        return synth.packing()
+    raise ValueError(cfg)
+
+
+def start_points(inst, cfg: str, W: int, rank: int):
+    if cfg == "P":
+        return np.stack([synth.x_bernoulli(inst, (3, rank * W + w), 0.5) for w in range(W)])
+    x = synth.x_lower(inst)
+    return np.stack([x] * W)
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_baseline(inst, x0, seconds_target: float = 15.0, max_iters: int = 400):
+    """The oracle as it stands, on the host cores: tabu iterations of one walker (bounded sample)."""
+    import oracle
+    O = oracle.Problem.from_instance(inst)
+    ow = oracle.TabuWalker(O, x0)
+    n_eval = int(np.sum(O.vars()[2] != 0))
+    t0 = time.perf_counter()
+    ow.run(1)
+    t1 = time.perf_counter() - t0
+    iters = int(max(1, min(max_iters, seconds_target / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    ow.run(iters)
+    dt = time.perf_counter() - t0
+    return {"value": n_eval * iters / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{iters} tabu iterations of 1 walker (after 1 warm-up iteration), all "
+                      f"{n_eval} non-fixed variables evaluated per iteration, OpenMP over variables",
+            "seconds": dt, "iters_per_s": iters / dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = args.config
+    inst = make_instance(cfg)
+    x0 = start_points(inst, cfg, 1, 0)[0]
+    import oracle
+    O = oracle.Problem.from_instance(inst)
+    ow = oracle.TabuWalker(O, x0)
+    n_eval = int(np.sum(O.vars()[2] != 0))
+    ow.run(args.warmup)
+    t0 = time.perf_counter()
+    ow.run(args.steps)
+    dt = time.perf_counter() - t0
+    value = n_eval * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator synth/, no dataset)",
+            "config": {"workload": CONFIGS[cfg]["desc"], "walkers": 1, "n": inst.n, "m": inst.m, "nnz": inst.nnz},
+            "tabu_iters_per_s": args.steps / dt,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"{args.steps} full tabu iterations of 1 walker after {args.warmup} warm-up"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--config", default="G", choices=sorted(CONFIGS))
+    ap.add_argument("--walkers", type=int, default=0)
+    ap.add_argument("--impl", default="chap", choices=["chap", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=200)
+    ap.add_argument("--e2e-iters", type=int, default=20)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    import paper_2605_05086_b200 as chap
+
+    cfg = args.config
+    W = args.walkers or CONFIGS[cfg]["walkers"]
+    inst = make_instance(cfg)
+    P = chap.Problem.from_instance(inst, device=local)
+    info = P.info
+    n_eval = info.n - info.n_fixed
+    x0 = torch.from_numpy(start_points(inst, cfg, W, rank)).to(dev)
+    prm = chap.default_params(graph_iters=32)
+    ws = chap.Walkers(P, x0, prm)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    ws.step(args.warmup)
+    torch.cuda.synchronize()
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ws.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    sec = ms_max / 1e3
+    value = n_eval * W * args.steps * world / sec
+    st = ws.get()["stats"]
+
+    # live per-kernel timing of the dominant kernel (same walker state continues)
+    kms = ws.profile(args.profile_iters)
+    names = ["k_eval_warp", "k_eval_block", "k_eval_long", "k_select", "k_apply"]
+    dom = int(np.argmax(kms[:3]))
+    mb = [int(info.model_bytes_kernel[i]) for i in range(3)]
+    achieved = mb[dom] * W / (kms[dom] * 1e-3) / 1e9
+    peak, peak_kind = measured_peak_hbm()
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            tj = json.load(open(tf))
+            if tj.get("config") == cfg and tj.get("kernel") == names[dom]:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_ms_profiled = float(np.sum(kms))
+    pass_bytes = int(info.model_bytes_pass) * W
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": names[dom], "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": mb[dom] * W,
+                "kernel_ms": {names[i]: float(kms[i]) for i in range(5)},
+                "kernel_share_of_step": float(kms[dom] / step_ms_profiled) if step_ms_profiled > 0 else None,
+                "whole_step": {"model_bytes": pass_bytes, "ms": ms_max / args.steps,
+                               "achieved": pass_bytes / (ms_max / args.steps * 1e-3) / 1e9,
+                               "frac": pass_bytes / (ms_max / args.steps * 1e-3) / 1e9 / peak}}
+
+    # e2e: the public C-ABI call with HOST buffers, copies inside the timed region
+    xh = start_points(inst, cfg, 1, rank)[0]
+    wh = np.ones(P.m_norm, np.float32)
+    P.eval_best_shift_host(xh, wh)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_iters):
+        P.eval_best_shift_host(xh, wh)
+    e2e_s = time.perf_counter() - t0
+    et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_s = float(et.item())
+    e2e = {"value": n_eval * args.e2e_iters * world / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": 8 * info.n + 4 * P.m_norm, "d2h_bytes_per_step": 16 * info.n + 24,
+           "call": "chap_eval_best_shift_host (x, w in; xhat, score, best out; synchronous)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(inst, start_points(inst, cfg, 1, 0)[0])
+
+    launches_per_iter = (1 if info.nnz_kernel[0] else 0) + (1 if info.nnz_kernel[1] else 0) + \
+                        (1 if info.nnz_kernel[2] else 0) + 2
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generator synth/, no dataset or weights)",
+                "config": {"workload": CONFIGS[cfg]["desc"], "walkers_per_gpu": W, "n": inst.n, "m": inst.m,
+                           "nnz": inst.nnz, "m_norm": P.m_norm, "nnz_with_cutoff": int(info.nnz_norm + info.nnz_cut),
+                           "non_fixed_vars": n_eval, "parallelism": f"replicas x{world}",
+                           "l2": "inputs larger than L2: A in CSC alone is "
+                                 f"{info.model_bytes_A / 1e6:.0f} MB vs 126 MB L2; no flush"},
+                "tabu_iters_per_s": W * args.steps * world / sec,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_iter * args.steps + 4,
+                "clocks": clk.summary(),
+                "walker": {"moves": int(st["n_moves"].sum()), "stuck": int(st["n_stuck"].sum()),
+                           "has_incumbent": int(st["has_incumbent"].sum()),
+                           "best_obj": float(np.min(st["best_obj"])), "violated": int(st["violated"].min())}}
+        print(json.dumps(line), flush=True)
+    ws.close()
+    P.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

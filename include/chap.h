@@ -1,0 +1,272 @@
+/* chap.h — C ABI of the B200-native best-shift tabu core of CHAP (arxiv 2605.05086).
+ *
+ * The library evaluates, for every variable j of a candidate point x̄ of
+ *     min c^T x  s.t.  lhs <= A x <= rhs,  l <= x <= u,  x_j ∈ Z (j ∈ I)
+ * the exact best-shift move of Eq. (1) (§3.1 "Best Shift Moves") using
+ * Algorithm 1 (breakpoint emission, segmented sort, scan, argmax) on
+ * sm_100a, then runs the tabu walk around it (PAPER.md:80-85 and §3.1 "Parallel Tabu Search
+ * Instances", :359-363) with incremental residual updates and constraint-weight
+ * bumps. The problem form is PAPER.md:269 with two-sided rows (north star), normalised
+ * internally to a.x <= b rows.
+ *
+ * Conventions (every function):
+ *  - returns chap_status; nothing throws across the ABI; chap_last_error() gives a
+ *    thread-local message for the last non-OK status on the calling thread;
+ *  - "HOST" pointers are ordinary CPU memory, "DEVICE" pointers are CUDA device memory on the
+ *    handle's device; all DEVICE outputs are caller-allocated and written stream-ordered on
+ *    the given cudaStream_t (passed as void*, NULL = the legacy default stream);
+ *  - handles are owned by the caller until *_destroy; a walkers object borrows its problem,
+ *    so the problem must outlive it; different handles may be used from different threads,
+ *    one handle must not be used concurrently;
+ *  - no function allocates device memory per call except the *_create functions and
+ *    chap_eval_best_shift_host (which allocates pinned staging once per problem).
+ * Readings R1..R17 of the paper are listed in DESIGN.md §3.
+ */
+#ifndef CHAP_H
+#define CHAP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHAP_ABI_VERSION 1
+
+typedef enum {
+  CHAP_OK = 0,
+  CHAP_ERR_INVALID_ARG = 1,       /* bad size/pointer, NaN, index out of range, duplicate (i,j),
+                                     x out of bounds or fractional on an integer variable, w < 0 */
+  CHAP_ERR_INFEASIBLE_BOUNDS = 2, /* l > u after rounding integer bounds inward, or an empty row
+                                     whose sides exclude 0                                       */
+  CHAP_ERR_CUDA = 3,              /* a CUDA runtime error (message has the CUDA error string)    */
+  CHAP_ERR_OOM = 4,               /* device or host allocation failed                            */
+  CHAP_ERR_NCCL = 5,              /* an NCCL call failed                                         */
+  CHAP_ERR_STATE = 6,             /* call not valid in the handle's current state                */
+  CHAP_ERR_UNSUPPORTED = 7        /* a column shape this build cannot evaluate (see message)     */
+} chap_status;
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+const char* chap_last_error(void);
+/* Static name of a status code. */
+const char* chap_status_string(chap_status s);
+/* CHAP_ABI_VERSION of the loaded library. */
+int32_t chap_abi_version(void);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Problem                                                                                  */
+/* ---------------------------------------------------------------------------------------- */
+
+typedef struct chap_problem chap_problem;
+
+typedef struct {
+  int32_t n, m;               /* as given                                                      */
+  int32_t m_norm;             /* normalised rows incl. the cutoff row, which is last            */
+  int32_t cutoff_row;         /* = m_norm - 1                                                  */
+  int64_t nnz_norm;           /* nonzeros of the normalised rows, cutoff row excluded          */
+  int64_t nnz_cut;            /* nonzeros of the cutoff row (#{j : c_j != 0})                  */
+  int32_t n_fixed, n_binary, n_integer, n_continuous;   /* variable classes after rounding    */
+  int32_t exact_integer_data; /* 1: A, lhs, rhs, l, u, c integral, |a| <= 1e6, all variables
+                                 integer -> scores and trajectories are bit-exact */
+  int32_t n_long_columns;     /* columns evaluated by the multi-block (chunked) path           */
+  double auto_cutoff_delta;   /* 1 if every c_j != 0 is integral on an integer variable, else
+                                 NaN (= 1e-6 max(1,|z|) when the cutoff is set) (R14)         */
+  int64_t device_bytes;       /* device memory held by the problem                            */
+  int64_t model_bytes_A;      /* algorithmic bytes of one pass over A in CSC:
+                                 12 (nnz_norm + nnz_cut) + 4 (n + 1)            */
+  int64_t model_bytes_pass;   /* algorithmic bytes of one best-shift pass of one walker: A in CSC,
+                                 static per-variable data (1 B binary, 17 B other), walker state
+                                 per variable (x̄: 1 bit binary / 8 B other; 4 B tabu expiry) and
+                                 12 B per normalised row (r f64 + w f32), each read once (§6)  */
+  int64_t model_bytes_kernel[3]; /* the same model split by eval kernel: [0] warp-task kernel
+                                 (incl. the 12 B/row row state), [1] block kernel, [2] chunked  */
+  int64_t nnz_kernel[3];      /* nonzeros (incl. cutoff entries) evaluated by each eval kernel */
+} chap_problem_info;
+
+/* Build a problem from HOST CSR data (copied; the caller may free its arrays on return).
+ *   row_ptr  [m+1] int64, row_ptr[0] = 0, non-decreasing, row_ptr[m] = nnz
+ *   col_idx  [nnz] int32 in [0, n); no duplicate (row, col); explicit zeros are dropped
+ *   val      [nnz] finite
+ *   lhs, rhs [m]   lhs <= rhs; -INF / +INF = that side absent; a free or empty row is dropped
+ *   lb, ub   [n]   +-INF allowed; integer bounds are rounded inward (ceil l, floor u)
+ *   is_integer [n] 0/1
+ *   c        [n]   finite; minimisation
+ *   device   CUDA device ordinal the problem lives on
+ * Normalisation: for each original row in order, the upper side a.x <= rhs if
+ * rhs is finite, then the lower side -a.x <= -lhs if lhs is finite; each side is its own row
+ * with its own weight and residual (R17). Row m_norm-1 is the cutoff row c.x <= z* - delta
+ * (PAPER.md:373), inactive (excluded from every score) until a cutoff is set.
+ * Variable classes: fixed (l = u), binary (integer, l = 0, u = 1), integer,
+ * continuous. Errors: INVALID_ARG, INFEASIBLE_BOUNDS, UNSUPPORTED (a non-binary column with
+ * more than 4094 nonzeros whose domain is not a bounded integer range of <= 4096 values),
+ * CUDA, OOM. */
+chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, const int64_t* row_ptr,
+                                const int32_t* col_idx, const double* val, const double* lhs,
+                                const double* rhs, const double* lb, const double* ub,
+                                const uint8_t* is_integer, const double* c, int32_t device,
+                                chap_problem** out);
+chap_status chap_problem_info_get(const chap_problem* p, chap_problem_info* out);
+/* HOST [m_norm-1] outputs: normalised row i came from original row orig_row[i], side[i] = +1
+ * (upper, a.x <= rhs) or -1 (lower, -a.x <= -lhs). */
+chap_status chap_problem_row_map(const chap_problem* p, int32_t* orig_row, int8_t* side);
+chap_status chap_problem_destroy(chap_problem* p);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Single-point evaluation (the parity entry point)                                          */
+/* ---------------------------------------------------------------------------------------- */
+
+typedef struct {
+  int32_t j;   /* variable index, -1 if no variable has s_j > 0                               */
+  int32_t pad;
+  double v;    /* its best shift x̂_j (NaN if j = -1)                                           */
+  double s;    /* its score s_j (-INF if j = -1)                                               */
+} chap_move;   /* 24 bytes */
+
+/* Eq. (1) for every variable at the point x, by Algorithm 1:
+ *   x      DEVICE [n] float64: within bounds, integral on integer variables (not checked here;
+ *          a violating x gives unspecified scores)
+ *   w      DEVICE [m_norm] float32 weights >= 0 (NULL = all 1); w[m_norm-1] is the cutoff
+ *          row's weight. Scores are exact when weights are integers <= 2^24 (R11).
+ *   cutoff_rhs  +INF = cutoff row inactive; finite = the row c.x <= cutoff_rhs is scored
+ *   xhat, score DEVICE [n] float64 outputs (either may be NULL): the best shift x̂_j and its raw
+ *          maximum score s_j over the candidate set {finite bounds} ∪ {breakpoints} within
+ *          [l_j, u_j] minus {x̄_j} (R2, R5); ties -> smallest |v - x̄_j|, then smallest v (R4).
+ *          A variable without candidates (fixed) reports (x̄_j, -INF). s_j may be <= 0 (R7).
+ *   best   DEVICE [1] chap_move out (may be NULL): argmax of s_j over s_j > 0, ties -> lowest j
+ *          (R6); j = -1 if none.
+ * Stream-ordered on cuda_stream; uses the problem's internal workspace, so calls on one
+ * problem must not overlap. */
+chap_status chap_eval_best_shift(const chap_problem* p, const double* x, const float* w,
+                                 double cutoff_rhs, double* xhat, double* score, chap_move* best,
+                                 void* cuda_stream);
+
+/* The same call with HOST buffers (x [n], w [m_norm] or NULL, xhat/score [n] or NULL, best
+ * [1] or NULL): copies in, evaluates, copies out, and synchronises the stream before
+ * returning. Used for the end-to-end (e2e) measurement. */
+chap_status chap_eval_best_shift_host(chap_problem* p, const double* x, const float* w,
+                                      double cutoff_rhs, double* xhat, double* score,
+                                      chap_move* best, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Tabu walkers                                                                              */
+/* ---------------------------------------------------------------------------------------- */
+
+typedef struct {
+  int32_t tenure;        /* T (default 10): a moved variable is inadmissible in k+1..k+T (R13) */
+  float weight_cap;      /* default 1e6; must be in [1, 2^24] so f32 weights stay exact (R11)  */
+  double cutoff_delta;   /* NaN = auto (R14)                                                   */
+  int32_t exchange_K;    /* iterations per epoch in chap_run_walkers (default 1000)            */
+  int32_t n_elite;       /* elite points exchanged per kind per rank (default 4)               */
+  int32_t n_restart;     /* walkers restarted from the elite per exchange (default W_total/8)  */
+  int32_t graph_iters;   /* iterations per captured CUDA graph in chap_tabu_step (default 16;
+                            0 = plain launches)                                               */
+} chap_params;
+
+/* Fill *out with the defaults above (n_restart = -1 meaning W_total/8). */
+chap_status chap_params_default(chap_params* out);
+
+typedef struct {
+  int64_t k;        /* iteration index                                                       */
+  int32_t j;        /* moved variable (user index), -1 = stuck: weights bumped, no move      */
+  int32_t pad;
+  double v;         /* new value of x_j (NaN if stuck)                                        */
+  double s;         /* its score; if stuck, the best admissible s_j (<= 0) or -INF if none    */
+  int64_t violated; /* active rows with r > 0 after the step (cutoff row included)           */
+  double obj;       /* c.x̄ after the step                                                     */
+} chap_step_record; /* 48 bytes; bit-identical to the oracle's log in the exact domain        */
+
+typedef struct {
+  int64_t k;              /* iterations done                                                  */
+  int64_t violated;       /* current violated active rows                                     */
+  double obj;             /* c.x̄                                                             */
+  double best_obj;        /* best incumbent objective (+INF if none)                          */
+  double cutoff_rhs;      /* current cutoff rhs (+INF if inactive)                            */
+  int32_t has_incumbent;  /* 1 if best_obj is set                                             */
+  int32_t pad;
+  int64_t n_moves;        /* moves applied                                                    */
+  int64_t n_stuck;        /* stuck iterations (weight bumps)                                  */
+} chap_walker_stats;      /* 64 bytes */
+
+typedef struct chap_walkers chap_walkers;
+
+/* W independent walkers (own solution, tabu list and weights) at start points
+ *   x0 DEVICE [W][n] float64 (user variable order), in bounds, integral on integer variables.
+ * Initial state: w = 1 on every row (cutoff included), tabu cleared, k = 0, cutoff inactive;
+ * residuals computed from scratch; a feasible start is recorded as incumbent at once and the
+ * cutoff set (R15). Errors: INVALID_ARG (W < 1, x0 invalid), OOM, CUDA. Synchronises. */
+chap_status chap_walkers_create(const chap_problem* p, int32_t W, const double* x0,
+                                const chap_params* params, void* cuda_stream, chap_walkers** out);
+
+/* n_iters tabu iterations of every walker, entirely on the device (CUDA graphs of
+ * params.graph_iters iterations). One iteration: best shift of every variable (Alg. 1);
+ * select the admissible (tabu_until_j <= k) argmax s_j, ties lowest j (R6); if s* > 0 apply it
+ * (x̄_j* <- x̂_j*, r_i += a_ij Δ over column j* — PAPER.md:343 — and tabu_until_j* = k+1+T),
+ * else bump w_i <- min(w_i + 1, cap) on every active row with r_i > 0 (R12); then if no active
+ * row is violated record the incumbent and set the cutoff rhs to c.x̄ - delta.
+ *   log  DEVICE [n_iters][W] chap_step_record (walker-minor) or NULL. Stream-ordered. */
+chap_status chap_tabu_step(chap_walkers* ws, int32_t n_iters, chap_step_record* log,
+                           void* cuda_stream);
+
+/* Export walker state (any pointer may be NULL); all DEVICE, user order, walker-major:
+ *   x [W][n] float64, r [W][m_norm] float64 (r of an inactive cutoff row is -INF),
+ *   w [W][m_norm] float32, tabu_until [W][n] int64 (absolute iteration), best_x [W][n] float64,
+ *   stats [W] chap_walker_stats. Stream-ordered. */
+chap_status chap_walkers_get(const chap_walkers* ws, double* x, double* r, float* w,
+                             int64_t* tabu_until, double* best_x, chap_walker_stats* stats,
+                             void* cuda_stream);
+/* Impose a cutoff from an external incumbent: every walker whose cutoff rhs is
+ * above z_best - delta gets rhs = z_best - delta (residual recomputed). Stream-ordered. */
+chap_status chap_walkers_set_cutoff(chap_walkers* ws, double z_best, void* cuda_stream);
+/* Restart walker `walker` from x DEVICE [n] (user order): residuals recomputed from scratch,
+ * weights kept, tabu cleared (SURVEY §8(e) restart rule). Stream-ordered. */
+chap_status chap_walkers_restart(chap_walkers* ws, int32_t walker, const double* x,
+                                 void* cuda_stream);
+chap_status chap_walkers_destroy(chap_walkers* ws);
+
+/* Diagnostic timing: n_iters tabu iterations (identical semantics to chap_tabu_step, no log)
+ * with plain launches and a CUDA-event pair around every launch on the walkers' stream;
+ * ms_per_iter HOST [5] receives the average device time per iteration of [0] the warp-task
+ * eval kernel, [1] the block eval kernel, [2] the chunked eval kernel, [3] the select kernel,
+ * [4] the apply kernel (0 for a kernel with no work). Synchronises. */
+chap_status chap_walkers_profile(chap_walkers* ws, int32_t n_iters, double* ms_per_iter,
+                                 void* cuda_stream);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Multi-GPU portfolio: independent walkers per GPU with an every-K exchange                 */
+/* ---------------------------------------------------------------------------------------- */
+
+typedef struct chap_comm chap_comm;
+
+/* NCCL unique id (128 bytes) created on one rank and broadcast by the caller (e.g. through
+ * torch.distributed) to every rank before chap_comm_create. */
+chap_status chap_comm_unique_id(uint8_t id[128]);
+chap_status chap_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
+                             chap_comm** out);
+chap_status chap_comm_destroy(chap_comm* comm);
+
+typedef struct {
+  double best_obj;          /* best incumbent over all walkers of all ranks (+INF if none)    */
+  int32_t has_incumbent;
+  int32_t best_walker;      /* global walker id of the incumbent's finder                      */
+  int64_t iterations;       /* iterations done per walker                                     */
+  int64_t epochs;
+  double seconds;           /* wall time of the call                                          */
+} chap_result;
+
+/* The portfolio loop: W_local walkers from x0 DEVICE [W_local][n] (global
+ * walker id = rank*W_local + w), epochs of params.exchange_K iterations; after each epoch an
+ * allgather of per-walker summaries and of each rank's elite points (n_elite best incumbents
+ * and n_elite least-violated points), a global cutoff z_best - delta for every walker, and a
+ * deterministic restart of the n_restart most violated walkers from the global elite.
+ * comm = NULL: single GPU, same rule with one rank. Stops after max_iters iterations or when
+ * time_limit_s (<= 0: none) has elapsed at an epoch end. best_x DEVICE [n] (or NULL) receives
+ * the best incumbent. Synchronises. */
+chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, const double* x0,
+                             const chap_params* params, chap_comm* comm, int64_t max_iters,
+                             double time_limit_s, double* best_x, chap_result* out,
+                             void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHAP_H */

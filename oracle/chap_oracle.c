@@ -232,6 +232,11 @@ static double score_of(const orc_problem* P, int32_t j, double v, const double* 
   return s;
 }
 
+static int cmp_double(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
 /* is (s1, v1) better than (s0, v0) at incumbent xj: higher score, then smaller |v - x_j|,
  * then smaller v (R4) */
 static int better(double s1, double v1, double s0, double v0, double xj) {
@@ -253,18 +258,14 @@ static void best_shift_var(const orc_problem* P, int32_t j, const double* x, con
     double v = 1.0 - xj;
     *xhat = v; *score = score_of(P, j, v, x, y, w, cutoff_rhs); return;
   }
-  /* candidate set (R5): finite bounds, then the breakpoint of every row of column j */
-  double cand[2];
-  int nb = 0;
-  if (isfinite(l)) cand[nb++] = l;
-  if (isfinite(u)) cand[nb++] = u;
-  for (int q = 0; q < nb; q++) {
-    double v = cand[q];
-    if (v == xj) continue;
-    double s = score_of(P, j, v, x, y, w, cutoff_rhs);
-    if (!have || better(s, v, bs, bv, xj)) { bs = s; bv = v; have = 1; }
-  }
+  /* candidate set (R5): the finite bounds and the breakpoint of every row of column j (and of
+   * the active cutoff row), within [l_j, u_j], minus x̄_j; collected, sorted and made unique so
+   * that each distinct value is scored once */
   int64_t e0 = P->cp[j], e1 = P->cp[j + 1];
+  double* cand = (double*)malloc(sizeof(double) * (size_t)(e1 - e0 + 3));
+  int64_t nc = 0;
+  if (isfinite(l)) cand[nc++] = l;
+  if (isfinite(u)) cand[nc++] = u;
   int is_integer = (vc == 2);
   for (int64_t e = e0; e <= e1; e++) {
     double a, ri;
@@ -273,11 +274,17 @@ static void best_shift_var(const orc_problem* P, int32_t j, const double* x, con
       if (!(cut_active && P->c[j] != 0.0)) break;
       a = P->c[j]; ri = y[P->m_norm - 1] - cutoff_rhs;
     }
-    double v = orc_breakpoint(xj, ri, a, is_integer);
+    cand[nc++] = orc_breakpoint(xj, ri, a, is_integer);
+  }
+  qsort(cand, (size_t)nc, sizeof(double), cmp_double);
+  for (int64_t q = 0; q < nc; q++) {
+    double v = cand[q];
+    if (q > 0 && v == cand[q - 1]) continue;
     if (!(v >= l && v <= u) || v == xj) continue;
     double s = score_of(P, j, v, x, y, w, cutoff_rhs);
     if (!have || better(s, v, bs, bv, xj)) { bs = s; bv = v; have = 1; }
   }
+  free(cand);
   if (!have) { *xhat = xj; *score = -INFINITY; return; }
   *xhat = bv; *score = bs;
 }

@@ -1,0 +1,791 @@
+// chap.cu — libchap: the C ABI of include/chap.h on sm_100a.
+//
+// Host side: input validation, row normalisation, variable classification and
+// the length-bucketed column dispatch, device upload, and the launch
+// sequences of chap_eval_best_shift and chap_tabu_step (captured as CUDA graphs).
+// Device side: eval.cuh (Algorithm 1), tabu.cuh (apply / bump / incumbent).
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <memory>
+#include <cmath>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "chap.h"
+#include "common.cuh"
+#include "eval.cuh"
+#include "host.h"
+#include "tabu.cuh"
+
+using namespace chap;
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+chap_status chap::fail(chap_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+extern "C" const char* chap_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char* chap_status_string(chap_status s) {
+  switch (s) {
+    case CHAP_OK: return "CHAP_OK";
+    case CHAP_ERR_INVALID_ARG: return "CHAP_ERR_INVALID_ARG";
+    case CHAP_ERR_INFEASIBLE_BOUNDS: return "CHAP_ERR_INFEASIBLE_BOUNDS";
+    case CHAP_ERR_CUDA: return "CHAP_ERR_CUDA";
+    case CHAP_ERR_OOM: return "CHAP_ERR_OOM";
+    case CHAP_ERR_NCCL: return "CHAP_ERR_NCCL";
+    case CHAP_ERR_STATE: return "CHAP_ERR_STATE";
+    case CHAP_ERR_UNSUPPORTED: return "CHAP_ERR_UNSUPPORTED";
+  }
+  return "CHAP_ERR_?";
+}
+
+extern "C" int32_t chap_abi_version(void) { return CHAP_ABI_VERSION; }
+
+
+static inline int ilog2_ceil(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return l;
+}
+
+static bool integral(double v) { return std::isfinite(v) && v == std::floor(v); }
+
+extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, const int64_t* row_ptr,
+                                           const int32_t* col_idx, const double* val,
+                                           const double* lhs, const double* rhs, const double* lb,
+                                           const double* ub, const uint8_t* is_integer,
+                                           const double* c, int32_t device, chap_problem** out) {
+  if (!out) return fail(CHAP_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 0 || m < 0 || nnz < 0) return fail(CHAP_ERR_INVALID_ARG, "negative size");
+  if ((m > 0 && (!row_ptr || !lhs || !rhs)) || (nnz > 0 && (!col_idx || !val)) ||
+      (n > 0 && (!lb || !ub || !is_integer || !c)))
+    return fail(CHAP_ERR_INVALID_ARG, "NULL input array");
+  if (m > 0 && (row_ptr[0] != 0 || row_ptr[m] != nnz)) return fail(CHAP_ERR_INVALID_ARG, "row_ptr[0] != 0 or row_ptr[m] != nnz");
+  if (m == 0 && nnz != 0) return fail(CHAP_ERR_INVALID_ARG, "nnz > 0 with m = 0");
+  for (int32_t i = 0; i < m; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i]) return fail(CHAP_ERR_INVALID_ARG, "row_ptr decreasing at row %d", i);
+    if (std::isnan(lhs[i]) || std::isnan(rhs[i])) return fail(CHAP_ERR_INVALID_ARG, "NaN side in row %d", i);
+    if (lhs[i] > rhs[i] || lhs[i] == INFINITY || rhs[i] == -INFINITY)
+      return fail(CHAP_ERR_INVALID_ARG, "row %d: lhs > rhs or infinite in the wrong direction", i);
+  }
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (col_idx[e] < 0 || col_idx[e] >= n) return fail(CHAP_ERR_INVALID_ARG, "col_idx[%lld] out of range", (long long)e);
+    if (!std::isfinite(val[e])) return fail(CHAP_ERR_INVALID_ARG, "non-finite val[%lld]", (long long)e);
+  }
+  {  // duplicate (i, j)
+    std::vector<int32_t> mark(n, -1);
+    for (int32_t i = 0; i < m; ++i)
+      for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+        if (mark[col_idx[e]] == i) return fail(CHAP_ERR_INVALID_ARG, "duplicate entry (%d, %d)", i, col_idx[e]);
+        mark[col_idx[e]] = i;
+      }
+  }
+  DeviceGuard guard(device);
+  if (!guard.ok) return fail(CHAP_ERR_CUDA, "cannot select CUDA device %d", device);
+
+  auto P = new chap_problem();
+  std::unique_ptr<chap_problem> holder(P);
+  P->device = device;
+  cudaDeviceGetAttribute(&P->sm_count, cudaDevAttrMultiProcessorCount, device);
+  chap_problem_info& I = P->info;
+  I.n = n;
+  I.m = m;
+  bool exact = true;
+
+  // variables: round integer bounds inward, classify
+  std::vector<double> l(n), u(n), cc(n);
+  std::vector<uint8_t> vclass(n);
+  for (int32_t j = 0; j < n; ++j) {
+    double lj = lb[j], uj = ub[j];
+    if (std::isnan(lj) || std::isnan(uj) || lj == INFINITY || uj == -INFINITY)
+      return fail(CHAP_ERR_INVALID_ARG, "bad bounds of variable %d", j);
+    if (!std::isfinite(c[j])) return fail(CHAP_ERR_INVALID_ARG, "non-finite c[%d]", j);
+    if (is_integer[j]) {
+      lj = std::ceil(lj);
+      uj = std::floor(uj);
+    }
+    if (lj > uj) return fail(CHAP_ERR_INFEASIBLE_BOUNDS, "variable %d: l > u after rounding", j);
+    l[j] = lj;
+    u[j] = uj;
+    cc[j] = c[j];
+    uint8_t vc;
+    if (lj == uj) vc = 0;
+    else if (is_integer[j] && lj == 0.0 && uj == 1.0) vc = 1;
+    else if (is_integer[j]) vc = 2;
+    else vc = 3;
+    vclass[j] = vc;
+    if (!is_integer[j]) exact = false;
+    if ((std::isfinite(lj) && !integral(lj)) || (std::isfinite(uj) && !integral(uj)) || !integral(c[j])) exact = false;
+    if (vc == 0) I.n_fixed++;
+    else if (vc == 1) I.n_binary++;
+    else if (vc == 2) I.n_integer++;
+    else I.n_continuous++;
+  }
+
+  // normalised rows: upper side then lower side per original row
+  std::vector<int64_t> nrow_ptr{0};
+  std::vector<int32_t> ncol;   // user column
+  std::vector<double> nval, nb;
+  for (int32_t i = 0; i < m; ++i) {
+    int64_t k = 0;
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) k += (val[e] != 0.0);
+    if (k == 0) {
+      if (lhs[i] > 0.0 || rhs[i] < 0.0) return fail(CHAP_ERR_INFEASIBLE_BOUNDS, "empty row %d excludes 0", i);
+      continue;
+    }
+    for (int s = 0; s < 2; ++s) {
+      const double bb = s == 0 ? rhs[i] : -lhs[i];
+      if (!std::isfinite(bb)) continue;
+      const double sg = s == 0 ? 1.0 : -1.0;
+      for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+        if (val[e] == 0.0) continue;
+        ncol.push_back(col_idx[e]);
+        nval.push_back(sg * val[e]);
+        if (!integral(val[e]) || std::fabs(val[e]) > 1e6) exact = false;
+      }
+      if (!integral(bb)) exact = false;
+      nb.push_back(bb);
+      P->orig_row.push_back(i);
+      P->side.push_back((int8_t)(s == 0 ? 1 : -1));
+      nrow_ptr.push_back((int64_t)ncol.size());
+    }
+  }
+  const int32_t mr = (int32_t)nb.size();      // rows without the cutoff row
+  const int32_t m_norm = mr + 1;
+  const int32_t cut_row = mr;
+  int64_t nnz_cut = 0;
+  bool delta_int = true;
+  for (int32_t j = 0; j < n; ++j)
+    if (cc[j] != 0.0) {
+      ++nnz_cut;
+      if (!integral(cc[j]) || vclass[j] == 3) delta_int = false;
+    }
+  const int64_t nnz_norm = (int64_t)ncol.size();
+  const int64_t nnz_total = nnz_norm + nnz_cut;
+  if (nnz_total >= (int64_t)INT32_MAX - 1 || m_norm >= INT32_MAX - 1)
+    return fail(CHAP_ERR_INVALID_ARG, "instance too large for 32-bit CSC offsets (%lld nonzeros)", (long long)nnz_total);
+  I.m_norm = m_norm;
+  I.cutoff_row = cut_row;
+  I.nnz_norm = nnz_norm;
+  I.nnz_cut = nnz_cut;
+  I.exact_integer_data = exact ? 1 : 0;
+  I.auto_cutoff_delta = delta_int ? 1.0 : NAN;
+
+  // column degrees (incl. the cutoff entry) and classes
+  std::vector<int32_t> deg(n, 0);
+  for (int64_t e = 0; e < nnz_norm; ++e) deg[ncol[e]]++;
+  for (int32_t j = 0; j < n; ++j) deg[j] += (cc[j] != 0.0);
+  std::vector<int32_t> cls(n), lgv(n, 0);
+  for (int32_t j = 0; j < n; ++j) {
+    const int d = deg[j];
+    if (vclass[j] == 0) {
+      cls[j] = CC_FIXED;
+    } else if (vclass[j] == 1) {
+      if (d <= 32) { cls[j] = CC_BIN; lgv[j] = std::max(1, ilog2_ceil(std::max(d, 1))); }
+      else if (d <= kBinWideMax) cls[j] = CC_BINW;
+      else cls[j] = CC_BINL;
+    } else {
+      if (d + 2 <= 32) { cls[j] = CC_GEN; lgv[j] = std::max(2, ilog2_ceil(d + 2)); }
+      else if (d + 2 <= kBlockElems) cls[j] = CC_GENB;
+      else if (vclass[j] == 2 && std::isfinite(l[j]) && std::isfinite(u[j]) && u[j] - l[j] + 1.0 <= kBucketMax)
+        cls[j] = CC_GENL;
+      else
+        return fail(CHAP_ERR_UNSUPPORTED,
+                    "variable %d: non-binary column with %d nonzeros and domain [%g, %g] (needs the "
+                    "multi-block merge sort, not in this build)", j, d, l[j], u[j]);
+    }
+  }
+  // internal order: by (class, group size, user index)
+  std::vector<int32_t> perm(n);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
+    if (cls[a] != cls[b]) return cls[a] < cls[b];
+    return lgv[a] < lgv[b];
+  });
+  std::vector<int32_t> iperm(n);
+  for (int32_t p = 0; p < n; ++p) iperm[perm[p]] = p;
+
+  // CSC in internal order; rows ascending within a column, cutoff entry last
+  std::vector<int32_t> col_ptr(n + 1, 0);
+  for (int32_t p = 0; p < n; ++p) col_ptr[p + 1] = col_ptr[p] + deg[perm[p]];
+  std::vector<int32_t> fill(col_ptr.begin(), col_ptr.end() - 1);
+  std::vector<int32_t> row_idx(nnz_total);
+  std::vector<double> cval(nnz_total);
+  for (int32_t i = 0; i < mr; ++i)
+    for (int64_t e = nrow_ptr[i]; e < nrow_ptr[i + 1]; ++e) {
+      const int32_t p = iperm[ncol[e]];
+      row_idx[fill[p]] = i;
+      cval[fill[p]] = nval[e];
+      fill[p]++;
+    }
+  for (int32_t j = 0; j < n; ++j)
+    if (cc[j] != 0.0) {
+      const int32_t p = iperm[j];
+      row_idx[fill[p]] = cut_row;
+      cval[fill[p]] = cc[j];
+      fill[p]++;
+    }
+  // CSR (internal columns) incl. the cutoff row
+  std::vector<int32_t> rp(m_norm + 1);
+  std::vector<int32_t> ci;
+  std::vector<double> cv;
+  ci.reserve(nnz_total);
+  cv.reserve(nnz_total);
+  rp[0] = 0;
+  for (int32_t i = 0; i < mr; ++i) {
+    for (int64_t e = nrow_ptr[i]; e < nrow_ptr[i + 1]; ++e) {
+      ci.push_back(iperm[ncol[e]]);
+      cv.push_back(nval[e]);
+    }
+    rp[i + 1] = (int32_t)ci.size();
+  }
+  for (int32_t j = 0; j < n; ++j)
+    if (cc[j] != 0.0) {
+      ci.push_back(iperm[j]);
+      cv.push_back(cc[j]);
+    }
+  rp[m_norm] = (int32_t)ci.size();
+  // per-variable arrays in internal order
+  std::vector<double> lbi(n), ubi(n), ci_(n);
+  std::vector<uint8_t> vci(n);
+  for (int32_t p = 0; p < n; ++p) {
+    const int32_t j = perm[p];
+    lbi[p] = l[j];
+    ubi[p] = u[j];
+    ci_[p] = cc[j];
+    vci[p] = vclass[j];
+  }
+  // tasks
+  std::vector<WTask> wt;
+  std::vector<int32_t> bcols;
+  std::vector<LChunk> chunks;
+  int32_t n_long = 0;
+  int64_t lscr = 0;
+  int32_t p = 0;
+  while (p < n) {
+    const int32_t j = perm[p];
+    const int k = cls[j];
+    if (k == CC_FIXED) { ++p; continue; }
+    if (k == CC_BIN || k == CC_GEN) {
+      const int lg = lgv[j];
+      const int per = 32 >> lg;
+      int cnt = 0;
+      while (p + cnt < n && cnt < per && cls[perm[p + cnt]] == k && lgv[perm[p + cnt]] == lg) ++cnt;
+      wt.push_back(WTask{p, (int16_t)cnt, (int8_t)k, (int8_t)lg});
+      p += cnt;
+      continue;
+    }
+    if (k == CC_BINW) {
+      wt.push_back(WTask{p, 1, (int8_t)CC_BINW, 5});
+    } else if (k == CC_GENB) {
+      bcols.push_back(p);
+    } else {  // CC_BINL, CC_GENL
+      const int d = deg[j];
+      const int nch = (d + kLongChunk - 1) / kLongChunk;
+      const int kind = (k == CC_BINL) ? 0 : 1;
+      const int dom = kind ? (int)(u[j] - l[j] + 1.0) : 0;
+      for (int q = 0; q < nch; ++q) {
+        LChunk ch;
+        ch.p = p;
+        ch.lc = n_long;
+        ch.e0 = col_ptr[p] + q * kLongChunk;
+        ch.e1 = std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * kLongChunk);
+        ch.chunk = q;
+        ch.nchunks = nch;
+        ch.kind = kind;
+        ch.dom = dom;
+        ch.scr = lscr;
+        chunks.push_back(ch);
+      }
+      lscr += kind ? (2LL * nch * dom + 2LL * nch) : nch;
+      ++n_long;
+    }
+    ++p;
+  }
+  I.n_long_columns = n_long;
+  {  // algorithmic-bytes model
+    int64_t mb[3] = {0, 0, 0}, nz[3] = {0, 0, 0};
+    for (int32_t q = 0; q < n; ++q) {
+      const int32_t j = perm[q];
+      const int k = cls[j];
+      if (k == CC_FIXED) continue;
+      const int kk = (k == CC_GENB) ? 1 : (k == CC_BINL || k == CC_GENL) ? 2 : 0;
+      const bool bin = vclass[j] == 1;
+      const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
+      mb[kk] += 12LL * deg[j] + (int64_t)std::llround(per_var * 8) / 8;
+      nz[kk] += deg[j];
+    }
+    mb[0] += 12LL * m_norm;
+    for (int q = 0; q < 3; ++q) { I.model_bytes_kernel[q] = mb[q]; I.nnz_kernel[q] = nz[q]; }
+    I.model_bytes_pass = mb[0] + mb[1] + mb[2];
+  }
+  P->lscr_per_walker = (size_t)std::max<int64_t>(lscr, 1);
+
+  // upload
+  DeviceBuffers& B = P->buf;
+  int32_t *d_col_ptr, *d_row_idx, *d_rp, *d_ci, *d_perm, *d_bcols;
+  double *d_val, *d_cv, *d_b, *d_lb, *d_ub, *d_c;
+  uint8_t* d_vc;
+  WTask* d_wt;
+  LChunk* d_ch;
+  TRY(B.upload(&d_col_ptr, col_ptr));
+  TRY(B.upload(&d_row_idx, row_idx));
+  TRY(B.upload(&d_val, cval));
+  TRY(B.upload(&d_rp, rp));
+  TRY(B.upload(&d_ci, ci));
+  TRY(B.upload(&d_cv, cv));
+  TRY(B.upload(&d_b, nb));
+  TRY(B.upload(&d_lb, lbi));
+  TRY(B.upload(&d_ub, ubi));
+  TRY(B.upload(&d_c, ci_));
+  TRY(B.upload(&d_vc, vci));
+  TRY(B.upload(&d_perm, perm));
+  TRY(B.upload(&d_wt, wt));
+  TRY(B.upload(&d_bcols, bcols));
+  TRY(B.upload(&d_ch, chunks));
+  DevProblem& D = P->dp;
+  D.n = n;
+  D.m_norm = m_norm;
+  D.cut_row = cut_row;
+  D.col_ptr = d_col_ptr;
+  D.row_idx = d_row_idx;
+  D.val = d_val;
+  D.rp = d_rp;
+  D.ci = d_ci;
+  D.cv = d_cv;
+  D.b = d_b;
+  D.lb = d_lb;
+  D.ub = d_ub;
+  D.c = d_c;
+  D.vclass = d_vc;
+  D.perm = d_perm;
+  D.wtasks = d_wt;
+  D.n_wtasks = (int32_t)wt.size();
+  D.bcols = d_bcols;
+  D.n_bcols = (int32_t)bcols.size();
+  D.chunks = d_ch;
+  D.n_chunks = (int32_t)chunks.size();
+  D.n_long = n_long;
+  D.n_fixed = I.n_fixed;
+  D.auto_delta = I.auto_cutoff_delta;
+
+  // launch geometry
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_warp, kEvalThreads, 0));
+  const int need = std::max(1, (D.n_wtasks + kEvalWarps - 1) / kEvalWarps);
+  P->warp_grid = std::max(1, std::min(need, std::max(1, occ) * P->sm_count));
+  P->rows_grid = std::max(1, std::min((m_norm + 7) / 8, 8 * P->sm_count));
+  P->pl.warp_blocks = D.n_wtasks > 0 ? P->warp_grid : 0;
+  P->pl.block_off = P->pl.warp_blocks;
+  P->pl.long_off = P->pl.block_off + D.n_bcols;
+  P->pl.total = P->pl.long_off + D.n_chunks;
+  const size_t block_smem = (size_t)kBlockElems * (3 * sizeof(double) + sizeof(uint32_t));
+  CUDA_TRY(cudaFuncSetAttribute(k_eval_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)block_smem));
+
+  // eval workspace
+  TRY(B.alloc(&P->e_x, n));
+  TRY(B.alloc(&P->e_rs, m_norm));
+  TRY(B.alloc(&P->e_tabu, n));
+  TRY(B.alloc(&P->e_bx, n));
+  TRY(B.alloc(&P->e_sc, 1));
+  TRY(B.alloc(&P->e_part, std::max(P->pl.total, 1)));
+  TRY(B.alloc(&P->e_lcount, std::max(n_long, 1)));
+  TRY(B.alloc(&P->e_lscr, P->lscr_per_walker));
+  CUDA_TRY(cudaMemset(P->e_sc, 0, sizeof(WalkerScalars)));
+  CUDA_TRY(cudaMemset(P->e_lcount, 0, sizeof(unsigned) * std::max(n_long, 1)));
+  CUDA_TRY(cudaMemset(P->e_tabu, 0, sizeof(int32_t) * std::max(n, 1)));
+  CUDA_TRY(cudaDeviceSynchronize());
+  I.device_bytes = (int64_t)B.bytes_total;
+  I.model_bytes_A = 12LL * nnz_total + 4LL * (n + 1);
+  *out = holder.release();
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_problem_info_get(const chap_problem* p, chap_problem_info* out) {
+  if (!p || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL argument");
+  *out = p->info;
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_problem_row_map(const chap_problem* p, int32_t* orig_row, int8_t* side) {
+  if (!p) return fail(CHAP_ERR_INVALID_ARG, "NULL problem");
+  const size_t k = p->orig_row.size();
+  if (orig_row && k) memcpy(orig_row, p->orig_row.data(), k * sizeof(int32_t));
+  if (side && k) memcpy(side, p->side.data(), k * sizeof(int8_t));
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_problem_destroy(chap_problem* p) {
+  if (!p) return CHAP_OK;
+  DeviceGuard g(p->device);
+  delete p;
+  return CHAP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// eval launches (shared by the eval API and the tabu step)
+// ------------------------------------------------------------------------------------------
+chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, double* oxhat,
+                               double* oscore, cudaStream_t s) {
+  const DevProblem& D = P->dp;
+  const int W = Wk.W;
+  if (D.n_wtasks > 0)
+    k_eval_warp<<<dim3(P->warp_grid, W), kEvalThreads, 0, s>>>(D, Wk, oxhat, oscore);
+  if (D.n_bcols > 0) {
+    const size_t smem = (size_t)kBlockElems * (3 * sizeof(double) + sizeof(uint32_t));
+    k_eval_block<<<dim3(D.n_bcols, W), kBlockThreads, smem, s>>>(D, Wk, oxhat, oscore, P->pl.block_off);
+  }
+  if (D.n_chunks > 0)
+    k_eval_long<<<dim3(D.n_chunks, W), kBlockThreads, 0, s>>>(D, Wk, oxhat, oscore, P->pl.long_off);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+static DevWalkers eval_walkers(const chap_problem* P) {
+  DevWalkers Wk{};
+  Wk.x = P->e_x;
+  Wk.xs = (size_t)P->dp.n;
+  Wk.rs = P->e_rs;
+  Wk.rss = (size_t)P->dp.m_norm;
+  Wk.tabu = P->e_tabu;
+  Wk.ts = (size_t)P->dp.n;
+  Wk.best_x = P->e_bx;
+  Wk.sc = P->e_sc;
+  Wk.part = P->e_part;
+  Wk.ps = std::max(P->pl.total, 1);
+  Wk.lcount = P->e_lcount;
+  Wk.lcs = std::max(P->dp.n_long, 1);
+  Wk.lscr = P->e_lscr;
+  Wk.lss = P->lscr_per_walker;
+  Wk.use_tabu = 0;
+  Wk.W = 1;
+  Wk.tenure = 0;
+  Wk.wcap = 1e6f;
+  Wk.delta = NAN;
+  return Wk;
+}
+
+int chap::grid_for(long long work, int threads, int cap) {
+  long long g = (work + threads - 1) / threads;
+  return (int)std::max<long long>(1, std::min<long long>(g, cap));
+}
+
+extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double* x, const float* w,
+                                            double cutoff_rhs, double* xhat, double* score,
+                                            chap_move* best, void* cuda_stream) {
+  if (!p || (!x && p->dp.n > 0)) return fail(CHAP_ERR_INVALID_ARG, "NULL problem or x");
+  if (std::isnan(cutoff_rhs) || cutoff_rhs == -INFINITY) return fail(CHAP_ERR_INVALID_ARG, "cutoff_rhs must be finite or +INF");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const DevProblem& D = p->dp;
+  DevWalkers Wk = eval_walkers(p);
+  k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs);
+  if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, nullptr);
+  k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_rs, D.m_norm, p->e_sc, 2, w);
+  CUDA_TRY(cudaGetLastError());
+  TRY(launch_eval(p, Wk, xhat, score, s));
+  if (D.n_fixed > 0 && (xhat || score))
+    k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
+  k_select<<<1, 256, 0, s>>>(Wk, p->pl.total, best);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_eval_best_shift_host(chap_problem* p, const double* x, const float* w,
+                                                 double cutoff_rhs, double* xhat, double* score,
+                                                 chap_move* best, void* cuda_stream) {
+  if (!p || (!x && p->dp.n > 0)) return fail(CHAP_ERR_INVALID_ARG, "NULL problem or x");
+  DeviceGuard g(p->device);
+  const int n = p->dp.n, mn = p->dp.m_norm;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (!p->h_x) {
+    CUDA_TRY(cudaMallocHost(&p->h_x, sizeof(double) * std::max(n, 1)));
+    CUDA_TRY(cudaMallocHost(&p->h_w, sizeof(float) * std::max(mn, 1)));
+    CUDA_TRY(cudaMallocHost(&p->h_out, sizeof(double) * 2 * std::max(n, 1)));
+    CUDA_TRY(cudaMallocHost(&p->h_best, sizeof(chap_move)));
+    TRY(p->buf.alloc(&p->d_xu, n));
+    TRY(p->buf.alloc(&p->d_wu, mn));
+    TRY(p->buf.alloc(&p->d_out, 2 * (size_t)n));
+    TRY(p->buf.alloc(&p->d_best, 1));
+  }
+  memcpy(p->h_x, x, sizeof(double) * n);
+  CUDA_TRY(cudaMemcpyAsync(p->d_xu, p->h_x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (w) {
+    memcpy(p->h_w, w, sizeof(float) * mn);
+    CUDA_TRY(cudaMemcpyAsync(p->d_wu, p->h_w, sizeof(float) * mn, cudaMemcpyHostToDevice, s));
+  }
+  TRY(chap_eval_best_shift(p, p->d_xu, w ? p->d_wu : nullptr, cutoff_rhs, xhat ? p->d_out : nullptr,
+                           score ? p->d_out + n : nullptr, best ? p->d_best : nullptr, cuda_stream));
+  if (xhat) CUDA_TRY(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (score) CUDA_TRY(cudaMemcpyAsync(p->h_out + n, p->d_out + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (best) CUDA_TRY(cudaMemcpyAsync(p->h_best, p->d_best, sizeof(chap_move), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (xhat) memcpy(xhat, p->h_out, sizeof(double) * n);
+  if (score) memcpy(score, p->h_out + n, sizeof(double) * n);
+  if (best) *best = *p->h_best;
+  return CHAP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// walkers
+// ------------------------------------------------------------------------------------------
+extern "C" chap_status chap_params_default(chap_params* out) {
+  if (!out) return fail(CHAP_ERR_INVALID_ARG, "NULL out");
+  out->tenure = 10;
+  out->weight_cap = 1e6f;
+  out->cutoff_delta = NAN;
+  out->exchange_K = 1000;
+  out->n_elite = 4;
+  out->n_restart = -1;
+  out->graph_iters = 16;
+  return CHAP_OK;
+}
+
+static chap_status check_params(const chap_params& q) {
+  if (q.tenure < 0) return fail(CHAP_ERR_INVALID_ARG, "tenure < 0");
+  if (!(q.weight_cap >= 1.0f && q.weight_cap <= 16777216.0f)) return fail(CHAP_ERR_INVALID_ARG, "weight_cap must be in [1, 2^24]");
+  if (!std::isnan(q.cutoff_delta) && !(q.cutoff_delta >= 0.0 && std::isfinite(q.cutoff_delta)))
+    return fail(CHAP_ERR_INVALID_ARG, "cutoff_delta must be NaN (auto) or finite >= 0");
+  if (q.graph_iters < 0) return fail(CHAP_ERR_INVALID_ARG, "graph_iters < 0");
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, const double* x0,
+                                           const chap_params* params, void* cuda_stream,
+                                           chap_walkers** out) {
+  if (!out) return fail(CHAP_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!p || W < 1 || (!x0 && p->dp.n > 0)) return fail(CHAP_ERR_INVALID_ARG, "NULL problem/x0 or W < 1");
+  chap_params prm;
+  if (params) prm = *params; else chap_params_default(&prm);
+  TRY(check_params(prm));
+  DeviceGuard g(p->device);
+  auto S = new chap_walkers();
+  std::unique_ptr<chap_walkers> holder(S);
+  S->P = p;
+  S->W = W;
+  S->prm = prm;
+  const DevProblem& D = p->dp;
+  const size_t n = (size_t)std::max(D.n, 1), mn = (size_t)D.m_norm;
+  DevWalkers& Wk = S->wk;
+  DeviceBuffers& B = S->buf;
+  TRY(B.alloc(&Wk.x, n * W));
+  TRY(B.alloc(&Wk.rs, mn * W));
+  TRY(B.alloc(&Wk.tabu, n * W));
+  TRY(B.alloc(&Wk.best_x, n * W));
+  TRY(B.alloc(&Wk.sc, W));
+  Wk.ps = std::max(p->pl.total, 1);
+  TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
+  Wk.lcs = std::max(D.n_long, 1);
+  TRY(B.alloc(&Wk.lcount, (size_t)Wk.lcs * W));
+  Wk.lss = p->lscr_per_walker;
+  TRY(B.alloc(&Wk.lscr, Wk.lss * W));
+  TRY(B.alloc(&S->d_bad, 1));
+  Wk.xs = n;
+  Wk.rss = mn;
+  Wk.ts = n;
+  Wk.use_tabu = 1;
+  Wk.W = W;
+  Wk.tenure = prm.tenure;
+  Wk.wcap = prm.weight_cap;
+  Wk.delta = prm.cutoff_delta;
+  CUDA_TRY(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&S->ev_out, cudaEventDisableTiming));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  CUDA_TRY(cudaMemsetAsync(Wk.sc, 0, sizeof(WalkerScalars) * W, s));
+  CUDA_TRY(cudaMemsetAsync(Wk.lcount, 0, sizeof(unsigned) * Wk.lcs * W, s));
+  CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
+  CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
+  if (D.n > 0)
+    k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
+  k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.rs, Wk.rss, Wk.sc, 1, nullptr);
+  k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, -1);
+  k_walker_finalize_init<<<W, 256, 0, s>>>(D, Wk, 0, -1);
+  k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, Wk);
+  k_flush_done<<<(W + 255) / 256, 256, 0, s>>>(Wk);
+  CUDA_TRY(cudaGetLastError());
+  int bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, S->d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (bad) return fail(CHAP_ERR_INVALID_ARG, "x0 out of bounds or fractional on an integer variable");
+  // apply grid: enough blocks for a bump over m_norm rows (4 rows per thread), capped by the SMs
+  S->apply_grid = grid_for((long long)mn, 4 * kApplyThreads, std::max(1, 2 * p->sm_count / std::max(1, std::min(W, 8))));
+  *out = holder.release();
+  return CHAP_OK;
+}
+
+static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
+  const chap_problem* P = S->P;
+  TRY(launch_eval(P, S->wk, nullptr, nullptr, s));
+  k_select<<<S->W, 256, 0, s>>>(S->wk, P->pl.total, nullptr);
+  k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_tabu_step(chap_walkers* S, int32_t n_iters, chap_step_record* log,
+                                      void* cuda_stream) {
+  if (!S || n_iters < 0) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or n_iters < 0");
+  if (n_iters == 0) return CHAP_OK;
+  DeviceGuard g(S->P->device);
+  cudaStream_t us = (cudaStream_t)cuda_stream;
+  cudaStream_t s = S->stream;
+  CUDA_TRY(cudaEventRecord(S->ev_in, us));
+  CUDA_TRY(cudaStreamWaitEvent(s, S->ev_in, 0));
+  k_set_log<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk, log);
+  CUDA_TRY(cudaGetLastError());
+  const int gi = S->prm.graph_iters;
+  int done = 0;
+  if (gi > 0 && n_iters >= gi) {
+    if (!S->gexec) {
+      cudaGraph_t graph;
+      CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      chap_status st = CHAP_OK;
+      for (int it = 0; it < gi && st == CHAP_OK; ++it) st = launch_iteration(S, s);
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (st != CHAP_OK) return st;
+      if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&S->gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+      S->g_iters = gi;
+    }
+    while (n_iters - done >= S->g_iters) {
+      CUDA_TRY(cudaGraphLaunch(S->gexec, s));
+      done += S->g_iters;
+    }
+  }
+  for (; done < n_iters; ++done) TRY(launch_iteration(S, s));
+  const DevProblem& D = S->P->dp;
+  k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * S->P->sm_count), S->W), 256, 0, s>>>(D, S->wk);
+  k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk);
+  k_set_log<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk, nullptr);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(S->ev_out, s));
+  CUDA_TRY(cudaStreamWaitEvent(us, S->ev_out, 0));
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_get(const chap_walkers* S, double* x, double* r, float* w,
+                                        int64_t* tabu_until, double* best_x, chap_walker_stats* stats,
+                                        void* cuda_stream) {
+  if (!S) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers");
+  DeviceGuard g(S->P->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const DevProblem& D = S->P->dp;
+  const int gx = grid_for(std::max(D.n, D.m_norm), 256, 4 * S->P->sm_count);
+  if (x || tabu_until || best_x) k_export_vars<<<dim3(gx, S->W), 256, 0, s>>>(D, S->wk, x, tabu_until, best_x);
+  if (r || w) k_export_rows<<<dim3(gx, S->W), 256, 0, s>>>(D, S->wk, r, w);
+  if (stats) k_export_stats<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk, stats);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_set_cutoff(chap_walkers* S, double z_best, void* cuda_stream) {
+  if (!S || !std::isfinite(z_best)) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or non-finite z_best");
+  DeviceGuard g(S->P->device);
+  k_set_cutoff<<<(S->W + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>(S->P->dp, S->wk, z_best);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_restart(chap_walkers* S, int32_t walker, const double* x,
+                                            void* cuda_stream) {
+  if (!S || walker < 0 || walker >= S->W || (!x && S->P->dp.n > 0))
+    return fail(CHAP_ERR_INVALID_ARG, "bad walker index or NULL x");
+  DeviceGuard g(S->P->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const DevProblem& D = S->P->dp;
+  DevWalkers& Wk = S->wk;
+  const int gx = grid_for(D.n, 256, 4 * S->P->sm_count);
+  // write into walker `walker` only: offset the destinations
+  if (D.n > 0) k_permute_in<<<dim3(gx, 1), 256, 0, s>>>(D, x, D.n, Wk.x + (size_t)walker * Wk.xs, Wk.xs, nullptr);
+  k_rows_init<<<dim3(S->P->rows_grid, 1), 256, 0, s>>>(D, Wk.x + (size_t)walker * Wk.xs, Wk.xs,
+                                                      Wk.rs + (size_t)walker * Wk.rss, Wk.rss, Wk.sc + walker, 0, nullptr);
+  k_tabu_clear<<<dim3(gx, 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, walker);
+  k_walker_finalize_init<<<1, 256, 0, s>>>(D, Wk, 1, walker);
+  k_flush_incumbent<<<dim3(gx, S->W), 256, 0, s>>>(D, Wk);
+  k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, double* ms, void* cuda_stream) {
+  if (!S || n_iters < 1 || !ms) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers/ms or n_iters < 1");
+  DeviceGuard g(S->P->device);
+  const chap_problem* P = S->P;
+  const DevProblem& D = P->dp;
+  cudaStream_t s = S->stream;
+  cudaStream_t us = (cudaStream_t)cuda_stream;
+  CUDA_TRY(cudaEventRecord(S->ev_in, us));
+  CUDA_TRY(cudaStreamWaitEvent(s, S->ev_in, 0));
+  k_set_log<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk, nullptr);
+  std::vector<cudaEvent_t> ev(10 * (size_t)n_iters);
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  const size_t smem = (size_t)kBlockElems * (3 * sizeof(double) + sizeof(uint32_t));
+  for (int it = 0; it < n_iters; ++it) {
+    cudaEvent_t* e = &ev[10 * (size_t)it];
+    cudaEventRecord(e[0], s);
+    if (D.n_wtasks > 0) k_eval_warp<<<dim3(P->warp_grid, S->W), kEvalThreads, 0, s>>>(D, S->wk, nullptr, nullptr);
+    cudaEventRecord(e[1], s);
+    cudaEventRecord(e[2], s);
+    if (D.n_bcols > 0)
+      k_eval_block<<<dim3(D.n_bcols, S->W), kBlockThreads, smem, s>>>(D, S->wk, nullptr, nullptr, P->pl.block_off);
+    cudaEventRecord(e[3], s);
+    cudaEventRecord(e[4], s);
+    if (D.n_chunks > 0)
+      k_eval_long<<<dim3(D.n_chunks, S->W), kBlockThreads, 0, s>>>(D, S->wk, nullptr, nullptr, P->pl.long_off);
+    cudaEventRecord(e[5], s);
+    cudaEventRecord(e[6], s);
+    k_select<<<S->W, 256, 0, s>>>(S->wk, P->pl.total, nullptr);
+    cudaEventRecord(e[7], s);
+    cudaEventRecord(e[8], s);
+    k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
+    cudaEventRecord(e[9], s);
+  }
+  CUDA_TRY(cudaGetLastError());
+  k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), S->W), 256, 0, s>>>(D, S->wk);
+  k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk);
+  CUDA_TRY(cudaStreamSynchronize(s));
+  for (int q = 0; q < 5; ++q) ms[q] = 0.0;
+  for (int it = 0; it < n_iters; ++it)
+    for (int q = 0; q < 5; ++q) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev[10 * (size_t)it + 2 * q], ev[10 * (size_t)it + 2 * q + 1]));
+      ms[q] += t;
+    }
+  for (int q = 0; q < 5; ++q) ms[q] /= n_iters;
+  if (D.n_wtasks == 0) ms[0] = 0.0;
+  if (D.n_bcols == 0) ms[1] = 0.0;
+  if (D.n_chunks == 0) ms[2] = 0.0;
+  for (auto& e : ev) cudaEventDestroy(e);
+  CUDA_TRY(cudaEventRecord(S->ev_out, s));
+  CUDA_TRY(cudaStreamWaitEvent(us, S->ev_out, 0));
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
+  if (!S) return CHAP_OK;
+  DeviceGuard g(S->P->device);
+  delete S;
+  return CHAP_OK;
+}

@@ -1,0 +1,150 @@
+// host.h — host-side internals of libchap shared by chap.cu and portfolio.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "chap.h"
+#include "common.cuh"
+
+namespace chap {
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+chap_status fail(chap_status s, const char* fmt, ...);
+
+#define CUDA_TRY(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? CHAP_ERR_OOM : CHAP_ERR_CUDA,        \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);  \
+  } while (0)
+
+#define TRY(call)                      \
+  do {                                 \
+    chap_status s_ = (call);           \
+    if (s_ != CHAP_OK) return s_;      \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+// problem
+// ------------------------------------------------------------------------------------------
+struct DeviceBuffers {
+  std::vector<void*> ptrs;
+  ~DeviceBuffers() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  chap_status alloc(T** out, size_t count) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(CHAP_ERR_OOM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+    ptrs.push_back(p);
+    *out = static_cast<T*>(p);
+    bytes_total += bytes;
+    return CHAP_OK;
+  }
+  template <class T>
+  chap_status upload(T** out, const std::vector<T>& h) {
+    TRY(alloc(out, h.size()));
+    if (!h.empty()) CUDA_TRY(cudaMemcpy(*out, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return CHAP_OK;
+  }
+  size_t bytes_total = 0;
+};
+
+}  // namespace chap
+
+using namespace chap;
+
+// The opaque handles of chap.h (global scope).
+struct chap_problem {
+  using DeviceBuffers = chap::DeviceBuffers;
+  int device = 0;
+  int sm_count = 148;
+  chap_problem_info info{};
+  std::vector<int32_t> orig_row;
+  std::vector<int8_t> side;
+  DeviceBuffers buf;
+  DevProblem dp{};
+  PartLayout pl{};
+  int warp_grid = 1;
+  int rows_grid = 1;
+  size_t lscr_per_walker = 1;   // doubles
+  // eval workspace (one virtual walker)
+  double* e_x = nullptr;
+  RowState* e_rs = nullptr;
+  int32_t* e_tabu = nullptr;
+  double* e_bx = nullptr;
+  WalkerScalars* e_sc = nullptr;
+  Cand* e_part = nullptr;
+  unsigned* e_lcount = nullptr;
+  double* e_lscr = nullptr;
+  // host-buffer variant staging (lazy)
+  double* h_x = nullptr;
+  float* h_w = nullptr;
+  double* h_out = nullptr;
+  chap_move* h_best = nullptr;
+  double* d_xu = nullptr;
+  float* d_wu = nullptr;
+  double* d_out = nullptr;
+  chap_move* d_best = nullptr;
+  ~chap_problem() {
+    if (h_x) cudaFreeHost(h_x);
+    if (h_w) cudaFreeHost(h_w);
+    if (h_out) cudaFreeHost(h_out);
+    if (h_best) cudaFreeHost(h_best);
+  }
+};
+
+struct chap_walkers {
+  using DeviceBuffers = chap::DeviceBuffers;
+  const chap_problem* P = nullptr;
+  int W = 0;
+  chap_params prm{};
+  DeviceBuffers buf;
+  DevWalkers wk{};
+  int* d_bad = nullptr;
+  cudaStream_t stream = nullptr;       // internal stream (graph capture / launch)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int g_iters = 0;
+  int apply_grid = 1;
+  ~chap_walkers() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+
+namespace chap {
+// shared launch helpers (chap.cu)
+chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, double* oxhat, double* oscore,
+                        cudaStream_t s);
+int grid_for(long long work, int threads, int cap);
+
+}  // namespace chap

@@ -1,0 +1,294 @@
+// tabu.cuh — walker state kernels: residual initialisation, apply (incremental residual update,
+// PAPER.md:343), weight bump (R12), incumbent / cutoff (R15), exports.
+#pragma once
+#include "common.cuh"
+#include "eval.cuh"
+
+namespace chap {
+
+// x_int[w][p] = x_user[w][perm[p]]; flags an out-of-bounds or fractional-integer value.
+__global__ void k_permute_in(DevProblem P, const double* __restrict__ xu, size_t xus, double* xi,
+                             size_t xis, int* bad) {
+  const int w = blockIdx.y;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) {
+    const double v = xu[(size_t)w * xus + P.perm[p]];
+    const uint8_t vc = P.vclass[p];
+    const bool ok = (v >= P.lb[p]) && (v <= P.ub[p]) && (vc == 3 || v == floor(v));
+    if (!ok && bad) atomicOr(bad, 1);
+    xi[(size_t)w * xis + p] = v;
+  }
+}
+
+// r_i = Σ_k a_ik x̄_k - b_i from scratch (warp per row, CSR). The cutoff row (last) is active
+// iff sc[w].cut_active (rhs sc[w].cutoff_rhs); otherwise r = -inf. init_w: 0 keep weights,
+// 1 set to 1, 2 copy from wsrc (eval API).
+__global__ void k_rows_init(DevProblem P, const double* __restrict__ x, size_t xs, RowState* rs,
+                            size_t rss, const WalkerScalars* sc, int init_w,
+                            const float* __restrict__ wsrc) {
+  const int w = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const double* xw = x + (size_t)w * xs;
+  RowState* rw = rs + (size_t)w * rss;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < P.m_norm; i += nwarps) {
+    const int e0 = P.rp[i], e1 = P.rp[i + 1];
+    double y = 0.0;
+    for (int e = e0 + lane; e < e1; e += 32) y += P.cv[e] * xw[P.ci[e]];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) y += __shfl_xor_sync(kFull, y, off);
+    if (lane == 0) {
+      double r;
+      if (i < P.cut_row) {
+        r = y - P.b[i];
+      } else {
+        r = sc[w].cut_active ? y - sc[w].cutoff_rhs : -INFINITY;
+      }
+      RowState s = rw[i];
+      s.r = r;
+      if (init_w == 1) s.w = 1.0f;
+      else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
+      s.pad = 0;
+      rw[i] = s;
+    }
+  }
+}
+
+__device__ __forceinline__ double auto_delta(const DevProblem& P, double delta_param, double z) {
+  if (!isnan(delta_param)) return delta_param;
+  if (!isnan(P.auto_delta)) return P.auto_delta;
+  return 1e-6 * fmax(1.0, fabs(z));   // R14
+}
+
+// Set the walker's incumbent from its current point (violated == 0): best_obj, cutoff rhs
+// c.x̄ - δ, residual of the cutoff row recomputed as y_cut - rhs.
+__device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWalkers& Wk,
+                                               WalkerScalars* sc, RowState* rw) {
+  const double z = sc->obj;
+  sc->best_obj = z;
+  sc->has_inc = 1;
+  sc->pending_copy = 1;
+  const double rhs = z - auto_delta(P, Wk.delta, z);
+  sc->cutoff_rhs = rhs;
+  sc->cut_active = 1;
+  const double r = z - rhs;
+  rw[P.cut_row].r = r;
+  sc->violated = (r > 0.0) ? 1 : 0;
+}
+
+// One block per walker: violated count, objective, k = 0 incumbent check (R15).
+// mode 0: walker create (k = 0, counters cleared); mode 1: restart (keeps k, counters, best).
+__global__ void __launch_bounds__(256) k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode,
+                                                              int only_walker) {
+  __shared__ double sm[32];
+  __shared__ long long smv[32];
+  const int w = (only_walker >= 0) ? only_walker : blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  WalkerScalars* sc = Wk.sc + w;
+  RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const double* x = Wk.x + (size_t)w * Wk.xs;
+  const int cut_active = sc->cut_active;
+  long long v = 0;
+  for (int i = tid; i < P.m_norm; i += blockDim.x) {
+    if (i == P.cut_row && !cut_active) continue;
+    v += (rw[i].r > 0.0) ? 1 : 0;
+  }
+  double z = 0.0;
+  for (int p = tid; p < P.n; p += blockDim.x) z += P.c[p] * x[p];
+  for (int off = 16; off > 0; off >>= 1) {
+    v += __shfl_xor_sync(kFull, v, off);
+    z += __shfl_xor_sync(kFull, z, off);
+  }
+  if (lane == 0) { smv[wid] = v; sm[wid] = z; }
+  __syncthreads();
+  if (tid == 0) {
+    long long vt = 0;
+    double zt = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { vt += smv[q]; zt += sm[q]; }
+    sc->violated = vt;
+    sc->obj = zt;
+    if (mode == 0) {
+      sc->k = 0;
+      sc->n_moves = 0;
+      sc->n_stuck = 0;
+      sc->has_inc = 0;
+      sc->best_obj = INFINITY;
+      sc->apply_counter = 0;
+      sc->log = nullptr;
+      sc->log_k0 = 0;
+    }
+    if (vt == 0) take_incumbent(P, Wk, sc, rw);
+  }
+}
+
+// Clear the tabu list of walker w (restart) or of all walkers.
+__global__ void k_tabu_clear(int32_t* tabu, size_t ts, int n, int only_walker) {
+  const int w = (only_walker >= 0) ? only_walker : blockIdx.y;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    tabu[(size_t)w * ts + p] = 0;
+}
+
+// Apply the selected move or bump weights, then (last block) finalise the iteration.
+__global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalkers Wk) {
+  __shared__ long long smv[32];
+  __shared__ int s_last;
+  const int w = blockIdx.y, tid = threadIdx.x;
+  WalkerScalars* sc = Wk.sc + w;
+  double* x = Wk.x + (size_t)w * Wk.xs;
+  RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const Decision d = sc->dec;
+  const int cut_active = sc->cut_active;
+  const int gtid = blockIdx.x * blockDim.x + tid, gstride = gridDim.x * blockDim.x;
+  // phase 0: an incumbent found by the previous iteration: best_x <- x (x unchanged since)
+  if (sc->pending_copy) {
+    double* bx = Wk.best_x + (size_t)w * Wk.xs;
+    for (int p = gtid; p < P.n; p += gstride) bx[p] = x[p];
+  }
+  long long dv = 0;
+  if (d.move) {
+    // r_i += a_ij Δ over column j* (PAPER.md:343); count feasibility transitions
+    const int e0 = P.col_ptr[d.p], e1 = P.col_ptr[d.p + 1];
+    for (int e = e0 + gtid; e < e1; e += gstride) {
+      const int i = P.row_idx[e];
+      if (i == P.cut_row && !cut_active) continue;
+      const double r0 = rw[i].r;
+      const double r1 = r0 + P.val[e] * d.delta;
+      rw[i].r = r1;
+      dv += (long long)(r1 > 0.0) - (long long)(r0 > 0.0);
+    }
+  } else {
+    // stuck: w_i <- min(w_i + 1, cap) on every active violated row (R12)
+    for (int i = gtid; i < P.m_norm; i += gstride) {
+      if (i == P.cut_row && !cut_active) continue;
+      if (rw[i].r > 0.0) rw[i].w = fminf(rw[i].w + 1.0f, Wk.wcap);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) dv += __shfl_xor_sync(kFull, dv, off);
+  if ((tid & 31) == 0) smv[tid >> 5] = dv;
+  __syncthreads();
+  if (tid == 0) {
+    long long t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += smv[q];
+    if (t) atomicAdd((unsigned long long*)&sc->violated, (unsigned long long)t);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&sc->apply_counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence();
+  volatile WalkerScalars* vsc = sc;
+  const long long k = vsc->k;
+  sc->pending_copy = 0;
+  if (d.move) {
+    x[d.p] = d.v;
+    Wk.tabu[(size_t)w * Wk.ts + d.p] = (int32_t)(k + 1 + Wk.tenure);
+    sc->obj = vsc->obj + P.c[d.p] * d.delta;
+    sc->n_moves = vsc->n_moves + 1;
+  } else {
+    sc->n_stuck = vsc->n_stuck + 1;
+  }
+  if (vsc->violated == 0) take_incumbent(P, Wk, sc, rw);   // PAPER.md:373, R15
+  chap_step_record* log = vsc->log;
+  if (log) {
+    chap_step_record rec;
+    rec.k = k;
+    rec.j = d.move ? d.j : -1;
+    rec.pad = 0;
+    rec.v = d.move ? d.v : NAN;
+    rec.s = d.s;
+    rec.violated = vsc->violated;
+    rec.obj = vsc->obj;
+    log[(size_t)(k - vsc->log_k0) * Wk.W + w] = rec;
+  }
+  sc->k = k + 1;
+  sc->apply_counter = 0;
+}
+
+// Complete a pending best_x copy (end of chap_tabu_step / before exports).
+__global__ void k_flush_incumbent(DevProblem P, DevWalkers Wk) {
+  const int w = blockIdx.y;
+  WalkerScalars* sc = Wk.sc + w;
+  if (!sc->pending_copy) return;
+  const double* x = Wk.x + (size_t)w * Wk.xs;
+  double* bx = Wk.best_x + (size_t)w * Wk.xs;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) bx[p] = x[p];
+}
+
+__global__ void k_flush_done(DevWalkers Wk) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < Wk.W) Wk.sc[w].pending_copy = 0;
+}
+
+// Per-walker log pointer and k offset for the coming chap_tabu_step call.
+__global__ void k_set_log(DevWalkers Wk, chap_step_record* log) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < Wk.W) {
+    Wk.sc[w].log = log;
+    Wk.sc[w].log_k0 = Wk.sc[w].k;
+  }
+}
+
+// Exports in user order.
+__global__ void k_export_vars(DevProblem P, DevWalkers Wk, double* x, int64_t* tabu, double* best_x) {
+  const int w = blockIdx.y;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) {
+    const size_t uo = (size_t)w * P.n + P.perm[p];
+    const size_t io = (size_t)w * Wk.xs + p;
+    if (x) x[uo] = Wk.x[io];
+    if (best_x) best_x[uo] = Wk.best_x[io];
+    if (tabu) tabu[uo] = (int64_t)Wk.tabu[(size_t)w * Wk.ts + p];
+  }
+}
+
+__global__ void k_export_rows(DevProblem P, DevWalkers Wk, double* r, float* wt) {
+  const int w = blockIdx.y;
+  const RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const int cut_active = Wk.sc[w].cut_active;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m_norm; i += gridDim.x * blockDim.x) {
+    const RowState s = rw[i];
+    if (r) r[(size_t)w * P.m_norm + i] = (i == P.cut_row && !cut_active) ? -INFINITY : s.r;
+    if (wt) wt[(size_t)w * P.m_norm + i] = s.w;
+  }
+}
+
+__global__ void k_export_stats(DevWalkers Wk, chap_walker_stats* st) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= Wk.W) return;
+  const WalkerScalars& s = Wk.sc[w];
+  chap_walker_stats o;
+  o.k = s.k;
+  o.violated = s.violated;
+  o.obj = s.obj;
+  o.best_obj = s.best_obj;
+  o.cutoff_rhs = s.cut_active ? s.cutoff_rhs : INFINITY;
+  o.has_incumbent = s.has_inc;
+  o.pad = 0;
+  o.n_moves = s.n_moves;
+  o.n_stuck = s.n_stuck;
+  st[w] = o;
+}
+
+// External cutoff: rhs = min(current, z - δ); residual and violated count updated.
+__global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= Wk.W) return;
+  WalkerScalars* sc = Wk.sc + w;
+  RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const double rhs = z - auto_delta(P, Wk.delta, z);
+  if (sc->cut_active && !(rhs < sc->cutoff_rhs)) return;
+  const double r_old = sc->cut_active ? rw[P.cut_row].r : -INFINITY;
+  const double r_new = sc->obj - rhs;
+  sc->violated += (long long)(r_new > 0.0) - (long long)(r_old > 0.0);
+  rw[P.cut_row].r = r_new;
+  sc->cutoff_rhs = rhs;
+  sc->cut_active = 1;
+}
+
+// Scalars of the eval API's single virtual walker: k = 0, cutoff from the call.
+__global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs) {
+  sc->k = 0;
+  sc->cut_active = cutoff_rhs < INFINITY;
+  sc->cutoff_rhs = cutoff_rhs;
+}
+
+}  // namespace chap

@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bit-exact on every per-variable (x̂_j, s_j), on the chosen move and on whole tabu trajectories,
+in the exact domain (integer data and weights) that every synthetic config uses.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import exact
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_2605_05086_b200 as chap  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _eval_both(inst, x, w=None, cutoff=math.inf, P=None, O=None):
+    P = P or chap.Problem.from_instance(inst)
+    O = O or oracle.Problem.from_instance(inst)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+    wt = None if w is None else torch.from_numpy(np.ascontiguousarray(w, np.float32)).cuda()
+    xhat, score, best = P.eval_best_shift(xt, wt, cutoff)
+    torch.cuda.synchronize()
+    oxhat, oscore, obest = O.best_shift(x, w, cutoff)
+    return (xhat.cpu().numpy(), score.cpu().numpy(), chap.move_from_bytes(best)), (oxhat, oscore, obest)
+
+
+def _assert_same(g, o, tag=""):
+    gx, gs, gm = g
+    ox, os_, ob = o
+    bad = np.nonzero((gx != ox) | (gs != os_))[0]
+    assert bad.size == 0, f"{tag}: {bad.size} vars differ, first {bad[:5]}: gpu {gx[bad[:5]]} {gs[bad[:5]]} " \
+                          f"oracle {ox[bad[:5]]} {os_[bad[:5]]}"
+    assert gm["j"] == ob[0], (tag, gm, ob)
+    if ob[0] >= 0:
+        assert gm["v"] == ob[1] and gm["s"] == ob[2], (tag, gm, ob)
+
+
+@pytest.mark.parametrize("case", json.load(open(os.path.join(GOLD, "alg1_worked.json")))["cases"],
+                         ids=lambda c: c["name"])
+def test_worked_cases(case):
+    inst = exact.rows_from_json(case)
+    g, o = _eval_both(inst, np.array(case["x"], float))
+    _assert_same(g, o, case["name"])
+    assert list(g[0]) == case["xhat"]
+
+
+def test_random_tiny_instances():
+    n_ok = 0
+    for seed in range(400):
+        kw = [{}, {"p_inf_bound": 0.3}, {"coef": 6, "bound": 9}, {"p_binary": 0.8}][seed % 4]
+        inst = synth.random_tiny(seed, **kw)
+        try:
+            O = oracle.Problem.from_instance(inst)
+        except oracle.OracleError:
+            continue
+        P = chap.Problem.from_instance(inst)
+        lb, ub = exact.bounds(inst)
+        x = np.clip(synth.random_point_tiny(inst, seed), lb, ub)
+        w = np.random.default_rng(seed).integers(0, 5, P.m_norm).astype(np.float32)
+        cut = math.inf if seed % 3 else float(inst.c @ x) - 1.0
+        g, o = _eval_both(inst, x, w, cut, P, O)
+        _assert_same(g, o, inst.name)
+        n_ok += 1
+    assert n_ok > 250
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_config_T(seed):
+    inst = synth.tiny(seed)
+    x = synth.x_random(inst, seed)
+    P = chap.Problem.from_instance(inst)
+    w = synth.weights_random(P.m_norm, seed)
+    g, o = _eval_both(inst, x, w, P=P)
+    _assert_same(g, o, inst.name)
+
+
+def _mixed_small(seed=5):
+    # spans every column class: short binary/general (warp), medium (block), long chunked
+    return synth.mixed(seed=seed, n=20_000, m=4_000, n_long=8, long_lo=600, long_hi=12_000)
+
+
+def test_all_column_classes():
+    inst = _mixed_small()
+    P = chap.Problem.from_instance(inst)
+    assert P.info.n_long_columns >= 2
+    for s in range(3):
+        x = synth.x_random(inst, s)
+        w = synth.weights_random(P.m_norm, s, hi=7)
+        cut = math.inf if s == 0 else float(inst.c @ x) - 50.0
+        g, o = _eval_both(inst, x, w, cut, P=P)
+        _assert_same(g, o, f"mixed s={s}")
+
+
+def test_config_S_full():
+    inst = synth.setcover()
+    x = synth.x_bernoulli(inst, (1, 0), 0.05)
+    g, o = _eval_both(inst, x)
+    _assert_same(g, o, "S")
+
+
+def test_host_buffer_variant_equals_device():
+    inst = _mixed_small(6)
+    P = chap.Problem.from_instance(inst)
+    x = synth.x_random(inst, 2)
+    w = synth.weights_random(P.m_norm, 2)
+    xh, sh, mh = P.eval_best_shift_host(x, w)
+    xd, sd, md = P.eval_best_shift(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(xh, xd.cpu().numpy()) and np.array_equal(sh, sd.cpu().numpy())
+    assert mh.tobytes() == chap.move_from_bytes(md).tobytes()
+
+
+def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16):
+    P = chap.Problem.from_instance(inst)
+    O = oracle.Problem.from_instance(inst)
+    prm = chap.default_params(graph_iters=graph_iters)
+    X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
+    Wk = chap.Walkers(P, X0, prm)
+    log = chap.records(Wk.step(n_iters, log=True)).reshape(n_iters, len(x0s))
+    st = Wk.get()
+    for wi, x0 in enumerate(x0s):
+        ow = oracle.TabuWalker(O, x0)
+        olog = ow.run(n_iters)
+        glog = log[:, wi]
+        for f in ("k", "j", "violated", "obj", "s"):
+            bad = np.nonzero(glog[f] != olog[f])[0]
+            assert bad.size == 0, (inst.name, wi, f, bad[:3], glog[bad[:3]], olog[bad[:3]])
+        mv = glog["j"] >= 0
+        assert np.array_equal(glog["v"][mv], olog["v"][mv])
+        assert np.array_equal(st["x"][wi], ow.x[: inst.n])
+        assert np.array_equal(st["w"][wi], ow.w)
+        assert np.array_equal(st["tabu_until"][wi], ow.tabu_until[: inst.n])
+        assert st["stats"][wi]["has_incumbent"] == int(ow.has_incumbent)
+        if ow.has_incumbent:
+            assert st["stats"][wi]["best_obj"] == ow.best_obj
+            assert np.array_equal(st["best_x"][wi], ow.best_x[: inst.n])
+        # residual invariant: r == A x - b (exact domain)
+        r = O.residuals(st["x"][wi], ow.cutoff_rhs)
+        assert np.array_equal(st["r"][wi], r)
+    return log
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_trajectory_config_T(seed):
+    inst = synth.tiny(seed)
+    _traj_compare(inst, [synth.x_lower(inst)], 600, graph_iters=16 if seed % 2 else 0)
+
+
+def test_trajectory_multi_walker():
+    inst = synth.tiny(3)
+    x0s = [synth.x_lower(inst)] + [np.clip(synth.x_random(inst, s), inst.lb, inst.ub) for s in range(5)]
+    _traj_compare(inst, x0s, 300)
+
+
+def test_trajectory_mixed_small():
+    inst = synth.mixed(seed=9, n=4000, m=800, n_long=4, long_lo=300, long_hi=6000)
+    _traj_compare(inst, [synth.x_lower(inst), synth.x_random(inst, 1)], 60)
+
+
+def test_trajectory_setcover_small():
+    inst = synth.setcover(seed=4, m=500, n=2500)
+    _traj_compare(inst, [synth.x_lower(inst)], 400)
+
+
+def test_invalid_x0_rejected():
+    inst = synth.tiny(0)
+    P = chap.Problem.from_instance(inst)
+    x0 = synth.x_lower(inst)
+    x0[31] = 0.5   # fractional on an integer variable
+    with pytest.raises(chap.ChapError) as e:
+        chap.Walkers(P, torch.from_numpy(x0[None, :]).cuda())
+    assert e.value.status == 1
