@@ -59,12 +59,6 @@ extern "C" const char* chap_status_string(chap_status s) {
 extern "C" int32_t chap_abi_version(void) { return CHAP_ABI_VERSION; }
 
 
-static inline int ilog2_ceil(int v) {
-  int l = 0;
-  while ((1 << l) < v) ++l;
-  return l;
-}
-
 static bool integral(double v) { return std::isfinite(v) && v == std::floor(v); }
 
 extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, const int64_t* row_ptr,
@@ -193,32 +187,33 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   std::vector<int32_t> deg(n, 0);
   for (int64_t e = 0; e < nnz_norm; ++e) deg[ncol[e]]++;
   for (int32_t j = 0; j < n; ++j) deg[j] += (cc[j] != 0.0);
-  std::vector<int32_t> cls(n), lgv(n, 0);
+  std::vector<int32_t> cls(n);
   for (int32_t j = 0; j < n; ++j) {
     const int d = deg[j];
     if (vclass[j] == 0) {
       cls[j] = CC_FIXED;
+    } else if (d == 0) {
+      cls[j] = CC_EMPTY;
     } else if (vclass[j] == 1) {
-      if (d <= 32) { cls[j] = CC_BIN; lgv[j] = std::max(1, ilog2_ceil(std::max(d, 1))); }
-      else if (d <= kBinWideMax) cls[j] = CC_BINW;
-      else cls[j] = CC_BINL;
+      cls[j] = (d <= kShortDeg) ? CC_BIN : CC_LBIN;
+    } else if (d + 2 <= kShortDeg) {
+      cls[j] = CC_GEN;
+    } else if (vclass[j] == 2 && std::isfinite(l[j]) && std::isfinite(u[j]) && u[j] - l[j] + 1.0 <= kBucketMax) {
+      cls[j] = CC_LBKT;
+    } else if (d + 2 <= kGenmMax) {
+      cls[j] = CC_GENM;
     } else {
-      if (d + 2 <= 32) { cls[j] = CC_GEN; lgv[j] = std::max(2, ilog2_ceil(d + 2)); }
-      else if (d + 2 <= kBlockElems) cls[j] = CC_GENB;
-      else if (vclass[j] == 2 && std::isfinite(l[j]) && std::isfinite(u[j]) && u[j] - l[j] + 1.0 <= kBucketMax)
-        cls[j] = CC_GENL;
-      else
-        return fail(CHAP_ERR_UNSUPPORTED,
-                    "variable %d: non-binary column with %d nonzeros and domain [%g, %g] (needs the "
-                    "multi-block merge sort, not in this build)", j, d, l[j], u[j]);
+      return fail(CHAP_ERR_UNSUPPORTED,
+                  "variable %d: non-binary column with %d nonzeros and domain [%g, %g] (needs the "
+                  "multi-block merge sort, not in this build)", j, d, l[j], u[j]);
     }
   }
-  // internal order: by (class, group size, user index)
+  // internal order: by (class, degree, user index) — heavy tiles first, similar degrees together
   std::vector<int32_t> perm(n);
   std::iota(perm.begin(), perm.end(), 0);
   std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
     if (cls[a] != cls[b]) return cls[a] < cls[b];
-    return lgv[a] < lgv[b];
+    return deg[a] > deg[b];
   });
   std::vector<int32_t> iperm(n);
   for (int32_t p = 0; p < n; ++p) iperm[perm[p]] = p;
@@ -273,10 +268,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     ci_[p] = cc[j];
     vci[p] = vclass[j];
   }
-  // tasks
-  std::vector<WTask> wt;
-  std::vector<int32_t> bcols;
-  std::vector<LChunk> chunks;
+  // tiles (PAPER.md:353-355 length dispatch): block tiles — chunks of long columns, single-column
+  // sorts — and warp tiles of packed short columns
+  std::vector<Tile> tiles;
+  std::vector<WTile> wtiles;
   int32_t n_long = 0;
   int64_t lscr = 0;
   int32_t p = 0;
@@ -284,40 +279,56 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     const int32_t j = perm[p];
     const int k = cls[j];
     if (k == CC_FIXED) { ++p; continue; }
-    if (k == CC_BIN || k == CC_GEN) {
-      const int lg = lgv[j];
-      const int per = 32 >> lg;
-      int cnt = 0;
-      while (p + cnt < n && cnt < per && cls[perm[p + cnt]] == k && lgv[perm[p + cnt]] == lg) ++cnt;
-      wt.push_back(WTask{p, (int16_t)cnt, (int8_t)k, (int8_t)lg});
+    if (k == CC_BIN || k == CC_GEN || k == CC_EMPTY) {
+      const int extra = (k == CC_GEN) ? 2 : 0;
+      const int cap = (k == CC_GEN) ? kWTileGen : kWTileNnz;
+      int cnt = 0, tot = 0;
+      while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k &&
+             tot + deg[perm[p + cnt]] + extra <= cap) {
+        tot += deg[perm[p + cnt]] + extra;
+        ++cnt;
+      }
+      WTile W{};
+      W.p0 = p;
+      W.e0 = col_ptr[p];
+      W.e1 = col_ptr[p + cnt];
+      W.ncols = (int16_t)cnt;
+      W.kind = (int8_t)k;
+      wtiles.push_back(W);
       p += cnt;
       continue;
     }
-    if (k == CC_BINW) {
-      wt.push_back(WTask{p, 1, (int8_t)CC_BINW, 5});
-    } else if (k == CC_GENB) {
-      bcols.push_back(p);
-    } else {  // CC_BINL, CC_GENL
-      const int d = deg[j];
-      const int nch = (d + kLongChunk - 1) / kLongChunk;
-      const int kind = (k == CC_BINL) ? 0 : 1;
-      const int dom = kind ? (int)(u[j] - l[j] + 1.0) : 0;
-      for (int q = 0; q < nch; ++q) {
-        LChunk ch;
-        ch.p = p;
-        ch.lc = n_long;
-        ch.e0 = col_ptr[p] + q * kLongChunk;
-        ch.e1 = std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * kLongChunk);
-        ch.chunk = q;
-        ch.nchunks = nch;
-        ch.kind = kind;
-        ch.dom = dom;
-        ch.scr = lscr;
-        chunks.push_back(ch);
-      }
-      lscr += kind ? (2LL * nch * dom + 2LL * nch) : nch;
-      ++n_long;
+    Tile T{};
+    T.kind = k;
+    T.p0 = p;
+    T.ncols = 1;
+    T.chunk = 0;
+    T.nchunks = 1;
+    T.lc = -1;
+    if (k == CC_GENM) {
+      T.e0 = col_ptr[p];
+      T.e1 = col_ptr[p + 1];
+      tiles.push_back(T);
+      ++p;
+      continue;
     }
+    // chunked: CC_LBIN, CC_LBKT
+    const int d = deg[j];
+    const int nch = std::max(1, (d + kTileNnz - 1) / kTileNnz);
+    const int dom = (k == CC_LBKT) ? (int)(u[j] - l[j] + 1.0) : 0;
+    T.nchunks = nch;
+    T.dom = dom;
+    T.lc = n_long;
+    T.scr = lscr;
+    for (int q = 0; q < nch; ++q) {
+      Tile C = T;
+      C.chunk = q;
+      C.e0 = col_ptr[p] + q * kTileNnz;
+      C.e1 = std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * kTileNnz);
+      tiles.push_back(C);
+    }
+    if (nch > 1) lscr += (k == CC_LBKT) ? (2LL * nch * dom + 2LL * nch) : nch;
+    ++n_long;
     ++p;
   }
   I.n_long_columns = n_long;
@@ -327,7 +338,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       const int32_t j = perm[q];
       const int k = cls[j];
       if (k == CC_FIXED) continue;
-      const int kk = (k == CC_GENB) ? 1 : (k == CC_BINL || k == CC_GENL) ? 2 : 0;
+      const int kk = (k == CC_GENM) ? 1 : (k == CC_LBIN || k == CC_LBKT) ? 2 : 0;   // CC_EMPTY: packed
       const bool bin = vclass[j] == 1;
       const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
       mb[kk] += 12LL * deg[j] + (int64_t)std::llround(per_var * 8) / 8;
@@ -341,11 +352,11 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
 
   // upload
   DeviceBuffers& B = P->buf;
-  int32_t *d_col_ptr, *d_row_idx, *d_rp, *d_ci, *d_perm, *d_bcols;
+  int32_t *d_col_ptr, *d_row_idx, *d_rp, *d_ci, *d_perm;
   double *d_val, *d_cv, *d_b, *d_lb, *d_ub, *d_c;
   uint8_t* d_vc;
-  WTask* d_wt;
-  LChunk* d_ch;
+  Tile* d_tiles;
+  WTile* d_wtiles;
   TRY(B.upload(&d_col_ptr, col_ptr));
   TRY(B.upload(&d_row_idx, row_idx));
   TRY(B.upload(&d_val, cval));
@@ -358,9 +369,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_c, ci_));
   TRY(B.upload(&d_vc, vci));
   TRY(B.upload(&d_perm, perm));
-  TRY(B.upload(&d_wt, wt));
-  TRY(B.upload(&d_bcols, bcols));
-  TRY(B.upload(&d_ch, chunks));
+  TRY(B.upload(&d_tiles, tiles));
+  TRY(B.upload(&d_wtiles, wtiles));
   DevProblem& D = P->dp;
   D.n = n;
   D.m_norm = m_norm;
@@ -377,36 +387,31 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.c = d_c;
   D.vclass = d_vc;
   D.perm = d_perm;
-  D.wtasks = d_wt;
-  D.n_wtasks = (int32_t)wt.size();
-  D.bcols = d_bcols;
-  D.n_bcols = (int32_t)bcols.size();
-  D.chunks = d_ch;
-  D.n_chunks = (int32_t)chunks.size();
+  D.tiles = d_tiles;
+  D.n_tiles = (int32_t)tiles.size();
+  D.wtiles = d_wtiles;
+  D.n_wtiles = (int32_t)wtiles.size();
   D.n_long = n_long;
   D.n_fixed = I.n_fixed;
   D.auto_delta = I.auto_cutoff_delta;
 
-  // launch geometry
+  // launch geometry: a persistent grid of (resident blocks) per walker set
+  CUDA_TRY(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
   int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_warp, kEvalThreads, 0));
-  const int need = std::max(1, (D.n_wtasks + kEvalWarps - 1) / kEvalWarps);
-  P->warp_grid = std::max(1, std::min(need, std::max(1, occ) * P->sm_count));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval, kTileThreads, kTileSmem));
+  P->eval_occ = std::max(1, occ);
+  const int work_blocks = std::max(D.n_tiles, (D.n_wtiles + kTileWarps - 1) / kTileWarps);
+  P->eval_grid = std::max(1, std::min(work_blocks, P->eval_occ * P->sm_count));
   P->rows_grid = std::max(1, std::min((m_norm + 7) / 8, 8 * P->sm_count));
-  P->pl.warp_blocks = D.n_wtasks > 0 ? P->warp_grid : 0;
-  P->pl.block_off = P->pl.warp_blocks;
-  P->pl.long_off = P->pl.block_off + D.n_bcols;
-  P->pl.total = P->pl.long_off + D.n_chunks;
-  const size_t block_smem = (size_t)kBlockElems * (3 * sizeof(double) + sizeof(uint32_t));
-  CUDA_TRY(cudaFuncSetAttribute(k_eval_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)block_smem));
-
   // eval workspace
   TRY(B.alloc(&P->e_x, n));
   TRY(B.alloc(&P->e_rs, m_norm));
   TRY(B.alloc(&P->e_tabu, n));
   TRY(B.alloc(&P->e_bx, n));
   TRY(B.alloc(&P->e_sc, 1));
-  TRY(B.alloc(&P->e_part, std::max(P->pl.total, 1)));
+  TRY(B.alloc(&P->e_part, P->eval_grid));
+  TRY(B.alloc(&P->e_selcnt, 1));
+  CUDA_TRY(cudaMemset(P->e_selcnt, 0, sizeof(unsigned)));
   TRY(B.alloc(&P->e_lcount, std::max(n_long, 1)));
   TRY(B.alloc(&P->e_lscr, P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_sc, 0, sizeof(WalkerScalars)));
@@ -443,18 +448,9 @@ extern "C" chap_status chap_problem_destroy(chap_problem* p) {
 // ------------------------------------------------------------------------------------------
 // eval launches (shared by the eval API and the tabu step)
 // ------------------------------------------------------------------------------------------
-chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, double* oxhat,
-                               double* oscore, cudaStream_t s) {
-  const DevProblem& D = P->dp;
-  const int W = Wk.W;
-  if (D.n_wtasks > 0)
-    k_eval_warp<<<dim3(P->warp_grid, W), kEvalThreads, 0, s>>>(D, Wk, oxhat, oscore);
-  if (D.n_bcols > 0) {
-    const size_t smem = (size_t)kBlockElems * (3 * sizeof(double) + sizeof(uint32_t));
-    k_eval_block<<<dim3(D.n_bcols, W), kBlockThreads, smem, s>>>(D, Wk, oxhat, oscore, P->pl.block_off);
-  }
-  if (D.n_chunks > 0)
-    k_eval_long<<<dim3(D.n_chunks, W), kBlockThreads, 0, s>>>(D, Wk, oxhat, oscore, P->pl.long_off);
+chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, double* oxhat,
+                              double* oscore, chap_move* best, cudaStream_t s) {
+  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -470,7 +466,8 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.best_x = P->e_bx;
   Wk.sc = P->e_sc;
   Wk.part = P->e_part;
-  Wk.ps = std::max(P->pl.total, 1);
+  Wk.ps = P->eval_grid;
+  Wk.sel_count = P->e_selcnt;
   Wk.lcount = P->e_lcount;
   Wk.lcs = std::max(P->dp.n_long, 1);
   Wk.lscr = P->e_lscr;
@@ -501,10 +498,9 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, nullptr);
   k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_rs, D.m_norm, p->e_sc, 2, w);
   CUDA_TRY(cudaGetLastError());
-  TRY(launch_eval(p, Wk, xhat, score, s));
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  k_select<<<1, 256, 0, s>>>(Wk, p->pl.total, best);
+  TRY(launch_eval(p, Wk, p->eval_grid, xhat, score, best, s));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -592,8 +588,10 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   TRY(B.alloc(&Wk.tabu, n * W));
   TRY(B.alloc(&Wk.best_x, n * W));
   TRY(B.alloc(&Wk.sc, W));
-  Wk.ps = std::max(p->pl.total, 1);
+  S->eval_grid = std::max(1, std::min(p->eval_grid, (p->eval_occ * p->sm_count + W - 1) / W));
+  Wk.ps = S->eval_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
+  TRY(B.alloc(&Wk.sel_count, W));
   Wk.lcs = std::max(D.n_long, 1);
   TRY(B.alloc(&Wk.lcount, (size_t)Wk.lcs * W));
   Wk.lss = p->lscr_per_walker;
@@ -613,6 +611,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   cudaStream_t s = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaMemsetAsync(Wk.sc, 0, sizeof(WalkerScalars) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.lcount, 0, sizeof(unsigned) * Wk.lcs * W, s));
+  CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
   if (D.n > 0)
@@ -635,8 +634,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
-  TRY(launch_eval(P, S->wk, nullptr, nullptr, s));
-  k_select<<<S->W, 256, 0, s>>>(S->wk, P->pl.total, nullptr);
+  TRY(launch_eval(P, S->wk, S->eval_grid, nullptr, nullptr, nullptr, s));
   k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -741,23 +739,11 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
   k_set_log<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk, nullptr);
   std::vector<cudaEvent_t> ev(10 * (size_t)n_iters);
   for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
-  const size_t smem = (size_t)kBlockElems * (3 * sizeof(double) + sizeof(uint32_t));
   for (int it = 0; it < n_iters; ++it) {
     cudaEvent_t* e = &ev[10 * (size_t)it];
-    cudaEventRecord(e[0], s);
-    if (D.n_wtasks > 0) k_eval_warp<<<dim3(P->warp_grid, S->W), kEvalThreads, 0, s>>>(D, S->wk, nullptr, nullptr);
+    for (int q = 0; q < 8; ++q) cudaEventRecord(e[q], s);
+    k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr);
     cudaEventRecord(e[1], s);
-    cudaEventRecord(e[2], s);
-    if (D.n_bcols > 0)
-      k_eval_block<<<dim3(D.n_bcols, S->W), kBlockThreads, smem, s>>>(D, S->wk, nullptr, nullptr, P->pl.block_off);
-    cudaEventRecord(e[3], s);
-    cudaEventRecord(e[4], s);
-    if (D.n_chunks > 0)
-      k_eval_long<<<dim3(D.n_chunks, S->W), kBlockThreads, 0, s>>>(D, S->wk, nullptr, nullptr, P->pl.long_off);
-    cudaEventRecord(e[5], s);
-    cudaEventRecord(e[6], s);
-    k_select<<<S->W, 256, 0, s>>>(S->wk, P->pl.total, nullptr);
-    cudaEventRecord(e[7], s);
     cudaEventRecord(e[8], s);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
     cudaEventRecord(e[9], s);
@@ -774,9 +760,7 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
       ms[q] += t;
     }
   for (int q = 0; q < 5; ++q) ms[q] /= n_iters;
-  if (D.n_wtasks == 0) ms[0] = 0.0;
-  if (D.n_bcols == 0) ms[1] = 0.0;
-  if (D.n_chunks == 0) ms[2] = 0.0;
+  ms[1] = ms[2] = ms[3] = 0.0;   // one fused eval+select kernel
   for (auto& e : ev) cudaEventDestroy(e);
   CUDA_TRY(cudaEventRecord(S->ev_out, s));
   CUDA_TRY(cudaStreamWaitEvent(us, S->ev_out, 0));

@@ -11,13 +11,18 @@ namespace chap {
 
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kEvalThreads = 256;                 // 8 warps per block in the warp-task kernel
-constexpr int kEvalWarps = kEvalThreads / kWarp;
-constexpr int kBinWideMax = 4096;                 // binary columns with 32 < deg <= this: warp/column
-constexpr int kBlockElems = 4096;                 // general columns with deg+2 <= this: block/column
-constexpr int kBlockThreads = 256;
-constexpr int kLongChunk = 4096;                  // nonzeros per block of a long (chunked) column
-constexpr int kBucketMax = 4096;                  // max integer domain of a chunked general column
+constexpr int kTileThreads = 256;                 // threads per eval block
+constexpr int kTileNnz = 1024;                    // nonzeros per chunk of a long column
+constexpr int kPer = kTileNnz / kTileThreads;     // slots per thread of a chunk tile
+constexpr int kGenmMax = 2048;                    // Alg. 1 elements of a single-column sort tile
+constexpr int kWSlots = 8;                        // slots per lane of a binary warp tile
+constexpr int kWTileNnz = 32 * kWSlots;           // nonzeros per binary warp tile
+constexpr int kWSlotsGen = 8;                     // slots per lane of a general warp tile
+constexpr int kWTileGen = 32 * kWSlotsGen;        // Alg. 1 elements per general warp tile
+constexpr int kWTileCols = 32;                    // columns per warp tile (one lane each)
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
+constexpr int kBucketMax = 4096;                  // max integer domain of a bucket-scanned column
 constexpr int kApplyThreads = 256;
 
 // Per normalised row and walker: the residual r_i = ȳ_i - b_i (double) and the
@@ -29,34 +34,38 @@ struct __align__(16) RowState {
   uint32_t pad;
 };
 
-// Column classes (the paper's length-specialised dispatch).
+// Column classes (the paper's length-specialised dispatch, re-designed).
 enum ColClass : int {
-  CC_FIXED = 0,   // l = u: no candidate
-  CC_BIN = 1,     // binary, deg <= 32: g lanes per column, several columns per warp (flip)
-  CC_BINW = 2,    // binary, 32 < deg <= kBinWideMax: one warp per column
-  CC_BINL = 3,    // binary, longer: chunked over blocks
-  CC_GEN = 4,     // integer/continuous, deg+2 <= 32: g lanes per column, warp sort-scan-argmax
-  CC_GENB = 5,    // deg+2 <= kBlockElems: one block per column, shared-memory sort-scan-argmax
-  CC_GENL = 6,    // longer, bounded integer domain <= kBucketMax: chunked bucket scan
+  CC_FIXED = 0,  // l = u: no candidate
+  CC_LBKT = 1,   // general integer, deg+2 > kShortDeg, bounded domain <= kBucketMax: bucket scan,
+                 // chunked over kTileNnz-nonzero tiles (merged by the last chunk)
+  CC_LBIN = 2,   // binary, deg > kShortDeg: flip partial sums over kTileNnz-nonzero chunks
+  CC_GENM = 3,   // general, kShortDeg < deg+2 <= kGenmMax, other domains: one tile, bitonic sort
+  CC_GEN = 4,    // general, deg+2 <= kShortDeg: packed warp tiles, sort-free prefix per candidate
+  CC_BIN = 5,    // binary, deg <= kShortDeg: packed tiles, flip sums
+  CC_EMPTY = 6,  // a column without nonzeros (and c_j = 0)
 };
 
-// A warp task: ncols consecutive internal columns of one class and group size g.
-struct WTask {
+// A warp tile: ncols consecutive packed columns (CC_BIN or CC_GEN) of one warp.
+struct WTile {
   int32_t p0;
+  int32_t e0, e1;    // nonzero range
   int16_t ncols;
-  int8_t kind;    // CC_BIN, CC_BINW, CC_GEN
-  int8_t lg;      // log2(g)
+  int8_t kind;
+  int8_t pad;
 };
 
-// One block of a chunked long column.
-struct LChunk {
-  int32_t p;       // internal column
-  int32_t lc;      // long-column slot
-  int32_t e0, e1;  // nonzero range of this chunk (CSC, internal)
+// A block tile (chunk of a long column, or one column sorted by the whole block).
+struct Tile {
+  int32_t kind;      // a ColClass (not CC_FIXED)
+  int32_t p0;        // first internal column
+  int32_t ncols;     // columns in a packed tile; 1 otherwise
+  int32_t e0, e1;    // nonzero range [e0, e1) (CSC, internal)
+  int32_t lc;        // long-column slot (chunked kinds)
   int32_t chunk, nchunks;
-  int32_t kind;    // 0 binary flip sums, 1 bucket (integer domain)
-  int32_t dom;     // u - l + 1 for kind 1
-  int64_t scr;     // offset (in doubles) of this column's scratch in a walker's scratch
+  int32_t dom;       // u - l + 1 (CC_LBKT)
+  int32_t pad;
+  int64_t scr;       // offset (doubles) of the column's chunk scratch in a walker's scratch
 };
 
 // Per-column result competing for the global best move.
@@ -112,9 +121,8 @@ struct DevProblem {
   const double* c;           // [n]
   const uint8_t* vclass;     // [n] 0 fixed 1 binary 2 integer 3 continuous
   const int32_t* perm;       // internal p -> user j
-  const WTask* wtasks; int32_t n_wtasks;
-  const int32_t* bcols; int32_t n_bcols;
-  const LChunk* chunks; int32_t n_chunks; int32_t n_long;
+  const Tile* tiles; int32_t n_tiles; int32_t n_long;   // block tiles
+  const WTile* wtiles; int32_t n_wtiles;                // warp tiles
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   double auto_delta;
 };
@@ -126,7 +134,8 @@ struct DevWalkers {
   int32_t* tabu;        size_t ts;     // [W][n]
   double* best_x;                      // [W][n]
   WalkerScalars* sc;                   // [W]
-  Cand* part;           int32_t ps;    // [W][ps]
+  Cand* part;           int32_t ps;    // [W][ps] one per eval block
+  unsigned* sel_count;                 // [W] last-block-done counter of the eval kernel
   unsigned* lcount;     int32_t lcs;   // [W][n_long]
   double* lscr;         size_t lss;    // [W][lss]
   int32_t use_tabu;
@@ -134,14 +143,6 @@ struct DevWalkers {
   int32_t tenure;
   float wcap;
   double delta;                        // NaN = auto
-};
-
-// Partial-array layout of the eval kernels (per walker).
-struct PartLayout {
-  int32_t warp_blocks;   // partials [0, warp_blocks)
-  int32_t block_off;     // [block_off, block_off + n_bcols)
-  int32_t long_off;      // [long_off, long_off + n_chunks)
-  int32_t total;
 };
 
 }  // namespace chap

@@ -1,18 +1,20 @@
-// eval.cuh — best-shift evaluation kernels (§3.1, Eq. (1) and Algorithm 1).
+// eval.cuh — best-shift evaluation (§3.1, Eq. (1) and Algorithm 1) on sm_100a.
 //
-// Three kernels cover all column lengths (the paper's length-specialised dispatch,
-// PAPER.md:353-355, re-designed for sm_100a):
-//   k_eval_warp   warp tasks: binary flips (g lanes per column), binary columns up
-//                 to kBinWideMax (one warp each), and general columns with deg+2 <= 32 whose
-//                 Algorithm 1 runs entirely in registers/shared memory of g lanes: emit (l.1-12),
-//                 rank sort (l.13), inclusive segmented scan (l.14), sigma (l.15), argmax (l.16);
-//   k_eval_block  one block per general column with deg+2 <= kBlockElems: shared-memory bitonic
-//                 sort, block scan, block argmax;
-//   k_eval_long   chunked long columns (4096 nonzeros per block): binary flip partial sums, or a
-//                 bucket (counting) scan over a bounded integer domain; the last block of a
-//                 column merges the chunk partials in chunk order (deterministic).
-// Every kernel also reduces its columns to one best admissible move per block (R6) in Cand
-// partials; k_select reduces those per walker.
+// One persistent kernel, k_eval, evaluates every variable of every walker and selects the best
+// admissible move (the paper's length-specialised dispatch, re-designed):
+//   phase A, block tiles (all warps of a block):
+//     CC_LBIN  a kTileNnz chunk of a long binary column: block partial flip sum;
+//     CC_LBKT  a chunk of a general integer column with a bounded domain: the sort of line 13
+//              becomes a counting (bucket) pass over [l, u];
+//     CC_GENM  one general column of <= kGenmMax entries: shared-memory bitonic sort + scan;
+//     the last chunk of a column merges the chunk partials in chunk order (deterministic);
+//   phase B, warp tiles (one warp, no block barriers):
+//     CC_BIN   packed binary columns: flip penalty per nonzero, per-column sum;
+//     CC_GEN   packed general columns: Algorithm 1 per column, sort-free (see wtile_gen);
+//     CC_EMPTY columns without nonzeros.
+// Every warp-tile slot issues its coalesced CSC loads and one 16-byte row-state gather before
+// using any of them. Each block keeps its best admissible move (R6); the last block of a walker
+// reduces the block partials to the walker's decision (the global select).
 #pragma once
 #include "common.cuh"
 
@@ -21,17 +23,11 @@ namespace chap {
 // PAPER.md:277-285 on residuals r0 = ȳ_i - b_i, r1 = y_ij - b_i; satisfied means r <= 0 (R10).
 __device__ __forceinline__ double penalty(double w, double r0, double r1) {
   const bool s0 = r0 <= 0.0, s1 = r1 <= 0.0;
-  double p = 0.0;
-  if (s0) {
-    p = s1 ? 0.0 : -w;
-  } else if (s1) {
-    p = w;
-  } else if (r1 < r0) {
-    p = 0.5 * w;
-  } else if (r1 > r0) {
-    p = -0.5 * w;
-  }
-  return p;
+  const double half = 0.5 * w;
+  const double vio = (r1 < r0) ? half : ((r1 > r0) ? -half : 0.0);   // both violated
+  const double from_vio = s1 ? w : vio;
+  const double from_sat = s1 ? 0.0 : -w;
+  return s0 ? from_sat : from_vio;
 }
 
 // Within one variable: higher score, then closer to x̄, then smaller value (R4).
@@ -103,14 +99,13 @@ __device__ __forceinline__ void write_part(Cand* dst, const Best& b) {
 }
 
 // The result of one column: outputs (eval API) and the admissible-best update (R6, R13).
-__device__ __forceinline__ void finish_column(const DevProblem& P, int p, double xb, double v,
-                                              double s, Best& b, double* oxhat, double* oscore,
-                                              const int32_t* tabu, long long k, int use_tabu) {
+__device__ __forceinline__ void finish_column_j(int p, int j, int32_t tabu_p, double xb, double v,
+                                                double s, Best& b, double* oxhat, double* oscore,
+                                                long long k, int use_tabu) {
   if (s == -INFINITY) v = xb;
-  const int j = P.perm[p];
   if (oxhat) oxhat[j] = v;
   if (oscore) oscore[j] = s;
-  if (use_tabu && (long long)tabu[p] > k) return;
+  if (use_tabu && (long long)tabu_p > k) return;
   if (better_move(s, j, b.s, b.j)) {
     b.s = s;
     b.v = v;
@@ -118,11 +113,23 @@ __device__ __forceinline__ void finish_column(const DevProblem& P, int p, double
     b.p = p;
   }
 }
+__device__ __forceinline__ void finish_column(const DevProblem& P, int p, double xb, double v,
+                                              double s, Best& b, double* oxhat, double* oscore,
+                                              const int32_t* tabu, long long k, int use_tabu) {
+  finish_column_j(p, P.perm[p], use_tabu ? tabu[p] : 0, xb, v, s, b, oxhat, oscore, k, use_tabu);
+}
 
-// One breakpoint element of Algorithm 1 lines 3-11 for row i of column j,
-// in the one-element-per-row form of DESIGN.md §2.3: an a<0 row gives (t, -1, δ); an a>0 row
-// gives (t, +1, δ) whose candidate value t is scored by the exclusive prefix (the sum before
-// its +1 entry = the sigma of the row's own (t, -1, 0) entry of line 9/10).
+// One 16-byte row-state gather (r f64, w f32). The inactive cutoff row holds r = -inf, w = 0,
+// which makes every one of its contributions vanish (no per-nonzero test needed).
+__device__ __forceinline__ void load_row(const RowState* rs, int i, double& r, double& w) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(rs) + i);
+  r = v.x;
+  w = (double)__int_as_float((int)__double2loint(v.y));
+}
+
+// Entry of Algorithm 1 lines 3-11 for row i of column j, in the one-element-
+// per-row form of DESIGN.md §2.3: an a<0 row gives (t, -1, δ); an a>0 row gives (t, +1, δ) whose
+// candidate value t is scored by the sum before its +1 entry (= its (t, -1, 0) partner's sigma).
 struct Elem {
   double t;
   double delta;
@@ -132,6 +139,14 @@ struct Elem {
   int plus;    // marker +1 (a > 0 rows)
 };
 
+// Line 3: t = x̄ - r/a. A zero residual (a tight row, common with integer data) gives t = x̄
+// exactly; the guard also keeps zero/inf numerators off the IEEE division's slow path.
+__device__ __forceinline__ double breakpoint(double xb, double r, double a) {
+  const bool plain = r != 0.0 && isfinite(r);
+  const double q = (plain ? r : 1.0) / a;
+  return plain ? xb - q : xb;
+}
+
 __device__ __forceinline__ Elem emit(double xb, double r, double a, double w, int is_int) {
   Elem e;
   e.beta = 0.0;
@@ -139,7 +154,9 @@ __device__ __forceinline__ Elem emit(double xb, double r, double a, double w, in
   e.valid = 0;
   e.plus = 0;
   e.delta = 0.0;
-  double t = xb - r / a;                             // (b_i - Σ_{k≠j} a_ik x̄_k) / a_ij  (l.3)
+  e.t = xb;
+  if (!isfinite(r)) return e;                       // the inert inactive cutoff row (w = 0)
+  double t = breakpoint(xb, r, a);                   // (b_i - Σ_{k≠j} a_ik x̄_k) / a_ij  (l.3)
   if (is_int) t = (a > 0.0) ? floor(t) : ceil(t);    // l.4
   e.t = t;
   if (a < 0.0) {                                      // imposes x_j >= t (l.5)
@@ -163,179 +180,291 @@ __device__ __forceinline__ Elem emit(double xb, double r, double a, double w, in
 }
 
 // ------------------------------------------------------------------------------------------
-// warp tasks
+// shared memory
 // ------------------------------------------------------------------------------------------
+struct WarpBin {                       // CC_BIN warp tile
+  double pen[kWTileNnz];
+  double xb[kWTileCols];
+  uint32_t head[kWTileNnz / 32];       // bit k: slot k starts a column
+};
+struct WarpGen {                       // CC_GEN warp tile: row entries at slots [0, nnz); the
+  double t[kWTileGen];                 // bound entries of column c at slots nnz + 2c, nnz + 2c + 1
+  double2 L[kWTileGen];                // per column c, region [cb + 2c, ...): (key, δ) of the
+                                       // column's in-range entries (see wtile_gen)
+  float w[kWTileGen];
+  uint8_t f[kWTileGen];                // GF_* flags
+  double xb[kWTileCols];
+  double l[kWTileCols];
+  double u[kWTileCols];
+  uint32_t head[kWTileGen / 32];
+  uint8_t cont[kWTileCols];            // continuous column
+};
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t kWarpSmem = (cmax(sizeof(WarpBin), sizeof(WarpGen)) + 15) / 16 * 16;
+struct SmemGenM {                      // CC_GENM block tile
+  double t[kGenmMax];
+  double del[kGenmMax];
+  double P[kGenmMax];
+  uint32_t mk[kGenmMax];
+};
+struct SmemBkt {                       // CC_LBKT block tile
+  double D[kBucketMax + 1];
+  uint8_t cand[kBucketMax];
+};
+constexpr size_t kTileSmem = cmax(kWarpSmem * kTileWarps, cmax(sizeof(SmemGenM), sizeof(SmemBkt)));
 
-struct WarpCtx {
+struct TileCtx {
   const double* x;
   const RowState* rs;
   const int32_t* tabu;
   long long k;
-  int cut_active;
   int use_tabu;
   double* oxhat;
   double* oscore;
 };
 
-// binary flips, g = 2^lg lanes per column
-__device__ __forceinline__ void task_bin(const DevProblem& P, const WarpCtx& C, const WTask& T,
-                                         int lane, Best& b) {
-  const int lg = T.lg, g = 1 << lg;
-  const int grp = lane >> lg, lig = lane & (g - 1);
-  const int p = T.p0 + grp;
-  const bool colv = grp < T.ncols;
-  double pen = 0.0, xb = 0.0;
-  if (colv) {
-    const int beg = P.col_ptr[p], d = P.col_ptr[p + 1] - beg;
-    xb = C.x[p];
-    if (lig < d) {
-      const int i = P.row_idx[beg + lig];
-      const double a = P.val[beg + lig];
-      if (i != P.cut_row || C.cut_active) {
-        const RowState s = C.rs[i];
-        pen = penalty((double)s.w, s.r, s.r + a * (1.0 - 2.0 * xb));
-      }
-    }
-  }
-  for (int off = g >> 1; off > 0; off >>= 1) pen += __shfl_xor_sync(kFull, pen, off);
-  if (colv && lig == 0)
-    finish_column(P, p, xb, 1.0 - xb, pen, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
+// ------------------------------------------------------------------------------------------
+// warp tiles
+// ------------------------------------------------------------------------------------------
+
+// Column of slot k = lane + 32 q of a packed tile: columns are contiguous runs of slots and
+// none is empty, so the column is (number of column starts <= k) - 1, read off a head bitmap.
+__device__ __forceinline__ void build_heads(uint32_t* head, int nwords, int lane, int nc, int cb) {
+  if (lane < nwords) head[lane] = 0u;
+  __syncwarp();
+  if (lane < nc) atomicOr(&head[cb >> 5], 1u << (cb & 31));
+  __syncwarp();
 }
 
-// binary flips, one warp per column of 32 < deg <= kBinWideMax
-__device__ __forceinline__ void task_binw(const DevProblem& P, const WarpCtx& C, const WTask& T,
-                                          int lane, Best& b) {
-  const int p = T.p0;
-  const int beg = P.col_ptr[p], end = P.col_ptr[p + 1];
-  const double xb = C.x[p];
-  const double dir = 1.0 - 2.0 * xb;
-  double pen = 0.0;
-#pragma unroll 4
-  for (int e = beg + lane; e < end; e += kWarp) {
-    const int i = P.row_idx[e];
-    const double a = P.val[e];
-    if (i != P.cut_row || C.cut_active) {
-      const RowState s = C.rs[i];
-      pen += penalty((double)s.w, s.r, s.r + a * dir);
-    }
+// packed binary columns, one warp (the only move of a binary is the flip)
+__device__ __forceinline__ void wtile_bin(const DevProblem& P, const TileCtx& C, const WTile& T,
+                                          int lane, WarpBin& S, Best& b) {
+  const int nc = T.ncols, nnz = T.e1 - T.e0;
+  const int p = T.p0 + lane;
+  int cb = 0, ce = 0, j = 0, tb = 0;
+  double xb = 0.0;
+  if (lane < nc) {
+    cb = __ldg(P.col_ptr + p) - T.e0;
+    ce = __ldg(P.col_ptr + p + 1) - T.e0;
+    j = __ldg(P.perm + p);
+    tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
+    xb = __ldg(C.x + p);
+    S.xb[lane] = xb;
   }
+  build_heads(S.head, kWSlots, lane, nc, cb);
+  const unsigned le = (2u << lane) - 1u;   // lanes <= lane
+  int pre = 0;                             // column starts before this slot round
+  constexpr int H = kWSlots / 2;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    int idx[H];
+    double av[H];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) pen += __shfl_xor_sync(kFull, pen, off);
-  if (lane == 0) finish_column(P, p, xb, 1.0 - xb, pen, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
-}
-
-// General (integer / continuous) columns with deg + 2 <= g lanes: Algorithm 1 in a lane group.
-// Lane k < deg holds row k's element, lane deg the lower-bound entry (l, -1, 0), lane deg+1 the
-// upper-bound entry (u, -1, 0) (l.1; infinite bounds dropped, R9).
-__device__ __forceinline__ void task_gen(const DevProblem& P, const WarpCtx& C, const WTask& T,
-                                         int lane, double* sm_d, double* sm_p, Best& b) {
-  const int lg = T.lg, g = 1 << lg;
-  const int grp = lane >> lg, lig = lane & (g - 1), base = grp << lg;
-  const int p = T.p0 + grp;
-  const bool colv = grp < T.ncols;
-  double xb = 0.0, l = 0.0, u = 0.0;
-  int d = 0;
-  Elem el;
-  el.t = 0.0; el.delta = 0.0; el.beta = 0.0; el.alpha = 0.0; el.valid = 0; el.plus = 0;
-  bool cand = false;
-  if (colv) {
-    const int beg = P.col_ptr[p];
-    d = P.col_ptr[p + 1] - beg;
-    xb = C.x[p];
-    l = P.lb[p];
-    u = P.ub[p];
-    const int is_int = P.vclass[p] != 3;
-    if (lig < d) {
-      const int i = P.row_idx[beg + lig];
-      const double a = P.val[beg + lig];
-      if (i != P.cut_row || C.cut_active) {
-        const RowState s = C.rs[i];
-        el = emit(xb, s.r, a, (double)s.w, is_int);
-        cand = el.valid && el.t >= l && el.t <= u && el.t != xb;
+    for (int q = 0; q < H; ++q) {
+      const int k = lane + 32 * (q + h * H);
+      idx[q] = 0;
+      av[q] = 0.0;
+      if (k < nnz) {
+        idx[q] = __ldg(P.row_idx + T.e0 + k);
+        av[q] = __ldg(P.val + T.e0 + k);
       }
-    } else if (lig == d) {
-      if (isfinite(l)) { el.valid = 1; el.t = l; cand = (l != xb); }
-    } else if (lig == d + 1) {
-      if (isfinite(u)) { el.valid = 1; el.t = u; cand = (u != xb); }
+    }
+    double r[H], w[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) load_row(C.rs, idx[q], r[q], w[q]);
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const int qq = q + h * H;
+      const int k = lane + 32 * qq;
+      const uint32_t hw = S.head[qq];
+      const int c = pre + __popc(hw & le) - 1;
+      pre += __popc(hw);
+      if (k < nnz) {
+        const double x = S.xb[c];
+        S.pen[k] = penalty(w[q], r[q], r[q] + av[q] * (1.0 - 2.0 * x));
+      }
     }
   }
-  // β and α of lines 1-12: group sums
-  double beta = el.beta, alpha = el.alpha;
-  for (int off = g >> 1; off > 0; off >>= 1) {
-    beta += __shfl_xor_sync(kFull, beta, off);
-    alpha += __shfl_xor_sync(kFull, alpha, off);
-  }
-  // line 13: lexicographic sort by (value, marker) — rank sort; ties by lane (unique ranks)
-  const unsigned kmax = __reduce_max_sync(kFull, colv ? (unsigned)(d + 2) : 0u);
-  const int mine = el.valid ? el.plus : 2;
-  int rank = 0;
-  for (unsigned q = 0; q < kmax; ++q) {
-    const int src = base + (int)q;
-    const double tq = __shfl_sync(kFull, el.t, src);
-    const int mq = __shfl_sync(kFull, mine, src);
-    const bool less = (mq != 2) && (tq < el.t || (tq == el.t && (mq < mine || (mq == mine && (int)q < lig))));
-    rank += less ? 1 : 0;
-  }
-  const unsigned vmask = __ballot_sync(kFull, el.valid);
-  const int nvalid = __popc((vmask >> base) & (g == 32 ? kFull : ((1u << g) - 1u)));
   __syncwarp();
-  if (el.valid) sm_d[base + rank] = el.delta;
+  if (lane < nc) {
+    double s = 0.0;
+    for (int e = cb; e < ce; ++e) s += S.pen[e];
+    finish_column_j(p, j, tb, xb, 1.0 - xb, s, b, C.oxhat, C.oscore, C.k, C.use_tabu);
+  }
   __syncwarp();
-  // line 14: inclusive scan of the deltas in sorted order (segmented by lane group)
-  double ps = (lig < nvalid) ? sm_d[base + lig] : 0.0;
-  for (int off = 1; off < g; off <<= 1) {
-    const double y = __shfl_up_sync(kFull, ps, off, g);
-    if (lig >= off) ps += y;
-  }
-  sm_p[base + lig] = ps;
-  __syncwarp();
-  // line 15: sigma; a +1 element scores its value by the prefix before it (its -1 partner)
-  double sig = -INFINITY, v = el.t;
-  if (el.valid && cand) {
-    const double pin = sm_p[base + rank];
-    const double pex = rank > 0 ? sm_p[base + rank - 1] : 0.0;
-    sig = beta + (el.plus ? pex : pin) + (el.t > xb ? alpha : 0.0);
-  }
-  // line 16: argmax within the group (R3, R4)
-  for (int off = g >> 1; off > 0; off >>= 1) {
-    const double so = __shfl_xor_sync(kFull, sig, off);
-    const double vo = __shfl_xor_sync(kFull, v, off);
-    if (better_shift(so, vo, sig, v, xb)) { sig = so; v = vo; }
-  }
-  if (colv && lig == 0) finish_column(P, p, xb, v, sig, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
 }
 
-__global__ void __launch_bounds__(kEvalThreads) k_eval_warp(DevProblem P, DevWalkers Wk,
-                                                            double* oxhat, double* oscore) {
-  __shared__ double sm_d[kEvalWarps][kWarp];
-  __shared__ double sm_p[kEvalWarps][kWarp];
-  __shared__ Best sm_b[kWarp];
-  const int walker = blockIdx.y;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const WalkerScalars* sc = Wk.sc + walker;
-  WarpCtx C;
-  C.x = Wk.x + (size_t)walker * Wk.xs;
-  C.rs = Wk.rs + (size_t)walker * Wk.rss;
-  C.tabu = Wk.tabu + (size_t)walker * Wk.ts;
-  C.k = sc->k;
-  C.cut_active = sc->cut_active;
-  C.use_tabu = Wk.use_tabu;
-  C.oxhat = oxhat;
-  C.oscore = oscore;
-  Best b;
-  b.init();
-  for (int t = blockIdx.x * kEvalWarps + wid; t < P.n_wtasks; t += gridDim.x * kEvalWarps) {
-    const WTask T = P.wtasks[t];
-    if (T.kind == CC_BIN) task_bin(P, C, T, lane, b);
-    else if (T.kind == CC_GEN) task_gen(P, C, T, lane, sm_d[wid], sm_p[wid], b);
-    else task_binw(P, C, T, lane, b);
+// Entry flags of a general warp tile. Lines 5-11 of Algorithm 1 are fixed by
+// the sign of a_ij and the order of x̄ and t: with w = w_i,
+//   a<0, x̄<t: δ=+w/2, β-=w/2, α+=w   a<0, x̄>t: δ=+w, β-=w          a<0, x̄=t: β-=w, α+=w
+//   a>0, x̄>t: δ=-w/2, β+=w, α-=w     a>0, x̄<t: δ=-w                 a>0, x̄=t: α-=w
+// (an a>0 entry's (t,-1,0) partner carries no delta; R3 makes t a candidate all the same).
+enum : uint8_t {
+  GF_POS = 1,      // a > 0
+  GF_LT = 2,       // x̄ < t
+  GF_GT = 4,       // x̄ > t
+  GF_ROW = 8,      // a row entry
+  GF_CAND = 32,    // the value is a candidate: finite, in [l, u], != x̄ (R2, R5)
+};
+__device__ __forceinline__ void gf_coeffs(uint8_t f, double w, double& D, double& A, double& B) {
+  const bool pos = f & GF_POS, lt = f & GF_LT, gt = f & GF_GT, row = f & GF_ROW;
+  const double hw = 0.5 * w;
+  const double Dn = lt ? hw : (gt ? w : 0.0), An = lt ? -hw : -w, Bn = gt ? 0.0 : w;
+  const double Dp = gt ? -hw : (lt ? -w : 0.0), Ap = gt ? w : 0.0, Bp = lt ? 0.0 : -w;
+  D = row ? (pos ? Dp : Dn) : 0.0;
+  A = row ? (pos ? Ap : An) : 0.0;
+  B = row ? (pos ? Bp : Bn) : 0.0;
+}
+
+// Packed general columns, one warp: Algorithm 1 per column, sort-free.
+// For a candidate value v the score Algorithm 1 reports (the largest sigma of the entries at v,
+// R3) is sigma(v) = β + Σ_{entries e: t_e < v, or t_e = v with marker -1} δ_e + α [v > x̄]
+// (DESIGN §2.3). Entries with t < l are in every such sum and fold into β; entries with t > u
+// are in none and drop. A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an entry
+// with δ = 0 adds nothing, so "marker -1" is δ > 0. For integer columns the test becomes one
+// compare of key_e = 2 t_e + [δ_e < 0] with 2 v. Phases: (1) slots in parallel: coalesced
+// loads, row-state gathers, lines 3-4 and the case of lines 5-11; (2) lane c, column c: β, α,
+// the in-range list, then sigma of every candidate (lines 13-15) and the argmax of line 16.
+__device__ __forceinline__ void wtile_gen(const DevProblem& P, const TileCtx& C, const WTile& T,
+                                          int lane, WarpGen& S, Best& b) {
+  const int nc = T.ncols, nnz = T.e1 - T.e0;
+  const int nel = nnz + 2 * nc;
+  const int p = T.p0 + lane;
+  int cb = 0, ce = 0, j = 0, tb = 0;
+  double xb = 0.0, l = 0.0, u = 0.0;
+  bool cont = false;
+  if (lane < nc) {
+    cb = __ldg(P.col_ptr + p) - T.e0;
+    ce = __ldg(P.col_ptr + p + 1) - T.e0;
+    j = __ldg(P.perm + p);
+    tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
+    xb = __ldg(C.x + p);
+    l = __ldg(P.lb + p);
+    u = __ldg(P.ub + p);
+    cont = __ldg(P.vclass + p) == 3;
+    S.xb[lane] = xb;
+    S.l[lane] = l;
+    S.u[lane] = u;
+    S.cont[lane] = cont;
   }
-  b = block_reduce_best(b, sm_b);
-  if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + blockIdx.x, b);
+  build_heads(S.head, kWSlotsGen, lane, nc, cb);
+  const unsigned le = (2u << lane) - 1u;
+  int pre = 0;
+  constexpr int H = kWSlotsGen / 2;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    int idx[H];
+    double av[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const int k = lane + 32 * (q + h * H);
+      idx[q] = 0;
+      av[q] = 1.0;
+      if (k < nnz) {
+        idx[q] = __ldg(P.row_idx + T.e0 + k);
+        av[q] = __ldg(P.val + T.e0 + k);
+      }
+    }
+    double r[H], w[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) load_row(C.rs, idx[q], r[q], w[q]);
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const int qq = q + h * H;
+      const int k = lane + 32 * qq;
+      const uint32_t hw = S.head[qq];
+      const int cr = pre + __popc(hw & le) - 1;
+      pre += __popc(hw);
+      if (k >= nel) continue;
+      double t = 0.0;
+      uint8_t f = 0;
+      if (k < nnz) {
+        const int c = cr;
+        const double x = S.xb[c];
+        t = breakpoint(x, r[q], av[q]);                             // line 3
+        if (!S.cont[c]) t = (av[q] > 0.0) ? floor(t) : ceil(t);    // line 4
+        f = GF_ROW | (av[q] > 0.0 ? GF_POS : 0) | (x < t ? GF_LT : 0) | (x > t ? GF_GT : 0);
+        if (x != t && t >= S.l[c] && t <= S.u[c]) f |= GF_CAND;
+        if (!isfinite(r[q])) f = 0;                                 // inert inactive cutoff row
+      } else {
+        const int c = (k - nnz) >> 1;
+        const double v = ((k - nnz) & 1) ? S.u[c] : S.l[c];
+        t = v;
+        if (isfinite(v) && v != S.xb[c]) f = GF_CAND;
+      }
+      S.t[k] = t;
+      S.w[k] = (float)w[q];
+      S.f[k] = f;
+    }
+  }
+  __syncwarp();
+  if (lane < nc) {
+    const int base = cb + 2 * lane;
+    double beta = 0.0, alpha = 0.0;
+    int m = 0;
+    for (int e = cb; e < ce; ++e) {
+      const uint8_t f = S.f[e];
+      const double t = S.t[e];
+      double D, A, B;
+      gf_coeffs(f, (double)S.w[e], D, A, B);
+      beta += A;
+      alpha += B;
+      if (t < l) {
+        beta += D;                       // in every candidate's prefix
+      } else if (t <= u && D != 0.0) {
+        // integer columns: key 2t + [+1 marker] (exact, |t| < 2^51); continuous: t, marker by sign
+        S.L[base + m] = make_double2(cont ? t : 2.0 * t + (D < 0.0 ? 1.0 : 0.0), D);
+        ++m;
+      }
+    }
+    double bs = -INFINITY, bv = xb;
+    for (int e = cb; e < ce + 2; ++e) {
+      const int k = (e < ce) ? e : nnz + 2 * lane + (e - ce);
+      if (!(S.f[k] & GF_CAND)) continue;
+      const double v = S.t[k];
+      double acc = beta + (v > xb ? alpha : 0.0);
+      if (!cont) {
+        const double kv = 2.0 * v;
+        for (int q = 0; q < m; ++q) {
+          const double2 L = S.L[base + q];
+          acc += (L.x <= kv) ? L.y : 0.0;
+        }
+      } else {
+        for (int q = 0; q < m; ++q) {
+          const double2 L = S.L[base + q];
+          acc += (L.x < v || (L.x == v && L.y > 0.0)) ? L.y : 0.0;
+        }
+      }
+      if (better_shift(acc, v, bs, bv, xb)) { bs = acc; bv = v; }
+    }
+    finish_column_j(p, j, tb, xb, bv, bs, b, C.oxhat, C.oscore, C.k, C.use_tabu);
+  }
+  __syncwarp();
+}
+
+// Columns without nonzeros: a binary flips with score 0; another variable's candidates are its
+// finite bounds other than x̄, all scoring 0 (R2, R4, R5); none -> (x̄, -inf).
+__device__ __forceinline__ void wtile_empty(const DevProblem& P, const TileCtx& C, const WTile& T,
+                                            int lane, Best& b) {
+  if (lane >= T.ncols) return;
+  const int p = T.p0 + lane;
+  const int j = __ldg(P.perm + p);
+  const int tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
+  const double xb = __ldg(C.x + p);
+  const double l = __ldg(P.lb + p), u = __ldg(P.ub + p);
+  double bs = -INFINITY, bv = xb;
+  if (__ldg(P.vclass + p) == 1) {
+    bs = 0.0;
+    bv = 1.0 - xb;
+  } else {
+    if (isfinite(l) && l != xb) { bs = 0.0; bv = l; }
+    if (isfinite(u) && u != xb && better_shift(0.0, u, bs, bv, xb)) { bs = 0.0; bv = u; }
+  }
+  finish_column_j(p, j, tb, xb, bv, bs, b, C.oxhat, C.oscore, C.k, C.use_tabu);
 }
 
 // ------------------------------------------------------------------------------------------
-// block per general column (deg + 2 <= kBlockElems)
+// block tiles
 // ------------------------------------------------------------------------------------------
 
 __device__ __forceinline__ double block_sum(double v, double* sm) {
@@ -358,8 +487,7 @@ __device__ void block_scan_inclusive(double* a, int L, double* sm) {
   const int s0 = tid * seg, s1 = min(L, s0 + seg);
   double run = 0.0;
   for (int q = s0; q < s1; ++q) { run += a[q]; a[q] = run; }
-  // exclusive scan of the per-thread totals
-  const int lane = tid & 31, wid = tid >> 5, nw = (T + 31) >> 5;
+  const int lane = tid & 31, wid = tid >> 5;
   double incl = run;
   for (int off = 1; off < 32; off <<= 1) {
     const double y = __shfl_up_sync(kFull, incl, off);
@@ -373,64 +501,61 @@ __device__ void block_scan_inclusive(double* a, int L, double* sm) {
   const double off = woff + incl - run;
   for (int q = s0; q < s1; ++q) a[q] += off;
   __syncthreads();
-  (void)nw;
 }
 
-__global__ void __launch_bounds__(kBlockThreads) k_eval_block(DevProblem P, DevWalkers Wk,
-                                                              double* oxhat, double* oscore,
-                                                              int part_off) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* st = reinterpret_cast<double*>(smem);            // [kBlockElems] value
-  double* sdel = st + kBlockElems;                            // [kBlockElems] delta (by element)
-  double* sp = sdel + kBlockElems;                            // [kBlockElems] prefix (by rank)
-  uint32_t* smk = reinterpret_cast<uint32_t*>(sp + kBlockElems);  // [kBlockElems] plus<<31|cand<<30|e
-  __shared__ double sm_red[32];
-  __shared__ Best sm_b[32];
-  const int walker = blockIdx.y, tid = threadIdx.x;
-  const WalkerScalars* sc = Wk.sc + walker;
-  const double* x = Wk.x + (size_t)walker * Wk.xs;
-  const RowState* rs = Wk.rs + (size_t)walker * Wk.rss;
-  const int32_t* tabu = Wk.tabu + (size_t)walker * Wk.ts;
-  const long long k = sc->k;
-  const int cut_active = sc->cut_active;
-  const int p = P.bcols[blockIdx.x];
+// block-wide argmax of (score, value) within one variable (R4); result in thread 0
+__device__ __forceinline__ void block_best_shift(double& bs, double& bv, double xb, Best* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int off = 16; off > 0; off >>= 1) {
+    const double so = __shfl_xor_sync(kFull, bs, off), vo = __shfl_xor_sync(kFull, bv, off);
+    if (better_shift(so, vo, bs, bv, xb)) { bs = so; bv = vo; }
+  }
+  __syncthreads();
+  if (lane == 0) { sm[wid].s = bs; sm[wid].v = bv; }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (better_shift(sm[q].s, sm[q].v, bs, bv, xb)) { bs = sm[q].s; bv = sm[q].v; }
+  __syncthreads();
+}
+
+// one general column in one tile: bitonic sort of (value, marker) pairs (l.13), block scan (l.14)
+__device__ __forceinline__ void tile_genm(const DevProblem& P, const TileCtx& C, const Tile& T,
+                                          SmemGenM& S, double* sm_red, Best* sm_b, Best& b) {
+  const int tid = threadIdx.x;
+  const int p = T.p0;
   const int beg = P.col_ptr[p], d = P.col_ptr[p + 1] - beg;
-  const double xb = x[p], l = P.lb[p], u = P.ub[p];
+  const double xb = C.x[p], l = P.lb[p], u = P.ub[p];
   const int is_int = P.vclass[p] != 3;
-  const int L = d + 2;
   int Lp = 1;
-  while (Lp < L) Lp <<= 1;
+  while (Lp < d + 2) Lp <<= 1;
   double beta = 0.0, alpha = 0.0;
   for (int e = tid; e < Lp; e += blockDim.x) {
     double t = INFINITY, del = 0.0;
     uint32_t mk = 0xffffffffu;
     if (e < d) {
-      const int i = P.row_idx[beg + e];
-      const double a = P.val[beg + e];
-      if (i != P.cut_row || cut_active) {
-        const RowState s = rs[i];
-        const Elem el = emit(xb, s.r, a, (double)s.w, is_int);
-        beta += el.beta;
-        alpha += el.alpha;
-        if (el.valid) {
-          const bool cand = el.t >= l && el.t <= u && el.t != xb;
-          t = el.t;
-          del = el.delta;
-          mk = ((uint32_t)el.plus << 31) | ((uint32_t)cand << 30) | (uint32_t)e;
-        }
+      double r, w;
+      load_row(C.rs, P.row_idx[beg + e], r, w);
+      const Elem el = emit(xb, r, P.val[beg + e], w, is_int);
+      beta += el.beta;
+      alpha += el.alpha;
+      if (el.valid && isfinite(el.t)) {
+        const bool cand = el.t >= l && el.t <= u && el.t != xb;
+        t = el.t;
+        del = el.delta;
+        mk = ((uint32_t)el.plus << 31) | ((uint32_t)cand << 30) | (uint32_t)e;
       }
     } else if (e == d) {
       if (isfinite(l)) { t = l; mk = ((uint32_t)(l != xb) << 30) | (uint32_t)e; }
     } else if (e == d + 1) {
       if (isfinite(u)) { t = u; mk = ((uint32_t)(u != xb) << 30) | (uint32_t)e; }
     }
-    st[e] = t;
-    smk[e] = mk;
-    sdel[e] = del;
+    S.t[e] = t;
+    S.mk[e] = mk;
+    S.del[e] = del;
   }
   beta = block_sum(beta, sm_red);
   alpha = block_sum(alpha, sm_red);
-  // bitonic sort of (value, marker) pairs (PAPER.md:324 line 13; R3 marker order)
   for (int size = 2; size <= Lp; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncthreads();
@@ -438,233 +563,267 @@ __global__ void __launch_bounds__(kBlockThreads) k_eval_block(DevProblem P, DevW
         const int lo = 2 * q - (q & (stride - 1));
         const int hi = lo + stride;
         const bool asc = (lo & size) == 0;
-        const double t0 = st[lo], t1 = st[hi];
-        const uint32_t m0 = smk[lo], m1 = smk[hi];
+        const double t0 = S.t[lo], t1 = S.t[hi];
+        const uint32_t m0 = S.mk[lo], m1 = S.mk[hi];
         const bool gt = (t0 > t1) || (t0 == t1 && m0 > m1);
         if (gt == asc) {
-          st[lo] = t1; st[hi] = t0;
-          smk[lo] = m1; smk[hi] = m0;
+          S.t[lo] = t1; S.t[hi] = t0;
+          S.mk[lo] = m1; S.mk[hi] = m0;
         }
       }
     }
   }
   __syncthreads();
   for (int q = tid; q < Lp; q += blockDim.x) {
-    const uint32_t mk = smk[q];
-    sp[q] = (mk == 0xffffffffu) ? 0.0 : sdel[mk & 0x3fffffffu];
+    const uint32_t mk = S.mk[q];
+    S.P[q] = (mk == 0xffffffffu) ? 0.0 : S.del[mk & 0x3fffffffu];
   }
   __syncthreads();
-  block_scan_inclusive(sp, Lp, sm_red);   // line 14
-  Best bb;
-  bb.init();
+  block_scan_inclusive(S.P, Lp, sm_red);
   double bs = -INFINITY, bv = xb;
   for (int q = tid; q < Lp; q += blockDim.x) {
-    const uint32_t mk = smk[q];
+    const uint32_t mk = S.mk[q];
     if (mk == 0xffffffffu || !((mk >> 30) & 1u)) continue;
-    const double t = st[q];
-    const double pre = (mk >> 31) ? (q > 0 ? sp[q - 1] : 0.0) : sp[q];
-    const double sig = beta + pre + (t > xb ? alpha : 0.0);   // line 15
+    const double t = S.t[q];
+    const double pre = (mk >> 31) ? (q > 0 ? S.P[q - 1] : 0.0) : S.P[q];
+    const double sig = beta + pre + (t > xb ? alpha : 0.0);
     if (better_shift(sig, t, bs, bv, xb)) { bs = sig; bv = t; }
   }
-  // line 16: block argmax (shift tie-break within one variable)
-  {
-    const int lane = tid & 31, wid = tid >> 5;
-    for (int off = 16; off > 0; off >>= 1) {
-      const double so = __shfl_xor_sync(kFull, bs, off), vo = __shfl_xor_sync(kFull, bv, off);
-      if (better_shift(so, vo, bs, bv, xb)) { bs = so; bv = vo; }
-    }
-    __syncthreads();
-    if (lane == 0) { sm_b[wid].s = bs; sm_b[wid].v = bv; }
-    __syncthreads();
-    if (tid == 0) {
-      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
-        if (better_shift(sm_b[q].s, sm_b[q].v, bs, bv, xb)) { bs = sm_b[q].s; bv = sm_b[q].v; }
-      finish_column(P, p, xb, bv, bs, bb, oxhat, oscore, tabu, k, Wk.use_tabu);
-      write_part(Wk.part + (size_t)walker * Wk.ps + part_off + blockIdx.x, bb);
-    }
-  }
+  block_best_shift(bs, bv, xb, sm_b);
+  if (tid == 0) finish_column(P, p, xb, bv, bs, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
+  __syncthreads();
 }
 
-// ------------------------------------------------------------------------------------------
-// chunked long columns
-// ------------------------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(kBlockThreads) k_eval_long(DevProblem P, DevWalkers Wk,
-                                                             double* oxhat, double* oscore,
-                                                             int part_off) {
-  __shared__ double sD[kBucketMax + 1];
-  __shared__ unsigned char sC[kBucketMax];
-  __shared__ double sm_red[32];
-  __shared__ Best sm_b[32];
-  __shared__ int s_last;
-  const int walker = blockIdx.y, tid = threadIdx.x;
-  const LChunk ch = P.chunks[blockIdx.x];
-  const WalkerScalars* sc = Wk.sc + walker;
-  const double* x = Wk.x + (size_t)walker * Wk.xs;
-  const RowState* rs = Wk.rs + (size_t)walker * Wk.rss;
-  const int32_t* tabu = Wk.tabu + (size_t)walker * Wk.ts;
-  double* scr = Wk.lscr + (size_t)walker * Wk.lss + ch.scr;
-  unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + ch.lc;
-  const long long k = sc->k;
-  const int cut_active = sc->cut_active;
-  const int p = ch.p;
-  const double xb = x[p];
-  Best bb;
-  bb.init();
-  if (ch.kind == 0) {
-    // binary flip partial sum over this chunk
-    const double dir = 1.0 - 2.0 * xb;
-    double pen = 0.0;
-    for (int e = ch.e0 + tid; e < ch.e1; e += blockDim.x) {
-      const int i = P.row_idx[e];
-      const double a = P.val[e];
-      if (i != P.cut_row || cut_active) {
-        const RowState s = rs[i];
-        pen += penalty((double)s.w, s.r, s.r + a * dir);
-      }
-    }
-    pen = block_sum(pen, sm_red);
-    if (tid == 0) scr[ch.chunk] = pen;
+// last-chunk handshake of a chunked column: returns true in every thread of the last block
+__device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(cnt, 1u) == (unsigned)(ch.nchunks - 1));
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      if (tid == 0) {
-        double s = 0.0;
-        for (int c = 0; c < ch.nchunks; ++c) s += __ldcg(scr + c);   // chunk order
-        *cnt = 0u;
-        finish_column(P, p, xb, 1.0 - xb, s, bb, oxhat, oscore, tabu, k, Wk.use_tabu);
-      }
+    *s_flag = (atomicAdd(cnt, 1u) == (unsigned)(nchunks - 1));
+  }
+  __syncthreads();
+  const bool last = *s_flag != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// The CSC stream of a chunk tile: kPer independent coalesced loads + gathers per thread.
+struct ChunkRows {
+  double a[kPer];
+  double r[kPer];
+  double w[kPer];
+  bool ok[kPer];
+};
+__device__ __forceinline__ void load_chunk(const DevProblem& P, const TileCtx& C, int e0, int nnz,
+                                           ChunkRows& R) {
+  int idx[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int k = threadIdx.x + q * kTileThreads;
+    R.ok[q] = k < nnz;
+    idx[q] = R.ok[q] ? __ldg(P.row_idx + e0 + k) : 0;
+    R.a[q] = R.ok[q] ? __ldg(P.val + e0 + k) : 1.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) load_row(C.rs, idx[q], R.r[q], R.w[q]);
+}
+
+// a chunk of a long binary column: partial flip sum, merged in chunk order
+__device__ __forceinline__ void tile_lbin(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                          const TileCtx& C, const Tile& T, double* sm_red,
+                                          int* s_flag, Best& b) {
+  const int tid = threadIdx.x;
+  const int p = T.p0;
+  const double xb = C.x[p];
+  const double dir = 1.0 - 2.0 * xb;
+  ChunkRows R;
+  load_chunk(P, C, T.e0, T.e1 - T.e0, R);
+  double pen = 0.0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q)
+    if (R.ok[q]) pen += penalty(R.w[q], R.r[q], R.r[q] + R.a[q] * dir);
+  pen = block_sum(pen, sm_red);
+  if (T.nchunks == 1) {
+    if (tid == 0) finish_column(P, p, xb, 1.0 - xb, pen, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
+    return;
+  }
+  double* scr = Wk.lscr + (size_t)walker * Wk.lss + T.scr;
+  unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.lc;
+  if (tid == 0) scr[T.chunk] = pen;
+  if (last_chunk(cnt, T.nchunks, s_flag) && tid == 0) {
+    double s = 0.0;
+    for (int c = 0; c < T.nchunks; ++c) s += __ldcg(scr + c);   // chunk order
+    *cnt = 0u;
+    finish_column(P, p, xb, 1.0 - xb, s, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
+  }
+  __syncthreads();
+}
+
+// a chunk of a general integer column with domain [l, u], dom = u - l + 1 <= kBucketMax: the
+// sort of line 13 becomes a counting pass. D[v-l] collects the -1 deltas at v and the +1
+// deltas at v-1, so sigma at candidate v = β + Σ_{v' <= v} D[v'] + α [v > x̄].
+__device__ __forceinline__ void tile_lbkt(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                          const TileCtx& C, const Tile& T, SmemBkt& S,
+                                          double* sm_red, Best* sm_b, int* s_flag, Best& b) {
+  const int tid = threadIdx.x;
+  const int p = T.p0, dom = T.dom;
+  const double xb = C.x[p], l = P.lb[p], u = P.ub[p];
+  for (int q = tid; q <= dom; q += blockDim.x) S.D[q] = 0.0;
+  for (int q = tid; q < dom; q += blockDim.x) S.cand[q] = 0;
+  ChunkRows R;
+  load_chunk(P, C, T.e0, T.e1 - T.e0, R);
+  __syncthreads();
+  double beta = 0.0, alpha = 0.0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    if (!R.ok[q]) continue;
+    const Elem el = emit(xb, R.r[q], R.a[q], R.w[q], 1);
+    beta += el.beta;
+    alpha += el.alpha;
+    if (!el.valid) continue;
+    const double t = el.t;
+    if (t >= l && t <= u && t != xb) S.cand[(int)(t - l)] = 1;
+    if (!el.plus) {
+      if (t < l) beta += el.delta;
+      else if (t <= u) atomicAdd(&S.D[(int)(t - l)], el.delta);
+    } else {
+      if (t < l) beta += el.delta;
+      else if (t < u) atomicAdd(&S.D[(int)(t - l) + 1], el.delta);
     }
-  } else {
-    // bounded integer domain [l, u], dom = u - l + 1 <= kBucketMax: the sort of line 13 becomes
-    // a counting (bucket) pass. D[v-l] collects the -1 deltas at v and the +1 deltas at v-1, so
-    // sigma at candidate v = β + Σ_{v' <= v} D[v'] + α[v > x̄].
-    const int dom = ch.dom;
-    const double l = P.lb[p], u = P.ub[p];
-    for (int q = tid; q <= dom; q += blockDim.x) sD[q] = 0.0;
-    for (int q = tid; q < dom; q += blockDim.x) sC[q] = 0;
-    __syncthreads();
-    double beta = 0.0, alpha = 0.0;
-    for (int e = ch.e0 + tid; e < ch.e1; e += blockDim.x) {
-      const int i = P.row_idx[e];
-      const double a = P.val[e];
-      if (i == P.cut_row && !cut_active) continue;
-      const RowState s = rs[i];
-      const Elem el = emit(xb, s.r, a, (double)s.w, 1);
-      beta += el.beta;
-      alpha += el.alpha;
-      if (!el.valid) continue;
-      const double t = el.t;
-      if (t >= l && t <= u && t != xb) sC[(int)(t - l)] = 1;
-      if (!el.plus) {
-        if (t < l) beta += el.delta;
-        else if (t <= u) atomicAdd(&sD[(int)(t - l)], el.delta);
-      } else {
-        if (t < l) beta += el.delta;
-        else if (t < u) atomicAdd(&sD[(int)(t - l) + 1], el.delta);
-      }
-    }
-    beta = block_sum(beta, sm_red);
-    alpha = block_sum(alpha, sm_red);
-    // chunk partials: [nchunks][dom] D, [nchunks][dom] cand (as doubles 0/1), [nchunks][2] β α
-    double* pD = scr + (size_t)ch.chunk * dom;
-    double* pC = scr + (size_t)ch.nchunks * dom + (size_t)ch.chunk * dom;
-    double* pBA = scr + (size_t)2 * ch.nchunks * dom + 2 * ch.chunk;
+  }
+  beta = block_sum(beta, sm_red);
+  alpha = block_sum(alpha, sm_red);
+  bool have_all = (T.nchunks == 1);
+  double B = beta, A = alpha;
+  if (!have_all) {
+    double* scr = Wk.lscr + (size_t)walker * Wk.lss + T.scr;
+    unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.lc;
+    double* pD = scr + (size_t)T.chunk * dom;
+    double* pC = scr + (size_t)T.nchunks * dom + (size_t)T.chunk * dom;
+    double* pBA = scr + (size_t)2 * T.nchunks * dom + 2 * T.chunk;
     for (int q = tid; q < dom; q += blockDim.x) {
-      pD[q] = sD[q];
-      pC[q] = sC[q] ? 1.0 : 0.0;
+      pD[q] = S.D[q];
+      pC[q] = S.cand[q] ? 1.0 : 0.0;
     }
     if (tid == 0) { pBA[0] = beta; pBA[1] = alpha; }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(cnt, 1u) == (unsigned)(ch.nchunks - 1));
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      for (int q = tid; q < dom; q += blockDim.x) {
-        double dsum = 0.0, csum = 0.0;
-        for (int c = 0; c < ch.nchunks; ++c) {
-          dsum += __ldcg(scr + (size_t)c * dom + q);
-          csum += __ldcg(scr + (size_t)ch.nchunks * dom + (size_t)c * dom + q);
-        }
-        sD[q] = dsum;
-        sC[q] = csum > 0.0 ? 1 : 0;
+    if (!last_chunk(cnt, T.nchunks, s_flag)) return;
+    for (int q = tid; q < dom; q += blockDim.x) {
+      double dsum = 0.0, csum = 0.0;
+      for (int c = 0; c < T.nchunks; ++c) {
+        dsum += __ldcg(scr + (size_t)c * dom + q);
+        csum += __ldcg(scr + (size_t)T.nchunks * dom + (size_t)c * dom + q);
       }
-      __syncthreads();
-      if (tid == 0) {
-        double bsum = 0.0, asum = 0.0;
-        for (int c = 0; c < ch.nchunks; ++c) {
-          bsum += __ldcg(scr + (size_t)2 * ch.nchunks * dom + 2 * c);
-          asum += __ldcg(scr + (size_t)2 * ch.nchunks * dom + 2 * c + 1);
-        }
-        sm_b[0].s = bsum;
-        sm_b[0].v = asum;
-        if (l != xb) sC[0] = 1;                 // (l, -1, 0)
-        if (u != xb) sC[dom - 1] = 1;           // (u, -1, 0)
-        *cnt = 0u;
-      }
-      __syncthreads();
-      const double B = sm_b[0].s, A = sm_b[0].v;
-      __syncthreads();
-      block_scan_inclusive(sD, dom, sm_red);
-      double bs = -INFINITY, bv = xb;
-      for (int q = tid; q < dom; q += blockDim.x) {
-        if (!sC[q]) continue;
-        const double v = l + (double)q;
-        if (v == xb) continue;
-        const double sig = B + sD[q] + (v > xb ? A : 0.0);
-        if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
-      }
-      const int lane = tid & 31, wid = tid >> 5;
-      for (int off = 16; off > 0; off >>= 1) {
-        const double so = __shfl_xor_sync(kFull, bs, off), vo = __shfl_xor_sync(kFull, bv, off);
-        if (better_shift(so, vo, bs, bv, xb)) { bs = so; bv = vo; }
-      }
-      __syncthreads();
-      if (lane == 0) { sm_b[wid].s = bs; sm_b[wid].v = bv; }
-      __syncthreads();
-      if (tid == 0) {
-        for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
-          if (better_shift(sm_b[q].s, sm_b[q].v, bs, bv, xb)) { bs = sm_b[q].s; bv = sm_b[q].v; }
-        finish_column(P, p, xb, bv, bs, bb, oxhat, oscore, tabu, k, Wk.use_tabu);
-      }
+      S.D[q] = dsum;
+      S.cand[q] = csum > 0.0 ? 1 : 0;
     }
+    if (tid == 0) {
+      double bsum = 0.0, asum = 0.0;
+      for (int c = 0; c < T.nchunks; ++c) {
+        bsum += __ldcg(scr + (size_t)2 * T.nchunks * dom + 2 * c);
+        asum += __ldcg(scr + (size_t)2 * T.nchunks * dom + 2 * c + 1);
+      }
+      sm_red[0] = bsum;
+      sm_red[1] = asum;
+      *cnt = 0u;
+    }
+    __syncthreads();
+    B = sm_red[0];
+    A = sm_red[1];
+    __syncthreads();
   }
-  if (tid == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_off + blockIdx.x, bb);
+  if (tid == 0) {
+    if (l != xb) S.cand[0] = 1;                 // (l, -1, 0)
+    if (u != xb) S.cand[dom - 1] = 1;           // (u, -1, 0)
+  }
+  __syncthreads();
+  block_scan_inclusive(S.D, dom, sm_red);
+  double bs = -INFINITY, bv = xb;
+  for (int q = tid; q < dom; q += blockDim.x) {
+    if (!S.cand[q]) continue;
+    const double v = l + (double)q;
+    if (v == xb) continue;
+    const double sig = B + S.D[q] + (v > xb ? A : 0.0);
+    if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
+  }
+  block_best_shift(bs, bv, xb, sm_b);
+  if (tid == 0) finish_column(P, p, xb, bv, bs, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------------------------
-// global select: best admissible move per walker, ties -> lowest j (R6)
+// the kernel
 // ------------------------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(256) k_select(DevWalkers Wk, int n_part, chap_move* best_out) {
+// grid = (blocks per walker, W). After its tiles every block publishes its best admissible move;
+// the last block of the walker reduces them (fixed order) to the decision.
+__global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalkers Wk, double* oxhat,
+                                                          double* oscore, chap_move* best_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double sm_red[32];
   __shared__ Best sm_b[32];
-  const int walker = blockIdx.x;
-  const Cand* part = Wk.part + (size_t)walker * Wk.ps;
+  __shared__ int s_flag;
+  const int walker = blockIdx.y;
+  const WalkerScalars* sc = Wk.sc + walker;
+  TileCtx C;
+  C.x = Wk.x + (size_t)walker * Wk.xs;
+  C.rs = Wk.rs + (size_t)walker * Wk.rss;
+  C.tabu = Wk.tabu + (size_t)walker * Wk.ts;
+  C.k = sc->k;
+  C.use_tabu = Wk.use_tabu;
+  C.oxhat = oxhat;
+  C.oscore = oscore;
   Best b;
   b.init();
-  for (int q = threadIdx.x; q < n_part; q += blockDim.x) {
-    const Cand c = part[q];
-    Best o;
-    o.s = c.s; o.v = c.v; o.j = c.j; o.p = c.p;
-    b.take(o);
+  // phase A: block tiles (chunks of long columns, single-column sorts)
+  for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+    const Tile T = P.tiles[t];
+    switch (T.kind) {
+      case CC_LBIN: tile_lbin(P, Wk, walker, C, T, sm_red, &s_flag, b); break;
+      case CC_LBKT: tile_lbkt(P, Wk, walker, C, T, *reinterpret_cast<SmemBkt*>(smem), sm_red, sm_b, &s_flag, b); break;
+      default: tile_genm(P, C, T, *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b); break;
+    }
   }
+  __syncthreads();
+  // phase B: warp tiles, each warp on its own slice of shared memory, no block barriers
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char* ws = smem + (size_t)wid * kWarpSmem;
+    const int nwarps = gridDim.x * kTileWarps;
+    for (int t = blockIdx.x * kTileWarps + wid; t < P.n_wtiles; t += nwarps) {
+      const WTile T = P.wtiles[t];
+      if (T.kind == CC_BIN) wtile_bin(P, C, T, lane, *reinterpret_cast<WarpBin*>(ws), b);
+      else if (T.kind == CC_GEN) wtile_gen(P, C, T, lane, *reinterpret_cast<WarpGen*>(ws), b);
+      else wtile_empty(P, C, T, lane, b);
+    }
+  }
+  // publish the block's best; the last block of this walker selects (R6)
   b = block_reduce_best(b, sm_b);
+  Cand* part = Wk.part + (size_t)walker * Wk.ps;
+  if (threadIdx.x == 0) write_part(part + blockIdx.x, b);
+  if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
+  Best g;
+  g.init();
+  for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+    Best o;
+    o.s = __ldcg(&part[q].s);
+    o.v = __ldcg(&part[q].v);
+    o.j = __ldcg(&part[q].j);
+    o.p = __ldcg(&part[q].p);
+    g.take(o);
+  }
+  g = block_reduce_best(g, sm_b);
   if (threadIdx.x == 0) {
-    WalkerScalars* sc = Wk.sc + walker;
-    const bool found = b.p >= 0;
+    WalkerScalars* scw = Wk.sc + walker;
+    const bool found = g.p >= 0;
     Decision d;
-    d.move = (found && b.s > 0.0) ? 1 : 0;
-    d.p = b.p;
-    d.j = found ? b.j : -1;
+    d.move = (found && g.s > 0.0) ? 1 : 0;
+    d.p = g.p;
+    d.j = found ? g.j : -1;
     d.pad = 0;
-    d.v = b.v;
-    d.s = found ? b.s : -INFINITY;
-    d.delta = d.move ? (b.v - Wk.x[(size_t)walker * Wk.xs + b.p]) : 0.0;
-    sc->dec = d;
+    d.v = g.v;
+    d.s = found ? g.s : -INFINITY;
+    d.delta = d.move ? (g.v - C.x[g.p]) : 0.0;
+    scw->dec = d;
     if (best_out) {
       chap_move mv;
       mv.j = d.move ? d.j : -1;
@@ -673,6 +832,7 @@ __global__ void __launch_bounds__(256) k_select(DevWalkers Wk, int n_part, chap_
       mv.s = d.move ? d.s : -INFINITY;
       best_out[walker] = mv;
     }
+    Wk.sel_count[walker] = 0u;
   }
 }
 

@@ -89,8 +89,8 @@ struct chap_problem {
   std::vector<int8_t> side;
   DeviceBuffers buf;
   DevProblem dp{};
-  PartLayout pl{};
-  int warp_grid = 1;
+  int eval_occ = 1;            // resident k_eval blocks per SM
+  int eval_grid = 1;           // k_eval blocks for one walker
   int rows_grid = 1;
   size_t lscr_per_walker = 1;   // doubles
   // eval workspace (one virtual walker)
@@ -100,6 +100,7 @@ struct chap_problem {
   double* e_bx = nullptr;
   WalkerScalars* e_sc = nullptr;
   Cand* e_part = nullptr;
+  unsigned* e_selcnt = nullptr;
   unsigned* e_lcount = nullptr;
   double* e_lscr = nullptr;
   // host-buffer variant staging (lazy)
@@ -132,6 +133,7 @@ struct chap_walkers {
   cudaGraphExec_t gexec = nullptr;
   int g_iters = 0;
   int apply_grid = 1;
+  int eval_grid = 1;           // k_eval blocks per walker
   ~chap_walkers() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ev_in) cudaEventDestroy(ev_in);
@@ -143,8 +145,8 @@ struct chap_walkers {
 
 namespace chap {
 // shared launch helpers (chap.cu)
-chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, double* oxhat, double* oscore,
-                        cudaStream_t s);
+chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, double* oxhat,
+                        double* oscore, chap_move* best, cudaStream_t s);
 int grid_for(long long work, int threads, int cap);
 
 }  // namespace chap

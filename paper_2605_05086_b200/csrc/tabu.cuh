@@ -20,7 +20,9 @@ __global__ void k_permute_in(DevProblem P, const double* __restrict__ xu, size_t
 }
 
 // r_i = Σ_k a_ik x̄_k - b_i from scratch (warp per row, CSR). The cutoff row (last) is active
-// iff sc[w].cut_active (rhs sc[w].cutoff_rhs); otherwise r = -inf. init_w: 0 keep weights,
+// iff sc[w].cut_active (rhs sc[w].cutoff_rhs); an inactive cutoff row is stored inert, r = -inf
+// and w = 0, so that it contributes nothing to any score without a per-nonzero test (its logical
+// weight while inactive is the initial 1: bumps skip inactive rows). init_w: 0 keep weights,
 // 1 set to 1, 2 copy from wsrc (eval API).
 __global__ void k_rows_init(DevProblem P, const double* __restrict__ x, size_t xs, RowState* rs,
                             size_t rss, const WalkerScalars* sc, int init_w,
@@ -47,6 +49,7 @@ __global__ void k_rows_init(DevProblem P, const double* __restrict__ x, size_t x
       s.r = r;
       if (init_w == 1) s.w = 1.0f;
       else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
+      if (i == P.cut_row && !sc[w].cut_active) s.w = 0.0f;
       s.pad = 0;
       rw[i] = s;
     }
@@ -68,6 +71,7 @@ __device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWal
   sc->has_inc = 1;
   sc->pending_copy = 1;
   const double rhs = z - auto_delta(P, Wk.delta, z);
+  if (!sc->cut_active) rw[P.cut_row].w = 1.0f;   // the inert row takes its logical weight
   sc->cutoff_rhs = rhs;
   sc->cut_active = 1;
   const double r = z - rhs;
@@ -247,7 +251,7 @@ __global__ void k_export_rows(DevProblem P, DevWalkers Wk, double* r, float* wt)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m_norm; i += gridDim.x * blockDim.x) {
     const RowState s = rw[i];
     if (r) r[(size_t)w * P.m_norm + i] = (i == P.cut_row && !cut_active) ? -INFINITY : s.r;
-    if (wt) wt[(size_t)w * P.m_norm + i] = s.w;
+    if (wt) wt[(size_t)w * P.m_norm + i] = (i == P.cut_row && !cut_active) ? 1.0f : s.w;
   }
 }
 
@@ -279,6 +283,7 @@ __global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
   const double r_old = sc->cut_active ? rw[P.cut_row].r : -INFINITY;
   const double r_new = sc->obj - rhs;
   sc->violated += (long long)(r_new > 0.0) - (long long)(r_old > 0.0);
+  if (!sc->cut_active) rw[P.cut_row].w = 1.0f;
   rw[P.cut_row].r = r_new;
   sc->cutoff_rhs = rhs;
   sc->cut_active = 1;

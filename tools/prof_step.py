@@ -1,0 +1,26 @@
+"""Profiling driver (ncu target): config G, one walker, plain launches (no graph) so that ncu
+sees individual k_eval / k_apply launches. Usage: python tools/prof_step.py [warmup] [iters] [cfg]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2605_05086_b200 as chap  # noqa: E402
+import synth  # noqa: E402
+
+warm = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+cfg = sys.argv[3] if len(sys.argv) > 3 else "G"
+inst = {"G": synth.mixed, "S": synth.setcover, "P": synth.packing}[cfg]()
+P = chap.Problem.from_instance(inst)
+W = 64 if cfg == "P" else 1
+x0 = np.stack([synth.x_lower(inst)] * W) if cfg != "P" else \
+    np.stack([synth.x_bernoulli(inst, (3, w), 0.5) for w in range(W)])
+ws = chap.Walkers(P, torch.from_numpy(x0).cuda(), chap.default_params(graph_iters=0))
+ws.step(warm)
+torch.cuda.synchronize()
+ws.step(iters)
+torch.cuda.synchronize()
+print("info", P.info.n_long_columns, list(P.info.nnz_kernel), list(P.info.model_bytes_kernel))
