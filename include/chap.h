@@ -254,6 +254,34 @@ typedef struct {
   double seconds;           /* wall time of the call                                          */
 } chap_result;
 
+/* Per-walker exchange summary (32 bytes), gathered from every rank. */
+typedef struct {
+  double best_obj;        /* best incumbent objective, +INF if none                            */
+  int64_t violated;       /* violated active rows of the current point (cutoff row included)   */
+  double sumviol;         /* sum over non-cutoff rows of max(0, r_i) at the current point      */
+  int32_t gid;            /* global walker id = rank * W_local + local index                   */
+  int32_t flags;          /* bit 0: has an incumbent; bit 1: this rank asks to stop            */
+} chap_walker_summary;
+
+/* The deterministic exchange rule of chap_run_walkers, a pure HOST function of the
+ * gathered summaries (identical on every rank; usable without a GPU). With W_total summaries s[]
+ * indexed by gid and ranks of W_local walkers each:
+ *   feasible elite  = up to n_elite walkers with an incumbent, by (best_obj, gid): best points;
+ *   infeasible elite = up to n_elite walkers by (violated, sumviol, gid): current points;
+ *   the elite list E is the feasible elite followed by the infeasible elite; for each member
+ *   elite_gid[q], elite_kind[q] (0: best point, 1: current point) and elite_slot[q], its slot in
+ *   the gathered point buffer (rank * 2 n_elite + [n_elite if kind 1] + its position among that
+ *   rank's own top-n_elite of the kind);
+ *   *z_best = min best_obj (+INF if none), *best_gid its walker (lowest gid on ties; -1);
+ *   the n_restart walkers with the highest (violated, gid) restart in that order:
+ *   restart_gid[q] from E[q mod |E|] (restart_src[q]); none if E is empty.
+ * Output arrays: elite_* [2 n_elite], restart_* [n_restart]. */
+chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, const chap_walker_summary* s,
+                               int32_t n_elite, int32_t n_restart, double* z_best,
+                               int32_t* best_gid, int32_t* n_elite_out, int32_t* elite_gid,
+                               int8_t* elite_kind, int32_t* elite_slot, int32_t* n_restart_out,
+                               int32_t* restart_gid, int32_t* restart_src);
+
 /* The portfolio loop: W_local walkers from x0 DEVICE [W_local][n] (global
  * walker id = rank*W_local + w), epochs of params.exchange_K iterations; after each epoch an
  * allgather of per-walker summaries and of each rank's elite points (n_elite best incumbents

@@ -88,6 +88,13 @@ def lib():
         L.orc_tabu_run.argtypes = [P, ctypes.POINTER(Params), ctypes.POINTER(Walker), ctypes.c_int64, P,
                                    ctypes.c_int]
         L.orc_tabu_run.restype = ctypes.c_int
+        L.orc_walker_restart.argtypes = [P, ctypes.POINTER(Params), ctypes.POINTER(Walker), P]
+        L.orc_walker_restart.restype = ctypes.c_int
+        L.orc_walker_set_cutoff.argtypes = [P, ctypes.POINTER(Params), ctypes.POINTER(Walker), ctypes.c_double]
+        L.orc_walker_summary.argtypes = [P, ctypes.POINTER(Walker), P, P]
+        L.orc_run_walkers.argtypes = [P, ctypes.POINTER(Params), P, ctypes.c_int32, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int]
+        L.orc_run_walkers.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -209,6 +216,21 @@ class TabuWalker:
             raise OracleError(st)
         return log
 
+    def restart(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        st = lib().orc_walker_restart(self.prob.h, ctypes.byref(self._prm), ctypes.byref(self.S), x.ctypes.data)
+        if st != ORC_OK:
+            raise OracleError(st)
+
+    def set_cutoff(self, z: float):
+        lib().orc_walker_set_cutoff(self.prob.h, ctypes.byref(self._prm), ctypes.byref(self.S), float(z))
+
+    def summary(self):
+        """(violated active rows, sum of positive residuals over non-cutoff rows)"""
+        v = ctypes.c_int64(); s = ctypes.c_double()
+        lib().orc_walker_summary(self.prob.h, ctypes.byref(self.S), ctypes.byref(v), ctypes.byref(s))
+        return v.value, s.value
+
     @property
     def k(self):
         return self.S.k
@@ -224,3 +246,17 @@ class TabuWalker:
     @property
     def has_incumbent(self):
         return bool(self.S.has_incumbent)
+
+
+def run_walkers(prob: Problem, walkers, K: int, n_epochs: int, n_elite: int, n_restart: int, threads: int = 0):
+    """orc_run_walkers: the single-process portfolio with the every-K exchange over
+    already-initialised TabuWalker objects (their states are updated in place)."""
+    arr = (Walker * len(walkers))(*[w.S for w in walkers])
+    prm = walkers[0]._prm
+    st = lib().orc_run_walkers(prob.h, ctypes.byref(prm), ctypes.cast(arr, ctypes.c_void_p), len(walkers), int(K),
+                               int(n_epochs), int(n_elite), int(n_restart), int(threads))
+    if st != ORC_OK:
+        raise OracleError(st)
+    for w, a in zip(walkers, arr):
+        w.S = a
+    return walkers

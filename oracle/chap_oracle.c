@@ -412,3 +412,103 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
   free(r); free(y); free(xhat); free(score);
   return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------------------- */
+/* portfolio exchange — engineering rule, not stated by the paper  */
+/* ---------------------------------------------------------------------------------------- */
+
+int orc_walker_restart(const orc_problem* P, const orc_params* prm, orc_walker* S, const double* x) {
+  for (int32_t j = 0; j < P->n; j++) {
+    if (!(x[j] >= P->lb[j] && x[j] <= P->ub[j])) return ORC_ERR_INVALID_ARG;
+    S->x[j] = x[j];
+    S->tabu_until[j] = 0;
+  }
+  double* r = (double*)malloc(sizeof(double) * P->m_norm);
+  incumbent_check(P, prm, S, r);
+  free(r);
+  return ORC_OK;
+}
+
+void orc_walker_set_cutoff(const orc_problem* P, const orc_params* prm, orc_walker* S, double z) {
+  double rhs = z - cutoff_delta(P, prm, z);
+  if (S->cutoff_rhs == INFINITY || rhs < S->cutoff_rhs) S->cutoff_rhs = rhs;
+}
+
+void orc_walker_summary(const orc_problem* P, const orc_walker* S, int64_t* violated, double* sumviol) {
+  double* r = (double*)malloc(sizeof(double) * P->m_norm);
+  orc_residuals(P, S->x, S->cutoff_rhs, r);
+  *violated = count_violated(P, r, S->cutoff_rhs < INFINITY);
+  double sv = 0.0;
+  for (int32_t i = 0; i < P->m_norm - 1; i++) sv += (r[i] > 0.0) ? r[i] : 0.0;
+  *sumviol = sv;
+  free(r);
+}
+
+typedef struct { double a; double b; int64_t c; int32_t id; } orc_key;
+
+static int key_less(const orc_key* x, const orc_key* y) {
+  if (x->a != y->a) return x->a < y->a;
+  if (x->b != y->b) return x->b < y->b;
+  if (x->c != y->c) return x->c < y->c;
+  return x->id < y->id;
+}
+
+/* selection of the k smallest keys, in order (plain insertion, W is small) */
+static int32_t top_k(orc_key* keys, int32_t n, int32_t k) {
+  for (int32_t i = 1; i < n; i++) {
+    orc_key v = keys[i];
+    int32_t q = i;
+    while (q > 0 && key_less(&v, &keys[q - 1])) { keys[q] = keys[q - 1]; q--; }
+    keys[q] = v;
+  }
+  return n < k ? n : k;
+}
+
+int orc_run_walkers(const orc_problem* P, const orc_params* prm, orc_walker* S, int32_t W, int64_t K,
+                    int64_t n_epochs, int32_t n_elite, int32_t n_restart, int n_threads) {
+  int32_t n = P->n;
+  orc_key* keys = (orc_key*)malloc(sizeof(orc_key) * (W + 1));
+  int64_t* viol = (int64_t*)malloc(sizeof(int64_t) * (W + 1));
+  double* sv = (double*)malloc(sizeof(double) * (W + 1));
+  double* elite = (double*)malloc(sizeof(double) * (size_t)(2 * n_elite + 1) * (n + 1));
+  for (int64_t ep = 0; ep < n_epochs; ep++) {
+    for (int32_t w = 0; w < W; w++) {
+      int st = orc_tabu_run(P, prm, &S[w], K, NULL, n_threads);
+      if (st != ORC_OK) return st;
+    }
+    if (ep == n_epochs - 1) break;       /* no exchange after the last epoch */
+    for (int32_t w = 0; w < W; w++) orc_walker_summary(P, &S[w], &viol[w], &sv[w]);
+    /* feasible elite */
+    int32_t nf = 0;
+    for (int32_t w = 0; w < W; w++)
+      if (S[w].has_incumbent) { keys[nf].a = S[w].best_obj; keys[nf].b = 0; keys[nf].c = 0; keys[nf].id = w; nf++; }
+    int32_t kf = top_k(keys, nf, n_elite);
+    int32_t ne = 0;
+    double z = INFINITY;
+    for (int32_t q = 0; q < kf; q++) {
+      memcpy(elite + (size_t)ne * n, S[keys[q].id].best_x, sizeof(double) * n);
+      ne++;
+      if (S[keys[q].id].best_obj < z) z = S[keys[q].id].best_obj;
+    }
+    /* infeasible elite: current points by (violated, sumviol, id) */
+    for (int32_t w = 0; w < W; w++) { keys[w].a = (double)viol[w]; keys[w].b = sv[w]; keys[w].c = 0; keys[w].id = w; }
+    int32_t ki = top_k(keys, W, n_elite);
+    for (int32_t q = 0; q < ki; q++) {
+      memcpy(elite + (size_t)ne * n, S[keys[q].id].x, sizeof(double) * n);
+      ne++;
+    }
+    /* cutoff from the global incumbent */
+    if (z < INFINITY)
+      for (int32_t w = 0; w < W; w++) orc_walker_set_cutoff(P, prm, &S[w], z);
+    /* restarts: highest (violated, id) first */
+    for (int32_t w = 0; w < W; w++) { keys[w].a = -(double)viol[w]; keys[w].b = 0; keys[w].c = -(int64_t)w; keys[w].id = w; }
+    int32_t kr = top_k(keys, W, n_restart);
+    if (ne > 0)
+      for (int32_t q = 0; q < kr; q++) {
+        int st = orc_walker_restart(P, prm, &S[keys[q].id], elite + (size_t)(q % ne) * n);
+        if (st != ORC_OK) return st;
+      }
+  }
+  free(keys); free(viol); free(sv); free(elite);
+  return ORC_OK;
+}

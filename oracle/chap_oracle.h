@@ -96,6 +96,27 @@ int orc_walker_init(const orc_problem* P, const orc_params* prm, const double* x
 int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int64_t n_iters,
                  orc_record* log, int n_threads);
 
+/* Restart a walker from x (copied): tabu cleared, weights and k kept, then the incumbent check of
+ * R15 (SURVEY §8(e) restart rule). */
+int orc_walker_restart(const orc_problem* P, const orc_params* prm, orc_walker* S, const double* x);
+/* Impose a cutoff from an external incumbent z: rhs = z - delta, only tightening. */
+void orc_walker_set_cutoff(const orc_problem* P, const orc_params* prm, orc_walker* S, double z);
+/* Exchange summary of a walker: active violated rows (cutoff included) and the total violation
+ * sum_{i < m_norm-1} max(0, r_i) of its current point. */
+void orc_walker_summary(const orc_problem* P, const orc_walker* S, int64_t* violated, double* sumviol);
+
+/* The portfolio of SURVEY §8(e) in one process: W walkers from x0s [W][n]; n_epochs epochs of K
+ * tabu iterations each; after every epoch but the last the exchange rule:
+ *   summaries (best_obj or +inf, violated, sumviol) of every walker;
+ *   feasible elite F = the n_elite walkers with an incumbent by (best_obj, id), their best points;
+ *   infeasible elite I = the n_elite walkers by (violated, sumviol, id), their current points;
+ *   z = min best_obj -> every walker's cutoff tightened to z - delta;
+ *   the n_restart walkers with the highest (violated, id) restart, in that order, from the elite
+ *   list E = F ++ I round-robin (E[q mod |E|]).
+ * Walker states are left in S[W] (caller-initialised with orc_walker_init). */
+int orc_run_walkers(const orc_problem* P, const orc_params* prm, orc_walker* S, int32_t W, int64_t K,
+                    int64_t n_epochs, int32_t n_elite, int32_t n_restart, int n_threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"libchap.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(the CUDA path has no fallback)")
 
-_lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+_lib = ctypes.CDLL(LIB_PATH)
 
 # ------------------------------------------------------------------------------------------
 # ABI structs (field order and sizes as in include/chap.h)
@@ -63,6 +63,12 @@ class chap_result(ctypes.Structure):
                 ("epochs", c_i64), ("seconds", c_f64)]
 
 
+class chap_walker_summary(ctypes.Structure):
+    _fields_ = [("best_obj", c_f64), ("violated", c_i64), ("sumviol", c_f64), ("gid", c_i32), ("flags", c_i32)]
+
+
+SUMMARY_DTYPE = np.dtype([("best_obj", "<f8"), ("violated", "<i8"), ("sumviol", "<f8"), ("gid", "<i4"),
+                          ("flags", "<i4")])
 MOVE_DTYPE = np.dtype([("j", "<i4"), ("pad", "<i4"), ("v", "<f8"), ("s", "<f8")])
 RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("pad", "<i4"), ("v", "<f8"), ("s", "<f8"),
                          ("violated", "<i8"), ("obj", "<f8")])
@@ -99,6 +105,7 @@ _SIGS = {
     "chap_comm_destroy": (ctypes.c_int, [_P]),
     "chap_run_walkers": (ctypes.c_int, [_P, c_i32, _P, ctypes.POINTER(chap_params), _P, c_i64, c_f64, _P,
                                         ctypes.POINTER(chap_result), _P]),
+    "chap_exchange_plan": (ctypes.c_int, [c_i32, c_i32, _P, c_i32, c_i32, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -315,3 +322,20 @@ def run_walkers(problem: Problem, x0, params: Optional[chap_params] = None, comm
                             comm.h if comm is not None else None, int(max_iters), float(time_limit_s), _ptr(bx),
                             ctypes.byref(res), _stream(stream)))
     return res, bx
+
+
+def exchange_plan(summaries: np.ndarray, W_local: int, n_elite: int, n_restart: int) -> dict:
+    """chap_exchange_plan (host only): the deterministic exchange decisions from gathered summaries
+    (a SUMMARY_DTYPE array indexed by global walker id)."""
+    s = np.ascontiguousarray(summaries, SUMMARY_DTYPE)
+    W = int(s.shape[0])
+    z = ctypes.c_double(); bg = ctypes.c_int32(); ne = ctypes.c_int32(); nr = ctypes.c_int32()
+    eg = np.zeros(max(2 * n_elite, 1), np.int32); ek = np.zeros(max(2 * n_elite, 1), np.int8)
+    es = np.zeros(max(2 * n_elite, 1), np.int32)
+    rg = np.zeros(max(n_restart, 1), np.int32); rs = np.zeros(max(n_restart, 1), np.int32)
+    _check(chap_exchange_plan(W, int(W_local), s.ctypes.data, int(n_elite), int(n_restart), ctypes.addressof(z),
+                              ctypes.addressof(bg), ctypes.addressof(ne), eg.ctypes.data, ek.ctypes.data,
+                              es.ctypes.data, ctypes.addressof(nr), rg.ctypes.data, rs.ctypes.data))
+    return {"z_best": z.value, "best_gid": bg.value, "elite_gid": eg[:ne.value].copy(),
+            "elite_kind": ek[:ne.value].copy(), "elite_slot": es[:ne.value].copy(),
+            "restart_gid": rg[:nr.value].copy(), "restart_src": rs[:nr.value].copy()}

@@ -9,8 +9,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libchap.so")
-SOURCES = ["chap.cu", "portfolio.cu"]
-HEADERS = ["common.cuh", "eval.cuh", "tabu.cuh"]
+SOURCES = ["chap.cu"]
+HEADERS = ["common.cuh", "eval.cuh", "tabu.cuh", "host.h", "portfolio.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared", "--expt-relaxed-constexpr"]
 
@@ -26,7 +26,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc] + NVCC_FLAGS + ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-o", SO + ".tmp"]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
-    cmd += ["-lnccl"]
+    cmd += ["-ldl"]   # NCCL is dlopen'ed at run time (csrc/portfolio.cuh)
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

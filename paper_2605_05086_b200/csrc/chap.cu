@@ -773,3 +773,5 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
   delete S;
   return CHAP_OK;
 }
+
+#include "portfolio.cuh"

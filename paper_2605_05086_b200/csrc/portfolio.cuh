@@ -1,0 +1,302 @@
+// portfolio.cuh — (included by chap.cu: one translation unit) the multi-GPU walker portfolio: one process per GPU,
+// W_local independent walkers per GPU, and every K iterations a deterministic
+// exchange over NCCL: an allgather of per-walker summaries and of each rank's elite points, the
+// global cutoff and restarts of the most violated walkers from the global elite.
+#pragma once
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <mutex>
+
+#include "host.h"
+#include "tabu.cuh"
+
+using namespace chap;
+
+// NCCL is resolved at run time: the process's already-loaded libnccl.so.2 (the one PyTorch ships)
+// is reused, so libchap never pins a second NCCL build into a process that also runs torch.
+namespace {
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString;
+  });
+  return api;
+}
+}  // namespace
+
+struct chap_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
+
+#define NCCL_TRY(call)                                                                       \
+  do {                                                                                       \
+    if (!nccl().ok) return fail(CHAP_ERR_NCCL, "libnccl.so.2 could not be loaded");           \
+    ncclResult_t r_ = (call);                                                                \
+    if (r_ != ncclSuccess)                                                                   \
+      return fail(CHAP_ERR_NCCL, "%s: %s (%s:%d)", #call, nccl().GetErrorString(r_), __FILE__, \
+                  __LINE__);                                                                 \
+  } while (0)
+
+extern "C" chap_status chap_comm_unique_id(uint8_t id[128]) {
+  if (!id) return fail(CHAP_ERR_INVALID_ARG, "NULL id");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId u;
+  NCCL_TRY(nccl().GetUniqueId(&u));
+  memcpy(id, &u, 128);
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
+                                        chap_comm** out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(CHAP_ERR_INVALID_ARG, "bad comm arguments");
+  *out = nullptr;
+  DeviceGuard g(device);
+  if (!g.ok) return fail(CHAP_ERR_CUDA, "cannot select CUDA device %d", device);
+  auto C = new chap_comm();
+  std::unique_ptr<chap_comm> holder(C);
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  NCCL_TRY(nccl().CommInitRank(&C->comm, nranks, u, rank));
+  C->nranks = nranks;
+  C->rank = rank;
+  C->device = device;
+  *out = holder.release();
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_comm_destroy(chap_comm* comm) {
+  if (!comm) return CHAP_OK;
+  DeviceGuard g(comm->device);
+  if (comm->comm && nccl().ok) nccl().CommDestroy(comm->comm);
+  delete comm;
+  return CHAP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// the exchange rule (host)
+// ------------------------------------------------------------------------------------------
+namespace {
+struct Key {
+  double a, b;
+  int64_t c;
+  int32_t gid;
+  bool operator<(const Key& o) const {
+    if (a != o.a) return a < o.a;
+    if (b != o.b) return b < o.b;
+    if (c != o.c) return c < o.c;
+    return gid < o.gid;
+  }
+};
+Key feas_key(const chap_walker_summary& s) { return Key{s.best_obj, 0.0, 0, s.gid}; }
+Key infeas_key(const chap_walker_summary& s) { return Key{(double)s.violated, s.sumviol, 0, s.gid}; }
+}  // namespace
+
+extern "C" chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, const chap_walker_summary* s,
+                                          int32_t n_elite, int32_t n_restart, double* z_best,
+                                          int32_t* best_gid, int32_t* n_elite_out, int32_t* elite_gid,
+                                          int8_t* elite_kind, int32_t* elite_slot, int32_t* n_restart_out,
+                                          int32_t* restart_gid, int32_t* restart_src) {
+  if (W_total < 1 || W_local < 1 || W_total % W_local || !s || n_elite < 0 || n_restart < 0 || !z_best ||
+      !best_gid || !n_elite_out || !n_restart_out || (n_elite && (!elite_gid || !elite_kind || !elite_slot)) ||
+      (n_restart && (!restart_gid || !restart_src)))
+    return fail(CHAP_ERR_INVALID_ARG, "bad exchange-plan arguments");
+  for (int32_t g = 0; g < W_total; ++g)
+    if (s[g].gid != g) return fail(CHAP_ERR_INVALID_ARG, "summaries must be indexed by gid");
+  // global feasible / infeasible elites
+  std::vector<Key> F, I;
+  for (int32_t g = 0; g < W_total; ++g) {
+    if (s[g].flags & 1) F.push_back(feas_key(s[g]));
+    I.push_back(infeas_key(s[g]));
+  }
+  std::sort(F.begin(), F.end());
+  std::sort(I.begin(), I.end());
+  const int nf = std::min<int>((int)F.size(), n_elite), ni = std::min<int>((int)I.size(), n_elite);
+  *z_best = F.empty() ? INFINITY : F[0].a;
+  *best_gid = F.empty() ? -1 : F[0].gid;
+  // slot of a walker's point in the gathered buffer: its rank's local top-n_elite of the kind
+  auto slot_of = [&](int32_t g, int kind) -> int32_t {
+    const int32_t r = g / W_local;
+    std::vector<Key> loc;
+    for (int32_t q = r * W_local; q < (r + 1) * W_local; ++q) {
+      if (kind == 0 && !(s[q].flags & 1)) continue;
+      loc.push_back(kind == 0 ? feas_key(s[q]) : infeas_key(s[q]));
+    }
+    std::sort(loc.begin(), loc.end());
+    for (int32_t q = 0; q < (int32_t)loc.size() && q < n_elite; ++q)
+      if (loc[q].gid == g) return r * 2 * n_elite + kind * n_elite + q;
+    return -1;   // unreachable: a global top-n_elite member is in its rank's local top-n_elite
+  };
+  int32_t ne = 0;
+  for (int q = 0; q < nf; ++q, ++ne) {
+    elite_gid[ne] = F[q].gid;
+    elite_kind[ne] = 0;
+    elite_slot[ne] = slot_of(F[q].gid, 0);
+  }
+  for (int q = 0; q < ni; ++q, ++ne) {
+    elite_gid[ne] = I[q].gid;
+    elite_kind[ne] = 1;
+    elite_slot[ne] = slot_of(I[q].gid, 1);
+  }
+  *n_elite_out = ne;
+  // restarts: highest (violated, gid) first
+  std::vector<Key> R;
+  for (int32_t g = 0; g < W_total; ++g) R.push_back(Key{-(double)s[g].violated, 0.0, -(int64_t)g, g});
+  std::sort(R.begin(), R.end());
+  const int nr = ne > 0 ? std::min<int>(n_restart, W_total) : 0;
+  for (int q = 0; q < nr; ++q) {
+    restart_gid[q] = R[q].gid;
+    restart_src[q] = q % ne;
+  }
+  *n_restart_out = nr;
+  return CHAP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// chap_run_walkers
+// ------------------------------------------------------------------------------------------
+
+// Restart walker w from an internal-order device point: r from scratch, weights kept, tabu
+// cleared, then the R15 incumbent check (mode 1 keeps k and the counters).
+static chap_status restart_internal(chap_walkers* S, int w, const double* x_int, cudaStream_t s) {
+  const chap_problem* P = S->P;
+  const DevProblem& D = P->dp;
+  DevWalkers& Wk = S->wk;
+  CUDA_TRY(cudaMemcpyAsync(Wk.x + (size_t)w * Wk.xs, x_int, sizeof(double) * D.n, cudaMemcpyDeviceToDevice, s));
+  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk.x + (size_t)w * Wk.xs, Wk.xs, Wk.rs + (size_t)w * Wk.rss,
+                                                    Wk.rss, Wk.sc + w, 0, nullptr);
+  k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, w);
+  k_walker_finalize_init<<<1, 256, 0, s>>>(D, Wk, 1, w);
+  k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), S->W), 256, 0, s>>>(D, Wk);
+  k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, const double* x0,
+                                        const chap_params* params, chap_comm* comm, int64_t max_iters,
+                                        double time_limit_s, double* best_x, chap_result* out,
+                                        void* cuda_stream) {
+  if (!p || W_local < 1 || !x0 || !out || max_iters < 0) return fail(CHAP_ERR_INVALID_ARG, "bad arguments");
+  chap_params prm;
+  if (params) prm = *params; else chap_params_default(&prm);
+  if (prm.exchange_K < 1 || prm.n_elite < 0) return fail(CHAP_ERR_INVALID_ARG, "exchange_K < 1 or n_elite < 0");
+  if (comm && comm->device != p->device) return fail(CHAP_ERR_INVALID_ARG, "comm and problem on different devices");
+  DeviceGuard g(p->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  const int W_total = nranks * W_local;
+  const int n_restart = prm.n_restart < 0 ? W_total / 8 : prm.n_restart;
+  const int E = prm.n_elite;
+  const int n = p->dp.n;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  chap_walkers* S = nullptr;
+  TRY(chap_walkers_create(p, W_local, x0, &prm, cuda_stream, &S));
+  std::unique_ptr<chap_walkers, chap_status (*)(chap_walkers*)> hold(S, chap_walkers_destroy);
+  DeviceBuffers buf;
+  chap_walker_summary *d_sum_local, *d_sum_all;
+  double *d_send, *d_recv;
+  TRY(buf.alloc(&d_sum_local, W_local));
+  TRY(buf.alloc(&d_sum_all, W_total));
+  TRY(buf.alloc(&d_send, (size_t)2 * std::max(E, 1) * std::max(n, 1)));
+  TRY(buf.alloc(&d_recv, (size_t)nranks * 2 * std::max(E, 1) * std::max(n, 1)));
+  std::vector<chap_walker_summary> h_local(W_local), h_all(W_total);
+  std::vector<int32_t> e_gid(2 * E + 1), e_slot(2 * E + 1), r_gid(W_total + 1), r_src(W_total + 1);
+  std::vector<int8_t> e_kind(2 * E + 1);
+  const DevWalkers& Wk = S->wk;
+  int64_t iters = 0, epochs = 0;
+  double z = INFINITY;
+  int32_t zg = -1;
+  bool stop = false;
+  while (!stop) {
+    const int64_t k = std::min<int64_t>(prm.exchange_K, max_iters - iters);
+    if (k > 0) TRY(chap_tabu_step(S, (int32_t)k, nullptr, cuda_stream));
+    iters += k;
+    ++epochs;
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const bool want_stop = iters >= max_iters || (time_limit_s > 0 && el >= time_limit_s);
+    // 1. summaries -> allgather
+    k_summaries<<<W_local, 256, 0, s>>>(p->dp, Wk, d_sum_local, rank * W_local, want_stop ? 1 : 0);
+    CUDA_TRY(cudaGetLastError());
+    if (comm) {
+      NCCL_TRY(nccl().AllGather(d_sum_local, d_sum_all, sizeof(chap_walker_summary) * W_local, ncclUint8, comm->comm, s));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(d_sum_all, d_sum_local, sizeof(chap_walker_summary) * W_local, cudaMemcpyDeviceToDevice, s));
+    }
+    CUDA_TRY(cudaMemcpyAsync(h_all.data(), d_sum_all, sizeof(chap_walker_summary) * W_total, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (const auto& x : h_all) stop = stop || (x.flags & 2);
+    // 2. the plan (identical on every rank)
+    int32_t ne = 0, nr = 0;
+    TRY(chap_exchange_plan(W_total, W_local, h_all.data(), E, n_restart, &z, &zg, &ne, e_gid.data(), e_kind.data(),
+                           e_slot.data(), &nr, r_gid.data(), r_src.data()));
+    if (stop && !best_x) break;
+    // 3. local elite points into the send buffer, allgather (internal variable order: every rank
+    //    holds the same problem, hence the same permutation)
+    if (E > 0) {
+      for (int kind = 0; kind < 2; ++kind) {
+        std::vector<std::pair<Key, int>> loc;
+        for (int w = 0; w < W_local; ++w) {
+          const auto& x = h_all[rank * W_local + w];
+          if (kind == 0 && !(x.flags & 1)) continue;
+          loc.push_back({kind == 0 ? feas_key(x) : infeas_key(x), w});
+        }
+        std::sort(loc.begin(), loc.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (int q = 0; q < (int)loc.size() && q < E; ++q) {
+          const int w = loc[q].second;
+          const double* src = (kind == 0 ? Wk.best_x : Wk.x) + (size_t)w * Wk.xs;
+          CUDA_TRY(cudaMemcpyAsync(d_send + (size_t)(kind * E + q) * n, src, sizeof(double) * n,
+                                   cudaMemcpyDeviceToDevice, s));
+        }
+      }
+      if (comm) {
+        NCCL_TRY(nccl().AllGather(d_send, d_recv, (size_t)2 * E * n, ncclFloat64, comm->comm, s));
+      } else {
+        CUDA_TRY(cudaMemcpyAsync(d_recv, d_send, sizeof(double) * 2 * E * n, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    if (stop) break;
+    // 4. global cutoff, restarts of local walkers
+    if (z < INFINITY) TRY(chap_walkers_set_cutoff(S, z, cuda_stream));
+    for (int q = 0; q < nr; ++q) {
+      const int gid = r_gid[q];
+      if (gid / W_local != rank) continue;
+      TRY(restart_internal(S, gid % W_local, d_recv + (size_t)e_slot[r_src[q]] * n, s));
+    }
+  }
+  // best point: the top feasible elite member (slot of E[0] when it is feasible)
+  out->best_obj = z;
+  out->has_incumbent = zg >= 0;
+  out->best_walker = zg;
+  out->iterations = iters;
+  out->epochs = epochs;
+  if (best_x && zg >= 0 && E > 0) {
+    // E[0] is the global best incumbent; export it in user order
+    const double* src = d_recv + (size_t)e_slot[0] * n;
+    k_export_point<<<grid_for(n, 256, 4 * p->sm_count), 256, 0, s>>>(p->dp, src, best_x);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  out->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return CHAP_OK;
+}

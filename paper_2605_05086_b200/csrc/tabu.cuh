@@ -297,3 +297,43 @@ __global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs) {
 }
 
 }  // namespace chap
+
+namespace chap {
+
+// Exchange summaries (chap_walker_summary) of every walker: one block per walker, the violation
+// sum over non-cutoff rows in fixed order.
+__global__ void __launch_bounds__(256) k_summaries(DevProblem P, DevWalkers Wk, chap_walker_summary* out,
+                                                   int gid0, int stop) {
+  __shared__ double sm[32];
+  const int w = blockIdx.x, tid = threadIdx.x;
+  const RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  double s = 0.0;
+  for (int i = tid; i < P.cut_row; i += blockDim.x) {
+    const double r = rw[i].r;
+    s += r > 0.0 ? r : 0.0;
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  if ((tid & 31) == 0) sm[tid >> 5] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sm[q];
+    const WalkerScalars& sc = Wk.sc[w];
+    chap_walker_summary o;
+    o.best_obj = sc.has_inc ? sc.best_obj : INFINITY;
+    o.violated = sc.violated;
+    o.sumviol = t;
+    o.gid = gid0 + w;
+    o.flags = (sc.has_inc ? 1 : 0) | (stop ? 2 : 0);
+    out[w] = o;
+  }
+}
+
+}  // namespace chap
+
+namespace chap {
+// One internal-order point to user order.
+__global__ void k_export_point(DevProblem P, const double* xi, double* xu) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) xu[P.perm[p]] = xi[p];
+}
+}  // namespace chap

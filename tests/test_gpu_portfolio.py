@@ -1,0 +1,55 @@
+"""GPU: chap_run_walkers (the portfolio with the every-K exchange) against the
+oracle's single-process orc_run_walkers — same best objective, same best point — without a
+communicator and through a one-rank NCCL communicator (the NCCL allgather path)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_2605_05086_b200 as chap  # noqa: E402
+
+
+def _case(inst, W, K, E, ne, nr, comm=None):
+    x0s = np.stack([np.clip(synth.x_random(inst, 100 + w), inst.lb, inst.ub) for w in range(W)])
+    O = oracle.Problem.from_instance(inst)
+    ws = [oracle.TabuWalker(O, x) for x in x0s]
+    oracle.run_walkers(O, ws, K, E, ne, nr)
+    P = chap.Problem.from_instance(inst)
+    prm = chap.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8)
+    res, bx = chap.run_walkers(P, torch.from_numpy(x0s).cuda(), prm, comm, max_iters=K * E)
+    torch.cuda.synchronize()
+    inc = [w for w in ws if w.has_incumbent]
+    assert res.iterations == K * E and res.epochs == E
+    if not inc:
+        assert not res.has_incumbent
+        return
+    best = min(inc, key=lambda w: w.best_obj)
+    gid = ws.index(min(inc, key=lambda w: (w.best_obj, ws.index(w))))
+    assert res.has_incumbent and res.best_obj == best.best_obj and res.best_walker == gid
+    assert np.array_equal(bx.cpu().numpy(), ws[gid].best_x[: inst.n])
+
+
+@pytest.mark.parametrize("seed", [1, 3, 5])
+def test_run_walkers_matches_oracle_portfolio(seed):
+    _case(synth.tiny(seed), W=6, K=40, E=4, ne=2, nr=2)
+
+
+def test_run_walkers_mixed_instance():
+    inst = synth.mixed(seed=9, n=3000, m=600, n_long=2, long_lo=200, long_hi=3000)
+    _case(inst, W=4, K=25, E=3, ne=1, nr=1)
+
+
+def test_run_walkers_one_rank_nccl():
+    comm = chap.Comm(chap.comm_unique_id(), 1, 0, 0)
+    try:
+        _case(synth.tiny(2), W=6, K=40, E=4, ne=2, nr=3, comm=comm)
+    finally:
+        comm.close()
