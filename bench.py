@@ -39,6 +39,10 @@ CONFIGS = {
     "S": dict(desc="S: synthetic set cover 10k rows x 50k binaries, ~500k nnz (BASELINE.json configs[1])", walkers=1),
     "P": dict(desc="P: packing MIP 20k rows x 100k binaries, ~1M nnz, 64 walkers (BASELINE.json configs[3])",
               walkers=64),
+    # diagnostic variants of G (not BASELINE configs): same structure, one variable class only
+    "Gbin": dict(desc="diagnostic: config G structure with every short variable binary", walkers=1),
+    "Gint": dict(desc="diagnostic: config G structure with every short variable bounded integer", walkers=1),
+    "Gnl": dict(desc="diagnostic: config G without its 100 long columns", walkers=1),
 }
 
 
@@ -49,6 +53,12 @@ def make_instance(cfg: str):
         return synth.setcover()
     if cfg == "P":
         return synth.packing()
+    if cfg == "Gbin":
+        return synth.mixed(p_binary=1.0, p_bounded=0.0)
+    if cfg == "Gint":
+        return synth.mixed(p_binary=0.0, p_bounded=1.0)
+    if cfg == "Gnl":
+        return synth.mixed(n_long=0)
     raise ValueError(cfg)
 
 

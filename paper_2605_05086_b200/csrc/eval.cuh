@@ -236,10 +236,23 @@ __device__ __forceinline__ void build_heads(uint32_t* head, int nwords, int lane
   __syncwarp();
 }
 
-// packed binary columns, one warp (the only move of a binary is the flip)
+// packed binary columns, one warp (the only move of a binary is the flip).
+// Memory round trips per tile: (stream loads || column loads) -> gathers; all kWSlots slots of a
+// lane are issued together.
 __device__ __forceinline__ void wtile_bin(const DevProblem& P, const TileCtx& C, const WTile& T,
                                           int lane, WarpBin& S, Best& b) {
   const int nc = T.ncols, nnz = T.e1 - T.e0;
+  const int* __restrict__ ridx = P.row_idx + T.e0;
+  const double* __restrict__ rval = P.val + T.e0;
+  int idx[kWSlots];
+  double av[kWSlots];
+#pragma unroll
+  for (int q = 0; q < kWSlots; ++q) {
+    const int k = lane + 32 * q;
+    const bool ok = k < nnz;
+    idx[q] = ok ? __ldcs(ridx + k) : 0;
+    av[q] = ok ? __ldcs(rval + k) : 0.0;
+  }
   const int p = T.p0 + lane;
   int cb = 0, ce = 0, j = 0, tb = 0;
   double xb = 0.0;
@@ -249,41 +262,21 @@ __device__ __forceinline__ void wtile_bin(const DevProblem& P, const TileCtx& C,
     j = __ldg(P.perm + p);
     tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
     xb = __ldg(C.x + p);
-    S.xb[lane] = xb;
   }
+  double r[kWSlots], w[kWSlots];
+#pragma unroll
+  for (int q = 0; q < kWSlots; ++q) load_row(C.rs, idx[q], r[q], w[q]);
+  if (lane < nc) S.xb[lane] = xb;
   build_heads(S.head, kWSlots, lane, nc, cb);
   const unsigned le = (2u << lane) - 1u;   // lanes <= lane
   int pre = 0;                             // column starts before this slot round
-  constexpr int H = kWSlots / 2;
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    int idx[H];
-    double av[H];
 #pragma unroll
-    for (int q = 0; q < H; ++q) {
-      const int k = lane + 32 * (q + h * H);
-      idx[q] = 0;
-      av[q] = 0.0;
-      if (k < nnz) {
-        idx[q] = __ldg(P.row_idx + T.e0 + k);
-        av[q] = __ldg(P.val + T.e0 + k);
-      }
-    }
-    double r[H], w[H];
-#pragma unroll
-    for (int q = 0; q < H; ++q) load_row(C.rs, idx[q], r[q], w[q]);
-#pragma unroll
-    for (int q = 0; q < H; ++q) {
-      const int qq = q + h * H;
-      const int k = lane + 32 * qq;
-      const uint32_t hw = S.head[qq];
-      const int c = pre + __popc(hw & le) - 1;
-      pre += __popc(hw);
-      if (k < nnz) {
-        const double x = S.xb[c];
-        S.pen[k] = penalty(w[q], r[q], r[q] + av[q] * (1.0 - 2.0 * x));
-      }
-    }
+  for (int q = 0; q < kWSlots; ++q) {
+    const int k = lane + 32 * q;
+    const uint32_t hw = S.head[q];
+    const int c = pre + __popc(hw & le) - 1;
+    pre += __popc(hw);
+    if (k < nnz) S.pen[k] = penalty(w[q], r[q], r[q] + av[q] * (1.0 - 2.0 * S.xb[c]));
   }
   __syncwarp();
   if (lane < nc) {
@@ -361,8 +354,8 @@ __device__ __forceinline__ void wtile_gen(const DevProblem& P, const TileCtx& C,
       idx[q] = 0;
       av[q] = 1.0;
       if (k < nnz) {
-        idx[q] = __ldg(P.row_idx + T.e0 + k);
-        av[q] = __ldg(P.val + T.e0 + k);
+        idx[q] = __ldcs(P.row_idx + T.e0 + k);
+        av[q] = __ldcs(P.val + T.e0 + k);
       }
     }
     double r[H], w[H];
@@ -621,8 +614,8 @@ __device__ __forceinline__ void load_chunk(const DevProblem& P, const TileCtx& C
   for (int q = 0; q < kPer; ++q) {
     const int k = threadIdx.x + q * kTileThreads;
     R.ok[q] = k < nnz;
-    idx[q] = R.ok[q] ? __ldg(P.row_idx + e0 + k) : 0;
-    R.a[q] = R.ok[q] ? __ldg(P.val + e0 + k) : 1.0;
+    idx[q] = R.ok[q] ? __ldcs(P.row_idx + e0 + k) : 0;
+    R.a[q] = R.ok[q] ? __ldcs(P.val + e0 + k) : 1.0;
   }
 #pragma unroll
   for (int q = 0; q < kPer; ++q) load_row(C.rs, idx[q], R.r[q], R.w[q]);
@@ -789,8 +782,12 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned char* ws = smem + (size_t)wid * kWarpSmem;
     const int nwarps = gridDim.x * kTileWarps;
-    for (int t = blockIdx.x * kTileWarps + wid; t < P.n_wtiles; t += nwarps) {
-      const WTile T = P.wtiles[t];
+    int t = blockIdx.x * kTileWarps + wid;
+    WTile Tn;
+    if (t < P.n_wtiles) Tn = P.wtiles[t];
+    for (; t < P.n_wtiles; t += nwarps) {
+      const WTile T = Tn;
+      if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];   // next descriptor in flight
       if (T.kind == CC_BIN) wtile_bin(P, C, T, lane, *reinterpret_cast<WarpBin*>(ws), b);
       else if (T.kind == CC_GEN) wtile_gen(P, C, T, lane, *reinterpret_cast<WarpGen*>(ws), b);
       else wtile_empty(P, C, T, lane, b);

@@ -170,11 +170,12 @@ def setcover(seed: int = 1, m: int = 10_000, n: int = 50_000) -> Instance:
 # Config G (configs[2]): mixed general-integer MIP, 2e5 rows x 1e6 vars, ~1e7 nnz, 100 long columns
 # --------------------------------------------------------------------------------------
 def mixed(seed: int = 2, n: int = 1_000_000, m: int = 200_000, n_long: int = 100,
-          long_lo: float = 1e3, long_hi: float = 1e5, short_mean: float = 7.0) -> Instance:
+          long_lo: float = 1e3, long_hi: float = 1e5, short_mean: float = 7.0,
+          p_binary: float = 0.70, p_bounded: float = 0.25) -> Instance:
     rng = np.random.default_rng([0x6E, seed])
     # variable classes: 70% binary, 25% integer [0, U] with U log-uniform{2..1000}, 5% integer [0, inf)
     u = rng.random(n)
-    vclass = np.where(u < 0.70, 0, np.where(u < 0.95, 1, 2))
+    vclass = np.where(u < p_binary, 0, np.where(u < p_binary + p_bounded, 1, 2))
     U = np.floor(np.exp(rng.uniform(np.log(2), np.log(1001), n)))
     lb = np.zeros(n)
     ub = np.where(vclass == 0, 1.0, np.where(vclass == 1, U, INF))
