@@ -78,10 +78,10 @@ typedef struct {
                                  static per-variable data (1 B binary, 17 B other), walker state
                                  per variable (x̄: 1 bit binary / 8 B other; 4 B tabu expiry) and
                                  12 B per normalised row (r f64 + w f32), each read once (§6)  */
-  int64_t model_bytes_kernel[3]; /* the same model split by tile kind of the eval kernel:
-                                 [0] packed tiles (incl. the 12 B/row row state), [1] single-
-                                 column sort tiles, [2] chunked long columns                   */
-  int64_t nnz_kernel[3];      /* nonzeros (incl. cutoff entries) in each tile kind             */
+  int64_t model_bytes_kernel[3]; /* the same model split by eval kernel: [0] k_eval_bin (packed
+                                 binary columns), [1] k_eval (every other column, incl. the
+                                 12 B/row row state), [2] unused (0)                          */
+  int64_t nnz_kernel[3];      /* nonzeros (incl. cutoff entries) evaluated by each kernel      */
 } chap_problem_info;
 
 /* Build a problem from HOST CSR data (copied; the caller may free its arrays on return).
@@ -226,9 +226,9 @@ chap_status chap_walkers_destroy(chap_walkers* ws);
 
 /* Diagnostic timing: n_iters tabu iterations (identical semantics to chap_tabu_step, no log)
  * with plain launches and a CUDA-event pair around every launch on the walkers' stream;
- * ms_per_iter HOST [5] receives the average device time per iteration of [0] the eval kernel
- * (best shift of every variable + the fused global select), [1]-[3] reserved (0), [4] the
- * apply kernel. Synchronises. */
+ * ms_per_iter HOST [5] receives the average device time per iteration of [0] k_eval_bin (packed
+ * binary columns), [1] k_eval (every other column + the fused global select), [2]-[3] reserved
+ * (0), [4] the apply kernel. Synchronises. */
 chap_status chap_walkers_profile(chap_walkers* ws, int32_t n_iters, double* ms_per_iter,
                                  void* cuda_stream);
 

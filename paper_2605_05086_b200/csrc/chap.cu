@@ -208,22 +208,47 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
                   "multi-block merge sort, not in this build)", j, d, l[j], u[j]);
     }
   }
-  // internal order: by (class, degree, user index) — heavy tiles first, similar degrees together
+  // internal order: fixed columns, then packed binary columns (so that the binary CSC region starts
+  // 16-byte aligned), then the other classes; within a class by degree, then user index
+  auto order = [](int k) { return k == CC_FIXED ? 0 : (k == CC_BIN ? 1 : 2 + k); };
   std::vector<int32_t> perm(n);
   std::iota(perm.begin(), perm.end(), 0);
   std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
-    if (cls[a] != cls[b]) return cls[a] < cls[b];
+    if (order(cls[a]) != order(cls[b])) return order(cls[a]) < order(cls[b]);
     return deg[a] > deg[b];
   });
   std::vector<int32_t> iperm(n);
   for (int32_t p = 0; p < n; ++p) iperm[perm[p]] = p;
+  // binary tiles (whole columns, <= kBinTile - 3 real nonzeros) and the inert padding that makes
+  // every binary tile start and end on a multiple of 4 nonzeros (TMA bulk copies need 16 B)
+  std::vector<int32_t> pad(n, 0);
+  std::vector<std::pair<int32_t, int32_t>> bin_ranges;   // [p0, p1)
+  {
+    int32_t p = 0, off = 0;
+    while (p < n && cls[perm[p]] == CC_FIXED) off += deg[perm[p++]];
+    if (p > 0 && (off & 3)) { pad[p - 1] = (4 - (off & 3)) & 3; }
+    while (p < n && cls[perm[p]] == CC_BIN) {
+      int cnt = 0, tot = 0;
+      while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == CC_BIN &&
+             tot + deg[perm[p + cnt]] <= kBinTile - 3) {
+        tot += deg[perm[p + cnt]];
+        ++cnt;
+      }
+      pad[p + cnt - 1] = (4 - (tot & 3)) & 3;
+      bin_ranges.push_back({p, p + cnt});
+      p += cnt;
+    }
+  }
+  int64_t npad = 0;
+  for (int32_t q = 0; q < n; ++q) npad += pad[q];
+  const int32_t dummy_row = m_norm;   // inert row state (r = -inf, w = 0) for padding entries
 
-  // CSC in internal order; rows ascending within a column, cutoff entry last
+  // CSC in internal order; rows ascending within a column, then the cutoff entry, then padding
   std::vector<int32_t> col_ptr(n + 1, 0);
-  for (int32_t p = 0; p < n; ++p) col_ptr[p + 1] = col_ptr[p] + deg[perm[p]];
+  for (int32_t p = 0; p < n; ++p) col_ptr[p + 1] = col_ptr[p] + deg[perm[p]] + pad[p];
   std::vector<int32_t> fill(col_ptr.begin(), col_ptr.end() - 1);
-  std::vector<int32_t> row_idx(nnz_total);
-  std::vector<double> cval(nnz_total);
+  std::vector<int32_t> row_idx(nnz_total + npad + 4, dummy_row);
+  std::vector<double> cval(nnz_total + npad + 4, 1.0);
   for (int32_t i = 0; i < mr; ++i)
     for (int64_t e = nrow_ptr[i]; e < nrow_ptr[i + 1]; ++e) {
       const int32_t p = iperm[ncol[e]];
@@ -271,15 +296,24 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   // tiles (PAPER.md:353-355 length dispatch): block tiles — chunks of long columns, single-column
   // sorts — and warp tiles of packed short columns
   std::vector<Tile> tiles;
-  std::vector<WTile> wtiles;
+  std::vector<WTile> wtiles, btiles;
+  for (const auto& r : bin_ranges) {
+    WTile W{};
+    W.p0 = r.first;
+    W.e0 = col_ptr[r.first];
+    W.e1 = col_ptr[r.second];   // includes the padding (a multiple of 4 nonzeros)
+    W.ncols = (int16_t)(r.second - r.first);
+    W.kind = (int8_t)CC_BIN;
+    btiles.push_back(W);
+  }
   int32_t n_long = 0;
   int64_t lscr = 0;
   int32_t p = 0;
   while (p < n) {
     const int32_t j = perm[p];
     const int k = cls[j];
-    if (k == CC_FIXED) { ++p; continue; }
-    if (k == CC_BIN || k == CC_GEN || k == CC_EMPTY) {
+    if (k == CC_FIXED || k == CC_BIN) { ++p; continue; }
+    if (k == CC_GEN || k == CC_EMPTY) {
       const int extra = (k == CC_GEN) ? 2 : 0;
       const int cap = (k == CC_GEN) ? kWTileGen : kWTileNnz;
       int cnt = 0, tot = 0;
@@ -313,7 +347,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       continue;
     }
     // chunked: CC_LBIN, CC_LBKT
-    const int d = deg[j];
+    const int d = col_ptr[p + 1] - col_ptr[p];   // incl. any padding (inert)
     const int nch = std::max(1, (d + kTileNnz - 1) / kTileNnz);
     const int dom = (k == CC_LBKT) ? (int)(u[j] - l[j] + 1.0) : 0;
     T.nchunks = nch;
@@ -338,13 +372,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       const int32_t j = perm[q];
       const int k = cls[j];
       if (k == CC_FIXED) continue;
-      const int kk = (k == CC_GENM) ? 1 : (k == CC_LBIN || k == CC_LBKT) ? 2 : 0;   // CC_EMPTY: packed
+      const int kk = (k == CC_BIN) ? 0 : 1;   // [0] k_eval_bin, [1] k_eval
       const bool bin = vclass[j] == 1;
       const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
       mb[kk] += 12LL * deg[j] + (int64_t)std::llround(per_var * 8) / 8;
       nz[kk] += deg[j];
     }
-    mb[0] += 12LL * m_norm;
+    mb[1] += 12LL * m_norm;
     for (int q = 0; q < 3; ++q) { I.model_bytes_kernel[q] = mb[q]; I.nnz_kernel[q] = nz[q]; }
     I.model_bytes_pass = mb[0] + mb[1] + mb[2];
   }
@@ -357,6 +391,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   uint8_t* d_vc;
   Tile* d_tiles;
   WTile* d_wtiles;
+  WTile* d_btiles;
   TRY(B.upload(&d_col_ptr, col_ptr));
   TRY(B.upload(&d_row_idx, row_idx));
   TRY(B.upload(&d_val, cval));
@@ -371,10 +406,12 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_perm, perm));
   TRY(B.upload(&d_tiles, tiles));
   TRY(B.upload(&d_wtiles, wtiles));
+  TRY(B.upload(&d_btiles, btiles));
   DevProblem& D = P->dp;
   D.n = n;
   D.m_norm = m_norm;
   D.cut_row = cut_row;
+  D.dummy_row = dummy_row;
   D.col_ptr = d_col_ptr;
   D.row_idx = d_row_idx;
   D.val = d_val;
@@ -391,6 +428,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.n_tiles = (int32_t)tiles.size();
   D.wtiles = d_wtiles;
   D.n_wtiles = (int32_t)wtiles.size();
+  D.btiles = d_btiles;
+  D.n_btiles = (int32_t)btiles.size();
   D.n_long = n_long;
   D.n_fixed = I.n_fixed;
   D.auto_delta = I.auto_cutoff_delta;
@@ -402,14 +441,20 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   P->eval_occ = std::max(1, occ);
   const int work_blocks = std::max(D.n_tiles, (D.n_wtiles + kTileWarps - 1) / kTileWarps);
   P->eval_grid = std::max(1, std::min(work_blocks, P->eval_occ * P->sm_count));
+  CUDA_TRY(cudaFuncSetAttribute(k_eval_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem));
+  int bocc = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_eval_bin, kBinThreads, kBinSmem));
+  P->bin_occ = std::max(1, bocc);
+  const int bwarps = kBinThreads / 32;
+  P->bin_grid = D.n_btiles ? std::max(1, std::min((D.n_btiles + bwarps - 1) / bwarps, P->bin_occ * P->sm_count)) : 0;
   P->rows_grid = std::max(1, std::min((m_norm + 7) / 8, 8 * P->sm_count));
   // eval workspace
   TRY(B.alloc(&P->e_x, n));
-  TRY(B.alloc(&P->e_rs, m_norm));
+  TRY(B.alloc(&P->e_rs, (size_t)m_norm + 1));
   TRY(B.alloc(&P->e_tabu, n));
   TRY(B.alloc(&P->e_bx, n));
   TRY(B.alloc(&P->e_sc, 1));
-  TRY(B.alloc(&P->e_part, P->eval_grid));
+  TRY(B.alloc(&P->e_part, P->eval_grid + P->bin_grid));
   TRY(B.alloc(&P->e_selcnt, 1));
   CUDA_TRY(cudaMemset(P->e_selcnt, 0, sizeof(unsigned)));
   TRY(B.alloc(&P->e_lcount, std::max(n_long, 1)));
@@ -448,9 +493,10 @@ extern "C" chap_status chap_problem_destroy(chap_problem* p) {
 // ------------------------------------------------------------------------------------------
 // eval launches (shared by the eval API and the tabu step)
 // ------------------------------------------------------------------------------------------
-chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, double* oxhat,
-                              double* oscore, chap_move* best, cudaStream_t s) {
-  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best);
+chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid,
+                              double* oxhat, double* oscore, chap_move* best, cudaStream_t s) {
+  if (bgrid > 0) k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
+  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -460,13 +506,13 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.x = P->e_x;
   Wk.xs = (size_t)P->dp.n;
   Wk.rs = P->e_rs;
-  Wk.rss = (size_t)P->dp.m_norm;
+  Wk.rss = (size_t)P->dp.m_norm + 1;
   Wk.tabu = P->e_tabu;
   Wk.ts = (size_t)P->dp.n;
   Wk.best_x = P->e_bx;
   Wk.sc = P->e_sc;
   Wk.part = P->e_part;
-  Wk.ps = P->eval_grid;
+  Wk.ps = P->eval_grid + P->bin_grid;
   Wk.sel_count = P->e_selcnt;
   Wk.lcount = P->e_lcount;
   Wk.lcs = std::max(P->dp.n_long, 1);
@@ -500,7 +546,7 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, xhat, score, best, s));
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, xhat, score, best, s));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -584,12 +630,13 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   DevWalkers& Wk = S->wk;
   DeviceBuffers& B = S->buf;
   TRY(B.alloc(&Wk.x, n * W));
-  TRY(B.alloc(&Wk.rs, mn * W));
+  TRY(B.alloc(&Wk.rs, (mn + 1) * W));
   TRY(B.alloc(&Wk.tabu, n * W));
   TRY(B.alloc(&Wk.best_x, n * W));
   TRY(B.alloc(&Wk.sc, W));
   S->eval_grid = std::max(1, std::min(p->eval_grid, (p->eval_occ * p->sm_count + W - 1) / W));
-  Wk.ps = S->eval_grid;
+  S->bin_grid = p->bin_grid ? std::max(1, std::min(p->bin_grid, (p->bin_occ * p->sm_count + W - 1) / W)) : 0;
+  Wk.ps = S->eval_grid + S->bin_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
   TRY(B.alloc(&Wk.sel_count, W));
   Wk.lcs = std::max(D.n_long, 1);
@@ -598,7 +645,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   TRY(B.alloc(&Wk.lscr, Wk.lss * W));
   TRY(B.alloc(&S->d_bad, 1));
   Wk.xs = n;
-  Wk.rss = mn;
+  Wk.rss = mn + 1;
   Wk.ts = n;
   Wk.use_tabu = 1;
   Wk.W = W;
@@ -634,7 +681,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
-  TRY(launch_eval(P, S->wk, S->eval_grid, nullptr, nullptr, nullptr, s));
+  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, nullptr, nullptr, nullptr, s));
   k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -742,8 +789,13 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
   for (int it = 0; it < n_iters; ++it) {
     cudaEvent_t* e = &ev[10 * (size_t)it];
     for (int q = 0; q < 8; ++q) cudaEventRecord(e[q], s);
-    k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr);
+    if (S->bin_grid > 0)
+      k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(D, S->wk, nullptr, nullptr);
     cudaEventRecord(e[1], s);
+    cudaEventRecord(e[2], s);
+    k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
+                                                                     S->bin_grid);
+    cudaEventRecord(e[3], s);
     cudaEventRecord(e[8], s);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
     cudaEventRecord(e[9], s);
@@ -760,7 +812,7 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
       ms[q] += t;
     }
   for (int q = 0; q < 5; ++q) ms[q] /= n_iters;
-  ms[1] = ms[2] = ms[3] = 0.0;   // one fused eval+select kernel
+  ms[2] = ms[3] = 0.0;           // [0] k_eval_bin, [1] k_eval (+ fused select)
   for (auto& e : ev) cudaEventDestroy(e);
   CUDA_TRY(cudaEventRecord(S->ev_out, s));
   CUDA_TRY(cudaStreamWaitEvent(us, S->ev_out, 0));
@@ -775,3 +827,14 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 }
 
 #include "portfolio.cuh"
+
+#ifdef CHAP_TIMING
+extern "C" chap_status chap_debug_counters(unsigned long long* out, int reset) {
+  CUDA_TRY(cudaMemcpyFromSymbol(out, chap::g_dbg, sizeof(unsigned long long) * 8));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    CUDA_TRY(cudaMemcpyToSymbol(chap::g_dbg, z, sizeof(z)));
+  }
+  return CHAP_OK;
+}
+#endif

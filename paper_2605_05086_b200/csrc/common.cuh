@@ -21,6 +21,9 @@ constexpr int kWSlotsGen = 8;                     // slots per lane of a general
 constexpr int kWTileGen = 32 * kWSlotsGen;        // Alg. 1 elements per general warp tile
 constexpr int kWTileCols = 32;                    // columns per warp tile (one lane each)
 constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kBinSlots = 4;                      // slots per lane of a pipelined binary tile
+constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per pipelined binary tile
+constexpr int kBinThreads = 256;                  // k_eval_bin block
 constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
 constexpr int kBucketMax = 4096;                  // max integer domain of a bucket-scanned column
 constexpr int kApplyThreads = 256;
@@ -109,6 +112,7 @@ struct WalkerScalars {
 // Everything the kernels need about the immutable problem (internal variable order).
 struct DevProblem {
   int32_t n, m_norm, cut_row;
+  int32_t dummy_row;         // = m_norm: the inert row (r = -inf, w = 0) of padding entries
   const int32_t* col_ptr;    // [n+1] CSC over normalised rows incl. the cutoff row (last entry)
   const int32_t* row_idx;    // [nnz_total]
   const double* val;         // [nnz_total]
@@ -122,7 +126,8 @@ struct DevProblem {
   const uint8_t* vclass;     // [n] 0 fixed 1 binary 2 integer 3 continuous
   const int32_t* perm;       // internal p -> user j
   const Tile* tiles; int32_t n_tiles; int32_t n_long;   // block tiles
-  const WTile* wtiles; int32_t n_wtiles;                // warp tiles
+  const WTile* wtiles; int32_t n_wtiles;                // warp tiles (general, empty)
+  const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   double auto_delta;
 };

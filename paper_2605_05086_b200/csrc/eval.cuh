@@ -188,14 +188,21 @@ struct WarpBin {                       // CC_BIN warp tile
   uint32_t head[kWTileNnz / 32];       // bit k: slot k starts a column
 };
 struct WarpGen {                       // CC_GEN warp tile: row entries at slots [0, nnz); the
-  double t[kWTileGen];                 // bound entries of column c at slots nnz + 2c, nnz + 2c + 1
-  double2 L[kWTileGen];                // per column c, region [cb + 2c, ...): (key, δ) of the
-                                       // column's in-range entries (see wtile_gen)
-  float w[kWTileGen];
+  double key[kWTileGen];               // bound entries of column c at slots nnz + 2c, nnz + 2c + 1
+  double D[kWTileGen];                 // entry delta (0 for bound / dropped entries)
+  union {
+    float2 AB[kWTileGen];              // phases 1-2: the entry's contributions to β and α
+    double sig[kWTileGen];             // phases 3-4: sigma of candidate slots
+  };
   uint8_t f[kWTileGen];                // GF_* flags
+  uint8_t seg[kWTileGen];              // column of a row slot
   double xb[kWTileCols];
   double l[kWTileCols];
   double u[kWTileCols];
+  double beta[kWTileCols];
+  double alpha[kWTileCols];
+  int32_t cb[kWTileCols];
+  int32_t ce[kWTileCols];
   uint32_t head[kWTileGen / 32];
   uint8_t cont[kWTileCols];            // continuous column
 };
@@ -312,35 +319,40 @@ __device__ __forceinline__ void gf_coeffs(uint8_t f, double w, double& D, double
 // Packed general columns, one warp: Algorithm 1 per column, sort-free.
 // For a candidate value v the score Algorithm 1 reports (the largest sigma of the entries at v,
 // R3) is sigma(v) = β + Σ_{entries e: t_e < v, or t_e = v with marker -1} δ_e + α [v > x̄]
-// (DESIGN §2.3). Entries with t < l are in every such sum and fold into β; entries with t > u
-// are in none and drop. A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an entry
-// with δ = 0 adds nothing, so "marker -1" is δ > 0. For integer columns the test becomes one
-// compare of key_e = 2 t_e + [δ_e < 0] with 2 v. Phases: (1) slots in parallel: coalesced
-// loads, row-state gathers, lines 3-4 and the case of lines 5-11; (2) lane c, column c: β, α,
-// the in-range list, then sigma of every candidate (lines 13-15) and the argmax of line 16.
+// (DESIGN §2.3). A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an entry with
+// δ = 0 adds nothing, so "marker -1" is δ > 0; for integer columns the condition is the single
+// compare key_e <= 2v with key_e = 2 t_e + [δ_e < 0] (exact while |t| < 2^51); continuous columns
+// compare (t, δ > 0) directly. Phases:
+//  (1) slots in parallel: coalesced CSC loads and row-state gathers issued together, then lines
+//      3-11 per entry: t, the emission case, δ, the β/α contributions and the key;
+//  (2) lane c: β and α of column c (lines 1-12 accumulators, fixed order);
+//  (3) candidate slots in parallel: sigma by a compare-add pass over the column's entries
+//      (lines 13-15: the sort and scan, done as direct prefix sums);
+//  (4) lane c: the argmax of line 16 with the R4 tie-break.
 __device__ __forceinline__ void wtile_gen(const DevProblem& P, const TileCtx& C, const WTile& T,
                                           int lane, WarpGen& S, Best& b) {
   const int nc = T.ncols, nnz = T.e1 - T.e0;
   const int nel = nnz + 2 * nc;
+  const int* __restrict__ ridx = P.row_idx + T.e0;
+  const double* __restrict__ rval = P.val + T.e0;
   const int p = T.p0 + lane;
   int cb = 0, ce = 0, j = 0, tb = 0;
-  double xb = 0.0, l = 0.0, u = 0.0;
-  bool cont = false;
+  double xb = 0.0;
   if (lane < nc) {
     cb = __ldg(P.col_ptr + p) - T.e0;
     ce = __ldg(P.col_ptr + p + 1) - T.e0;
     j = __ldg(P.perm + p);
     tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
     xb = __ldg(C.x + p);
-    l = __ldg(P.lb + p);
-    u = __ldg(P.ub + p);
-    cont = __ldg(P.vclass + p) == 3;
     S.xb[lane] = xb;
-    S.l[lane] = l;
-    S.u[lane] = u;
-    S.cont[lane] = cont;
+    S.l[lane] = __ldg(P.lb + p);
+    S.u[lane] = __ldg(P.ub + p);
+    S.cont[lane] = __ldg(P.vclass + p) == 3;
+    S.cb[lane] = cb;
+    S.ce[lane] = ce;
   }
   build_heads(S.head, kWSlotsGen, lane, nc, cb);
+  // (1) lines 3-11, in two halves of kWSlotsGen/2 loads + gathers in flight
   const unsigned le = (2u << lane) - 1u;
   int pre = 0;
   constexpr int H = kWSlotsGen / 2;
@@ -351,12 +363,9 @@ __device__ __forceinline__ void wtile_gen(const DevProblem& P, const TileCtx& C,
 #pragma unroll
     for (int q = 0; q < H; ++q) {
       const int k = lane + 32 * (q + h * H);
-      idx[q] = 0;
-      av[q] = 1.0;
-      if (k < nnz) {
-        idx[q] = __ldcs(P.row_idx + T.e0 + k);
-        av[q] = __ldcs(P.val + T.e0 + k);
-      }
+      const bool ok = k < nnz;
+      idx[q] = ok ? __ldcs(ridx + k) : 0;
+      av[q] = ok ? __ldcs(rval + k) : 1.0;
     }
     double r[H], w[H];
 #pragma unroll
@@ -369,66 +378,84 @@ __device__ __forceinline__ void wtile_gen(const DevProblem& P, const TileCtx& C,
       const int cr = pre + __popc(hw & le) - 1;
       pre += __popc(hw);
       if (k >= nel) continue;
-      double t = 0.0;
+      double key = 0.0, D = 0.0;
+      float A = 0.f, B = 0.f;
       uint8_t f = 0;
       if (k < nnz) {
         const int c = cr;
         const double x = S.xb[c];
-        t = breakpoint(x, r[q], av[q]);                             // line 3
-        if (!S.cont[c]) t = (av[q] > 0.0) ? floor(t) : ceil(t);    // line 4
-        f = GF_ROW | (av[q] > 0.0 ? GF_POS : 0) | (x < t ? GF_LT : 0) | (x > t ? GF_GT : 0);
-        if (x != t && t >= S.l[c] && t <= S.u[c]) f |= GF_CAND;
-        if (!isfinite(r[q])) f = 0;                                 // inert inactive cutoff row
+        const bool cont = S.cont[c];
+        double t = breakpoint(x, r[q], av[q]);                     // line 3
+        if (!cont) t = (av[q] > 0.0) ? floor(t) : ceil(t);         // line 4
+        const bool pos = av[q] > 0.0, lt = x < t, gt = x > t;      // lines 5-11
+        const double wq = w[q], hw2 = 0.5 * wq;
+        D = pos ? (gt ? -hw2 : (lt ? -wq : 0.0)) : (lt ? hw2 : (gt ? wq : 0.0));
+        A = (float)(pos ? (gt ? wq : 0.0) : (lt ? -hw2 : -wq));
+        B = (float)(pos ? (lt ? 0.0 : -wq) : (gt ? 0.0 : wq));
+        key = cont ? t : 2.0 * t + (D < 0.0 ? 1.0 : 0.0);
+        if (x != t && t >= S.l[c] && t <= S.u[c]) f = GF_CAND;
+        if (!isfinite(r[q])) { D = 0.0; A = B = 0.f; f = 0; }     // inert inactive cutoff row
+        S.seg[k] = (uint8_t)c;
+        S.AB[k] = make_float2(A, B);
       } else {
         const int c = (k - nnz) >> 1;
         const double v = ((k - nnz) & 1) ? S.u[c] : S.l[c];
-        t = v;
+        key = S.cont[c] ? v : 2.0 * v;                             // the candidate value, encoded
         if (isfinite(v) && v != S.xb[c]) f = GF_CAND;
       }
-      S.t[k] = t;
-      S.w[k] = (float)w[q];
+      S.key[k] = key;
+      S.D[k] = D;
       S.f[k] = f;
     }
   }
   __syncwarp();
+  // (2) β, α of column `lane`
   if (lane < nc) {
-    const int base = cb + 2 * lane;
     double beta = 0.0, alpha = 0.0;
-    int m = 0;
     for (int e = cb; e < ce; ++e) {
-      const uint8_t f = S.f[e];
-      const double t = S.t[e];
-      double D, A, B;
-      gf_coeffs(f, (double)S.w[e], D, A, B);
-      beta += A;
-      alpha += B;
-      if (t < l) {
-        beta += D;                       // in every candidate's prefix
-      } else if (t <= u && D != 0.0) {
-        // integer columns: key 2t + [+1 marker] (exact, |t| < 2^51); continuous: t, marker by sign
-        S.L[base + m] = make_double2(cont ? t : 2.0 * t + (D < 0.0 ? 1.0 : 0.0), D);
-        ++m;
+      const float2 ab = S.AB[e];
+      beta += (double)ab.x;
+      alpha += (double)ab.y;
+    }
+    S.beta[lane] = beta;
+    S.alpha[lane] = alpha;
+  }
+  __syncwarp();
+  // (3) sigma of every candidate slot
+#pragma unroll 1
+  for (int q = 0; q < kWSlotsGen; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= nel || !(S.f[k] & GF_CAND)) continue;
+    const int c = (k < nnz) ? S.seg[k] : ((k - nnz) >> 1);
+    const bool cont = S.cont[c];
+    const double kv = S.key[k];
+    // the candidate's value and its "minus" key 2v
+    const double v = cont ? kv : floor(0.5 * kv);
+    const double km = cont ? kv : 2.0 * v;
+    const int e0 = S.cb[c], e1 = S.ce[c];
+    double acc = S.beta[c] + (v > S.xb[c] ? S.alpha[c] : 0.0);
+    if (!cont) {
+      for (int e = e0; e < e1; ++e) acc += (S.key[e] <= km) ? S.D[e] : 0.0;
+    } else {
+      for (int e = e0; e < e1; ++e) {
+        const double te = S.key[e], de = S.D[e];
+        acc += (te < v || (te == v && de > 0.0)) ? de : 0.0;
       }
     }
+    S.sig[k] = acc;
+  }
+  __syncwarp();
+  // (4) argmax per column (R3, R4)
+  if (lane < nc) {
+    const bool cont = S.cont[lane];
     double bs = -INFINITY, bv = xb;
     for (int e = cb; e < ce + 2; ++e) {
       const int k = (e < ce) ? e : nnz + 2 * lane + (e - ce);
       if (!(S.f[k] & GF_CAND)) continue;
-      const double v = S.t[k];
-      double acc = beta + (v > xb ? alpha : 0.0);
-      if (!cont) {
-        const double kv = 2.0 * v;
-        for (int q = 0; q < m; ++q) {
-          const double2 L = S.L[base + q];
-          acc += (L.x <= kv) ? L.y : 0.0;
-        }
-      } else {
-        for (int q = 0; q < m; ++q) {
-          const double2 L = S.L[base + q];
-          acc += (L.x < v || (L.x == v && L.y > 0.0)) ? L.y : 0.0;
-        }
-      }
-      if (better_shift(acc, v, bs, bv, xb)) { bs = acc; bv = v; }
+      const double kv = S.key[k];
+      const double v = cont ? kv : floor(0.5 * kv);
+      const double sg = S.sig[k];
+      if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
     }
     finish_column_j(p, j, tb, xb, bv, bs, b, C.oxhat, C.oscore, C.k, C.use_tabu);
   }
@@ -750,7 +777,8 @@ __device__ __forceinline__ void tile_lbkt(const DevProblem& P, const DevWalkers&
 // grid = (blocks per walker, W). After its tiles every block publishes its best admissible move;
 // the last block of the walker reduces them (fixed order) to the decision.
 __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalkers Wk, double* oxhat,
-                                                          double* oscore, chap_move* best_out) {
+                                                          double* oscore, chap_move* best_out,
+                                                          int part_base) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double sm_red[32];
   __shared__ Best sm_b[32];
@@ -796,11 +824,11 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   // publish the block's best; the last block of this walker selects (R6)
   b = block_reduce_best(b, sm_b);
   Cand* part = Wk.part + (size_t)walker * Wk.ps;
-  if (threadIdx.x == 0) write_part(part + blockIdx.x, b);
+  if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
   Best g;
   g.init();
-  for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+  for (int q = threadIdx.x; q < part_base + (int)gridDim.x; q += blockDim.x) {
     Best o;
     o.s = __ldcg(&part[q].s);
     o.v = __ldcg(&part[q].v);
@@ -831,6 +859,95 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
     }
     Wk.sel_count[walker] = 0u;
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// binary kernel
+// ------------------------------------------------------------------------------------------
+// k_eval_bin evaluates the packed binary columns (flip scores). It is built like a
+// plain gather loop so that many warps per SM keep their loads in flight: per warp tile (whole
+// columns, <= kBinTile nonzeros, <= 32 columns, starting on a multiple of 4 nonzeros) every lane
+// issues its coalesced CSC loads and its 16-byte row-state gathers back to back; the column of a
+// slot comes from a redux.sync head mask, x̄ of the column from a shuffle; lane c sums column c.
+struct __align__(16) BinWarp {
+  double pen[kBinTile];
+};
+constexpr size_t kBinSmem = sizeof(BinWarp) * (kBinThreads / 32);
+
+__global__ void __launch_bounds__(kBinThreads, 6) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
+                                                              double* oscore) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Best sm_b[32];
+  const int walker = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const WalkerScalars* sc = Wk.sc + walker;
+  const double* __restrict__ X = Wk.x + (size_t)walker * Wk.xs;
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)walker * Wk.rss);
+  const int32_t* __restrict__ TB = Wk.tabu + (size_t)walker * Wk.ts;
+  const long long kk = sc->k;
+  const int use_tabu = Wk.use_tabu;
+  double* pen = reinterpret_cast<BinWarp*>(smem)[wid].pen;
+  Best b;
+  b.init();
+  const int nwarps = gridDim.x * (kBinThreads / 32);
+  int t = blockIdx.x * (kBinThreads / 32) + wid;
+  WTile Tn;
+  if (t < P.n_btiles) Tn = P.btiles[t];
+  const unsigned le = (2u << lane) - 1u;
+  for (; t < P.n_btiles; t += nwarps) {
+    const WTile T = Tn;
+    if (t + nwarps < P.n_btiles) Tn = P.btiles[t + nwarps];
+    const int nc = T.ncols, len = T.e1 - T.e0;
+    const int* __restrict__ ridx = P.row_idx + T.e0;
+    const double* __restrict__ rval = P.val + T.e0;
+    // column data of lane c (issued before the slot loads are consumed)
+    const int p = T.p0 + lane;
+    int cb = 0x7fffffff, ce = 0, j = 0, tb = 0;
+    double xb = 0.0;
+    if (lane < nc) {
+      cb = __ldg(P.col_ptr + p) - T.e0;
+      ce = __ldg(P.col_ptr + p + 1) - T.e0;
+      j = __ldg(P.perm + p);
+      tb = use_tabu ? __ldg(TB + p) : 0;
+      xb = __ldg(X + p);
+    }
+#pragma unroll
+    for (int h = 0; h < kBinSlots / 2; ++h) {
+      int id[2];
+      double av[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int k = lane + 32 * (2 * h + q);
+        id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
+        av[q] = k < len ? __ldcs(rval + k) : 0.0;
+      }
+      double2 rv[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) rv[q] = __ldg(RS + id[q]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int qq = 2 * h + q;
+        const int k = lane + 32 * qq;
+        // column of slot k: column starts in rounds < qq plus those at or before this lane
+        const unsigned hm = __reduce_or_sync(kFull, (cb >> 5) == qq ? (1u << (cb & 31)) : 0u);
+        const unsigned before = __reduce_add_sync(kFull, (cb >> 5) < qq ? 1u : 0u);
+        int col = (int)before + __popc(hm & le) - 1;
+        col = col < 0 ? 0 : col;
+        const double x = __shfl_sync(kFull, xb, col);
+        const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
+        if (k < len) pen[k] = penalty(w, r, r + av[q] * (1.0 - 2.0 * x));
+      }
+    }
+    __syncwarp();
+    if (lane < nc) {
+      double s = 0.0;
+      for (int e = cb; e < ce; ++e) s += pen[e];
+      finish_column_j(p, j, tb, xb, 1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
+    }
+    __syncwarp();
+  }
+  b = block_reduce_best(b, sm_b);
+  if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + blockIdx.x, b);
 }
 
 // Outputs of fixed variables (internal [0, n_fixed)): (x̄, -inf) (R2 leaves no candidate).

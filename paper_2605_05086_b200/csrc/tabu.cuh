@@ -32,6 +32,13 @@ __global__ void k_rows_init(DevProblem P, const double* __restrict__ x, size_t x
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const double* xw = x + (size_t)w * xs;
   RowState* rw = rs + (size_t)w * rss;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    RowState d;
+    d.r = -INFINITY;
+    d.w = 0.0f;
+    d.pad = 0;
+    rw[P.dummy_row] = d;   // inert padding row
+  }
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < P.m_norm; i += nwarps) {
     const int e0 = P.rp[i], e1 = P.rp[i + 1];
     double y = 0.0;
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     const int e0 = P.col_ptr[d.p], e1 = P.col_ptr[d.p + 1];
     for (int e = e0 + gtid; e < e1; e += gstride) {
       const int i = P.row_idx[e];
-      if (i == P.cut_row && !cut_active) continue;
+      if ((i == P.cut_row && !cut_active) || i == P.dummy_row) continue;
       const double r0 = rw[i].r;
       const double r1 = r0 + P.val[e] * d.delta;
       rw[i].r = r1;
