@@ -68,7 +68,8 @@ typedef struct {
   int32_t n_fixed, n_binary, n_integer, n_continuous;   /* variable classes after rounding    */
   int32_t exact_integer_data; /* 1: A, lhs, rhs, l, u, c integral, |a| <= 1e6, all variables
                                  integer -> scores and trajectories are bit-exact */
-  int32_t n_long_columns;     /* columns evaluated by the multi-block (chunked) path           */
+  int32_t n_long_columns;     /* columns evaluated in warp chunks (long binary, long bounded
+                                 integer), merged by atomics + a last-chunk ticket            */
   double auto_cutoff_delta;   /* 1 if every c_j != 0 is integral on an integer variable, else
                                  NaN (= 1e-6 max(1,|z|) when the cutoff is set) (R14)         */
   int64_t device_bytes;       /* device memory held by the problem                            */
@@ -78,10 +79,14 @@ typedef struct {
                                  static per-variable data (1 B binary, 17 B other), walker state
                                  per variable (x̄: 1 bit binary / 8 B other; 4 B tabu expiry) and
                                  12 B per normalised row (r f64 + w f32), each read once (§6)  */
-  int64_t model_bytes_kernel[3]; /* the same model split by eval kernel: [0] k_eval_bin (packed
-                                 binary columns), [1] k_eval (every other column, incl. the
-                                 12 B/row row state), [2] unused (0)                          */
+  int64_t model_bytes_kernel[3]; /* the same model split by eval kernel: [0] k_eval_bin (binary
+                                 columns), [1] k_eval_gen (general, empty and long bounded-
+                                 integer columns), [2] k_eval (sorted general columns and the
+                                 12 B/row row state)                                          */
   int64_t nnz_kernel[3];      /* nonzeros (incl. cutoff entries) evaluated by each kernel      */
+  int32_t eval_launches;      /* kernel launches of one best-shift pass (1-3: the eval kernels
+                                 with work, k_eval always); a tabu iteration adds the apply   */
+  int32_t pad_;
 } chap_problem_info;
 
 /* Build a problem from HOST CSR data (copied; the caller may free its arrays on return).
@@ -226,9 +231,10 @@ chap_status chap_walkers_destroy(chap_walkers* ws);
 
 /* Diagnostic timing: n_iters tabu iterations (identical semantics to chap_tabu_step, no log)
  * with plain launches and a CUDA-event pair around every launch on the walkers' stream;
- * ms_per_iter HOST [5] receives the average device time per iteration of [0] k_eval_bin (packed
- * binary columns), [1] k_eval (every other column + the fused global select), [2]-[3] reserved
- * (0), [4] the apply kernel. Synchronises. */
+ * ms_per_iter HOST [5] receives the average device time per iteration of [0] k_eval_bin (binary
+ * columns), [1] k_eval_gen (general, empty, long bounded-integer columns), [2] k_eval (sorted
+ * general columns + the fused global select), [3] reserved (0), [4] the apply kernel.
+ * Synchronises. */
 chap_status chap_walkers_profile(chap_walkers* ws, int32_t n_iters, double* ms_per_iter,
                                  void* cuda_stream);
 

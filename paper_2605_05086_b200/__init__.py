@@ -36,7 +36,8 @@ class chap_problem_info(ctypes.Structure):
                 ("nnz_cut", c_i64), ("n_fixed", c_i32), ("n_binary", c_i32), ("n_integer", c_i32),
                 ("n_continuous", c_i32), ("exact_integer_data", c_i32), ("n_long_columns", c_i32),
                 ("auto_cutoff_delta", c_f64), ("device_bytes", c_i64), ("model_bytes_A", c_i64),
-                ("model_bytes_pass", c_i64), ("model_bytes_kernel", c_i64 * 3), ("nnz_kernel", c_i64 * 3)]
+                ("model_bytes_pass", c_i64), ("model_bytes_kernel", c_i64 * 3), ("nnz_kernel", c_i64 * 3),
+                ("eval_launches", c_i32), ("pad_", c_i32)]
 
 
 class chap_move(ctypes.Structure):

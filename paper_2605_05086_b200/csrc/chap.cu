@@ -296,7 +296,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   // tiles (PAPER.md:353-355 length dispatch): block tiles — chunks of long columns, single-column
   // sorts — and warp tiles of packed short columns
   std::vector<Tile> tiles;
-  std::vector<WTile> wtiles, btiles;
+  std::vector<WTile> wtiles, btiles, bchunks, gchunks;
+  std::vector<LongCol> lcols;
   for (const auto& r : bin_ranges) {
     WTile W{};
     W.p0 = r.first;
@@ -346,22 +347,27 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       ++p;
       continue;
     }
-    // chunked: CC_LBIN, CC_LBKT
+    // long columns: warp chunks of kWChunk nonzeros, accumulated with atomics into per-column
+    // accumulators (binary: the flip sum; bounded integer: bucket deltas, candidate bits, β, α);
+    // the column's last chunk finalises
     const int d = col_ptr[p + 1] - col_ptr[p];   // incl. any padding (inert)
-    const int nch = std::max(1, (d + kTileNnz - 1) / kTileNnz);
+    const int nch = std::max(1, (d + kWChunk - 1) / kWChunk);
     const int dom = (k == CC_LBKT) ? (int)(u[j] - l[j] + 1.0) : 0;
-    T.nchunks = nch;
-    T.dom = dom;
-    T.lc = n_long;
-    T.scr = lscr;
     for (int q = 0; q < nch; ++q) {
-      Tile C = T;
-      C.chunk = q;
-      C.e0 = col_ptr[p] + q * kTileNnz;
-      C.e1 = std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * kTileNnz);
-      tiles.push_back(C);
+      WTile W{};
+      W.p0 = p;
+      W.e0 = col_ptr[p] + q * kWChunk;
+      W.e1 = n_long;
+      W.ncols = (int16_t)(std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * kWChunk) - W.e0);
+      W.kind = (int8_t)k;
+      (k == CC_LBIN ? bchunks : gchunks).push_back(W);
     }
-    if (nch > 1) lscr += (k == CC_LBKT) ? (2LL * nch * dom + 2LL * nch) : nch;
+    LongCol L{};
+    L.scr = lscr;
+    L.nchunks = nch;
+    L.dom = dom;
+    lcols.push_back(L);
+    lscr += (k == CC_LBKT) ? ((int64_t)dom + 1 + 2 + (dom + 63) / 64) : 1;
     ++n_long;
     ++p;
   }
@@ -372,13 +378,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       const int32_t j = perm[q];
       const int k = cls[j];
       if (k == CC_FIXED) continue;
-      const int kk = (k == CC_BIN) ? 0 : 1;   // [0] k_eval_bin, [1] k_eval
+      const int kk = (k == CC_BIN || k == CC_LBIN) ? 0 : (k == CC_GENM ? 2 : 1);
       const bool bin = vclass[j] == 1;
       const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
       mb[kk] += 12LL * deg[j] + (int64_t)std::llround(per_var * 8) / 8;
       nz[kk] += deg[j];
     }
-    mb[1] += 12LL * m_norm;
+    mb[2] += 12LL * m_norm;   // the row state, read once per pass (attributed to the last kernel)
     for (int q = 0; q < 3; ++q) { I.model_bytes_kernel[q] = mb[q]; I.nnz_kernel[q] = nz[q]; }
     I.model_bytes_pass = mb[0] + mb[1] + mb[2];
   }
@@ -392,6 +398,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   Tile* d_tiles;
   WTile* d_wtiles;
   WTile* d_btiles;
+  LongCol* d_lcols;
+  WTile *d_bchunks, *d_gchunks;
   TRY(B.upload(&d_col_ptr, col_ptr));
   TRY(B.upload(&d_row_idx, row_idx));
   TRY(B.upload(&d_val, cval));
@@ -407,6 +415,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_tiles, tiles));
   TRY(B.upload(&d_wtiles, wtiles));
   TRY(B.upload(&d_btiles, btiles));
+  TRY(B.upload(&d_bchunks, bchunks));
+  TRY(B.upload(&d_gchunks, gchunks));
+  if (lcols.empty()) lcols.push_back(LongCol{});
+  TRY(B.upload(&d_lcols, lcols));
   DevProblem& D = P->dp;
   D.n = n;
   D.m_norm = m_norm;
@@ -430,6 +442,11 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.n_wtiles = (int32_t)wtiles.size();
   D.btiles = d_btiles;
   D.n_btiles = (int32_t)btiles.size();
+  D.lcols = d_lcols;
+  D.bchunks = d_bchunks;
+  D.n_bchunks = (int32_t)bchunks.size();
+  D.gchunks = d_gchunks;
+  D.n_gchunks = (int32_t)gchunks.size();
   D.n_long = n_long;
   D.n_fixed = I.n_fixed;
   D.auto_delta = I.auto_cutoff_delta;
@@ -439,14 +456,22 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval, kTileThreads, kTileSmem));
   P->eval_occ = std::max(1, occ);
-  const int work_blocks = std::max(D.n_tiles, (D.n_wtiles + kTileWarps - 1) / kTileWarps);
-  P->eval_grid = std::max(1, std::min(work_blocks, P->eval_occ * P->sm_count));
+  P->eval_grid = std::max(1, std::min(std::max(D.n_tiles, 1), P->eval_occ * P->sm_count));
+  CUDA_TRY(cudaFuncSetAttribute(k_eval_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGenSmem));
+  int gocc = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gocc, k_eval_gen, kGenThreads, kGenSmem));
+  P->gen_occ = std::max(1, gocc);
+  const int gwarps = kGenThreads / 32;
+  const int gwork = D.n_wtiles + D.n_gchunks;
+  P->gen_grid = gwork ? std::max(1, std::min((gwork + gwarps - 1) / gwarps, P->gen_occ * P->sm_count)) : 0;
   CUDA_TRY(cudaFuncSetAttribute(k_eval_bin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem));
   int bocc = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_eval_bin, kBinThreads, kBinSmem));
   P->bin_occ = std::max(1, bocc);
   const int bwarps = kBinThreads / 32;
-  P->bin_grid = D.n_btiles ? std::max(1, std::min((D.n_btiles + bwarps - 1) / bwarps, P->bin_occ * P->sm_count)) : 0;
+  const int bwork = D.n_btiles + D.n_bchunks;
+  P->bin_grid = bwork ? std::max(1, std::min((bwork + bwarps - 1) / bwarps, P->bin_occ * P->sm_count)) : 0;
+  P->info.eval_launches = 1 + (P->bin_grid > 0) + (P->gen_grid > 0);
   P->rows_grid = std::max(1, std::min((m_norm + 7) / 8, 8 * P->sm_count));
   // eval workspace
   TRY(B.alloc(&P->e_x, n));
@@ -454,13 +479,14 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.alloc(&P->e_tabu, n));
   TRY(B.alloc(&P->e_bx, n));
   TRY(B.alloc(&P->e_sc, 1));
-  TRY(B.alloc(&P->e_part, P->eval_grid + P->bin_grid));
+  TRY(B.alloc(&P->e_part, P->eval_grid + P->bin_grid + P->gen_grid));
   TRY(B.alloc(&P->e_selcnt, 1));
   CUDA_TRY(cudaMemset(P->e_selcnt, 0, sizeof(unsigned)));
   TRY(B.alloc(&P->e_lcount, std::max(n_long, 1)));
   TRY(B.alloc(&P->e_lscr, P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_sc, 0, sizeof(WalkerScalars)));
   CUDA_TRY(cudaMemset(P->e_lcount, 0, sizeof(unsigned) * std::max(n_long, 1)));
+  CUDA_TRY(cudaMemset(P->e_lscr, 0, sizeof(double) * P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_tabu, 0, sizeof(int32_t) * std::max(n, 1)));
   CUDA_TRY(cudaDeviceSynchronize());
   I.device_bytes = (int64_t)B.bytes_total;
@@ -493,10 +519,11 @@ extern "C" chap_status chap_problem_destroy(chap_problem* p) {
 // ------------------------------------------------------------------------------------------
 // eval launches (shared by the eval API and the tabu step)
 // ------------------------------------------------------------------------------------------
-chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid,
+chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                               double* oxhat, double* oscore, chap_move* best, cudaStream_t s) {
   if (bgrid > 0) k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
-  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid);
+  if (ggrid > 0) k_eval_gen<<<dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s>>>(P->dp, Wk, oxhat, oscore, bgrid);
+  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -512,7 +539,7 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.best_x = P->e_bx;
   Wk.sc = P->e_sc;
   Wk.part = P->e_part;
-  Wk.ps = P->eval_grid + P->bin_grid;
+  Wk.ps = P->eval_grid + P->bin_grid + P->gen_grid;
   Wk.sel_count = P->e_selcnt;
   Wk.lcount = P->e_lcount;
   Wk.lcs = std::max(P->dp.n_long, 1);
@@ -546,7 +573,7 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, xhat, score, best, s));
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, xhat, score, best, s));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -636,7 +663,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   TRY(B.alloc(&Wk.sc, W));
   S->eval_grid = std::max(1, std::min(p->eval_grid, (p->eval_occ * p->sm_count + W - 1) / W));
   S->bin_grid = p->bin_grid ? std::max(1, std::min(p->bin_grid, (p->bin_occ * p->sm_count + W - 1) / W)) : 0;
-  Wk.ps = S->eval_grid + S->bin_grid;
+  S->gen_grid = p->gen_grid ? std::max(1, std::min(p->gen_grid, (p->gen_occ * p->sm_count + W - 1) / W)) : 0;
+  Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
   TRY(B.alloc(&Wk.sel_count, W));
   Wk.lcs = std::max(D.n_long, 1);
@@ -658,6 +686,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   cudaStream_t s = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaMemsetAsync(Wk.sc, 0, sizeof(WalkerScalars) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.lcount, 0, sizeof(unsigned) * Wk.lcs * W, s));
+  CUDA_TRY(cudaMemsetAsync(Wk.lscr, 0, sizeof(double) * Wk.lss * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
@@ -681,7 +710,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
-  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, nullptr, nullptr, nullptr, s));
+  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, nullptr, nullptr, nullptr, s));
   k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -793,9 +822,13 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
       k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(D, S->wk, nullptr, nullptr);
     cudaEventRecord(e[1], s);
     cudaEventRecord(e[2], s);
-    k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
-                                                                     S->bin_grid);
+    if (S->gen_grid > 0)
+      k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid);
     cudaEventRecord(e[3], s);
+    cudaEventRecord(e[4], s);
+    k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
+                                                                     S->bin_grid + S->gen_grid);
+    cudaEventRecord(e[5], s);
     cudaEventRecord(e[8], s);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
     cudaEventRecord(e[9], s);
@@ -812,7 +845,7 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
       ms[q] += t;
     }
   for (int q = 0; q < 5; ++q) ms[q] /= n_iters;
-  ms[2] = ms[3] = 0.0;           // [0] k_eval_bin, [1] k_eval (+ fused select)
+  ms[3] = 0.0;                   // [0] k_eval_bin, [1] k_eval_gen, [2] k_eval (+ fused select)
   for (auto& e : ev) cudaEventDestroy(e);
   CUDA_TRY(cudaEventRecord(S->ev_out, s));
   CUDA_TRY(cudaStreamWaitEvent(us, S->ev_out, 0));

@@ -17,13 +17,14 @@ constexpr int kPer = kTileNnz / kTileThreads;     // slots per thread of a chunk
 constexpr int kGenmMax = 2048;                    // Alg. 1 elements of a single-column sort tile
 constexpr int kWSlots = 8;                        // slots per lane of a binary warp tile
 constexpr int kWTileNnz = 32 * kWSlots;           // nonzeros per binary warp tile
-constexpr int kWSlotsGen = 8;                     // slots per lane of a general warp tile
+constexpr int kWSlotsGen = 4;                     // slots per lane of a general warp tile
 constexpr int kWTileGen = 32 * kWSlotsGen;        // Alg. 1 elements per general warp tile
 constexpr int kWTileCols = 32;                    // columns per warp tile (one lane each)
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kBinSlots = 4;                      // slots per lane of a pipelined binary tile
 constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per pipelined binary tile
 constexpr int kBinThreads = 256;                  // k_eval_bin block
+constexpr int kGenThreads = 256;                  // k_eval_gen block
 constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
 constexpr int kBucketMax = 4096;                  // max integer domain of a bucket-scanned column
 constexpr int kApplyThreads = 256;
@@ -52,11 +53,19 @@ enum ColClass : int {
 // A warp tile: ncols consecutive packed columns (CC_BIN or CC_GEN) of one warp.
 struct WTile {
   int32_t p0;
-  int32_t e0, e1;    // nonzero range
-  int16_t ncols;
-  int8_t kind;
+  int32_t e0;
+  int32_t e1;        // nonzero range [e0, e1); a chunk of a long column: the long-column index
+  int16_t ncols;     // columns; a chunk of a long column: its nonzeros (<= kWChunk)
+  int8_t kind;       // CC_BIN, CC_GEN, CC_EMPTY, or a warp chunk of a long column: CC_LBIN, CC_LBKT
   int8_t pad;
 };
+// A long column split into warp chunks: where its accumulators live in walker scratch.
+struct LongCol {
+  int64_t scr;       // offset (doubles) of the accumulators in walker scratch
+  int32_t nchunks;
+  int32_t dom;       // CC_LBKT: u - l + 1
+};
+constexpr int kWChunk = 128;                      // nonzeros per warp chunk of a long column
 
 // A block tile (chunk of a long column, or one column sorted by the whole block).
 struct Tile {
@@ -128,6 +137,9 @@ struct DevProblem {
   const Tile* tiles; int32_t n_tiles; int32_t n_long;   // block tiles
   const WTile* wtiles; int32_t n_wtiles;                // warp tiles (general, empty)
   const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles
+  const WTile* bchunks; int32_t n_bchunks;              // warp chunks of long binary columns
+  const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns
+  const LongCol* lcols;                                 // [n_long]
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   double auto_delta;
 };

@@ -1,20 +1,20 @@
 // eval.cuh — best-shift evaluation (§3.1, Eq. (1) and Algorithm 1) on sm_100a.
 //
-// One persistent kernel, k_eval, evaluates every variable of every walker and selects the best
-// admissible move (the paper's length-specialised dispatch, re-designed):
-//   phase A, block tiles (all warps of a block):
-//     CC_LBIN  a kTileNnz chunk of a long binary column: block partial flip sum;
-//     CC_LBKT  a chunk of a general integer column with a bounded domain: the sort of line 13
-//              becomes a counting (bucket) pass over [l, u];
-//     CC_GENM  one general column of <= kGenmMax entries: shared-memory bitonic sort + scan;
-//     the last chunk of a column merges the chunk partials in chunk order (deterministic);
-//   phase B, warp tiles (one warp, no block barriers):
-//     CC_BIN   packed binary columns: flip penalty per nonzero, per-column sum;
-//     CC_GEN   packed general columns: Algorithm 1 per column, sort-free (see wtile_gen);
-//     CC_EMPTY columns without nonzeros.
+// Three kernels per pass, each a lean gather loop over its own tile list (the paper's length-
+// specialised dispatch, re-designed for sm_100a):
+//   k_eval_bin  warp tiles of packed binary columns (flip penalty per nonzero, per-column sum,
+//               PAPER.md:295) and warp chunks of long binary columns (atomic partial sums);
+//   k_eval_gen  warp tiles of packed general columns (Algorithm 1 per column, sort-free, see
+//               gen_tile), empty columns, and warp chunks of long bounded-integer columns whose
+//               sort (line 13) becomes a counting pass over [l, u] (atomic bucket deltas);
+//   k_eval      block tiles of general columns of <= kGenmMax entries (shared-memory bitonic sort
+//               and scan), then the global select: the last block of a walker reduces every
+//               block's best admissible move to the walker's decision (R6).
+// A long column's last chunk (a ticket counter) finalises it and zeroes its accumulators. With the
+// integer weights of R11 every delta, β, α and penalty is a multiple of 1/2 and every partial sum
+// is exact, so the order of the atomic additions does not change any result.
 // Every warp-tile slot issues its coalesced CSC loads and one 16-byte row-state gather before
-// using any of them. Each block keeps its best admissible move (R6); the last block of a walker
-// reduces the block partials to the walker's decision (the global select).
+// using any of them.
 #pragma once
 #include "common.cuh"
 
@@ -182,43 +182,14 @@ __device__ __forceinline__ Elem emit(double xb, double r, double a, double w, in
 // ------------------------------------------------------------------------------------------
 // shared memory
 // ------------------------------------------------------------------------------------------
-struct WarpBin {                       // CC_BIN warp tile
-  double pen[kWTileNnz];
-  double xb[kWTileCols];
-  uint32_t head[kWTileNnz / 32];       // bit k: slot k starts a column
-};
-struct WarpGen {                       // CC_GEN warp tile: row entries at slots [0, nnz); the
-  double key[kWTileGen];               // bound entries of column c at slots nnz + 2c, nnz + 2c + 1
-  double D[kWTileGen];                 // entry delta (0 for bound / dropped entries)
-  union {
-    float2 AB[kWTileGen];              // phases 1-2: the entry's contributions to β and α
-    double sig[kWTileGen];             // phases 3-4: sigma of candidate slots
-  };
-  uint8_t f[kWTileGen];                // GF_* flags
-  uint8_t seg[kWTileGen];              // column of a row slot
-  double xb[kWTileCols];
-  double l[kWTileCols];
-  double u[kWTileCols];
-  double beta[kWTileCols];
-  double alpha[kWTileCols];
-  int32_t cb[kWTileCols];
-  int32_t ce[kWTileCols];
-  uint32_t head[kWTileGen / 32];
-  uint8_t cont[kWTileCols];            // continuous column
-};
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-constexpr size_t kWarpSmem = (cmax(sizeof(WarpBin), sizeof(WarpGen)) + 15) / 16 * 16;
 struct SmemGenM {                      // CC_GENM block tile
   double t[kGenmMax];
   double del[kGenmMax];
   double P[kGenmMax];
   uint32_t mk[kGenmMax];
 };
-struct SmemBkt {                       // CC_LBKT block tile
-  double D[kBucketMax + 1];
-  uint8_t cand[kBucketMax];
-};
-constexpr size_t kTileSmem = cmax(kWarpSmem * kTileWarps, cmax(sizeof(SmemGenM), sizeof(SmemBkt)));
+constexpr size_t kTileSmem = sizeof(SmemGenM);
 
 struct TileCtx {
   const double* x;
@@ -233,66 +204,6 @@ struct TileCtx {
 // ------------------------------------------------------------------------------------------
 // warp tiles
 // ------------------------------------------------------------------------------------------
-
-// Column of slot k = lane + 32 q of a packed tile: columns are contiguous runs of slots and
-// none is empty, so the column is (number of column starts <= k) - 1, read off a head bitmap.
-__device__ __forceinline__ void build_heads(uint32_t* head, int nwords, int lane, int nc, int cb) {
-  if (lane < nwords) head[lane] = 0u;
-  __syncwarp();
-  if (lane < nc) atomicOr(&head[cb >> 5], 1u << (cb & 31));
-  __syncwarp();
-}
-
-// packed binary columns, one warp (the only move of a binary is the flip).
-// Memory round trips per tile: (stream loads || column loads) -> gathers; all kWSlots slots of a
-// lane are issued together.
-__device__ __forceinline__ void wtile_bin(const DevProblem& P, const TileCtx& C, const WTile& T,
-                                          int lane, WarpBin& S, Best& b) {
-  const int nc = T.ncols, nnz = T.e1 - T.e0;
-  const int* __restrict__ ridx = P.row_idx + T.e0;
-  const double* __restrict__ rval = P.val + T.e0;
-  int idx[kWSlots];
-  double av[kWSlots];
-#pragma unroll
-  for (int q = 0; q < kWSlots; ++q) {
-    const int k = lane + 32 * q;
-    const bool ok = k < nnz;
-    idx[q] = ok ? __ldcs(ridx + k) : 0;
-    av[q] = ok ? __ldcs(rval + k) : 0.0;
-  }
-  const int p = T.p0 + lane;
-  int cb = 0, ce = 0, j = 0, tb = 0;
-  double xb = 0.0;
-  if (lane < nc) {
-    cb = __ldg(P.col_ptr + p) - T.e0;
-    ce = __ldg(P.col_ptr + p + 1) - T.e0;
-    j = __ldg(P.perm + p);
-    tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
-    xb = __ldg(C.x + p);
-  }
-  double r[kWSlots], w[kWSlots];
-#pragma unroll
-  for (int q = 0; q < kWSlots; ++q) load_row(C.rs, idx[q], r[q], w[q]);
-  if (lane < nc) S.xb[lane] = xb;
-  build_heads(S.head, kWSlots, lane, nc, cb);
-  const unsigned le = (2u << lane) - 1u;   // lanes <= lane
-  int pre = 0;                             // column starts before this slot round
-#pragma unroll
-  for (int q = 0; q < kWSlots; ++q) {
-    const int k = lane + 32 * q;
-    const uint32_t hw = S.head[q];
-    const int c = pre + __popc(hw & le) - 1;
-    pre += __popc(hw);
-    if (k < nnz) S.pen[k] = penalty(w[q], r[q], r[q] + av[q] * (1.0 - 2.0 * S.xb[c]));
-  }
-  __syncwarp();
-  if (lane < nc) {
-    double s = 0.0;
-    for (int e = cb; e < ce; ++e) s += S.pen[e];
-    finish_column_j(p, j, tb, xb, 1.0 - xb, s, b, C.oxhat, C.oscore, C.k, C.use_tabu);
-  }
-  __syncwarp();
-}
 
 // Entry flags of a general warp tile. Lines 5-11 of Algorithm 1 are fixed by
 // the sign of a_ij and the order of x̄ and t: with w = w_i,
@@ -314,152 +225,6 @@ __device__ __forceinline__ void gf_coeffs(uint8_t f, double w, double& D, double
   D = row ? (pos ? Dp : Dn) : 0.0;
   A = row ? (pos ? Ap : An) : 0.0;
   B = row ? (pos ? Bp : Bn) : 0.0;
-}
-
-// Packed general columns, one warp: Algorithm 1 per column, sort-free.
-// For a candidate value v the score Algorithm 1 reports (the largest sigma of the entries at v,
-// R3) is sigma(v) = β + Σ_{entries e: t_e < v, or t_e = v with marker -1} δ_e + α [v > x̄]
-// (DESIGN §2.3). A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an entry with
-// δ = 0 adds nothing, so "marker -1" is δ > 0; for integer columns the condition is the single
-// compare key_e <= 2v with key_e = 2 t_e + [δ_e < 0] (exact while |t| < 2^51); continuous columns
-// compare (t, δ > 0) directly. Phases:
-//  (1) slots in parallel: coalesced CSC loads and row-state gathers issued together, then lines
-//      3-11 per entry: t, the emission case, δ, the β/α contributions and the key;
-//  (2) lane c: β and α of column c (lines 1-12 accumulators, fixed order);
-//  (3) candidate slots in parallel: sigma by a compare-add pass over the column's entries
-//      (lines 13-15: the sort and scan, done as direct prefix sums);
-//  (4) lane c: the argmax of line 16 with the R4 tie-break.
-__device__ __forceinline__ void wtile_gen(const DevProblem& P, const TileCtx& C, const WTile& T,
-                                          int lane, WarpGen& S, Best& b) {
-  const int nc = T.ncols, nnz = T.e1 - T.e0;
-  const int nel = nnz + 2 * nc;
-  const int* __restrict__ ridx = P.row_idx + T.e0;
-  const double* __restrict__ rval = P.val + T.e0;
-  const int p = T.p0 + lane;
-  int cb = 0, ce = 0, j = 0, tb = 0;
-  double xb = 0.0;
-  if (lane < nc) {
-    cb = __ldg(P.col_ptr + p) - T.e0;
-    ce = __ldg(P.col_ptr + p + 1) - T.e0;
-    j = __ldg(P.perm + p);
-    tb = C.use_tabu ? __ldg(C.tabu + p) : 0;
-    xb = __ldg(C.x + p);
-    S.xb[lane] = xb;
-    S.l[lane] = __ldg(P.lb + p);
-    S.u[lane] = __ldg(P.ub + p);
-    S.cont[lane] = __ldg(P.vclass + p) == 3;
-    S.cb[lane] = cb;
-    S.ce[lane] = ce;
-  }
-  build_heads(S.head, kWSlotsGen, lane, nc, cb);
-  // (1) lines 3-11, in two halves of kWSlotsGen/2 loads + gathers in flight
-  const unsigned le = (2u << lane) - 1u;
-  int pre = 0;
-  constexpr int H = kWSlotsGen / 2;
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    int idx[H];
-    double av[H];
-#pragma unroll
-    for (int q = 0; q < H; ++q) {
-      const int k = lane + 32 * (q + h * H);
-      const bool ok = k < nnz;
-      idx[q] = ok ? __ldcs(ridx + k) : 0;
-      av[q] = ok ? __ldcs(rval + k) : 1.0;
-    }
-    double r[H], w[H];
-#pragma unroll
-    for (int q = 0; q < H; ++q) load_row(C.rs, idx[q], r[q], w[q]);
-#pragma unroll
-    for (int q = 0; q < H; ++q) {
-      const int qq = q + h * H;
-      const int k = lane + 32 * qq;
-      const uint32_t hw = S.head[qq];
-      const int cr = pre + __popc(hw & le) - 1;
-      pre += __popc(hw);
-      if (k >= nel) continue;
-      double key = 0.0, D = 0.0;
-      float A = 0.f, B = 0.f;
-      uint8_t f = 0;
-      if (k < nnz) {
-        const int c = cr;
-        const double x = S.xb[c];
-        const bool cont = S.cont[c];
-        double t = breakpoint(x, r[q], av[q]);                     // line 3
-        if (!cont) t = (av[q] > 0.0) ? floor(t) : ceil(t);         // line 4
-        const bool pos = av[q] > 0.0, lt = x < t, gt = x > t;      // lines 5-11
-        const double wq = w[q], hw2 = 0.5 * wq;
-        D = pos ? (gt ? -hw2 : (lt ? -wq : 0.0)) : (lt ? hw2 : (gt ? wq : 0.0));
-        A = (float)(pos ? (gt ? wq : 0.0) : (lt ? -hw2 : -wq));
-        B = (float)(pos ? (lt ? 0.0 : -wq) : (gt ? 0.0 : wq));
-        key = cont ? t : 2.0 * t + (D < 0.0 ? 1.0 : 0.0);
-        if (x != t && t >= S.l[c] && t <= S.u[c]) f = GF_CAND;
-        if (!isfinite(r[q])) { D = 0.0; A = B = 0.f; f = 0; }     // inert inactive cutoff row
-        S.seg[k] = (uint8_t)c;
-        S.AB[k] = make_float2(A, B);
-      } else {
-        const int c = (k - nnz) >> 1;
-        const double v = ((k - nnz) & 1) ? S.u[c] : S.l[c];
-        key = S.cont[c] ? v : 2.0 * v;                             // the candidate value, encoded
-        if (isfinite(v) && v != S.xb[c]) f = GF_CAND;
-      }
-      S.key[k] = key;
-      S.D[k] = D;
-      S.f[k] = f;
-    }
-  }
-  __syncwarp();
-  // (2) β, α of column `lane`
-  if (lane < nc) {
-    double beta = 0.0, alpha = 0.0;
-    for (int e = cb; e < ce; ++e) {
-      const float2 ab = S.AB[e];
-      beta += (double)ab.x;
-      alpha += (double)ab.y;
-    }
-    S.beta[lane] = beta;
-    S.alpha[lane] = alpha;
-  }
-  __syncwarp();
-  // (3) sigma of every candidate slot
-#pragma unroll 1
-  for (int q = 0; q < kWSlotsGen; ++q) {
-    const int k = lane + 32 * q;
-    if (k >= nel || !(S.f[k] & GF_CAND)) continue;
-    const int c = (k < nnz) ? S.seg[k] : ((k - nnz) >> 1);
-    const bool cont = S.cont[c];
-    const double kv = S.key[k];
-    // the candidate's value and its "minus" key 2v
-    const double v = cont ? kv : floor(0.5 * kv);
-    const double km = cont ? kv : 2.0 * v;
-    const int e0 = S.cb[c], e1 = S.ce[c];
-    double acc = S.beta[c] + (v > S.xb[c] ? S.alpha[c] : 0.0);
-    if (!cont) {
-      for (int e = e0; e < e1; ++e) acc += (S.key[e] <= km) ? S.D[e] : 0.0;
-    } else {
-      for (int e = e0; e < e1; ++e) {
-        const double te = S.key[e], de = S.D[e];
-        acc += (te < v || (te == v && de > 0.0)) ? de : 0.0;
-      }
-    }
-    S.sig[k] = acc;
-  }
-  __syncwarp();
-  // (4) argmax per column (R3, R4)
-  if (lane < nc) {
-    const bool cont = S.cont[lane];
-    double bs = -INFINITY, bv = xb;
-    for (int e = cb; e < ce + 2; ++e) {
-      const int k = (e < ce) ? e : nnz + 2 * lane + (e - ce);
-      if (!(S.f[k] & GF_CAND)) continue;
-      const double kv = S.key[k];
-      const double v = cont ? kv : floor(0.5 * kv);
-      const double sg = S.sig[k];
-      if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
-    }
-    finish_column_j(p, j, tb, xb, bv, bs, b, C.oxhat, C.oscore, C.k, C.use_tabu);
-  }
-  __syncwarp();
 }
 
 // Columns without nonzeros: a binary flips with score 0; another variable's candidates are its
@@ -627,149 +392,6 @@ __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_fl
   return last;
 }
 
-// The CSC stream of a chunk tile: kPer independent coalesced loads + gathers per thread.
-struct ChunkRows {
-  double a[kPer];
-  double r[kPer];
-  double w[kPer];
-  bool ok[kPer];
-};
-__device__ __forceinline__ void load_chunk(const DevProblem& P, const TileCtx& C, int e0, int nnz,
-                                           ChunkRows& R) {
-  int idx[kPer];
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int k = threadIdx.x + q * kTileThreads;
-    R.ok[q] = k < nnz;
-    idx[q] = R.ok[q] ? __ldcs(P.row_idx + e0 + k) : 0;
-    R.a[q] = R.ok[q] ? __ldcs(P.val + e0 + k) : 1.0;
-  }
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) load_row(C.rs, idx[q], R.r[q], R.w[q]);
-}
-
-// a chunk of a long binary column: partial flip sum, merged in chunk order
-__device__ __forceinline__ void tile_lbin(const DevProblem& P, const DevWalkers& Wk, int walker,
-                                          const TileCtx& C, const Tile& T, double* sm_red,
-                                          int* s_flag, Best& b) {
-  const int tid = threadIdx.x;
-  const int p = T.p0;
-  const double xb = C.x[p];
-  const double dir = 1.0 - 2.0 * xb;
-  ChunkRows R;
-  load_chunk(P, C, T.e0, T.e1 - T.e0, R);
-  double pen = 0.0;
-#pragma unroll
-  for (int q = 0; q < kPer; ++q)
-    if (R.ok[q]) pen += penalty(R.w[q], R.r[q], R.r[q] + R.a[q] * dir);
-  pen = block_sum(pen, sm_red);
-  if (T.nchunks == 1) {
-    if (tid == 0) finish_column(P, p, xb, 1.0 - xb, pen, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
-    return;
-  }
-  double* scr = Wk.lscr + (size_t)walker * Wk.lss + T.scr;
-  unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.lc;
-  if (tid == 0) scr[T.chunk] = pen;
-  if (last_chunk(cnt, T.nchunks, s_flag) && tid == 0) {
-    double s = 0.0;
-    for (int c = 0; c < T.nchunks; ++c) s += __ldcg(scr + c);   // chunk order
-    *cnt = 0u;
-    finish_column(P, p, xb, 1.0 - xb, s, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
-  }
-  __syncthreads();
-}
-
-// a chunk of a general integer column with domain [l, u], dom = u - l + 1 <= kBucketMax: the
-// sort of line 13 becomes a counting pass. D[v-l] collects the -1 deltas at v and the +1
-// deltas at v-1, so sigma at candidate v = β + Σ_{v' <= v} D[v'] + α [v > x̄].
-__device__ __forceinline__ void tile_lbkt(const DevProblem& P, const DevWalkers& Wk, int walker,
-                                          const TileCtx& C, const Tile& T, SmemBkt& S,
-                                          double* sm_red, Best* sm_b, int* s_flag, Best& b) {
-  const int tid = threadIdx.x;
-  const int p = T.p0, dom = T.dom;
-  const double xb = C.x[p], l = P.lb[p], u = P.ub[p];
-  for (int q = tid; q <= dom; q += blockDim.x) S.D[q] = 0.0;
-  for (int q = tid; q < dom; q += blockDim.x) S.cand[q] = 0;
-  ChunkRows R;
-  load_chunk(P, C, T.e0, T.e1 - T.e0, R);
-  __syncthreads();
-  double beta = 0.0, alpha = 0.0;
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    if (!R.ok[q]) continue;
-    const Elem el = emit(xb, R.r[q], R.a[q], R.w[q], 1);
-    beta += el.beta;
-    alpha += el.alpha;
-    if (!el.valid) continue;
-    const double t = el.t;
-    if (t >= l && t <= u && t != xb) S.cand[(int)(t - l)] = 1;
-    if (!el.plus) {
-      if (t < l) beta += el.delta;
-      else if (t <= u) atomicAdd(&S.D[(int)(t - l)], el.delta);
-    } else {
-      if (t < l) beta += el.delta;
-      else if (t < u) atomicAdd(&S.D[(int)(t - l) + 1], el.delta);
-    }
-  }
-  beta = block_sum(beta, sm_red);
-  alpha = block_sum(alpha, sm_red);
-  bool have_all = (T.nchunks == 1);
-  double B = beta, A = alpha;
-  if (!have_all) {
-    double* scr = Wk.lscr + (size_t)walker * Wk.lss + T.scr;
-    unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.lc;
-    double* pD = scr + (size_t)T.chunk * dom;
-    double* pC = scr + (size_t)T.nchunks * dom + (size_t)T.chunk * dom;
-    double* pBA = scr + (size_t)2 * T.nchunks * dom + 2 * T.chunk;
-    for (int q = tid; q < dom; q += blockDim.x) {
-      pD[q] = S.D[q];
-      pC[q] = S.cand[q] ? 1.0 : 0.0;
-    }
-    if (tid == 0) { pBA[0] = beta; pBA[1] = alpha; }
-    if (!last_chunk(cnt, T.nchunks, s_flag)) return;
-    for (int q = tid; q < dom; q += blockDim.x) {
-      double dsum = 0.0, csum = 0.0;
-      for (int c = 0; c < T.nchunks; ++c) {
-        dsum += __ldcg(scr + (size_t)c * dom + q);
-        csum += __ldcg(scr + (size_t)T.nchunks * dom + (size_t)c * dom + q);
-      }
-      S.D[q] = dsum;
-      S.cand[q] = csum > 0.0 ? 1 : 0;
-    }
-    if (tid == 0) {
-      double bsum = 0.0, asum = 0.0;
-      for (int c = 0; c < T.nchunks; ++c) {
-        bsum += __ldcg(scr + (size_t)2 * T.nchunks * dom + 2 * c);
-        asum += __ldcg(scr + (size_t)2 * T.nchunks * dom + 2 * c + 1);
-      }
-      sm_red[0] = bsum;
-      sm_red[1] = asum;
-      *cnt = 0u;
-    }
-    __syncthreads();
-    B = sm_red[0];
-    A = sm_red[1];
-    __syncthreads();
-  }
-  if (tid == 0) {
-    if (l != xb) S.cand[0] = 1;                 // (l, -1, 0)
-    if (u != xb) S.cand[dom - 1] = 1;           // (u, -1, 0)
-  }
-  __syncthreads();
-  block_scan_inclusive(S.D, dom, sm_red);
-  double bs = -INFINITY, bv = xb;
-  for (int q = tid; q < dom; q += blockDim.x) {
-    if (!S.cand[q]) continue;
-    const double v = l + (double)q;
-    if (v == xb) continue;
-    const double sig = B + S.D[q] + (v > xb ? A : 0.0);
-    if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
-  }
-  block_best_shift(bs, bv, xb, sm_b);
-  if (tid == 0) finish_column(P, p, xb, bv, bs, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
-  __syncthreads();
-}
-
 // ------------------------------------------------------------------------------------------
 // the kernel
 // ------------------------------------------------------------------------------------------
@@ -795,32 +417,10 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   C.oscore = oscore;
   Best b;
   b.init();
-  // phase A: block tiles (chunks of long columns, single-column sorts)
-  for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-    const Tile T = P.tiles[t];
-    switch (T.kind) {
-      case CC_LBIN: tile_lbin(P, Wk, walker, C, T, sm_red, &s_flag, b); break;
-      case CC_LBKT: tile_lbkt(P, Wk, walker, C, T, *reinterpret_cast<SmemBkt*>(smem), sm_red, sm_b, &s_flag, b); break;
-      default: tile_genm(P, C, T, *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b); break;
-    }
-  }
+  // block tiles: single-column sorts
+  for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x)
+    tile_genm(P, C, P.tiles[t], *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b);
   __syncthreads();
-  // phase B: warp tiles, each warp on its own slice of shared memory, no block barriers
-  {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned char* ws = smem + (size_t)wid * kWarpSmem;
-    const int nwarps = gridDim.x * kTileWarps;
-    int t = blockIdx.x * kTileWarps + wid;
-    WTile Tn;
-    if (t < P.n_wtiles) Tn = P.wtiles[t];
-    for (; t < P.n_wtiles; t += nwarps) {
-      const WTile T = Tn;
-      if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];   // next descriptor in flight
-      if (T.kind == CC_BIN) wtile_bin(P, C, T, lane, *reinterpret_cast<WarpBin*>(ws), b);
-      else if (T.kind == CC_GEN) wtile_gen(P, C, T, lane, *reinterpret_cast<WarpGen*>(ws), b);
-      else wtile_empty(P, C, T, lane, b);
-    }
-  }
   // publish the block's best; the last block of this walker selects (R6)
   b = block_reduce_best(b, sm_b);
   Cand* part = Wk.part + (size_t)walker * Wk.ps;
@@ -866,15 +466,67 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
 // ------------------------------------------------------------------------------------------
 // k_eval_bin evaluates the packed binary columns (flip scores). It is built like a
 // plain gather loop so that many warps per SM keep their loads in flight: per warp tile (whole
-// columns, <= kBinTile nonzeros, <= 32 columns, starting on a multiple of 4 nonzeros) every lane
-// issues its coalesced CSC loads and its 16-byte row-state gathers back to back; the column of a
-// slot comes from a redux.sync head mask, x̄ of the column from a shuffle; lane c sums column c.
+// columns, <= kBinTile nonzeros, <= 32 columns, starting on a multiple of 4 nonzeros) lane l owns
+// slots 4l..4l+3: one 16-byte index load, two 16-byte value loads and four 16-byte row-state
+// gathers, all issued back to back. The column of a slot comes from the tile's 128-bit head mask
+// (redux.sync), x̄ of the column from a ballot (binaries are 0/1); column sums are a segmented
+// scan (in-lane, then a 5-step shuffle scan across lanes), so shared memory only carries the 32
+// finished sums — every random access of the kernel is the row-state gather itself.
+// A chunk of a long binary column (one column, <= kWChunk nonzeros) sums by a warp reduction and
+// adds its partial to the column's accumulator; the last chunk finishes the column.
 struct __align__(16) BinWarp {
-  double pen[kBinTile];
+  double cs[32];   // column sums
 };
 constexpr size_t kBinSmem = sizeof(BinWarp) * (kBinThreads / 32);
 
-__global__ void __launch_bounds__(kBinThreads, 6) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
+// A warp chunk (<= kWChunk nonzeros) of a long binary column: warp-reduced flip sum added to the
+// column's accumulator; the last chunk (ticket) finishes the column and zeroes the accumulator.
+__device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                           const double* __restrict__ X, const double2* __restrict__ RS,
+                                           const int32_t* __restrict__ TB, const WTile& T, int lane,
+                                           Best& b, double* oxhat, double* oscore, long long kk,
+                                           int use_tabu) {
+  const int p = T.p0, len = T.ncols;
+  const int* __restrict__ ridx = P.row_idx + T.e0;
+  const double* __restrict__ rval = P.val + T.e0;
+  const double xb = __ldg(X + p);
+  const double dir = 1.0 - 2.0 * xb;
+  int id[kWChunk / 32];
+  double av[kWChunk / 32];
+#pragma unroll
+  for (int q = 0; q < kWChunk / 32; ++q) {
+    const int k = lane + 32 * q;
+    id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
+    av[q] = k < len ? __ldcs(rval + k) : 0.0;
+  }
+  double own = 0.0;
+#pragma unroll
+  for (int q = 0; q < kWChunk / 32; ++q) {
+    const double2 rv = __ldg(RS + id[q]);
+    const double r = rv.x, w = (double)__int_as_float((int)__double2loint(rv.y));
+    own += penalty(w, r, r + av[q] * dir);   // the inert dummy row adds 0
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) own += __shfl_xor_sync(kFull, own, off);
+  if (lane != 0) return;
+  const LongCol L = P.lcols[T.e1];
+  double s = own;
+  if (L.nchunks > 1) {
+    double* acc = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
+    unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.e1;
+    atomicAdd(acc, own);
+    __threadfence();
+    if (atomicAdd(cnt, 1u) != (unsigned)(L.nchunks - 1)) return;
+    __threadfence();
+    s = __ldcg(acc);
+    *acc = 0.0;
+    *cnt = 0u;
+  }
+  finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, 1.0 - xb, s, b, oxhat,
+                  oscore, kk, use_tabu);
+}
+
+__global__ void __launch_bounds__(kBinThreads, 4) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
                                                               double* oscore) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
@@ -886,68 +538,430 @@ __global__ void __launch_bounds__(kBinThreads, 6) k_eval_bin(DevProblem P, DevWa
   const int32_t* __restrict__ TB = Wk.tabu + (size_t)walker * Wk.ts;
   const long long kk = sc->k;
   const int use_tabu = Wk.use_tabu;
-  double* pen = reinterpret_cast<BinWarp*>(smem)[wid].pen;
+  double* cs = reinterpret_cast<BinWarp*>(smem)[wid].cs;
   Best b;
   b.init();
   const int nwarps = gridDim.x * (kBinThreads / 32);
   int t = blockIdx.x * (kBinThreads / 32) + wid;
+  // chunks of long columns first (their ticket latency overlaps the packed tiles)
+  for (; t < P.n_bchunks; t += nwarps)
+    lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
+  t -= P.n_bchunks;
   WTile Tn;
   if (t < P.n_btiles) Tn = P.btiles[t];
-  const unsigned le = (2u << lane) - 1u;
+  const int hwi = lane >> 3, sh = 4 * (lane & 7);   // head word and bit offset of my 4 slots
   for (; t < P.n_btiles; t += nwarps) {
     const WTile T = Tn;
     if (t + nwarps < P.n_btiles) Tn = P.btiles[t + nwarps];
     const int nc = T.ncols, len = T.e1 - T.e0;
-    const int* __restrict__ ridx = P.row_idx + T.e0;
-    const double* __restrict__ rval = P.val + T.e0;
-    // column data of lane c (issued before the slot loads are consumed)
+    // slots 4 lane .. 4 lane + 3: one 16-byte index load, two 16-byte value loads
+    const bool act = 4 * lane < len;
+    int4 id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
+    double2 a01 = make_double2(0.0, 0.0), a23 = a01;
+    if (act) {
+      id = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0) + lane);
+      a01 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane);
+      a23 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane + 1);
+    }
+    // column data of lane c
     const int p = T.p0 + lane;
-    int cb = 0x7fffffff, ce = 0, j = 0, tb = 0;
+    int cb = 0x7fffffff, j = 0, tb = 0;
     double xb = 0.0;
     if (lane < nc) {
       cb = __ldg(P.col_ptr + p) - T.e0;
-      ce = __ldg(P.col_ptr + p + 1) - T.e0;
       j = __ldg(P.perm + p);
       tb = use_tabu ? __ldg(TB + p) : 0;
       xb = __ldg(X + p);
     }
+    double2 rv[4];
+    rv[0] = __ldg(RS + id.x);
+    rv[1] = __ldg(RS + id.y);
+    rv[2] = __ldg(RS + id.z);
+    rv[3] = __ldg(RS + id.w);
+    // column heads of the 128 slots (4 words) and x̄ of every column (one bit each)
+    const unsigned h0 = __reduce_or_sync(kFull, (cb >> 5) == 0 ? (1u << (cb & 31)) : 0u);
+    const unsigned h1 = __reduce_or_sync(kFull, (cb >> 5) == 1 ? (1u << (cb & 31)) : 0u);
+    const unsigned h2 = __reduce_or_sync(kFull, (cb >> 5) == 2 ? (1u << (cb & 31)) : 0u);
+    const unsigned h3 = __reduce_or_sync(kFull, (cb >> 5) == 3 ? (1u << (cb & 31)) : 0u);
+    const unsigned xm = __ballot_sync(kFull, xb != 0.0);
+    const unsigned hw = hwi == 0 ? h0 : (hwi == 1 ? h1 : (hwi == 2 ? h2 : h3));
+    const unsigned hnext = hwi == 0 ? h1 : (hwi == 1 ? h2 : (hwi == 2 ? h3 : 1u));
+    const int base = (hwi > 0 ? __popc(h0) : 0) + (hwi > 1 ? __popc(h1) : 0) + (hwi > 2 ? __popc(h2) : 0) - 1;
+    const unsigned hb = (hw >> sh) & 0xFu;                      // heads among my slots
+    const unsigned hn = (lane & 7) == 7 ? (hnext & 1u) : ((hw >> (sh + 4)) & 1u);   // head after them
+    // flip penalties and the within-lane segmented prefix
+    double sq[4];
+    int cq[4];
 #pragma unroll
-    for (int h = 0; h < kBinSlots / 2; ++h) {
-      int id[2];
-      double av[2];
+    for (int q = 0; q < 4; ++q) {
+      cq[q] = base + __popc(hw & ((2u << (sh + q)) - 1u));
+      const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
+      const double x = (double)((xm >> (cq[q] & 31)) & 1u);
+      const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
+      const double pk = penalty(w, r, r + a * (1.0 - 2.0 * x));   // inert rows: 0
+      sq[q] = (q == 0 || ((hb >> q) & 1u)) ? pk : sq[q - 1] + pk;
+    }
+    // columns crossing lanes: segmented scan of the lanes' last runs
+    double v = sq[3];
+    bool f = hb != 0u;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int k = lane + 32 * (2 * h + q);
-        id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
-        av[q] = k < len ? __ldcs(rval + k) : 0.0;
+    for (int off = 1; off < 32; off <<= 1) {
+      const double y = __shfl_up_sync(kFull, v, off);
+      const bool g = __shfl_up_sync(kFull, f, off);
+      if (lane >= off) {
+        if (!f) v += y;
+        f = f || g;
       }
-      double2 rv[2];
+    }
+    double carry = __shfl_up_sync(kFull, v, 1);
+    if (lane == 0 || (hb & 1u)) carry = 0.0;
+    // a slot that ends its column publishes the column's sum
 #pragma unroll
-      for (int q = 0; q < 2; ++q) rv[q] = __ldg(RS + id[q]);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int qq = 2 * h + q;
-        const int k = lane + 32 * qq;
-        // column of slot k: column starts in rounds < qq plus those at or before this lane
-        const unsigned hm = __reduce_or_sync(kFull, (cb >> 5) == qq ? (1u << (cb & 31)) : 0u);
-        const unsigned before = __reduce_add_sync(kFull, (cb >> 5) < qq ? 1u : 0u);
-        int col = (int)before + __popc(hm & le) - 1;
-        col = col < 0 ? 0 : col;
-        const double x = __shfl_sync(kFull, xb, col);
-        const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
-        if (k < len) pen[k] = penalty(w, r, r + av[q] * (1.0 - 2.0 * x));
-      }
+    for (int q = 0; q < 4; ++q) {
+      const bool cont = (hb & ((2u << q) - 1u)) == 0u;          // no head in slots 0..q: continues
+      const double tot = sq[q] + (cont ? carry : 0.0);
+      const bool end = (q < 3) ? (((hb >> (q + 1)) & 1u) != 0u) : (hn != 0u);
+      const int k = 4 * lane + q;
+      if (k < len && (end || k == len - 1)) cs[cq[q]] = tot;
     }
     __syncwarp();
-    if (lane < nc) {
-      double s = 0.0;
-      for (int e = cb; e < ce; ++e) s += pen[e];
-      finish_column_j(p, j, tb, xb, 1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
-    }
+    if (lane < nc) finish_column_j(p, j, tb, xb, 1.0 - xb, cs[lane], b, oxhat, oscore, kk, use_tabu);
     __syncwarp();
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + blockIdx.x, b);
+}
+
+// ------------------------------------------------------------------------------------------
+// general-column kernel
+// ------------------------------------------------------------------------------------------
+// k_eval_gen evaluates the packed general columns (and empty columns) with Algorithm 1 per
+// column, sort-free. For a candidate value v the score Algorithm 1 reports (the largest sigma of
+// the entries at v, R3) is sigma(v) = β + Σ_{entries e: t_e < v, or t_e = v with marker -1} δ_e
+// + α [v > x̄]. A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an
+// entry with δ = 0 adds nothing, so "marker -1" is δ > 0; for integer columns the condition is the
+// single compare key_e <= 2v with key_e = 2 t_e + [δ_e < 0] (exact while |t| < 2^51); continuous
+// columns compare (t, δ > 0). Phases: (1) slots in parallel: loads, gathers, lines 3-11 per entry;
+// (2) lane c: β, α of column c; (3) candidate slots in parallel: sigma by a compare-add pass over
+// the column's entries (lines 13-15: sort and scan as direct prefix sums); (4) lane c: line 16's
+// argmax with R4. Built lean like k_eval_bin: per-column data stay in the registers of lane c and
+// reach the slots by shuffles; slot -> column by a redux.sync head mask; per warp only key, delta,
+// (β, α | sigma) and flags live in shared memory.
+struct __align__(16) GenWarp {
+  double key[kWTileGen];
+  double D[kWTileGen];
+  union {
+    float2 AB[kWTileGen];
+    double sig[kWTileGen];
+  };
+  uint8_t f[kWTileGen];
+};
+constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
+
+__device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __restrict__ X,
+                                         const double2* __restrict__ RS, const int32_t* __restrict__ TB,
+                                         const WTile& T, int lane, GenWarp& S, Best& b, double* oxhat,
+                                         double* oscore, long long kk, int use_tabu) {
+  const int nc = T.ncols, nnz = T.e1 - T.e0;
+  const int nel = nnz + 2 * nc;
+  const int* __restrict__ ridx = P.row_idx + T.e0;
+  const double* __restrict__ rval = P.val + T.e0;
+  const int p = T.p0 + lane;
+  const unsigned le = (2u << lane) - 1u;
+  int cb = 0x7fffffff, ce = 0, j = 0, tb = 0;
+  double xb = 0.0, l = 0.0, u = 0.0;
+  int cont = 0;
+  if (lane < nc) {
+    cb = __ldg(P.col_ptr + p) - T.e0;
+    ce = __ldg(P.col_ptr + p + 1) - T.e0;
+    j = __ldg(P.perm + p);
+    tb = use_tabu ? __ldg(TB + p) : 0;
+    xb = __ldg(X + p);
+    l = __ldg(P.lb + p);
+    u = __ldg(P.ub + p);
+    cont = __ldg(P.vclass + p) == 3;
+  }
+  // (1) lines 3-11, slots in parallel; two slots of loads + gathers in flight per lane
+#pragma unroll
+  for (int h = 0; h < kWSlotsGen / 2; ++h) {
+    int id[2];
+    double av[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int k = lane + 32 * (2 * h + q);
+      id[q] = k < nnz ? __ldcs(ridx + k) : P.dummy_row;
+      av[q] = k < nnz ? __ldcs(rval + k) : 1.0;
+    }
+    double2 rv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) rv[q] = __ldg(RS + id[q]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int qq = 2 * h + q;
+      const int k = lane + 32 * qq;
+      const unsigned hm = __reduce_or_sync(kFull, (cb >> 5) == qq ? (1u << (cb & 31)) : 0u);
+      const unsigned before = __reduce_add_sync(kFull, (cb >> 5) < qq ? 1u : 0u);
+      int col = (int)before + __popc(hm & le) - 1;
+      const int bcol = (k - nnz) >> 1;
+      col = (k < nnz) ? (col < 0 ? 0 : col) : (bcol < 0 ? 0 : (bcol > 31 ? 31 : bcol));
+      const double x = __shfl_sync(kFull, xb, col);
+      const double lc = __shfl_sync(kFull, l, col);
+      const double uc = __shfl_sync(kFull, u, col);
+      const int cc = __shfl_sync(kFull, cont, col);
+      if (k >= nel) continue;
+      double key = 0.0, D = 0.0;
+      float A = 0.f, B = 0.f;
+      uint8_t f = 0;
+      if (k < nnz) {
+        const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
+        double t = breakpoint(x, r, av[q]);                        // line 3
+        if (!cc) t = (av[q] > 0.0) ? floor(t) : ceil(t);           // line 4
+        const bool pos = av[q] > 0.0, lt = x < t, gt = x > t;      // lines 5-11
+        const double hw2 = 0.5 * w;
+        D = pos ? (gt ? -hw2 : (lt ? -w : 0.0)) : (lt ? hw2 : (gt ? w : 0.0));
+        A = (float)(pos ? (gt ? w : 0.0) : (lt ? -hw2 : -w));
+        B = (float)(pos ? (lt ? 0.0 : -w) : (gt ? 0.0 : w));
+        key = cc ? t : 2.0 * t + (D < 0.0 ? 1.0 : 0.0);
+        if (x != t && t >= lc && t <= uc) f = GF_CAND;
+        if (!isfinite(r)) { D = 0.0; A = B = 0.f; f = 0; }       // inert rows (cutoff, padding)
+      } else {
+        const double v = ((k - nnz) & 1) ? uc : lc;
+        key = cc ? v : 2.0 * v;                                    // the candidate value, encoded
+        if (isfinite(v) && v != x) f = GF_CAND;
+      }
+      S.key[k] = key;
+      S.D[k] = D;
+      S.AB[k] = make_float2(A, B);
+      S.f[k] = f;
+    }
+  }
+  __syncwarp();
+  // (2) β, α of column `lane`
+  double beta = 0.0, alpha = 0.0;
+  if (lane < nc)
+    for (int e = cb; e < ce; ++e) {
+      const float2 ab = S.AB[e];
+      beta += (double)ab.x;
+      alpha += (double)ab.y;
+    }
+  __syncwarp();
+  // (3) sigma of every candidate slot (lines 13-15)
+#pragma unroll
+  for (int qq = 0; qq < kWSlotsGen; ++qq) {
+    const int k = lane + 32 * qq;
+    const unsigned hm = __reduce_or_sync(kFull, (cb >> 5) == qq ? (1u << (cb & 31)) : 0u);
+    const unsigned before = __reduce_add_sync(kFull, (cb >> 5) < qq ? 1u : 0u);
+    int col = (int)before + __popc(hm & le) - 1;
+    const int bcol = (k - nnz) >> 1;
+    col = (k < nnz) ? (col < 0 ? 0 : col) : (bcol < 0 ? 0 : (bcol > 31 ? 31 : bcol));
+    const int e0 = __shfl_sync(kFull, cb, col), e1 = __shfl_sync(kFull, ce, col);
+    const double bc = __shfl_sync(kFull, beta, col), ac = __shfl_sync(kFull, alpha, col);
+    const double x = __shfl_sync(kFull, xb, col);
+    const int cc = __shfl_sync(kFull, cont, col);
+    if (k >= nel || !(S.f[k] & GF_CAND)) continue;
+    const double kv = S.key[k];
+    const double v = cc ? kv : floor(0.5 * kv);
+    double acc = bc + (v > x ? ac : 0.0);
+    if (!cc) {
+      const double km = 2.0 * v;
+      for (int e = e0; e < e1; ++e) acc += (S.key[e] <= km) ? S.D[e] : 0.0;
+    } else {
+      for (int e = e0; e < e1; ++e) {
+        const double te = S.key[e], de = S.D[e];
+        acc += (te < v || (te == v && de > 0.0)) ? de : 0.0;
+      }
+    }
+    S.sig[k] = acc;
+  }
+  __syncwarp();
+  // (4) argmax per column (R3, R4)
+  if (lane < nc) {
+    double bs = -INFINITY, bv = xb;
+    for (int e = cb; e < ce + 2; ++e) {
+      const int k = (e < ce) ? e : nnz + 2 * lane + (e - ce);
+      if (!(S.f[k] & GF_CAND)) continue;
+      const double kv = S.key[k];
+      const double v = cont ? kv : floor(0.5 * kv);
+      const double sg = S.sig[k];
+      if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
+    }
+    finish_column_j(p, j, tb, xb, bv, bs, b, oxhat, oscore, kk, use_tabu);
+  }
+  __syncwarp();
+}
+
+// A warp chunk of a long general integer column with domain [l, u], dom = u - l + 1 <= kBucketMax:
+// the sort of line 13 becomes a counting pass. D[v-l] collects the marker -1 deltas at v and the
+// marker +1 deltas at v-1, so sigma(v) = β + Σ_{v' <= v} D[v'] + α [v > x̄]. Every
+// chunk adds its entries into the column's accumulators (D, β, α, candidate bits) in walker
+// scratch. Breakpoints of a long column crowd onto few values, so the additions are aggregated
+// per warp first (lanes with equal buckets: __match_any_sync, the lowest lane adds the group's
+// sum), which bounds the same-address atomics per bucket by one per 32 entries. The last chunk
+// (ticket) scans D in coalesced rounds of 32 buckets, takes line 16's argmax with R4 and zeroes
+// the accumulators for the next pass.
+__device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                           const double* __restrict__ X, const double2* __restrict__ RS,
+                                           const int32_t* __restrict__ TB, const WTile& T, int lane,
+                                           double* stage, Best& b, double* oxhat, double* oscore,
+                                           long long kk, int use_tabu) {
+  const LongCol L = P.lcols[T.e1];
+  const int p = T.p0, dom = L.dom, len = T.ncols;
+  const int* __restrict__ ridx = P.row_idx + T.e0;
+  const double* __restrict__ rval = P.val + T.e0;
+  const double xb = __ldg(X + p), l = __ldg(P.lb + p), u = __ldg(P.ub + p);
+  double* Dg = Wk.lscr + (size_t)walker * Wk.lss + L.scr;   // [dom + 1]
+  double* BA = Dg + dom + 1;                                 // β, α
+  unsigned* Cw = reinterpret_cast<unsigned*>(BA + 2);        // candidate bits
+  int id[kWSlotsGen];
+  double av[kWSlotsGen];
+#pragma unroll
+  for (int q = 0; q < kWSlotsGen; ++q) {
+    const int k = lane + 32 * q;
+    id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
+    av[q] = k < len ? __ldcs(rval + k) : 1.0;
+  }
+  double2 rv[kWSlotsGen];
+#pragma unroll
+  for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + id[q]);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  double beta = 0.0, alpha = 0.0;
+#pragma unroll
+  for (int q = 0; q < kWSlotsGen; ++q) {
+    const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
+    const Elem el = emit(xb, r, av[q], w, 1);   // inert rows emit nothing
+    beta += el.beta;
+    alpha += el.alpha;
+    const double t = el.t;
+    int bq = -1, cq = -1;
+    double dq = 0.0;
+    if (el.valid) {
+      if (t >= l && t <= u && t != xb) cq = (int)(t - l);
+      if (t < l) beta += el.delta;
+      else if (!el.plus) { if (t <= u) { bq = (int)(t - l); dq = el.delta; } }
+      else if (t < u) { bq = (int)(t - l) + 1; dq = el.delta; }
+    }
+    // bucket deltas: one atomic per distinct bucket of the 32 entries
+    const unsigned mD = __match_any_sync(kFull, bq);
+    stage[lane] = dq;
+    __syncwarp();
+    if (bq >= 0 && (mD & lt_mask) == 0) {
+      double sum = dq;
+      for (unsigned mm = mD & (mD - 1); mm; mm &= mm - 1) sum += stage[__ffs(mm) - 1];
+      atomicAdd(Dg + bq, sum);
+    }
+    __syncwarp();
+    // candidate bits: one OR per distinct word, skipped once the bits are set
+    const int wq = cq >= 0 ? (cq >> 5) : -1;
+    const unsigned mC = __match_any_sync(kFull, wq);
+    const unsigned bits = __reduce_or_sync(mC, cq >= 0 ? (1u << (cq & 31)) : 0u);
+    if (wq >= 0 && (mC & lt_mask) == 0 && (__ldcg(Cw + wq) & bits) != bits) atomicOr(Cw + wq, bits);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    beta += __shfl_xor_sync(kFull, beta, off);
+    alpha += __shfl_xor_sync(kFull, alpha, off);
+  }
+  int last = 0;
+  if (L.nchunks > 1) {   // every lane's additions are visible before the ticket
+    __threadfence();
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (L.nchunks == 1) {
+      last = 1;
+    } else {
+      unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.e1;
+      if (beta != 0.0) atomicAdd(BA, beta);
+      if (alpha != 0.0) atomicAdd(BA + 1, alpha);
+      __threadfence();
+      last = atomicAdd(cnt, 1u) == (unsigned)(L.nchunks - 1);
+      if (last) *cnt = 0u;
+    }
+  }
+  last = __shfl_sync(kFull, last, 0);
+  if (!last) return;
+  __threadfence();
+  double B = beta, A = alpha;
+  if (L.nchunks > 1) {
+    B = __ldcg(BA);
+    A = __ldcg(BA + 1);
+  }
+  __syncwarp();
+  if (lane == 0) { BA[0] = 0.0; BA[1] = 0.0; Dg[dom] = 0.0; }
+  // line 14: prefix sums of D in coalesced rounds of 32 buckets; line 16 with R4
+  double carry = 0.0, bs = -INFINITY, bv = xb;
+  for (int base = 0; base < dom; base += 32) {
+    const int q = base + lane;
+    const double d = q < dom ? __ldcg(Dg + q) : 0.0;
+    const unsigned cw = __ldcg(Cw + (base >> 5));
+    double incl = d;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double y = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const double pre = carry + incl;
+    carry = __shfl_sync(kFull, pre, 31);
+    if (q < dom) {
+      Dg[q] = 0.0;
+      const double v = l + (double)q;
+      const bool cand = ((cw >> lane) & 1u) || q == 0 || q == dom - 1;
+      if (cand && v != xb) {   // the bounds are always candidates (R2), x̄ never
+        const double sig = B + pre + (v > xb ? A : 0.0);
+        if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
+      }
+    }
+    if (lane == 0) Cw[base >> 5] = 0u;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double so = __shfl_xor_sync(kFull, bs, off), vo = __shfl_xor_sync(kFull, bv, off);
+    if (better_shift(so, vo, bs, bv, xb)) { bs = so; bv = vo; }
+  }
+  if (lane == 0)
+    finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, bv, bs, b, oxhat,
+                    oscore, kk, use_tabu);
+}
+
+__global__ void __launch_bounds__(kGenThreads, 4) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
+                                                              double* oscore, int part_base) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Best sm_b[32];
+  const int walker = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const WalkerScalars* sc = Wk.sc + walker;
+  const double* __restrict__ X = Wk.x + (size_t)walker * Wk.xs;
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)walker * Wk.rss);
+  const int32_t* __restrict__ TB = Wk.tabu + (size_t)walker * Wk.ts;
+  const long long kk = sc->k;
+  const int use_tabu = Wk.use_tabu;
+  GenWarp& S = reinterpret_cast<GenWarp*>(smem)[wid];
+  TileCtx C;
+  C.x = X;
+  C.rs = Wk.rs + (size_t)walker * Wk.rss;
+  C.tabu = TB;
+  C.k = kk;
+  C.use_tabu = use_tabu;
+  C.oxhat = oxhat;
+  C.oscore = oscore;
+  Best b;
+  b.init();
+  const int nwarps = gridDim.x * (kGenThreads / 32);
+  int t = blockIdx.x * (kGenThreads / 32) + wid;
+  // chunks of long columns first (their ticket latency overlaps the packed tiles)
+  for (; t < P.n_gchunks; t += nwarps)
+    lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, S.D, b, oxhat, oscore, kk, use_tabu);
+  t -= P.n_gchunks;
+  WTile Tn;
+  if (t < P.n_wtiles) Tn = P.wtiles[t];
+  for (; t < P.n_wtiles; t += nwarps) {
+    const WTile T = Tn;
+    if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];
+    if (T.kind == CC_GEN) gen_tile(P, X, RS, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
+    else wtile_empty(P, C, T, lane, b);
+  }
+  b = block_reduce_best(b, sm_b);
+  if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
 }
 
 // Outputs of fixed variables (internal [0, n_fixed)): (x̄, -inf) (R2 leaves no candidate).

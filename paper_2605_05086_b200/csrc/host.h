@@ -93,6 +93,8 @@ struct chap_problem {
   int eval_grid = 1;           // k_eval blocks for one walker
   int bin_occ = 1;             // resident k_eval_bin blocks per SM
   int bin_grid = 0;            // k_eval_bin blocks for one walker (0: no binary tiles)
+  int gen_occ = 1;
+  int gen_grid = 0;            // k_eval_gen blocks for one walker
   int rows_grid = 1;
   size_t lscr_per_walker = 1;   // doubles
   // eval workspace (one virtual walker)
@@ -137,6 +139,7 @@ struct chap_walkers {
   int apply_grid = 1;
   int eval_grid = 1;           // k_eval blocks per walker
   int bin_grid = 0;            // k_eval_bin blocks per walker
+  int gen_grid = 0;            // k_eval_gen blocks per walker
   ~chap_walkers() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ev_in) cudaEventDestroy(ev_in);
@@ -148,8 +151,8 @@ struct chap_walkers {
 
 namespace chap {
 // shared launch helpers (chap.cu)
-chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, double* oxhat,
-                        double* oscore, chap_move* best, cudaStream_t s);
+chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
+                        double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
 int grid_for(long long work, int threads, int cap);
 
 }  // namespace chap

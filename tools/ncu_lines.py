@@ -1,5 +1,5 @@
 """Aggregate an ncu source page (--print-source=cuda,sass --csv) per CUDA source line:
-instructions executed and warp-stall samples. Usage: python tools/ncu_lines.py page.csv [top]"""
+instructions executed and warp-stall samples. Usage: python tools/ncu_lines.py page.csv [top] [inst|stall]"""
 import csv
 import sys
 from collections import defaultdict
@@ -31,5 +31,6 @@ for r in rows:
 tot_i = sum(v[0] for v in agg.values()) or 1
 tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total instructions {tot_i:.3e}, stall samples {tot_s:.0f}")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+key = 0 if (len(sys.argv) > 3 and sys.argv[3] == "inst") else 1
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
     print(f"{k[0]}:{k[1]:<5d} inst {100*v[0]/tot_i:5.1f}%  stall {100*v[1]/tot_s:5.1f}%  {v[2]}")
