@@ -200,7 +200,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       cls[j] = CC_GEN;
     } else if (vclass[j] == 2 && std::isfinite(l[j]) && std::isfinite(u[j]) && u[j] - l[j] + 1.0 <= kBucketMax) {
       cls[j] = CC_LBKT;
-    } else if (d + 2 <= kGenmMax) {
+    } else if (d + 2 + 3 <= kGenmMax) {   // + up to 3 padding entries
       cls[j] = CC_GENM;
     } else {
       return fail(CHAP_ERR_UNSUPPORTED,
@@ -219,24 +219,40 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   });
   std::vector<int32_t> iperm(n);
   for (int32_t p = 0; p < n; ++p) iperm[perm[p]] = p;
-  // binary tiles (whole columns, <= kBinTile - 3 real nonzeros) and the inert padding that makes
-  // every binary tile start and end on a multiple of 4 nonzeros (TMA bulk copies need 16 B)
+  // packed tiles (whole columns: binary <= kBinTile - 3, general <= kWTileGen - 3 nonzeros, <= 32
+  // columns) and long columns start on a multiple of 4 nonzeros (16-byte vector loads): inert
+  // padding entries (the dummy row) are appended to the column before such a start
   std::vector<int32_t> pad(n, 0);
-  std::vector<std::pair<int32_t, int32_t>> bin_ranges;   // [p0, p1)
+  std::vector<std::pair<int32_t, int32_t>> bin_ranges, gen_ranges;   // [p0, p1)
   {
-    int32_t p = 0, off = 0;
-    while (p < n && cls[perm[p]] == CC_FIXED) off += deg[perm[p++]];
-    if (p > 0 && (off & 3)) { pad[p - 1] = (4 - (off & 3)) & 3; }
-    while (p < n && cls[perm[p]] == CC_BIN) {
-      int cnt = 0, tot = 0;
-      while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == CC_BIN &&
-             tot + deg[perm[p + cnt]] <= kBinTile - 3) {
-        tot += deg[perm[p + cnt]];
-        ++cnt;
+    int64_t off = 0;
+    auto align_at = [&](int32_t p) {
+      if (p > 0 && (off & 3)) {
+        const int a = (int)((4 - (off & 3)) & 3);
+        pad[p - 1] += a;
+        off += a;
       }
-      pad[p + cnt - 1] = (4 - (tot & 3)) & 3;
-      bin_ranges.push_back({p, p + cnt});
-      p += cnt;
+    };
+    int32_t p = 0;
+    while (p < n) {
+      const int k = cls[perm[p]];
+      if (k == CC_BIN || k == CC_GEN) {
+        align_at(p);
+        const int cap = (k == CC_BIN ? kBinTile : kWTileGen) - 3;
+        int cnt = 0, tot = 0;
+        while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k &&
+               tot + deg[perm[p + cnt]] <= cap) {
+          tot += deg[perm[p + cnt]];
+          ++cnt;
+        }
+        (k == CC_BIN ? bin_ranges : gen_ranges).push_back({p, p + cnt});
+        off += tot;
+        p += cnt;
+      } else {
+        if (k == CC_LBIN || k == CC_LBKT) align_at(p);
+        off += deg[perm[p]];
+        ++p;
+      }
     }
   }
   int64_t npad = 0;
@@ -307,6 +323,15 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     W.kind = (int8_t)CC_BIN;
     btiles.push_back(W);
   }
+  for (const auto& r : gen_ranges) {
+    WTile W{};
+    W.p0 = r.first;
+    W.e0 = col_ptr[r.first];
+    W.e1 = col_ptr[r.second];
+    W.ncols = (int16_t)(r.second - r.first);
+    W.kind = (int8_t)CC_GEN;
+    wtiles.push_back(W);
+  }
   int32_t n_long = 0;
   int64_t lscr = 0;
   int32_t p = 0;
@@ -314,15 +339,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     const int32_t j = perm[p];
     const int k = cls[j];
     if (k == CC_FIXED || k == CC_BIN) { ++p; continue; }
-    if (k == CC_GEN || k == CC_EMPTY) {
-      const int extra = (k == CC_GEN) ? 2 : 0;
-      const int cap = (k == CC_GEN) ? kWTileGen : kWTileNnz;
-      int cnt = 0, tot = 0;
-      while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k &&
-             tot + deg[perm[p + cnt]] + extra <= cap) {
-        tot += deg[perm[p + cnt]] + extra;
-        ++cnt;
-      }
+    if (k == CC_GEN) { ++p; continue; }   // packed in gen_ranges
+    if (k == CC_EMPTY) {
+      int cnt = 0;
+      while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k) ++cnt;
       WTile W{};
       W.p0 = p;
       W.e0 = col_ptr[p];

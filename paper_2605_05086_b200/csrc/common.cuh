@@ -24,6 +24,10 @@ constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kBinSlots = 4;                      // slots per lane of a pipelined binary tile
 constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per pipelined binary tile
 constexpr int kBinThreads = 256;                  // k_eval_bin block
+#ifndef CHAP_GEN_MINB
+#define CHAP_GEN_MINB 3
+#endif
+constexpr int kGenMinBlocks = CHAP_GEN_MINB;         // k_eval_gen resident blocks per SM (register budget)
 constexpr int kGenThreads = 256;                  // k_eval_gen block
 constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
 constexpr int kBucketMax = 4096;                  // max integer domain of a bucket-scanned column

@@ -637,40 +637,65 @@ __global__ void __launch_bounds__(kBinThreads, 4) k_eval_bin(DevProblem P, DevWa
 // ------------------------------------------------------------------------------------------
 // k_eval_gen evaluates the packed general columns (and empty columns) with Algorithm 1 per
 // column, sort-free. For a candidate value v the score Algorithm 1 reports (the largest sigma of
-// the entries at v, R3) is sigma(v) = β + Σ_{entries e: t_e < v, or t_e = v with marker -1} δ_e
-// + α [v > x̄]. A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an
-// entry with δ = 0 adds nothing, so "marker -1" is δ > 0; for integer columns the condition is the
-// single compare key_e <= 2v with key_e = 2 t_e + [δ_e < 0] (exact while |t| < 2^51); continuous
-// columns compare (t, δ > 0). Phases: (1) slots in parallel: loads, gathers, lines 3-11 per entry;
-// (2) lane c: β, α of column c; (3) candidate slots in parallel: sigma by a compare-add pass over
-// the column's entries (lines 13-15: sort and scan as direct prefix sums); (4) lane c: line 16's
-// argmax with R4. Built lean like k_eval_bin: per-column data stay in the registers of lane c and
-// reach the slots by shuffles; slot -> column by a redux.sync head mask; per warp only key, delta,
-// (β, α | sigma) and flags live in shared memory.
+// the entries at v, R3) is sigma(v) = β + α [v > x̄] + Σ_{entries e: t_e < v, or t_e = v with
+// marker -1} δ_e. A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an
+// entry with δ = 0 adds nothing, so "marker -1" is δ > 0, and the condition is the single compare
+// key_e <= v with key_e = t_e if δ_e > 0 and otherwise key_e = the next value above t_e (t_e + 1
+// on an integer column, the next double on a continuous one): nothing lies strictly between them,
+// so key_e <= v <=> t_e < v exactly.
+// A tile holds whole columns (<= 32) with <= kWTileGen nonzeros, starting on a multiple of 4;
+// lane l owns slots 4l..4l+3 (vector CSC loads, four row-state gathers in flight).
+// Phases: (1) slots: lines 3-11 per entry (key, δ, β/α parts, candidate flag) into shared memory,
+// and the candidate slots compacted in slot (= column) order; (2) work items of up to 4 candidates
+// of one column, one item per lane: one pass over the column's entries sums Σ_{key_e <= v} δ_e
+// for the item's candidates (lines 13-15 as direct prefix sums), and keeps the best candidate
+// above and the best below x̄ apart, so that α, known only at the end, is added once; (3) lane c:
+// β, α and the two bound candidates l, u (R2), then line 16's argmax with R4.
+// Every δ, β and α part is ±w or ±w/2 of a float weight, exact in float. When a tile's weights are
+// integers <= 2^16 and its keys and candidates integers of magnitude <= 2^22 (the common case of
+// the tabu dynamics on integer columns), every partial sum is a multiple of 1/2 below 2^23 in
+// magnitude and every key exact in float, so phases 2 and 3 run in exact float arithmetic;
+// otherwise in double.
+constexpr float kFastMag = 4194304.0f;   // 2^22
 struct __align__(16) GenWarp {
-  double key[kWTileGen];
-  double D[kWTileGen];
   union {
-    float2 AB[kWTileGen];
-    double sig[kWTileGen];
+    double kd[kWTileGen];  // key (double path)
+    float kf[kWTileGen];   // key clamped to ±(2^22 + 1) (float path)
   };
-  uint8_t f[kWTileGen];
+  float D[kWTileGen];      // δ
+  float2 AB[kWTileGen];    // β, α parts of the entry
+  double v[kWTileGen];     // the candidate value t_e
+  double it[2 * 32][4];    // per item: best below x̄ (σ', v), best above x̄ (σ', v)
+  double cx[32], cl[32], cu[32];
+  int cb[32], ce[32], cr[32], cn[32];   // slot range, first candidate rank, candidates
+  uint8_t cidx[kWTileGen]; // candidate slots, compacted
 };
 constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
+
+__device__ __forceinline__ double next_up(double t) {   // the next double above t
+  if (t == 0.0) return 4.9406564584124654e-324;
+  if (isinf(t)) return t;
+  const long long bits = __double_as_longlong(t);
+  return __longlong_as_double(t > 0.0 ? bits + 1 : bits - 1);
+}
 
 __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __restrict__ X,
                                          const double2* __restrict__ RS, const int32_t* __restrict__ TB,
                                          const WTile& T, int lane, GenWarp& S, Best& b, double* oxhat,
                                          double* oscore, long long kk, int use_tabu) {
-  const int nc = T.ncols, nnz = T.e1 - T.e0;
-  const int nel = nnz + 2 * nc;
-  const int* __restrict__ ridx = P.row_idx + T.e0;
-  const double* __restrict__ rval = P.val + T.e0;
+  const int nc = T.ncols, len = T.e1 - T.e0;
+  const bool act = 4 * lane < len;
+  int4 id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
+  double2 a01 = make_double2(1.0, 1.0), a23 = a01;
+  if (act) {
+    id = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0) + lane);
+    a01 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane);
+    a23 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane + 1);
+  }
+  // column data of lane c
   const int p = T.p0 + lane;
-  const unsigned le = (2u << lane) - 1u;
-  int cb = 0x7fffffff, ce = 0, j = 0, tb = 0;
+  int cb = 0x7fffffff, ce = 0, j = 0, tb = 0, cint = 1;
   double xb = 0.0, l = 0.0, u = 0.0;
-  int cont = 0;
   if (lane < nc) {
     cb = __ldg(P.col_ptr + p) - T.e0;
     ce = __ldg(P.col_ptr + p + 1) - T.e0;
@@ -679,111 +704,214 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
     xb = __ldg(X + p);
     l = __ldg(P.lb + p);
     u = __ldg(P.ub + p);
-    cont = __ldg(P.vclass + p) == 3;
+    cint = __ldg(P.vclass + p) != 3;
   }
-  // (1) lines 3-11, slots in parallel; two slots of loads + gathers in flight per lane
-#pragma unroll
-  for (int h = 0; h < kWSlotsGen / 2; ++h) {
-    int id[2];
-    double av[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int k = lane + 32 * (2 * h + q);
-      id[q] = k < nnz ? __ldcs(ridx + k) : P.dummy_row;
-      av[q] = k < nnz ? __ldcs(rval + k) : 1.0;
-    }
-    double2 rv[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) rv[q] = __ldg(RS + id[q]);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int qq = 2 * h + q;
-      const int k = lane + 32 * qq;
-      const unsigned hm = __reduce_or_sync(kFull, (cb >> 5) == qq ? (1u << (cb & 31)) : 0u);
-      const unsigned before = __reduce_add_sync(kFull, (cb >> 5) < qq ? 1u : 0u);
-      int col = (int)before + __popc(hm & le) - 1;
-      const int bcol = (k - nnz) >> 1;
-      col = (k < nnz) ? (col < 0 ? 0 : col) : (bcol < 0 ? 0 : (bcol > 31 ? 31 : bcol));
-      const double x = __shfl_sync(kFull, xb, col);
-      const double lc = __shfl_sync(kFull, l, col);
-      const double uc = __shfl_sync(kFull, u, col);
-      const int cc = __shfl_sync(kFull, cont, col);
-      if (k >= nel) continue;
-      double key = 0.0, D = 0.0;
-      float A = 0.f, B = 0.f;
-      uint8_t f = 0;
-      if (k < nnz) {
-        const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
-        double t = breakpoint(x, r, av[q]);                        // line 3
-        if (!cc) t = (av[q] > 0.0) ? floor(t) : ceil(t);           // line 4
-        const bool pos = av[q] > 0.0, lt = x < t, gt = x > t;      // lines 5-11
-        const double hw2 = 0.5 * w;
-        D = pos ? (gt ? -hw2 : (lt ? -w : 0.0)) : (lt ? hw2 : (gt ? w : 0.0));
-        A = (float)(pos ? (gt ? w : 0.0) : (lt ? -hw2 : -w));
-        B = (float)(pos ? (lt ? 0.0 : -w) : (gt ? 0.0 : w));
-        key = cc ? t : 2.0 * t + (D < 0.0 ? 1.0 : 0.0);
-        if (x != t && t >= lc && t <= uc) f = GF_CAND;
-        if (!isfinite(r)) { D = 0.0; A = B = 0.f; f = 0; }       // inert rows (cutoff, padding)
-      } else {
-        const double v = ((k - nnz) & 1) ? uc : lc;
-        key = cc ? v : 2.0 * v;                                    // the candidate value, encoded
-        if (isfinite(v) && v != x) f = GF_CAND;
-      }
-      S.key[k] = key;
-      S.D[k] = D;
-      S.AB[k] = make_float2(A, B);
-      S.f[k] = f;
-    }
-  }
-  __syncwarp();
-  // (2) β, α of column `lane`
-  double beta = 0.0, alpha = 0.0;
-  if (lane < nc)
-    for (int e = cb; e < ce; ++e) {
-      const float2 ab = S.AB[e];
-      beta += (double)ab.x;
-      alpha += (double)ab.y;
-    }
-  __syncwarp();
-  // (3) sigma of every candidate slot (lines 13-15)
-#pragma unroll
-  for (int qq = 0; qq < kWSlotsGen; ++qq) {
-    const int k = lane + 32 * qq;
-    const unsigned hm = __reduce_or_sync(kFull, (cb >> 5) == qq ? (1u << (cb & 31)) : 0u);
-    const unsigned before = __reduce_add_sync(kFull, (cb >> 5) < qq ? 1u : 0u);
-    int col = (int)before + __popc(hm & le) - 1;
-    const int bcol = (k - nnz) >> 1;
-    col = (k < nnz) ? (col < 0 ? 0 : col) : (bcol < 0 ? 0 : (bcol > 31 ? 31 : bcol));
-    const int e0 = __shfl_sync(kFull, cb, col), e1 = __shfl_sync(kFull, ce, col);
-    const double bc = __shfl_sync(kFull, beta, col), ac = __shfl_sync(kFull, alpha, col);
-    const double x = __shfl_sync(kFull, xb, col);
-    const int cc = __shfl_sync(kFull, cont, col);
-    if (k >= nel || !(S.f[k] & GF_CAND)) continue;
-    const double kv = S.key[k];
-    const double v = cc ? kv : floor(0.5 * kv);
-    double acc = bc + (v > x ? ac : 0.0);
-    if (!cc) {
-      const double km = 2.0 * v;
-      for (int e = e0; e < e1; ++e) acc += (S.key[e] <= km) ? S.D[e] : 0.0;
-    } else {
-      for (int e = e0; e < e1; ++e) {
-        const double te = S.key[e], de = S.D[e];
-        acc += (te < v || (te == v && de > 0.0)) ? de : 0.0;
-      }
-    }
-    S.sig[k] = acc;
-  }
-  __syncwarp();
-  // (4) argmax per column (R3, R4)
+  double2 rv[4];
+  rv[0] = __ldg(RS + id.x);
+  rv[1] = __ldg(RS + id.y);
+  rv[2] = __ldg(RS + id.z);
+  rv[3] = __ldg(RS + id.w);
   if (lane < nc) {
+    S.cx[lane] = xb;
+    S.cl[lane] = l;
+    S.cu[lane] = u;
+    S.cb[lane] = cb;
+    S.ce[lane] = ce;
+  }
+  const unsigned im = __ballot_sync(kFull, cint != 0);
+  // float path: integer columns, finite bounds within ±2^22 (as candidates)
+  bool fast = lane >= nc || (cint && (!isfinite(l) || fabs(l) <= (double)kFastMag) &&
+                             (!isfinite(u) || fabs(u) <= (double)kFastMag));
+  const int hwi = lane >> 3, sh = 4 * (lane & 7);
+  const unsigned h0 = __reduce_or_sync(kFull, (cb >> 5) == 0 ? (1u << (cb & 31)) : 0u);
+  const unsigned h1 = __reduce_or_sync(kFull, (cb >> 5) == 1 ? (1u << (cb & 31)) : 0u);
+  const unsigned h2 = __reduce_or_sync(kFull, (cb >> 5) == 2 ? (1u << (cb & 31)) : 0u);
+  const unsigned h3 = __reduce_or_sync(kFull, (cb >> 5) == 3 ? (1u << (cb & 31)) : 0u);
+  const unsigned hw = hwi == 0 ? h0 : (hwi == 1 ? h1 : (hwi == 2 ? h2 : h3));
+  const int base = (hwi > 0 ? __popc(h0) : 0) + (hwi > 1 ? __popc(h1) : 0) + (hwi > 2 ? __popc(h2) : 0) - 1;
+  __syncwarp();
+  // (1) lines 3-11 per entry
+  unsigned cmask = 0u;
+  double kq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = 4 * lane + q;
+    const int c = base + __popc(hw & ((2u << (sh + q)) - 1u));
+    const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
+    const double x = S.cx[c], lc = S.cl[c], uc = S.cu[c];
+    const double r = rv[q].x;
+    const float wf = __int_as_float((int)__double2loint(rv[q].y));
+    const bool ci = (im >> c) & 1u;
+    double t = breakpoint(x, r, a);                                  // line 3
+    if (ci) t = (a > 0.0) ? floor(t) : ceil(t);                      // line 4
+    const bool pos = a > 0.0, lt = x < t, gt = x > t;                // lines 5-11
+    const float hw2 = 0.5f * wf;
+    float D = pos ? (gt ? -hw2 : (lt ? -wf : 0.f)) : (lt ? hw2 : (gt ? wf : 0.f));
+    float Bp = pos ? (gt ? wf : 0.f) : (lt ? -hw2 : -wf);            // β part
+    float Ap = pos ? (lt ? 0.f : -wf) : (gt ? 0.f : wf);             // α part
+    const bool fin = isfinite(r) && k < len;                         // inert rows (cutoff, padding)
+    if (!fin) { D = 0.f; Ap = Bp = 0.f; }
+    const bool cand = fin && x != t && t >= lc && t <= uc;           // R2, R5
+    if (cand) cmask |= 1u << q;
+    if (fin && !(wf == truncf(wf) && wf <= 65536.f)) fast = false;
+    if (cand && !(fabs(t) <= (double)kFastMag)) fast = false;
+    kq[q] = D > 0.f ? t : (ci ? t + 1.0 : next_up(t));
+    S.D[k] = D;
+    S.v[k] = t;
+    S.AB[k] = make_float2(Bp, Ap);
+  }
+  fast = __all_sync(kFull, fast);
+  if (fast) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      S.kf[4 * lane + q] = (float)fmin(fmax(kq[q], -(double)kFastMag - 1.0), (double)kFastMag + 1.0);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) S.kd[4 * lane + q] = kq[q];
+  }
+  // compaction of the candidate slots (slot order = column order)
+  const int cnt = __popc(cmask);
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += y;
+  }
+  {
+    int rk = incl - cnt;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if ((cmask >> q) & 1u) S.cidx[rk++] = (uint8_t)(4 * lane + q);
+  }
+  const int n_cand = __shfl_sync(kFull, incl, 31);
+  auto rank_before = [&](int slot) -> int {   // candidates in slots < slot (all lanes call)
+    const int ln = min(slot >> 2, 31);
+    const int ex = __shfl_sync(kFull, incl - cnt, ln);
+    const unsigned cm = __shfl_sync(kFull, cmask, ln);
+    return slot >= 128 ? n_cand : ex + __popc(cm & ((1u << (slot & 3)) - 1u));
+  };
+  const int r0 = rank_before(lane < nc ? cb : 0);
+  const int r1 = rank_before(lane < nc ? ce : 0);
+  const int ncand = r1 - r0;
+  const int nit = lane < nc ? (ncand + 3) >> 2 : 0;   // work items of column `lane`
+  int ip = nit;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(kFull, ip, off);
+    if (lane >= off) ip += y;
+  }
+  const int n_items = __shfl_sync(kFull, ip, 31);
+  ip -= nit;   // first item of column `lane`
+  if (lane < nc) {
+    S.cr[lane] = r0;
+    S.cn[lane] = ncand;
+  }
+  __syncwarp();
+  // (2) one work item per lane
+  for (int i0 = 0; i0 < n_items; i0 += 32) {
+    const int I = i0 + lane;
+    // the item's column: the last column c with ip_c <= I (ip is nondecreasing over the lanes)
+    int c = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int ct = c + step;
+      const int ipt = __shfl_sync(kFull, ip, ct & 31);
+      if (ct < 32 && ipt <= I) c = ct;
+    }
+    const int g = I - __shfl_sync(kFull, ip, c);   // item of the column
+    if (I < n_items) {
+      const int e0 = S.cb[c], e1 = S.ce[c], r0c = S.cr[c] + 4 * g, r1c = min(S.cr[c] + S.cn[c], r0c + 4);
+      const double x = S.cx[c];
+      double vq[4], acc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) vq[q] = (r0c + q < r1c) ? S.v[S.cidx[r0c + q]] : -INFINITY;
+      if (fast) {
+        float vf[4], af[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          vf[q] = (r0c + q < r1c) ? (float)vq[q] : -INFINITY;
+          af[q] = 0.f;
+        }
+        for (int e = e0; e < e1; ++e) {
+          const float ke = S.kf[e], de = S.D[e];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ke <= vf[q]) af[q] += de;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = (double)af[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = 0.0;
+        for (int e = e0; e < e1; ++e) {
+          const double ke = S.kd[e], de = (double)S.D[e];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ke <= vq[q]) acc[q] += de;
+        }
+      }
+      double slt = -INFINITY, vlt = x, sgt = -INFINITY, vgt = x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (r0c + q >= r1c) continue;
+        if (vq[q] > x) {
+          if (better_shift(acc[q], vq[q], sgt, vgt, x)) { sgt = acc[q]; vgt = vq[q]; }
+        } else if (better_shift(acc[q], vq[q], slt, vlt, x)) {
+          slt = acc[q]; vlt = vq[q];
+        }
+      }
+      S.it[I][0] = slt;
+      S.it[I][1] = vlt;
+      S.it[I][2] = sgt;
+      S.it[I][3] = vgt;
+    }
+  }
+  __syncwarp();
+  // (3) lane c: β, α, the bounds (R2), line 16 over the column's items and bounds (R4)
+  if (lane < nc) {
+    double beta, alpha, pl, pu;
+    if (fast) {
+      const float lf = isfinite(l) ? (float)l : -INFINITY, uf = isfinite(u) ? (float)u : INFINITY;
+      float bf = 0.f, af = 0.f, plf = 0.f, puf = 0.f;
+      for (int e = cb; e < ce; ++e) {
+        const float2 ab = S.AB[e];
+        const float ke = S.kf[e], de = S.D[e];
+        bf += ab.x;
+        af += ab.y;
+        if (ke <= lf) plf += de;
+        if (ke <= uf) puf += de;
+      }
+      beta = bf; alpha = af; pl = plf; pu = puf;
+    } else {
+      beta = alpha = pl = pu = 0.0;
+      for (int e = cb; e < ce; ++e) {
+        const float2 ab = S.AB[e];
+        const double ke = S.kd[e], de = (double)S.D[e];
+        beta += (double)ab.x;
+        alpha += (double)ab.y;
+        if (ke <= l) pl += de;
+        if (ke <= u) pu += de;
+      }
+    }
     double bs = -INFINITY, bv = xb;
-    for (int e = cb; e < ce + 2; ++e) {
-      const int k = (e < ce) ? e : nnz + 2 * lane + (e - ce);
-      if (!(S.f[k] & GF_CAND)) continue;
-      const double kv = S.key[k];
-      const double v = cont ? kv : floor(0.5 * kv);
-      const double sg = S.sig[k];
-      if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
+    for (int i = ip; i < ip + nit; ++i) {
+      const double s0 = S.it[i][0], s1 = S.it[i][2];
+      if (s0 != -INFINITY) {
+        const double sg = beta + s0, v = S.it[i][1];
+        if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
+      }
+      if (s1 != -INFINITY) {
+        const double sg = beta + alpha + s1, v = S.it[i][3];
+        if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
+      }
+    }
+    if (isfinite(l) && l != xb) {   // l < x̄: no α
+      const double sg = beta + pl;
+      if (better_shift(sg, l, bs, bv, xb)) { bs = sg; bv = l; }
+    }
+    if (isfinite(u) && u != xb) {   // u > x̄
+      const double sg = beta + alpha + pu;
+      if (better_shift(sg, u, bs, bv, xb)) { bs = sg; bv = u; }
     }
     finish_column_j(p, j, tb, xb, bv, bs, b, oxhat, oscore, kk, use_tabu);
   }
@@ -923,7 +1051,7 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
                     oscore, kk, use_tabu);
 }
 
-__global__ void __launch_bounds__(kGenThreads, 4) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
+__global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
                                                               double* oscore, int part_base) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
@@ -950,7 +1078,7 @@ __global__ void __launch_bounds__(kGenThreads, 4) k_eval_gen(DevProblem P, DevWa
   int t = blockIdx.x * (kGenThreads / 32) + wid;
   // chunks of long columns first (their ticket latency overlaps the packed tiles)
   for (; t < P.n_gchunks; t += nwarps)
-    lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, S.D, b, oxhat, oscore, kk, use_tabu);
+    lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, &S.it[0][0], b, oxhat, oscore, kk, use_tabu);
   t -= P.n_gchunks;
   WTile Tn;
   if (t < P.n_wtiles) Tn = P.wtiles[t];

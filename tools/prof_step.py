@@ -15,7 +15,7 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 cfg = sys.argv[3] if len(sys.argv) > 3 else "G"
 inst = {"G": synth.mixed, "S": synth.setcover, "P": synth.packing,
         "Gbin": lambda: synth.mixed(p_binary=1.0, p_bounded=0.0),
-        "Gnl": lambda: synth.mixed(n_long=0)}[cfg]()
+        "Gnl": lambda: synth.mixed(n_long=0), "Gint": lambda: synth.mixed(p_binary=0.0, p_bounded=1.0)}[cfg]()
 P = chap.Problem.from_instance(inst)
 W = 64 if cfg == "P" else 1
 x0 = np.stack([synth.x_lower(inst)] * W) if cfg != "P" else \
