@@ -371,14 +371,15 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     // accumulators (binary: the flip sum; bounded integer: bucket deltas, candidate bits, β, α);
     // the column's last chunk finalises
     const int d = col_ptr[p + 1] - col_ptr[p];   // incl. any padding (inert)
-    const int nch = std::max(1, (d + kWChunk - 1) / kWChunk);
+    const int csz = (k == CC_LBKT) ? kBktChunk : kWChunk;
+    const int nch = std::max(1, (d + csz - 1) / csz);
     const int dom = (k == CC_LBKT) ? (int)(u[j] - l[j] + 1.0) : 0;
     for (int q = 0; q < nch; ++q) {
       WTile W{};
       W.p0 = p;
-      W.e0 = col_ptr[p] + q * kWChunk;
+      W.e0 = col_ptr[p] + q * csz;
       W.e1 = n_long;
-      W.ncols = (int16_t)(std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * kWChunk) - W.e0);
+      W.ncols = (int16_t)(std::min(col_ptr[p + 1], col_ptr[p] + (q + 1) * csz) - W.e0);
       W.kind = (int8_t)k;
       (k == CC_LBIN ? bchunks : gchunks).push_back(W);
     }

@@ -69,7 +69,8 @@ struct LongCol {
   int32_t nchunks;
   int32_t dom;       // CC_LBKT: u - l + 1
 };
-constexpr int kWChunk = 128;                      // nonzeros per warp chunk of a long column
+constexpr int kWChunk = 128;                      // nonzeros per warp chunk of a long binary column
+constexpr int kBktChunk = 512;                    // nonzeros per warp chunk of a long bounded-integer column
 
 // A block tile (chunk of a long column, or one column sorted by the whole block).
 struct Tile {

@@ -671,6 +671,10 @@ struct __align__(16) GenWarp {
   uint8_t cidx[kWTileGen]; // candidate slots, compacted
 };
 constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
+// a long bounded-integer chunk uses the warp's GenWarp area: int32 histogram, candidate words, stage
+constexpr int kWarpDom = 1024;
+constexpr int kLbktHistBytes = 4 * (kWarpDom + 1 + 3);
+static_assert(kLbktHistBytes + kWarpDom / 8 + 32 * 8 <= (int)sizeof(GenWarp), "LBKT scratch exceeds GenWarp");
 
 __device__ __forceinline__ double next_up(double t) {   // the next double above t
   if (t == 0.0) return 4.9406564584124654e-324;
@@ -918,19 +922,20 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
   __syncwarp();
 }
 
-// A warp chunk of a long general integer column with domain [l, u], dom = u - l + 1 <= kBucketMax:
-// the sort of line 13 becomes a counting pass. D[v-l] collects the marker -1 deltas at v and the
-// marker +1 deltas at v-1, so sigma(v) = β + Σ_{v' <= v} D[v'] + α [v > x̄]. Every
-// chunk adds its entries into the column's accumulators (D, β, α, candidate bits) in walker
-// scratch. Breakpoints of a long column crowd onto few values, so the additions are aggregated
-// per warp first (lanes with equal buckets: __match_any_sync, the lowest lane adds the group's
-// sum), which bounds the same-address atomics per bucket by one per 32 entries. The last chunk
-// (ticket) scans D in coalesced rounds of 32 buckets, takes line 16's argmax with R4 and zeroes
-// the accumulators for the next pass.
+// A warp chunk (<= kBktChunk nonzeros) of a long general integer column with domain [l, u],
+// dom = u - l + 1 <= kBucketMax: the sort of line 13 becomes a counting pass. D[v-l] collects the
+// marker -1 deltas at v and the marker +1 deltas at v-1, so sigma(v) = β + Σ_{v' <= v} D[v'] +
+// α [v > x̄]. Every chunk adds its entries into the column's accumulators (D, β, α,
+// candidate bits) in walker scratch. Breakpoints of a long column crowd onto few values, so a
+// chunk first counts into a warp-private shared-memory histogram of 2δ in int32 (exact while the
+// weights are integers <= 2^16: |Σ 2δ| <= 2^27) and then adds each nonzero bucket once; rounds
+// with other weights, or domains above kWarpDom, aggregate per warp instead (lanes with equal
+// buckets: __match_any_sync, the lowest lane adds the group's sum). The last chunk (ticket) scans D
+// in coalesced rounds of 32 buckets, takes line 16's argmax with R4 and zeroes the accumulators.
 __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
                                            const int32_t* __restrict__ TB, const WTile& T, int lane,
-                                           double* stage, Best& b, double* oxhat, double* oscore,
+                                           unsigned char* wmem, Best& b, double* oxhat, double* oscore,
                                            long long kk, int use_tabu) {
   const LongCol L = P.lcols[T.e1];
   const int p = T.p0, dom = L.dom, len = T.ncols;
@@ -940,19 +945,37 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
   double* Dg = Wk.lscr + (size_t)walker * Wk.lss + L.scr;   // [dom + 1]
   double* BA = Dg + dom + 1;                                 // β, α
   unsigned* Cw = reinterpret_cast<unsigned*>(BA + 2);        // candidate bits
+  int* hist = reinterpret_cast<int*>(wmem);                              // [kWarpDom + 1]
+  unsigned* hcw = reinterpret_cast<unsigned*>(wmem + kLbktHistBytes);    // [kWarpDom / 32]
+  double* stage = reinterpret_cast<double*>(wmem + kLbktHistBytes + kWarpDom / 8);   // [32]
+  const bool local = dom <= kWarpDom;
+  const int nwords = (dom + 31) >> 5;
+  if (local) {
+    for (int q = lane; q <= dom; q += 32) hist[q] = 0;
+    for (int q = lane; q < nwords; q += 32) hcw[q] = 0u;
+    __syncwarp();
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
+  double beta = 0.0, alpha = 0.0;
+  for (int r0 = 0; r0 < len; r0 += 32 * kWSlotsGen) {
   int id[kWSlotsGen];
   double av[kWSlotsGen];
 #pragma unroll
   for (int q = 0; q < kWSlotsGen; ++q) {
-    const int k = lane + 32 * q;
+    const int k = r0 + lane + 32 * q;
     id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
     av[q] = k < len ? __ldcs(rval + k) : 1.0;
   }
   double2 rv[kWSlotsGen];
 #pragma unroll
   for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + id[q]);
-  const unsigned lt_mask = (1u << lane) - 1u;
-  double beta = 0.0, alpha = 0.0;
+  bool fast = local;
+#pragma unroll
+  for (int q = 0; q < kWSlotsGen; ++q) {
+    const float wf = __int_as_float((int)__double2loint(rv[q].y));
+    if (isfinite(rv[q].x) && !(wf == truncf(wf) && wf <= 65536.f)) fast = false;
+  }
+  fast = __all_sync(kFull, fast);
 #pragma unroll
   for (int q = 0; q < kWSlotsGen; ++q) {
     const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
@@ -967,6 +990,11 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
       if (t < l) beta += el.delta;
       else if (!el.plus) { if (t <= u) { bq = (int)(t - l); dq = el.delta; } }
       else if (t < u) { bq = (int)(t - l) + 1; dq = el.delta; }
+    }
+    if (fast) {
+      if (bq >= 0) atomicAdd(hist + bq, (int)(2.0 * dq));
+      if (cq >= 0) atomicOr(hcw + (cq >> 5), 1u << (cq & 31));
+      continue;
     }
     // bucket deltas: one atomic per distinct bucket of the 32 entries
     const unsigned mD = __match_any_sync(kFull, bq);
@@ -983,6 +1011,18 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     const unsigned mC = __match_any_sync(kFull, wq);
     const unsigned bits = __reduce_or_sync(mC, cq >= 0 ? (1u << (cq & 31)) : 0u);
     if (wq >= 0 && (mC & lt_mask) == 0 && (__ldcg(Cw + wq) & bits) != bits) atomicOr(Cw + wq, bits);
+  }
+  }
+  if (local) {   // one addition per nonzero bucket and candidate word
+    __syncwarp();
+    for (int q = lane; q <= dom; q += 32) {
+      const int h = hist[q];
+      if (h != 0) atomicAdd(Dg + q, 0.5 * (double)h);
+    }
+    for (int q = lane; q < nwords; q += 32) {
+      const unsigned c = hcw[q];
+      if (c != 0u && (__ldcg(Cw + q) & c) != c) atomicOr(Cw + q, c);
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -1078,7 +1118,8 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   int t = blockIdx.x * (kGenThreads / 32) + wid;
   // chunks of long columns first (their ticket latency overlaps the packed tiles)
   for (; t < P.n_gchunks; t += nwarps)
-    lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, &S.it[0][0], b, oxhat, oscore, kk, use_tabu);
+    lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
+  __syncwarp();
   t -= P.n_gchunks;
   WTile Tn;
   if (t < P.n_wtiles) Tn = P.wtiles[t];
