@@ -314,6 +314,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   std::vector<Tile> tiles;
   std::vector<WTile> wtiles, btiles, bchunks, gchunks;
   std::vector<LongCol> lcols;
+  std::vector<int32_t> lfin;
   for (const auto& r : bin_ranges) {
     WTile W{};
     W.p0 = r.first;
@@ -387,6 +388,9 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     L.scr = lscr;
     L.nchunks = nch;
     L.dom = dom;
+    L.p = p;
+    L.kind = k;
+    if (k == CC_LBKT || nch > 1) lfin.push_back(n_long);
     lcols.push_back(L);
     lscr += (k == CC_LBKT) ? ((int64_t)dom + 1 + 2 + (dom + 63) / 64) : 1;
     ++n_long;
@@ -439,6 +443,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_bchunks, bchunks));
   TRY(B.upload(&d_gchunks, gchunks));
   if (lcols.empty()) lcols.push_back(LongCol{});
+  int32_t* d_lfin;
+  TRY(B.upload(&d_lfin, lfin));
   TRY(B.upload(&d_lcols, lcols));
   DevProblem& D = P->dp;
   D.n = n;
@@ -464,6 +470,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.btiles = d_btiles;
   D.n_btiles = (int32_t)btiles.size();
   D.lcols = d_lcols;
+  D.lfin = d_lfin;
+  D.n_lfin = (int32_t)lfin.size();
   D.bchunks = d_bchunks;
   D.n_bchunks = (int32_t)bchunks.size();
   D.gchunks = d_gchunks;
@@ -477,7 +485,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval, kTileThreads, kTileSmem));
   P->eval_occ = std::max(1, occ);
-  P->eval_grid = std::max(1, std::min(std::max(D.n_tiles, 1), P->eval_occ * P->sm_count));
+  const int ework = std::max(std::max(D.n_tiles, (D.n_lfin + kTileWarps - 1) / kTileWarps), 1);
+  P->eval_grid = std::max(1, std::min(ework, P->eval_occ * P->sm_count));
   CUDA_TRY(cudaFuncSetAttribute(k_eval_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGenSmem));
   int gocc = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gocc, k_eval_gen, kGenThreads, kGenSmem));

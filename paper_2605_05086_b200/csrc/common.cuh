@@ -24,6 +24,10 @@ constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kBinSlots = 4;                      // slots per lane of a pipelined binary tile
 constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per pipelined binary tile
 constexpr int kBinThreads = 256;                  // k_eval_bin block
+#ifndef CHAP_BIN_MINB
+#define CHAP_BIN_MINB 4
+#endif
+constexpr int kBinMinBlocks = CHAP_BIN_MINB;
 #ifndef CHAP_GEN_MINB
 #define CHAP_GEN_MINB 3
 #endif
@@ -68,6 +72,8 @@ struct LongCol {
   int64_t scr;       // offset (doubles) of the accumulators in walker scratch
   int32_t nchunks;
   int32_t dom;       // CC_LBKT: u - l + 1
+  int32_t p;         // the column (internal order)
+  int32_t kind;      // CC_LBIN or CC_LBKT
 };
 constexpr int kWChunk = 128;                      // nonzeros per warp chunk of a long binary column
 constexpr int kBktChunk = 512;                    // nonzeros per warp chunk of a long bounded-integer column
@@ -145,6 +151,7 @@ struct DevProblem {
   const WTile* bchunks; int32_t n_bchunks;              // warp chunks of long binary columns
   const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns
   const LongCol* lcols;                                 // [n_long]
+  const int32_t* lfin; int32_t n_lfin;                  // long columns k_eval finishes
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   double auto_delta;
 };

@@ -396,71 +396,6 @@ __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_fl
 // the kernel
 // ------------------------------------------------------------------------------------------
 
-// grid = (blocks per walker, W). After its tiles every block publishes its best admissible move;
-// the last block of the walker reduces them (fixed order) to the decision.
-__global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalkers Wk, double* oxhat,
-                                                          double* oscore, chap_move* best_out,
-                                                          int part_base) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double sm_red[32];
-  __shared__ Best sm_b[32];
-  __shared__ int s_flag;
-  const int walker = blockIdx.y;
-  const WalkerScalars* sc = Wk.sc + walker;
-  TileCtx C;
-  C.x = Wk.x + (size_t)walker * Wk.xs;
-  C.rs = Wk.rs + (size_t)walker * Wk.rss;
-  C.tabu = Wk.tabu + (size_t)walker * Wk.ts;
-  C.k = sc->k;
-  C.use_tabu = Wk.use_tabu;
-  C.oxhat = oxhat;
-  C.oscore = oscore;
-  Best b;
-  b.init();
-  // block tiles: single-column sorts
-  for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x)
-    tile_genm(P, C, P.tiles[t], *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b);
-  __syncthreads();
-  // publish the block's best; the last block of this walker selects (PAPER.md:85, R6)
-  b = block_reduce_best(b, sm_b);
-  Cand* part = Wk.part + (size_t)walker * Wk.ps;
-  if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
-  if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
-  Best g;
-  g.init();
-  for (int q = threadIdx.x; q < part_base + (int)gridDim.x; q += blockDim.x) {
-    Best o;
-    o.s = __ldcg(&part[q].s);
-    o.v = __ldcg(&part[q].v);
-    o.j = __ldcg(&part[q].j);
-    o.p = __ldcg(&part[q].p);
-    g.take(o);
-  }
-  g = block_reduce_best(g, sm_b);
-  if (threadIdx.x == 0) {
-    WalkerScalars* scw = Wk.sc + walker;
-    const bool found = g.p >= 0;
-    Decision d;
-    d.move = (found && g.s > 0.0) ? 1 : 0;
-    d.p = g.p;
-    d.j = found ? g.j : -1;
-    d.pad = 0;
-    d.v = g.v;
-    d.s = found ? g.s : -INFINITY;
-    d.delta = d.move ? (g.v - C.x[g.p]) : 0.0;
-    scw->dec = d;
-    if (best_out) {
-      chap_move mv;
-      mv.j = d.move ? d.j : -1;
-      mv.pad = 0;
-      mv.v = d.move ? d.v : NAN;
-      mv.s = d.move ? d.s : -INFINITY;
-      best_out[walker] = mv;
-    }
-    Wk.sel_count[walker] = 0u;
-  }
-}
-
 // ------------------------------------------------------------------------------------------
 // binary kernel
 // ------------------------------------------------------------------------------------------
@@ -510,23 +445,16 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
   for (int off = 16; off > 0; off >>= 1) own += __shfl_xor_sync(kFull, own, off);
   if (lane != 0) return;
   const LongCol L = P.lcols[T.e1];
-  double s = own;
-  if (L.nchunks > 1) {
-    double* acc = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
-    unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.e1;
-    atomicAdd(acc, own);
-    __threadfence();
-    if (atomicAdd(cnt, 1u) != (unsigned)(L.nchunks - 1)) return;
-    __threadfence();
-    s = __ldcg(acc);
-    *acc = 0.0;
-    *cnt = 0u;
+  const double s = own;
+  if (L.nchunks > 1) {   // k_eval finishes the column after this kernel
+    atomicAdd(Wk.lscr + (size_t)walker * Wk.lss + L.scr, own);
+    return;
   }
   finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, 1.0 - xb, s, b, oxhat,
                   oscore, kk, use_tabu);
 }
 
-__global__ void __launch_bounds__(kBinThreads, 4) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
+__global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
                                                               double* oscore) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
@@ -547,9 +475,9 @@ __global__ void __launch_bounds__(kBinThreads, 4) k_eval_bin(DevProblem P, DevWa
   for (; t < P.n_bchunks; t += nwarps)
     lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
   t -= P.n_bchunks;
+  const int hwi = lane >> 3, sh = 4 * (lane & 7);   // head word and bit offset of my 4 slots
   WTile Tn;
   if (t < P.n_btiles) Tn = P.btiles[t];
-  const int hwi = lane >> 3, sh = 4 * (lane & 7);   // head word and bit offset of my 4 slots
   for (; t < P.n_btiles; t += nwarps) {
     const WTile T = Tn;
     if (t + nwarps < P.n_btiles) Tn = P.btiles[t + nwarps];
@@ -1029,58 +957,62 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     beta += __shfl_xor_sync(kFull, beta, off);
     alpha += __shfl_xor_sync(kFull, alpha, off);
   }
-  int last = 0;
-  if (L.nchunks > 1) {   // every lane's additions are visible before the ticket
-    __threadfence();
-    __syncwarp();
+  if (lane == 0) {   // k_eval scans and finishes the column after this kernel
+    if (beta != 0.0) atomicAdd(BA, beta);
+    if (alpha != 0.0) atomicAdd(BA + 1, alpha);
   }
-  if (lane == 0) {
-    if (L.nchunks == 1) {
-      last = 1;
-    } else {
-      unsigned* cnt = Wk.lcount + (size_t)walker * Wk.lcs + T.e1;
-      if (beta != 0.0) atomicAdd(BA, beta);
-      if (alpha != 0.0) atomicAdd(BA + 1, alpha);
-      __threadfence();
-      last = atomicAdd(cnt, 1u) == (unsigned)(L.nchunks - 1);
-      if (last) *cnt = 0u;
+}
+
+// The end of a long bounded-integer column (k_eval, after every chunk has added its part): line 14
+// as a scan of D in coalesced rounds of 32 buckets, line 16 with R4; the accumulators are zeroed
+// for the next pass.
+__device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                              const LongCol& L, int lane, Best& b, double* oxhat,
+                                              double* oscore, long long kk, int use_tabu) {
+  const int p = L.p, dom = L.dom;
+  const double* X = Wk.x + (size_t)walker * Wk.xs;
+  const int32_t* TB = Wk.tabu + (size_t)walker * Wk.ts;
+  const double xb = __ldg(X + p), l = __ldg(P.lb + p);
+  double* Dg = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
+  double* BA = Dg + dom + 1;
+  unsigned* Cw = reinterpret_cast<unsigned*>(BA + 2);
+  const double B = __ldcg(BA), A = __ldcg(BA + 1);
+  double carry = 0.0, bs = -INFINITY, bv = xb;
+  // rounds of 32 buckets, four rounds' loads in flight at a time
+  for (int b0 = 0; b0 < dom; b0 += 128) {
+    double d[4];
+    unsigned cw[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int q = b0 + 32 * h + lane;
+      d[h] = q < dom ? __ldcg(Dg + q) : 0.0;
+      cw[h] = (b0 + 32 * h < dom) ? __ldcg(Cw + ((b0 >> 5) + h)) : 0u;
     }
-  }
-  last = __shfl_sync(kFull, last, 0);
-  if (!last) return;
-  __threadfence();
-  double B = beta, A = alpha;
-  if (L.nchunks > 1) {
-    B = __ldcg(BA);
-    A = __ldcg(BA + 1);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int q = b0 + 32 * h + lane;
+      double incl = d[h];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const double pre = carry + incl;
+      carry = __shfl_sync(kFull, pre, 31);
+      if (q < dom) {
+        Dg[q] = 0.0;
+        const double v = l + (double)q;
+        const bool cand = ((cw[h] >> lane) & 1u) || q == 0 || q == dom - 1;
+        if (cand && v != xb) {   // the bounds are always candidates (R2), x̄ never
+          const double sig = B + pre + (v > xb ? A : 0.0);
+          if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
+        }
+      }
+      if (lane == 0 && b0 + 32 * h < dom) Cw[(b0 >> 5) + h] = 0u;
+    }
   }
   __syncwarp();
   if (lane == 0) { BA[0] = 0.0; BA[1] = 0.0; Dg[dom] = 0.0; }
-  // line 14: prefix sums of D in coalesced rounds of 32 buckets; line 16 with R4
-  double carry = 0.0, bs = -INFINITY, bv = xb;
-  for (int base = 0; base < dom; base += 32) {
-    const int q = base + lane;
-    const double d = q < dom ? __ldcg(Dg + q) : 0.0;
-    const unsigned cw = __ldcg(Cw + (base >> 5));
-    double incl = d;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double y = __shfl_up_sync(kFull, incl, off);
-      if (lane >= off) incl += y;
-    }
-    const double pre = carry + incl;
-    carry = __shfl_sync(kFull, pre, 31);
-    if (q < dom) {
-      Dg[q] = 0.0;
-      const double v = l + (double)q;
-      const bool cand = ((cw >> lane) & 1u) || q == 0 || q == dom - 1;
-      if (cand && v != xb) {   // the bounds are always candidates (R2), x̄ never
-        const double sig = B + pre + (v > xb ? A : 0.0);
-        if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
-      }
-    }
-    if (lane == 0) Cw[base >> 5] = 0u;
-  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const double so = __shfl_xor_sync(kFull, bs, off), vo = __shfl_xor_sync(kFull, bv, off);
@@ -1089,6 +1021,19 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
   if (lane == 0)
     finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, bv, bs, b, oxhat,
                     oscore, kk, use_tabu);
+}
+
+// The end of a long binary column of several chunks: the summed flip score.
+__device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                              const LongCol& L, Best& b, double* oxhat, double* oscore,
+                                              long long kk, int use_tabu) {
+  const int p = L.p;
+  double* acc = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
+  const double s = __ldcg(acc);
+  *acc = 0.0;
+  const double xb = __ldg(Wk.x + (size_t)walker * Wk.xs + p);
+  finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(Wk.tabu + (size_t)walker * Wk.ts + p) : 0, xb,
+                  1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
 }
 
 __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
@@ -1131,6 +1076,84 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
+}
+
+// ------------------------------------------------------------------------------------------
+// k_eval: long-column ends, single-column sort tiles, the global select
+// ------------------------------------------------------------------------------------------
+// grid = (blocks per walker, W). After its tiles every block publishes its best admissible move;
+// the last block of the walker reduces them (fixed order) to the decision.
+__global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalkers Wk, double* oxhat,
+                                                          double* oscore, chap_move* best_out,
+                                                          int part_base) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double sm_red[32];
+  __shared__ Best sm_b[32];
+  __shared__ int s_flag;
+  const int walker = blockIdx.y;
+  const WalkerScalars* sc = Wk.sc + walker;
+  TileCtx C;
+  C.x = Wk.x + (size_t)walker * Wk.xs;
+  C.rs = Wk.rs + (size_t)walker * Wk.rss;
+  C.tabu = Wk.tabu + (size_t)walker * Wk.ts;
+  C.k = sc->k;
+  C.use_tabu = Wk.use_tabu;
+  C.oxhat = oxhat;
+  C.oscore = oscore;
+  Best b;
+  b.init();
+  // long columns, finished after all their chunks (k_eval_bin / k_eval_gen ran before this kernel)
+  {
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5), w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int q = w0; q < P.n_lfin; q += nw) {
+      const LongCol L = P.lcols[P.lfin[q]];
+      if (L.kind == CC_LBKT) lbkt_finalize(P, Wk, walker, L, lane, b, oxhat, oscore, C.k, C.use_tabu);
+      else if (lane == 0) lbin_finalize(P, Wk, walker, L, b, oxhat, oscore, C.k, C.use_tabu);
+    }
+  }
+  // block tiles: single-column sorts
+  for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x)
+    tile_genm(P, C, P.tiles[t], *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b);
+  __syncthreads();
+  // publish the block's best; the last block of this walker selects (PAPER.md:85, R6)
+  b = block_reduce_best(b, sm_b);
+  Cand* part = Wk.part + (size_t)walker * Wk.ps;
+  if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
+  if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
+  Best g;
+  g.init();
+  for (int q = threadIdx.x; q < part_base + (int)gridDim.x; q += blockDim.x) {
+    Best o;
+    o.s = __ldcg(&part[q].s);
+    o.v = __ldcg(&part[q].v);
+    o.j = __ldcg(&part[q].j);
+    o.p = __ldcg(&part[q].p);
+    g.take(o);
+  }
+  g = block_reduce_best(g, sm_b);
+  if (threadIdx.x == 0) {
+    WalkerScalars* scw = Wk.sc + walker;
+    const bool found = g.p >= 0;
+    Decision d;
+    d.move = (found && g.s > 0.0) ? 1 : 0;
+    d.p = g.p;
+    d.j = found ? g.j : -1;
+    d.pad = 0;
+    d.v = g.v;
+    d.s = found ? g.s : -INFINITY;
+    d.delta = d.move ? (g.v - C.x[g.p]) : 0.0;
+    scw->dec = d;
+    if (best_out) {
+      chap_move mv;
+      mv.j = d.move ? d.j : -1;
+      mv.pad = 0;
+      mv.v = d.move ? d.v : NAN;
+      mv.s = d.move ? d.s : -INFINITY;
+      best_out[walker] = mv;
+    }
+    Wk.sel_count[walker] = 0u;
+  }
 }
 
 // Outputs of fixed variables (internal [0, n_fixed)): (x̄, -inf) (R2 leaves no candidate).
