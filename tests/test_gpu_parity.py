@@ -110,6 +110,49 @@ def test_config_S_full():
     _assert_same(g, o, "S")
 
 
+@pytest.fixture(scope="module")
+def config_G():
+    """BASELINE configs[2] at full size (10.4 M nonzeros), the instance bench.py times."""
+    inst = synth.mixed()
+    return inst, chap.Problem.from_instance(inst), oracle.Problem.from_instance(inst)
+
+
+def test_config_G_full_eval(config_G):
+    """Every variable of the 10^7-nonzero instance, bench.py's launch configuration (one walker's
+    eval grid), at the start point and at a random point with random weights and an active cutoff."""
+    inst, P, O = config_G
+    x = synth.x_lower(inst)
+    g, o = _eval_both(inst, x, P=P, O=O)
+    _assert_same(g, o, "G x_lower")
+    x = synth.x_random(inst, 3)
+    w = synth.weights_random(P.m_norm, 3, hi=9)
+    cut = float(inst.c @ x) - 1000.0
+    g, o = _eval_both(inst, x, w, cut, P=P, O=O)
+    _assert_same(g, o, "G random")
+
+
+def test_config_G_full_trajectory(config_G):
+    """40 tabu iterations on the full instance with bench.py's parameters (one CUDA graph of 32
+    iterations + 8 plain launches): every record, the final point, weights and residuals; then the
+    eval at the walker's final state."""
+    inst, P, O = config_G
+    x0 = synth.x_lower(inst)
+    prm = chap.default_params(graph_iters=32)
+    Wk = chap.Walkers(P, torch.from_numpy(x0[None, :]).cuda(), prm)
+    log = chap.records(Wk.step(40, log=True)).reshape(40, 1)[:, 0]
+    st = Wk.get()
+    ow = oracle.TabuWalker(O, x0)
+    olog = ow.run(40)
+    for f in ("k", "j", "violated", "obj", "s"):
+        bad = np.nonzero(log[f] != olog[f])[0]
+        assert bad.size == 0, (f, bad[:3], log[bad[:3]], olog[bad[:3]])
+    assert np.array_equal(st["x"][0], ow.x[: inst.n])
+    assert np.array_equal(st["w"][0], ow.w)
+    assert np.array_equal(st["r"][0], O.residuals(st["x"][0], ow.cutoff_rhs))
+    g, o = _eval_both(inst, st["x"][0], st["w"][0], ow.cutoff_rhs, P=P, O=O)
+    _assert_same(g, o, "G after 40 iterations")
+
+
 def test_host_buffer_variant_equals_device():
     inst = _mixed_small(6)
     P = chap.Problem.from_instance(inst)
