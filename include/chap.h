@@ -229,12 +229,12 @@ chap_status chap_walkers_restart(chap_walkers* ws, int32_t walker, const double*
                                  void* cuda_stream);
 chap_status chap_walkers_destroy(chap_walkers* ws);
 
-/* Diagnostic timing: n_iters tabu iterations (identical semantics to chap_tabu_step, no log)
- * with plain launches and a CUDA-event pair around every launch on the walkers' stream;
- * ms_per_iter HOST [5] receives the average device time per iteration of [0] k_eval_bin (binary
- * columns), [1] k_eval_gen (general, empty, long bounded-integer columns), [2] k_eval (sorted
- * general columns + the fused global select), [3] reserved (0), [4] the apply kernel.
- * Synchronises. */
+/* Diagnostic timing: n_iters tabu iterations (identical semantics to chap_tabu_step, no log),
+ * captured as one CUDA graph with a CUDA-event pair around every kernel node (so no launch latency
+ * is inside an interval) and run once on the walkers' stream; ms_per_iter HOST [5] receives the
+ * average device time per iteration of [0] k_eval_bin (binary columns), [1] k_eval_gen (general,
+ * empty, long bounded-integer columns), [2] k_eval (long-column ends, sorted general columns, the
+ * global select), [3] reserved (0), [4] the apply kernel. Synchronises. */
 chap_status chap_walkers_profile(chap_walkers* ws, int32_t n_iters, double* ms_per_iter,
                                  void* cuda_stream);
 

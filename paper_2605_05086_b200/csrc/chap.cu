@@ -845,25 +845,39 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
   k_set_log<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk, nullptr);
   std::vector<cudaEvent_t> ev(10 * (size_t)n_iters);
   for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  // one CUDA graph of n_iters iterations with event-record nodes between the kernels, so that the
+  // intervals measure the kernels as chap_tabu_step's graphs run them (no launch latency inside)
+  CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int it = 0; it < n_iters; ++it) {
     cudaEvent_t* e = &ev[10 * (size_t)it];
-    for (int q = 0; q < 8; ++q) cudaEventRecord(e[q], s);
+    for (int q = 0; q < 8; ++q) cudaEventRecordWithFlags(e[q], s, cudaEventRecordExternal);
     if (S->bin_grid > 0)
       k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(D, S->wk, nullptr, nullptr);
-    cudaEventRecord(e[1], s);
-    cudaEventRecord(e[2], s);
+    cudaEventRecordWithFlags(e[1], s, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(e[2], s, cudaEventRecordExternal);
     if (S->gen_grid > 0)
       k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid);
-    cudaEventRecord(e[3], s);
-    cudaEventRecord(e[4], s);
+    cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(e[4], s, cudaEventRecordExternal);
     k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
                                                                      S->bin_grid + S->gen_grid);
-    cudaEventRecord(e[5], s);
-    cudaEventRecord(e[8], s);
+    cudaEventRecordWithFlags(e[5], s, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(e[8], s, cudaEventRecordExternal);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
-    cudaEventRecord(e[9], s);
+    cudaEventRecordWithFlags(e[9], s, cudaEventRecordExternal);
   }
-  CUDA_TRY(cudaGetLastError());
+  {
+    cudaGraph_t graph;
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    CUDA_TRY(cudaGetLastError());
+    if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "profile graph capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t gx;
+    const cudaError_t ci = cudaGraphInstantiate(&gx, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ci != cudaSuccess) return fail(CHAP_ERR_CUDA, "profile graph instantiate: %s", cudaGetErrorString(ci));
+    CUDA_TRY(cudaGraphLaunch(gx, s));
+    cudaGraphExecDestroy(gx);
+  }
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), S->W), 256, 0, s>>>(D, S->wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(S->wk);
   CUDA_TRY(cudaStreamSynchronize(s));
