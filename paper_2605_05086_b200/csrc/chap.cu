@@ -588,6 +588,20 @@ int chap::grid_for(long long work, int threads, int cap) {
   return (int)std::max<long long>(1, std::min<long long>(g, cap));
 }
 
+// Residuals of walker w from scratch (r = A x - b, the cutoff row from a grid-wide c.x), weights
+// kept, and the violated count: the state k_walker_finalize_init completes.
+chap_status chap::walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s) {
+  const DevProblem& D = P->dp;
+  k_acc_zero<<<1, 1, 0, s>>>(Wk.sc, w);
+  if (D.n > 0)
+    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, w);
+  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk.x + (size_t)w * Wk.xs, Wk.xs, Wk.rs + (size_t)w * Wk.rss,
+                                                    Wk.rss, Wk.sc + w, 0, nullptr);
+  k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.rs, Wk.rss, Wk.sc, w);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
 extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double* x, const float* w,
                                             double cutoff_rhs, double* xhat, double* score,
                                             chap_move* best, void* cuda_stream) {
@@ -599,6 +613,8 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   DevWalkers Wk = eval_walkers(p);
   k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs);
   if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, nullptr);
+  if (cutoff_rhs < INFINITY && D.n > 0)
+    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1);
   k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_rs, D.m_norm, p->e_sc, 2, w);
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
@@ -722,9 +738,12 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
   if (D.n > 0)
     k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
+  k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1);
+  if (D.n > 0) k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, -1);
   k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.rs, Wk.rss, Wk.sc, 1, nullptr);
+  k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.rs, Wk.rss, Wk.sc, -1);
   k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, -1);
-  k_walker_finalize_init<<<W, 256, 0, s>>>(D, Wk, 0, -1);
+  k_walker_finalize_init<<<W, 1, 0, s>>>(D, Wk, 0, -1);
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());
@@ -823,10 +842,9 @@ extern "C" chap_status chap_walkers_restart(chap_walkers* S, int32_t walker, con
   const int gx = grid_for(D.n, 256, 4 * S->P->sm_count);
   // write into walker `walker` only: offset the destinations
   if (D.n > 0) k_permute_in<<<dim3(gx, 1), 256, 0, s>>>(D, x, D.n, Wk.x + (size_t)walker * Wk.xs, Wk.xs, nullptr);
-  k_rows_init<<<dim3(S->P->rows_grid, 1), 256, 0, s>>>(D, Wk.x + (size_t)walker * Wk.xs, Wk.xs,
-                                                      Wk.rs + (size_t)walker * Wk.rss, Wk.rss, Wk.sc + walker, 0, nullptr);
+  TRY(chap::walker_recompute(S->P, Wk, walker, s));
   k_tabu_clear<<<dim3(gx, 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, walker);
-  k_walker_finalize_init<<<1, 256, 0, s>>>(D, Wk, 1, walker);
+  k_walker_finalize_init<<<1, 1, 0, s>>>(D, Wk, 1, walker);
   k_flush_incumbent<<<dim3(gx, S->W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());

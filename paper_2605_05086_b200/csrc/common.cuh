@@ -127,6 +127,8 @@ struct WalkerScalars {
   unsigned pad1;
   long long log_k0;           // k of log row 0 (set per chap_tabu_step)
   chap_step_record* log;      // current log base (NULL = no log)
+  double cdot;                // c.x of the current point (k_cut_dot), for the cutoff row and obj
+  long long vcount;           // violated active rows (k_viol_count)
 };
 
 // Everything the kernels need about the immutable problem (internal variable order).

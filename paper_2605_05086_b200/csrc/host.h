@@ -154,5 +154,6 @@ namespace chap {
 chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                         double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
 int grid_for(long long work, int threads, int cap);
+chap_status walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s);
 
 }  // namespace chap

@@ -183,10 +183,9 @@ static chap_status restart_internal(chap_walkers* S, int w, const double* x_int,
   const DevProblem& D = P->dp;
   DevWalkers& Wk = S->wk;
   CUDA_TRY(cudaMemcpyAsync(Wk.x + (size_t)w * Wk.xs, x_int, sizeof(double) * D.n, cudaMemcpyDeviceToDevice, s));
-  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk.x + (size_t)w * Wk.xs, Wk.xs, Wk.rs + (size_t)w * Wk.rss,
-                                                    Wk.rss, Wk.sc + w, 0, nullptr);
+  TRY(chap::walker_recompute(P, Wk, w, s));
   k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, w);
-  k_walker_finalize_init<<<1, 256, 0, s>>>(D, Wk, 1, w);
+  k_walker_finalize_init<<<1, 1, 0, s>>>(D, Wk, 1, w);
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), S->W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());

@@ -40,6 +40,18 @@ __global__ void k_rows_init(DevProblem P, const double* __restrict__ x, size_t x
     rw[P.dummy_row] = d;   // inert padding row
   }
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < P.m_norm; i += nwarps) {
+    if (i == P.cut_row) {   // c.x comes from k_cut_dot (a grid-wide sum): no warp walks this row
+      if (lane == 0) {
+        RowState s = rw[i];
+        s.r = sc[w].cut_active ? sc[w].cdot - sc[w].cutoff_rhs : -INFINITY;
+        if (init_w == 1) s.w = 1.0f;
+        else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
+        if (!sc[w].cut_active) s.w = 0.0f;
+        s.pad = 0;
+        rw[i] = s;
+      }
+      continue;
+    }
     const int e0 = P.rp[i], e1 = P.rp[i + 1];
     double y = 0.0;
     for (int e = e0 + lane; e < e1; e += 32) y += P.cv[e] * xw[P.ci[e]];
@@ -88,33 +100,14 @@ __device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWal
 
 // One block per walker: violated count, objective, k = 0 incumbent check (R15).
 // mode 0: walker create (k = 0, counters cleared); mode 1: restart (keeps k, counters, best).
-__global__ void __launch_bounds__(256) k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode,
-                                                              int only_walker) {
-  __shared__ double sm[32];
-  __shared__ long long smv[32];
+__global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, int only_walker) {
   const int w = (only_walker >= 0) ? only_walker : blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x;
   WalkerScalars* sc = Wk.sc + w;
   RowState* rw = Wk.rs + (size_t)w * Wk.rss;
-  const double* x = Wk.x + (size_t)w * Wk.xs;
-  const int cut_active = sc->cut_active;
-  long long v = 0;
-  for (int i = tid; i < P.m_norm; i += blockDim.x) {
-    if (i == P.cut_row && !cut_active) continue;
-    v += (rw[i].r > 0.0) ? 1 : 0;
-  }
-  double z = 0.0;
-  for (int p = tid; p < P.n; p += blockDim.x) z += P.c[p] * x[p];
-  for (int off = 16; off > 0; off >>= 1) {
-    v += __shfl_xor_sync(kFull, v, off);
-    z += __shfl_xor_sync(kFull, z, off);
-  }
-  if (lane == 0) { smv[wid] = v; sm[wid] = z; }
-  __syncthreads();
   if (tid == 0) {
-    long long vt = 0;
-    double zt = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { vt += smv[q]; zt += sm[q]; }
+    const long long vt = sc->vcount;   // k_viol_count
+    const double zt = sc->cdot;        // k_cut_dot
     sc->violated = vt;
     sc->obj = zt;
     if (mode == 0) {
@@ -128,6 +121,52 @@ __global__ void __launch_bounds__(256) k_walker_finalize_init(DevProblem P, DevW
       sc->log_k0 = 0;
     }
     if (vt == 0) take_incumbent(P, Wk, sc, rw);
+  }
+}
+
+// Zero the grid-wide accumulators of walker `only_walker` (>= 0) or of every walker (blockIdx.x).
+__global__ void k_acc_zero(WalkerScalars* sc, int only_walker) {
+  const int w = only_walker >= 0 ? only_walker : blockIdx.x;
+  sc[w].cdot = 0.0;
+  sc[w].vcount = 0;
+}
+
+// c.x of each walker's point (the cutoff row's activity and the objective), grid-wide: block
+// partials added to sc[w].cdot (exact for the integer data of DESIGN §5).
+__global__ void __launch_bounds__(256) k_cut_dot(DevProblem P, const double* __restrict__ x, size_t xs,
+                                                  WalkerScalars* sc, int only_walker) {
+  __shared__ double sm[8];
+  const int w = only_walker >= 0 ? only_walker : blockIdx.y;
+  const double* xw = x + (size_t)w * xs;
+  double z = 0.0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) z += P.c[p] * xw[p];
+  for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = z;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sm[q];
+    if (t != 0.0) atomicAdd(&sc[w].cdot, t);
+  }
+}
+
+// Violated active rows of each walker (r > 0; the inactive cutoff row excluded), grid-wide.
+__global__ void __launch_bounds__(256) k_viol_count(DevProblem P, const RowState* rs, size_t rss,
+                                                     WalkerScalars* sc, int only_walker) {
+  __shared__ unsigned long long sm[8];
+  const int w = only_walker >= 0 ? only_walker : blockIdx.y;
+  const RowState* rw = rs + (size_t)w * rss;
+  const int cut_active = sc[w].cut_active;
+  unsigned long long v = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m_norm; i += gridDim.x * blockDim.x)
+    if (!(i == P.cut_row && !cut_active) && rw[i].r > 0.0) ++v;
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sm[q];
+    if (t) atomicAdd((unsigned long long*)&sc[w].vcount, t);
   }
 }
 
@@ -301,6 +340,7 @@ __global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs) {
   sc->k = 0;
   sc->cut_active = cutoff_rhs < INFINITY;
   sc->cutoff_rhs = cutoff_rhs;
+  sc->cdot = 0.0;
 }
 
 }  // namespace chap
