@@ -148,7 +148,8 @@ chap_status chap_eval_best_shift(const chap_problem* p, const double* x, const f
 
 /* The same call with HOST buffers (x [n], w [m_norm] or NULL, xhat/score [n] or NULL, best
  * [1] or NULL): copies in, evaluates, copies out, and synchronises the stream before
- * returning. Used for the end-to-end (e2e) measurement. */
+ * returning. Page-locked (pinned) buffers are copied by DMA directly; pageable ones pass through
+ * pinned staging owned by the problem. Used for the end-to-end (e2e) measurement. */
 chap_status chap_eval_best_shift_host(chap_problem* p, const double* x, const float* w,
                                       double cutoff_rhs, double* xhat, double* score,
                                       chap_move* best, void* cuda_stream);

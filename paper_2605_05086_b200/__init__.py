@@ -207,12 +207,18 @@ class Problem:
         return xhat, score, best
 
     def eval_best_shift_host(self, x: np.ndarray, w: Optional[np.ndarray] = None, cutoff_rhs: float = math.inf,
-                             outputs: bool = True, stream=None):
-        """chap_eval_best_shift_host: HOST numpy buffers in and out (copies inside the call)."""
+                             outputs: bool = True, stream=None, out=None):
+        """chap_eval_best_shift_host: HOST numpy buffers in and out (copies inside the call).
+        `out` = (xhat, score) float64 [n] arrays to fill (e.g. page-locked, copied by DMA directly)."""
         x = np.ascontiguousarray(x, np.float64)
         w = None if w is None else np.ascontiguousarray(w, np.float32)
-        xhat = np.empty(self.n) if outputs else None
-        score = np.empty(self.n) if outputs else None
+        if out is not None:
+            xhat, score = out
+            assert xhat.dtype == np.float64 and score.dtype == np.float64 and xhat.flags.c_contiguous \
+                and score.flags.c_contiguous and xhat.size == self.n and score.size == self.n
+        else:
+            xhat = np.empty(self.n) if outputs else None
+            score = np.empty(self.n) if outputs else None
         best = np.zeros(1, MOVE_DTYPE)
         _check(chap_eval_best_shift_host(self.h, _ptr(x), _ptr(w), float(cutoff_rhs), _ptr(xhat), _ptr(score),
                                          _ptr(best), _stream(stream)))

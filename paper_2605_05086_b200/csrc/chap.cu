@@ -641,20 +641,39 @@ extern "C" chap_status chap_eval_best_shift_host(chap_problem* p, const double* 
     TRY(p->buf.alloc(&p->d_out, 2 * (size_t)n));
     TRY(p->buf.alloc(&p->d_best, 1));
   }
-  memcpy(p->h_x, x, sizeof(double) * n);
-  CUDA_TRY(cudaMemcpyAsync(p->d_xu, p->h_x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  // page-locked caller buffers are copied by DMA directly; pageable ones through pinned staging
+  auto pinned = [](const void* ptr) {
+    cudaPointerAttributes a;
+    if (!ptr || cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  };
+  const double* hx = x;
+  if (!pinned(x)) {
+    memcpy(p->h_x, x, sizeof(double) * n);
+    hx = p->h_x;
+  }
+  CUDA_TRY(cudaMemcpyAsync(p->d_xu, hx, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   if (w) {
-    memcpy(p->h_w, w, sizeof(float) * mn);
-    CUDA_TRY(cudaMemcpyAsync(p->d_wu, p->h_w, sizeof(float) * mn, cudaMemcpyHostToDevice, s));
+    const float* hw = w;
+    if (!pinned(w)) {
+      memcpy(p->h_w, w, sizeof(float) * mn);
+      hw = p->h_w;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->d_wu, hw, sizeof(float) * mn, cudaMemcpyHostToDevice, s));
   }
   TRY(chap_eval_best_shift(p, p->d_xu, w ? p->d_wu : nullptr, cutoff_rhs, xhat ? p->d_out : nullptr,
                            score ? p->d_out + n : nullptr, best ? p->d_best : nullptr, cuda_stream));
-  if (xhat) CUDA_TRY(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-  if (score) CUDA_TRY(cudaMemcpyAsync(p->h_out + n, p->d_out + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  const bool px = pinned(xhat), ps = pinned(score);
+  if (xhat) CUDA_TRY(cudaMemcpyAsync(px ? xhat : p->h_out, p->d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (score)
+    CUDA_TRY(cudaMemcpyAsync(ps ? score : p->h_out + n, p->d_out + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   if (best) CUDA_TRY(cudaMemcpyAsync(p->h_best, p->d_best, sizeof(chap_move), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  if (xhat) memcpy(xhat, p->h_out, sizeof(double) * n);
-  if (score) memcpy(score, p->h_out + n, sizeof(double) * n);
+  if (xhat && !px) memcpy(xhat, p->h_out, sizeof(double) * n);
+  if (score && !ps) memcpy(score, p->h_out + n, sizeof(double) * n);
   if (best) *best = *p->h_best;
   return CHAP_OK;
 }
