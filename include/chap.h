@@ -239,6 +239,16 @@ chap_status chap_walkers_destroy(chap_walkers* ws);
 chap_status chap_walkers_profile(chap_walkers* ws, int32_t n_iters, double* ms_per_iter,
                                  void* cuda_stream);
 
+/* Per-kernel device time of the iterations chap_tabu_step runs while timing is on, measured inside
+ * the captured graphs without events: every block stamps %globaltimer at its start (atomic min)
+ * and end (atomic max) per kernel, and the apply kernel's finalising thread accumulates
+ * end - start of each kernel of the iteration. out HOST [6] (may be NULL) first receives the sums:
+ * ns of [0] k_eval_bin, [1] k_eval_gen, [2] k_eval, [3] k_apply (its start to the finalisation),
+ * [4] first eval kernel start to apply finalisation, [5] iterations timed (synchronous read).
+ * Then mode 1 turns timing on and zeroes the sums, 0 turns it off, -1 only reads. Turning it on or
+ * off re-captures the iteration graph at the next chap_tabu_step. */
+chap_status chap_walkers_timing(chap_walkers* ws, int32_t mode, uint64_t* out, void* cuda_stream);
+
 /* ---------------------------------------------------------------------------------------- */
 /* Multi-GPU portfolio: independent walkers per GPU with an every-K exchange                 */
 /* ---------------------------------------------------------------------------------------- */

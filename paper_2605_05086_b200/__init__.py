@@ -101,6 +101,7 @@ _SIGS = {
     "chap_walkers_restart": (ctypes.c_int, [_P, c_i32, _P, _P]),
     "chap_walkers_destroy": (ctypes.c_int, [_P]),
     "chap_walkers_profile": (ctypes.c_int, [_P, c_i32, _P, _P]),
+    "chap_walkers_timing": (ctypes.c_int, [_P, c_i32, _P, _P]),
     "chap_comm_unique_id": (ctypes.c_int, [_P]),
     "chap_comm_create": (ctypes.c_int, [_P, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "chap_comm_destroy": (ctypes.c_int, [_P]),
@@ -284,6 +285,13 @@ class Walkers:
         ms = np.zeros(5)
         _check(chap_walkers_profile(self.h, int(n_iters), ms.ctypes.data, _stream(stream)))
         return ms
+
+    def timing(self, mode: int, stream=None) -> np.ndarray:
+        """chap_walkers_timing: the accumulated [bin, gen, eval, apply, span] ns and iteration count;
+        then mode 1 = on and zeroed, 0 = off, -1 = read only."""
+        out = np.zeros(6, np.uint64)
+        _check(chap_walkers_timing(self.h, int(mode), out.ctypes.data, _stream(stream)))
+        return out
 
     def set_cutoff(self, z_best: float, stream=None):
         _check(chap_walkers_set_cutoff(self.h, float(z_best), _stream(stream)))

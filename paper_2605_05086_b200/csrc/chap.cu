@@ -942,13 +942,35 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 
 #include "portfolio.cuh"
 
-#ifdef CHAP_TIMING
-extern "C" chap_status chap_debug_counters(unsigned long long* out, int reset) {
-  CUDA_TRY(cudaMemcpyFromSymbol(out, chap::g_dbg, sizeof(unsigned long long) * 8));
-  if (reset) {
-    unsigned long long z[8] = {0};
-    CUDA_TRY(cudaMemcpyToSymbol(chap::g_dbg, z, sizeof(z)));
+extern "C" chap_status chap_walkers_timing(chap_walkers* S, int32_t mode, uint64_t* out, void* cuda_stream) {
+  if (!S || mode < -1 || mode > 1) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or mode not in {-1, 0, 1}");
+  DeviceGuard g(S->P->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (out) {
+    for (int q = 0; q < 6; ++q) out[q] = 0;
+    if (S->kt_buf) {
+      unsigned long long h[kKtWords];
+      CUDA_TRY(cudaMemcpyAsync(h, S->kt_buf, sizeof(h), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      for (int q = 0; q < 6; ++q) out[q] = h[8 + q];
+    }
+  }
+  if (mode == -1) return CHAP_OK;
+  if (mode == 1) {
+    if (!S->kt_buf) TRY(S->buf.alloc(&S->kt_buf, kKtWords));
+    unsigned long long h[kKtWords];
+    for (int q = 0; q < 8; ++q) h[q] = (q & 1) ? 0ull : ~0ull;
+    for (int q = 8; q < kKtWords; ++q) h[q] = 0ull;
+    CUDA_TRY(cudaMemcpyAsync(S->kt_buf, h, sizeof(h), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  unsigned long long* want = mode == 1 ? S->kt_buf : nullptr;
+  if (S->wk.kt != want) {   // the captured graph holds the kernel arguments: capture again
+    S->wk.kt = want;
+    if (S->gexec) {
+      cudaGraphExecDestroy(S->gexec);
+      S->gexec = nullptr;
+    }
   }
   return CHAP_OK;
 }
-#endif

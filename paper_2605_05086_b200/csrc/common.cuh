@@ -131,6 +131,17 @@ struct WalkerScalars {
   long long vcount;           // violated active rows (k_viol_count)
 };
 
+// Per-kernel device time (chap_walkers_timing): %globaltimer at every block's start (atomic min)
+// and end (atomic max) into DevWalkers::kt when it is non-NULL; k_apply accumulates the spans.
+__device__ __forceinline__ unsigned long long kt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define KT_BEGIN(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMin((WK).kt + 2 * (q), chap::kt_now()); } while (0)
+#define KT_END(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMax((WK).kt + 2 * (q) + 1, chap::kt_now()); } while (0)
+constexpr int kKtWords = 16;   // [2q, 2q+1] start/end of kernel q (0 bin, 1 gen, 2 eval, 3 apply); [8..13] sums
+
 // Everything the kernels need about the immutable problem (internal variable order).
 struct DevProblem {
   int32_t n, m_norm, cut_row;
@@ -174,6 +185,7 @@ struct DevWalkers {
   int32_t tenure;
   float wcap;
   double delta;                        // NaN = auto
+  unsigned long long* kt;              // [kKtWords] kernel timing, NULL = off
 };
 
 }  // namespace chap

@@ -467,6 +467,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   const long long kk = sc->k;
   const int use_tabu = Wk.use_tabu;
   double* cs = reinterpret_cast<BinWarp*>(smem)[wid].cs;
+  KT_BEGIN(Wk, 0);
   Best b;
   b.init();
   const int nwarps = gridDim.x * (kBinThreads / 32);
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + blockIdx.x, b);
+  KT_END(Wk, 0);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1049,6 +1051,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   const long long kk = sc->k;
   const int use_tabu = Wk.use_tabu;
   GenWarp& S = reinterpret_cast<GenWarp*>(smem)[wid];
+  KT_BEGIN(Wk, 1);
   TileCtx C;
   C.x = X;
   C.rs = Wk.rs + (size_t)walker * Wk.rss;
@@ -1076,6 +1079,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
+  KT_END(Wk, 1);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1092,6 +1096,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   __shared__ int s_flag;
   const int walker = blockIdx.y;
   const WalkerScalars* sc = Wk.sc + walker;
+  KT_BEGIN(Wk, 2);
   TileCtx C;
   C.x = Wk.x + (size_t)walker * Wk.xs;
   C.rs = Wk.rs + (size_t)walker * Wk.rss;
@@ -1120,6 +1125,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   b = block_reduce_best(b, sm_b);
   Cand* part = Wk.part + (size_t)walker * Wk.ps;
   if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
+  KT_END(Wk, 2);
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
   Best g;
   g.init();
@@ -1154,6 +1160,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
     }
     Wk.sel_count[walker] = 0u;
   }
+  KT_END(Wk, 2);
 }
 
 // Outputs of fixed variables (internal [0, n_fixed)): (x̄, -inf) (R2 leaves no candidate).

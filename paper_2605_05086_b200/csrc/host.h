@@ -132,6 +132,7 @@ struct chap_walkers {
   DeviceBuffers buf;
   DevWalkers wk{};
   int* d_bad = nullptr;
+  unsigned long long* kt_buf = nullptr;   // chap_walkers_timing accumulators (kKtWords)
   cudaStream_t stream = nullptr;       // internal stream (graph capture / launch)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t gexec = nullptr;

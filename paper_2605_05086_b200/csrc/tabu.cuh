@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   double* x = Wk.x + (size_t)w * Wk.xs;
   RowState* rw = Wk.rs + (size_t)w * Wk.rss;
   const Decision d = sc->dec;
+  KT_BEGIN(Wk, 3);
   const int cut_active = sc->cut_active;
   const int gtid = blockIdx.x * blockDim.x + tid, gstride = gridDim.x * blockDim.x;
   // phase 0: an incumbent found by the previous iteration: best_x <- x (x unchanged since)
@@ -252,6 +253,15 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   }
   sc->k = k + 1;
   sc->apply_counter = 0;
+  if (Wk.kt && w == 0) {   // kernel timing: accumulate this iteration's spans, re-arm
+    unsigned long long* kt = Wk.kt;
+    const unsigned long long now = kt_now();
+    for (int q = 0; q < 3; ++q) kt[8 + q] += kt[2 * q + 1] - kt[2 * q];
+    kt[11] += now - kt[6];
+    kt[12] += now - kt[0];
+    kt[13] += 1;
+    for (int q = 0; q < 4; ++q) { kt[2 * q] = ~0ull; kt[2 * q + 1] = 0ull; }
+  }
 }
 
 // Complete a pending best_x copy (end of chap_tabu_step / before exports).
