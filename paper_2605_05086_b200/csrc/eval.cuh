@@ -598,6 +598,7 @@ struct __align__(16) GenWarp {
   double it[2 * 32][4];    // per item: best below x̄ (σ', v), best above x̄ (σ', v)
   double cx[32], cl[32], cu[32];
   int cb[32], ce[32], cr[32], cn[32];   // slot range, first candidate rank, candidates
+  int cj[32], ctb[32];     // user index and tabu expiry of column c (read at the finish)
   uint8_t cidx[kWTileGen]; // candidate slots, compacted
 };
 constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
@@ -628,13 +629,13 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
   }
   // column data of lane c
   const int p = T.p0 + lane;
-  int cb = 0x7fffffff, ce = 0, j = 0, tb = 0, cint = 1;
+  int cb = 0x7fffffff, ce = 0, cint = 1;
   double xb = 0.0, l = 0.0, u = 0.0;
   if (lane < nc) {
     cb = __ldg(P.col_ptr + p) - T.e0;
     ce = __ldg(P.col_ptr + p + 1) - T.e0;
-    j = __ldg(P.perm + p);
-    tb = use_tabu ? __ldg(TB + p) : 0;
+    S.cj[lane] = __ldg(P.perm + p);
+    S.ctb[lane] = use_tabu ? __ldg(TB + p) : 0;
     xb = __ldg(X + p);
     l = __ldg(P.lb + p);
     u = __ldg(P.ub + p);
@@ -698,7 +699,7 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
   if (fast) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      S.kf[4 * lane + q] = (float)fmin(fmax(kq[q], -(double)kFastMag - 1.0), (double)kFastMag + 1.0);
+      S.kf[4 * lane + q] = fminf(fmaxf((float)kq[q], -kFastMag - 1.0f), kFastMag + 1.0f);
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) S.kd[4 * lane + q] = kq[q];
@@ -803,6 +804,8 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
   __syncwarp();
   // (3) lane c: β, α, the bounds (R2), line 16 over the column's items and bounds (R4)
   if (lane < nc) {
+    const double xb = S.cx[lane], l = S.cl[lane], u = S.cu[lane];
+    const int cb = S.cb[lane], ce = S.ce[lane];
     double beta, alpha, pl, pu;
     if (fast) {
       const float lf = isfinite(l) ? (float)l : -INFINITY, uf = isfinite(u) ? (float)u : INFINITY;
@@ -847,7 +850,7 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
       const double sg = beta + alpha + pu;
       if (better_shift(sg, u, bs, bv, xb)) { bs = sg; bv = u; }
     }
-    finish_column_j(p, j, tb, xb, bv, bs, b, oxhat, oscore, kk, use_tabu);
+    finish_column_j(p, S.cj[lane], S.ctb[lane], xb, bv, bs, b, oxhat, oscore, kk, use_tabu);
   }
   __syncwarp();
 }
