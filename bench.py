@@ -217,6 +217,12 @@ def main():
     prm = chap.default_params(graph_iters=32)
     ws = chap.Walkers(P, x0, prm)
     ws.timing(1)   # per-kernel %globaltimer spans inside the graphs (no events), on before the warm-up
+    comm = None    # the portfolio exchange every exchange_K iterations: NCCL across ranks
+    if world > 1:
+        uid = [chap.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = chap.Comm(uid[0], world, rank, local)
+    K_x = int(prm.exchange_K)
 
     def barrier():
         if world > 1:
@@ -232,7 +238,14 @@ def main():
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
-        ws.step(args.steps)
+        done = n_exchanges = 0
+        while done < args.steps:   # epochs of exchange_K tabu iterations with the exchange between
+            k = min(K_x, args.steps - done)
+            ws.step(k)
+            done += k
+            if done < args.steps:
+                ws.exchange(comm)
+                n_exchanges += 1
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -324,18 +337,23 @@ def main():
                 "data": "synthetic (seeded generator synth/, no dataset or weights)",
                 "config": {"workload": CONFIGS[cfg]["desc"], "walkers_per_gpu": W, "n": inst.n, "m": inst.m,
                            "nnz": inst.nnz, "m_norm": P.m_norm, "nnz_with_cutoff": int(info.nnz_norm + info.nnz_cut),
-                           "non_fixed_vars": n_eval, "parallelism": f"replicas x{world}",
+                           "non_fixed_vars": n_eval,
+                           "parallelism": f"walker portfolio x{world}: independent walkers per GPU, "
+                                          f"exchange (NCCL allgather) every {K_x} iterations",
+                           "exchanges_in_timed_region": n_exchanges,
                            "l2": "inputs larger than L2: A in CSC alone is "
                                  f"{info.model_bytes_A / 1e6:.0f} MB vs 126 MB L2; no flush"},
                 "tabu_iters_per_s": W * args.steps * world / sec,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_iter * args.steps + 4,
+                "gpu_launches": launches_per_iter * args.steps + 4 + 2 * n_exchanges,
                 "clocks": clk.summary(),
                 "walker": {"moves": int(st["n_moves"].sum()), "stuck": int(st["n_stuck"].sum()),
                            "has_incumbent": int(st["has_incumbent"].sum()),
                            "best_obj": float(np.min(st["best_obj"])), "violated": int(st["violated"].min())}}
         print(json.dumps(line), flush=True)
     ws.close()
+    if comm is not None:
+        comm.close()
     P.close()
     if world > 1:
         dist.destroy_process_group()

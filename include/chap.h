@@ -299,6 +299,16 @@ chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, const chap_walk
                                int8_t* elite_kind, int32_t* elite_slot, int32_t* n_restart_out,
                                int32_t* restart_gid, int32_t* restart_src);
 
+/* One portfolio exchange on existing walkers, the step chap_run_walkers runs every
+ * exchange_K iterations: per-walker summaries are all-gathered (NCCL when comm is non-NULL),
+ * chap_exchange_plan picks the elite, their points are all-gathered, every walker's cutoff is
+ * tightened to the best incumbent and the planned local walkers restart from elite
+ * points (weights kept, tabu cleared). The best incumbent seen by any exchange of these walkers
+ * persists across calls: z_best HOST [1] and z_walker HOST [1] (global walker id, -1 if none) may
+ * be NULL. Every rank must call it the same number of times. Synchronises the stream. */
+chap_status chap_walkers_exchange(chap_walkers* ws, chap_comm* comm, double* z_best, int32_t* z_walker,
+                                  void* cuda_stream);
+
 /* The portfolio loop: W_local walkers from x0 DEVICE [W_local][n] (global
  * walker id = rank*W_local + w), epochs of params.exchange_K iterations; after each epoch an
  * allgather of per-walker summaries and of each rank's elite points (n_elite best incumbents

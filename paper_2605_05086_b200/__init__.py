@@ -102,6 +102,7 @@ _SIGS = {
     "chap_walkers_destroy": (ctypes.c_int, [_P]),
     "chap_walkers_profile": (ctypes.c_int, [_P, c_i32, _P, _P]),
     "chap_walkers_timing": (ctypes.c_int, [_P, c_i32, _P, _P]),
+    "chap_walkers_exchange": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "chap_comm_unique_id": (ctypes.c_int, [_P]),
     "chap_comm_create": (ctypes.c_int, [_P, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "chap_comm_destroy": (ctypes.c_int, [_P]),
@@ -292,6 +293,14 @@ class Walkers:
         out = np.zeros(6, np.uint64)
         _check(chap_walkers_timing(self.h, int(mode), out.ctypes.data, _stream(stream)))
         return out
+
+    def exchange(self, comm: Optional["Comm"] = None, stream=None):
+        """chap_walkers_exchange: one portfolio exchange; returns (best objective, its global walker id)."""
+        z = ctypes.c_double()
+        g = ctypes.c_int32()
+        _check(chap_walkers_exchange(self.h, comm.h if comm is not None else None, ctypes.addressof(z),
+                                     ctypes.addressof(g), _stream(stream)))
+        return z.value, g.value
 
     def set_cutoff(self, z_best: float, stream=None):
         _check(chap_walkers_set_cutoff(self.h, float(z_best), _stream(stream)))

@@ -124,6 +124,9 @@ struct chap_problem {
   }
 };
 
+struct chap_exchange_state;
+void chap_exchange_state_free(chap_exchange_state* x);   // portfolio.cuh
+
 struct chap_walkers {
   using DeviceBuffers = chap::DeviceBuffers;
   const chap_problem* P = nullptr;
@@ -133,6 +136,7 @@ struct chap_walkers {
   DevWalkers wk{};
   int* d_bad = nullptr;
   unsigned long long* kt_buf = nullptr;   // chap_walkers_timing accumulators (kKtWords)
+  chap_exchange_state* xs = nullptr;   // portfolio exchange buffers and state (portfolio.cuh)
   cudaStream_t stream = nullptr;       // internal stream (graph capture / launch)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -142,6 +146,7 @@ struct chap_walkers {
   int bin_grid = 0;            // k_eval_bin blocks per walker
   int gen_grid = 0;            // k_eval_gen blocks per walker
   ~chap_walkers() {
+    if (xs) chap_exchange_state_free(xs);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);

@@ -192,6 +192,116 @@ static chap_status restart_internal(chap_walkers* S, int w, const double* x_int,
   return CHAP_OK;
 }
 
+// The exchange state of a walkers object (buffers sized for one communicator size).
+struct chap_exchange_state {
+  int nranks = 0;
+  DeviceBuffers buf;
+  chap_walker_summary *d_sum_local = nullptr, *d_sum_all = nullptr;
+  double *d_send = nullptr, *d_recv = nullptr;
+  std::vector<chap_walker_summary> h_all;
+  std::vector<int32_t> e_gid, e_slot, r_gid, r_src;
+  std::vector<int8_t> e_kind;
+  double z = INFINITY;   // best incumbent objective seen by any exchange (persists)
+  int32_t zg = -1;       // its global walker id
+};
+
+void chap_exchange_state_free(chap_exchange_state* x) { delete x; }
+
+// One portfolio exchange: summaries -> allgather -> plan -> elite points -> allgather ->
+// cutoff -> restarts. want_stop marks this rank's summaries; *stop = any rank marked. With
+// need_points = false and *stop set, the point exchange is skipped.
+static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want_stop, bool need_points,
+                                     bool* stop, cudaStream_t s) {
+  const chap_problem* p = S->P;
+  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  const int W_local = S->W, W_total = nranks * W_local;
+  const chap_params& prm = S->prm;
+  const int n_restart = prm.n_restart < 0 ? W_total / 8 : prm.n_restart;
+  const int E = prm.n_elite;
+  const int n = p->dp.n;
+  if (!S->xs) S->xs = new chap_exchange_state();
+  chap_exchange_state& X = *S->xs;
+  if (X.nranks != nranks) {   // (re)allocate for this communicator size; z and zg persist
+    X.buf = DeviceBuffers();
+    X.nranks = nranks;
+    TRY(X.buf.alloc(&X.d_sum_local, W_local));
+    TRY(X.buf.alloc(&X.d_sum_all, W_total));
+    TRY(X.buf.alloc(&X.d_send, (size_t)2 * std::max(E, 1) * std::max(n, 1)));
+    TRY(X.buf.alloc(&X.d_recv, (size_t)nranks * 2 * std::max(E, 1) * std::max(n, 1)));
+    X.h_all.resize(W_total);
+    X.e_gid.resize(2 * E + 1);
+    X.e_slot.resize(2 * E + 1);
+    X.e_kind.resize(2 * E + 1);
+    X.r_gid.resize(W_total + 1);
+    X.r_src.resize(W_total + 1);
+  }
+  const DevWalkers& Wk = S->wk;
+  // 1. summaries -> allgather
+  k_summaries<<<W_local, 256, 0, s>>>(p->dp, Wk, X.d_sum_local, rank * W_local, want_stop ? 1 : 0);
+  CUDA_TRY(cudaGetLastError());
+  if (comm) {
+    NCCL_TRY(nccl().AllGather(X.d_sum_local, X.d_sum_all, sizeof(chap_walker_summary) * W_local, ncclUint8, comm->comm, s));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(X.d_sum_all, X.d_sum_local, sizeof(chap_walker_summary) * W_local, cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(X.h_all.data(), X.d_sum_all, sizeof(chap_walker_summary) * W_total, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  bool st = false;
+  for (const auto& x : X.h_all) st = st || (x.flags & 2);
+  *stop = st;
+  // 2. the plan (identical on every rank)
+  int32_t ne = 0, nr = 0;
+  TRY(chap_exchange_plan(W_total, W_local, X.h_all.data(), E, n_restart, &X.z, &X.zg, &ne, X.e_gid.data(),
+                         X.e_kind.data(), X.e_slot.data(), &nr, X.r_gid.data(), X.r_src.data()));
+  if (st && !need_points) return CHAP_OK;
+  // 3. local elite points into the send buffer, allgather (internal variable order: every rank
+  //    holds the same problem, hence the same permutation)
+  if (E > 0) {
+    for (int kind = 0; kind < 2; ++kind) {
+      std::vector<std::pair<Key, int>> loc;
+      for (int w = 0; w < W_local; ++w) {
+        const auto& x = X.h_all[rank * W_local + w];
+        if (kind == 0 && !(x.flags & 1)) continue;
+        loc.push_back({kind == 0 ? feas_key(x) : infeas_key(x), w});
+      }
+      std::sort(loc.begin(), loc.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (int q = 0; q < (int)loc.size() && q < E; ++q) {
+        const int w = loc[q].second;
+        const double* src = (kind == 0 ? Wk.best_x : Wk.x) + (size_t)w * Wk.xs;
+        CUDA_TRY(cudaMemcpyAsync(X.d_send + (size_t)(kind * E + q) * n, src, sizeof(double) * n,
+                                 cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    if (comm) {
+      NCCL_TRY(nccl().AllGather(X.d_send, X.d_recv, (size_t)2 * E * n, ncclFloat64, comm->comm, s));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(X.d_recv, X.d_send, sizeof(double) * 2 * E * n, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  if (st) return CHAP_OK;
+  // 4. global cutoff, restarts of local walkers
+  if (X.z < INFINITY) TRY(chap_walkers_set_cutoff(S, X.z, s));
+  for (int q = 0; q < nr; ++q) {
+    const int gid = X.r_gid[q];
+    if (gid / W_local != rank) continue;
+    TRY(restart_internal(S, gid % W_local, X.d_recv + (size_t)X.e_slot[X.r_src[q]] * n, s));
+  }
+  return CHAP_OK;
+}
+
+extern "C" chap_status chap_walkers_exchange(chap_walkers* S, chap_comm* comm, double* z_best,
+                                             int32_t* z_walker, void* cuda_stream) {
+  if (!S) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers");
+  if (S->prm.exchange_K < 1 || S->prm.n_elite < 0) return fail(CHAP_ERR_INVALID_ARG, "n_elite < 0");
+  if (comm && comm->device != S->P->device) return fail(CHAP_ERR_INVALID_ARG, "comm and walkers on different devices");
+  DeviceGuard g(S->P->device);
+  bool stop = false;
+  TRY(exchange_internal(S, comm, false, false, &stop, (cudaStream_t)cuda_stream));
+  if (z_best) *z_best = S->xs->z;
+  if (z_walker) *z_walker = S->xs->zg;
+  return CHAP_OK;
+}
+
 extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, const double* x0,
                                         const chap_params* params, chap_comm* comm, int64_t max_iters,
                                         double time_limit_s, double* best_x, chap_result* out,
@@ -203,29 +313,13 @@ extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, 
   if (comm && comm->device != p->device) return fail(CHAP_ERR_INVALID_ARG, "comm and problem on different devices");
   DeviceGuard g(p->device);
   const auto t0 = std::chrono::steady_clock::now();
-  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
-  const int W_total = nranks * W_local;
-  const int n_restart = prm.n_restart < 0 ? W_total / 8 : prm.n_restart;
   const int E = prm.n_elite;
   const int n = p->dp.n;
   cudaStream_t s = (cudaStream_t)cuda_stream;
   chap_walkers* S = nullptr;
   TRY(chap_walkers_create(p, W_local, x0, &prm, cuda_stream, &S));
   std::unique_ptr<chap_walkers, chap_status (*)(chap_walkers*)> hold(S, chap_walkers_destroy);
-  DeviceBuffers buf;
-  chap_walker_summary *d_sum_local, *d_sum_all;
-  double *d_send, *d_recv;
-  TRY(buf.alloc(&d_sum_local, W_local));
-  TRY(buf.alloc(&d_sum_all, W_total));
-  TRY(buf.alloc(&d_send, (size_t)2 * std::max(E, 1) * std::max(n, 1)));
-  TRY(buf.alloc(&d_recv, (size_t)nranks * 2 * std::max(E, 1) * std::max(n, 1)));
-  std::vector<chap_walker_summary> h_local(W_local), h_all(W_total);
-  std::vector<int32_t> e_gid(2 * E + 1), e_slot(2 * E + 1), r_gid(W_total + 1), r_src(W_total + 1);
-  std::vector<int8_t> e_kind(2 * E + 1);
-  const DevWalkers& Wk = S->wk;
   int64_t iters = 0, epochs = 0;
-  double z = INFINITY;
-  int32_t zg = -1;
   bool stop = false;
   while (!stop) {
     const int64_t k = std::min<int64_t>(prm.exchange_K, max_iters - iters);
@@ -234,64 +328,18 @@ extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, 
     ++epochs;
     const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const bool want_stop = iters >= max_iters || (time_limit_s > 0 && el >= time_limit_s);
-    // 1. summaries -> allgather
-    k_summaries<<<W_local, 256, 0, s>>>(p->dp, Wk, d_sum_local, rank * W_local, want_stop ? 1 : 0);
-    CUDA_TRY(cudaGetLastError());
-    if (comm) {
-      NCCL_TRY(nccl().AllGather(d_sum_local, d_sum_all, sizeof(chap_walker_summary) * W_local, ncclUint8, comm->comm, s));
-    } else {
-      CUDA_TRY(cudaMemcpyAsync(d_sum_all, d_sum_local, sizeof(chap_walker_summary) * W_local, cudaMemcpyDeviceToDevice, s));
-    }
-    CUDA_TRY(cudaMemcpyAsync(h_all.data(), d_sum_all, sizeof(chap_walker_summary) * W_total, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    for (const auto& x : h_all) stop = stop || (x.flags & 2);
-    // 2. the plan (identical on every rank)
-    int32_t ne = 0, nr = 0;
-    TRY(chap_exchange_plan(W_total, W_local, h_all.data(), E, n_restart, &z, &zg, &ne, e_gid.data(), e_kind.data(),
-                           e_slot.data(), &nr, r_gid.data(), r_src.data()));
-    if (stop && !best_x) break;
-    // 3. local elite points into the send buffer, allgather (internal variable order: every rank
-    //    holds the same problem, hence the same permutation)
-    if (E > 0) {
-      for (int kind = 0; kind < 2; ++kind) {
-        std::vector<std::pair<Key, int>> loc;
-        for (int w = 0; w < W_local; ++w) {
-          const auto& x = h_all[rank * W_local + w];
-          if (kind == 0 && !(x.flags & 1)) continue;
-          loc.push_back({kind == 0 ? feas_key(x) : infeas_key(x), w});
-        }
-        std::sort(loc.begin(), loc.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-        for (int q = 0; q < (int)loc.size() && q < E; ++q) {
-          const int w = loc[q].second;
-          const double* src = (kind == 0 ? Wk.best_x : Wk.x) + (size_t)w * Wk.xs;
-          CUDA_TRY(cudaMemcpyAsync(d_send + (size_t)(kind * E + q) * n, src, sizeof(double) * n,
-                                   cudaMemcpyDeviceToDevice, s));
-        }
-      }
-      if (comm) {
-        NCCL_TRY(nccl().AllGather(d_send, d_recv, (size_t)2 * E * n, ncclFloat64, comm->comm, s));
-      } else {
-        CUDA_TRY(cudaMemcpyAsync(d_recv, d_send, sizeof(double) * 2 * E * n, cudaMemcpyDeviceToDevice, s));
-      }
-    }
-    if (stop) break;
-    // 4. global cutoff, restarts of local walkers
-    if (z < INFINITY) TRY(chap_walkers_set_cutoff(S, z, cuda_stream));
-    for (int q = 0; q < nr; ++q) {
-      const int gid = r_gid[q];
-      if (gid / W_local != rank) continue;
-      TRY(restart_internal(S, gid % W_local, d_recv + (size_t)e_slot[r_src[q]] * n, s));
-    }
+    TRY(exchange_internal(S, comm, want_stop, best_x != nullptr, &stop, s));
   }
+  const chap_exchange_state& X = *S->xs;
   // best point: the top feasible elite member (slot of E[0] when it is feasible)
-  out->best_obj = z;
-  out->has_incumbent = zg >= 0;
-  out->best_walker = zg;
+  out->best_obj = X.z;
+  out->has_incumbent = X.zg >= 0;
+  out->best_walker = X.zg;
   out->iterations = iters;
   out->epochs = epochs;
-  if (best_x && zg >= 0 && E > 0) {
+  if (best_x && X.zg >= 0 && E > 0) {
     // E[0] is the global best incumbent; export it in user order
-    const double* src = d_recv + (size_t)e_slot[0] * n;
+    const double* src = X.d_recv + (size_t)X.e_slot[0] * n;
     k_export_point<<<grid_for(n, 256, 4 * p->sm_count), 256, 0, s>>>(p->dp, src, best_x);
     CUDA_TRY(cudaGetLastError());
   }

@@ -53,3 +53,35 @@ def test_run_walkers_one_rank_nccl():
         _case(synth.tiny(2), W=6, K=40, E=4, ne=2, nr=3, comm=comm)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("seed,comm_kind", [(1, None), (4, "nccl")])
+def test_walkers_exchange_epochs_match_oracle(seed, comm_kind):
+    """chap_walkers_exchange between chap_tabu_step epochs (what bench.py times) reproduces the
+    oracle portfolio walker by walker: point, weights, tabu list, incumbent."""
+    inst = synth.tiny(seed)
+    W, K, E, ne, nr = 6, 30, 4, 2, 2
+    x0s = np.stack([np.clip(synth.x_random(inst, 200 + w), inst.lb, inst.ub) for w in range(W)])
+    O = oracle.Problem.from_instance(inst)
+    ows = [oracle.TabuWalker(O, x) for x in x0s]
+    oracle.run_walkers(O, ows, K, E, ne, nr)
+    P = chap.Problem.from_instance(inst)
+    comm = chap.Comm(chap.comm_unique_id(), 1, 0, 0) if comm_kind else None
+    try:
+        ws = chap.Walkers(P, torch.from_numpy(x0s).cuda(),
+                          chap.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8))
+        for e in range(E):
+            ws.step(K)
+            if e < E - 1:
+                ws.exchange(comm)
+        st = ws.get()
+    finally:
+        if comm is not None:
+            comm.close()
+    for w, ow in enumerate(ows):
+        assert np.array_equal(st["x"][w], ow.x[: inst.n]), w
+        assert np.array_equal(st["w"][w], ow.w), w
+        assert np.array_equal(st["tabu_until"][w], ow.tabu_until[: inst.n]), w
+        assert st["stats"][w]["has_incumbent"] == int(ow.has_incumbent), w
+        if ow.has_incumbent:
+            assert st["stats"][w]["best_obj"] == ow.best_obj, w
