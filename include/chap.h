@@ -69,7 +69,7 @@ typedef struct {
   int32_t exact_integer_data; /* 1: A, lhs, rhs, l, u, c integral, |a| <= 1e6, all variables
                                  integer -> scores and trajectories are bit-exact */
   int32_t n_long_columns;     /* columns evaluated in warp chunks (long binary, long bounded
-                                 integer), merged by atomics + a last-chunk ticket            */
+                                 integer), added up by atomics, finished by k_eval          */
   double auto_cutoff_delta;   /* 1 if every c_j != 0 is integral on an integer variable, else
                                  NaN (= 1e-6 max(1,|z|) when the cutoff is set) (R14)         */
   int64_t device_bytes;       /* device memory held by the problem                            */

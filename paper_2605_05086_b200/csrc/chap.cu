@@ -358,9 +358,6 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     T.kind = k;
     T.p0 = p;
     T.ncols = 1;
-    T.chunk = 0;
-    T.nchunks = 1;
-    T.lc = -1;
     if (k == CC_GENM) {
       T.e0 = col_ptr[p];
       T.e1 = col_ptr[p + 1];
@@ -370,7 +367,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     }
     // long columns: warp chunks of kWChunk nonzeros, accumulated with atomics into per-column
     // accumulators (binary: the flip sum; bounded integer: bucket deltas, candidate bits, β, α);
-    // the column's last chunk finalises
+    // k_eval finishes the column
     const int d = col_ptr[p + 1] - col_ptr[p];   // incl. any padding (inert)
     const int csz = (k == CC_LBKT) ? kBktChunk : kWChunk;
     const int nch = std::max(1, (d + csz - 1) / csz);
@@ -512,10 +509,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.alloc(&P->e_part, P->eval_grid + P->bin_grid + P->gen_grid));
   TRY(B.alloc(&P->e_selcnt, 1));
   CUDA_TRY(cudaMemset(P->e_selcnt, 0, sizeof(unsigned)));
-  TRY(B.alloc(&P->e_lcount, std::max(n_long, 1)));
   TRY(B.alloc(&P->e_lscr, P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_sc, 0, sizeof(WalkerScalars)));
-  CUDA_TRY(cudaMemset(P->e_lcount, 0, sizeof(unsigned) * std::max(n_long, 1)));
   CUDA_TRY(cudaMemset(P->e_lscr, 0, sizeof(double) * P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_tabu, 0, sizeof(int32_t) * std::max(n, 1)));
   CUDA_TRY(cudaDeviceSynchronize());
@@ -571,8 +566,6 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.part = P->e_part;
   Wk.ps = P->eval_grid + P->bin_grid + P->gen_grid;
   Wk.sel_count = P->e_selcnt;
-  Wk.lcount = P->e_lcount;
-  Wk.lcs = std::max(P->dp.n_long, 1);
   Wk.lscr = P->e_lscr;
   Wk.lss = P->lscr_per_walker;
   Wk.use_tabu = 0;
@@ -732,8 +725,6 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
   TRY(B.alloc(&Wk.sel_count, W));
-  Wk.lcs = std::max(D.n_long, 1);
-  TRY(B.alloc(&Wk.lcount, (size_t)Wk.lcs * W));
   Wk.lss = p->lscr_per_walker;
   TRY(B.alloc(&Wk.lscr, Wk.lss * W));
   TRY(B.alloc(&S->d_bad, 1));
@@ -750,7 +741,6 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   CUDA_TRY(cudaEventCreateWithFlags(&S->ev_out, cudaEventDisableTiming));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaMemsetAsync(Wk.sc, 0, sizeof(WalkerScalars) * W, s));
-  CUDA_TRY(cudaMemsetAsync(Wk.lcount, 0, sizeof(unsigned) * Wk.lcs * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.lscr, 0, sizeof(double) * Wk.lss * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));

@@ -11,27 +11,23 @@ namespace chap {
 
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kTileThreads = 256;                 // threads per eval block
-constexpr int kTileNnz = 1024;                    // nonzeros per chunk of a long column
-constexpr int kPer = kTileNnz / kTileThreads;     // slots per thread of a chunk tile
+constexpr int kTileThreads = 256;                 // k_eval block
+constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kGenmMax = 2048;                    // Alg. 1 elements of a single-column sort tile
-constexpr int kWSlots = 8;                        // slots per lane of a binary warp tile
-constexpr int kWTileNnz = 32 * kWSlots;           // nonzeros per binary warp tile
 constexpr int kWSlotsGen = 4;                     // slots per lane of a general warp tile
 constexpr int kWTileGen = 32 * kWSlotsGen;        // Alg. 1 elements per general warp tile
 constexpr int kWTileCols = 32;                    // columns per warp tile (one lane each)
-constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kBinSlots = 4;                      // slots per lane of a pipelined binary tile
-constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per pipelined binary tile
+constexpr int kBinSlots = 4;                      // slots per lane of a binary warp tile
+constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per binary warp tile
 constexpr int kBinThreads = 256;                  // k_eval_bin block
 #ifndef CHAP_BIN_MINB
 #define CHAP_BIN_MINB 4
 #endif
-constexpr int kBinMinBlocks = CHAP_BIN_MINB;
+constexpr int kBinMinBlocks = CHAP_BIN_MINB;      // k_eval_bin resident blocks per SM (register budget)
 #ifndef CHAP_GEN_MINB
 #define CHAP_GEN_MINB 3
 #endif
-constexpr int kGenMinBlocks = CHAP_GEN_MINB;         // k_eval_gen resident blocks per SM (register budget)
+constexpr int kGenMinBlocks = CHAP_GEN_MINB;      // k_eval_gen resident blocks per SM (register budget)
 constexpr int kGenThreads = 256;                  // k_eval_gen block
 constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
 constexpr int kBucketMax = 4096;                  // max integer domain of a bucket-scanned column
@@ -49,9 +45,9 @@ struct __align__(16) RowState {
 // Column classes (the paper's length-specialised dispatch, re-designed).
 enum ColClass : int {
   CC_FIXED = 0,  // l = u: no candidate
-  CC_LBKT = 1,   // general integer, deg+2 > kShortDeg, bounded domain <= kBucketMax: bucket scan,
-                 // chunked over kTileNnz-nonzero tiles (merged by the last chunk)
-  CC_LBIN = 2,   // binary, deg > kShortDeg: flip partial sums over kTileNnz-nonzero chunks
+  CC_LBKT = 1,   // general integer, deg+2 > kShortDeg, bounded domain <= kBucketMax: bucket scan
+                 // over kBktChunk-nonzero warp chunks, finished by k_eval
+  CC_LBIN = 2,   // binary, deg > kShortDeg: flip partial sums over kWChunk-nonzero warp chunks
   CC_GENM = 3,   // general, kShortDeg < deg+2 <= kGenmMax, other domains: one tile, bitonic sort
   CC_GEN = 4,    // general, deg+2 <= kShortDeg: packed warp tiles, sort-free prefix per candidate
   CC_BIN = 5,    // binary, deg <= kShortDeg: packed tiles, flip sums
@@ -80,15 +76,11 @@ constexpr int kBktChunk = 512;                    // nonzeros per warp chunk of 
 
 // A block tile (chunk of a long column, or one column sorted by the whole block).
 struct Tile {
-  int32_t kind;      // a ColClass (not CC_FIXED)
-  int32_t p0;        // first internal column
-  int32_t ncols;     // columns in a packed tile; 1 otherwise
+  int32_t kind;      // CC_GENM
+  int32_t p0;        // the column (internal)
+  int32_t ncols;     // 1
   int32_t e0, e1;    // nonzero range [e0, e1) (CSC, internal)
-  int32_t lc;        // long-column slot (chunked kinds)
-  int32_t chunk, nchunks;
-  int32_t dom;       // u - l + 1 (CC_LBKT)
   int32_t pad;
-  int64_t scr;       // offset (doubles) of the column's chunk scratch in a walker's scratch
 };
 
 // Per-column result competing for the global best move.
@@ -178,7 +170,6 @@ struct DevWalkers {
   WalkerScalars* sc;                   // [W]
   Cand* part;           int32_t ps;    // [W][ps] one per eval block
   unsigned* sel_count;                 // [W] last-block-done counter of the eval kernel
-  unsigned* lcount;     int32_t lcs;   // [W][n_long]
   double* lscr;         size_t lss;    // [W][lss]
   int32_t use_tabu;
   int32_t W;

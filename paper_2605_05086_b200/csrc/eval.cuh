@@ -10,7 +10,8 @@
 //   k_eval      block tiles of general columns of <= kGenmMax entries (shared-memory bitonic sort
 //               and scan), then the global select: the last block of a walker reduces every
 //               block's best admissible move to the walker's decision (R6).
-// A long column's last chunk (a ticket counter) finalises it and zeroes its accumulators. With the
+// A long column's chunks only add into its accumulators; k_eval, which runs after both chunk
+// kernels, finishes the column and zeroes the accumulators (no tickets or fences). With the
 // integer weights of R11 every delta, β, α and penalty is a multiple of 1/2 and every partial sum
 // is exact, so the order of the atomic additions does not change any result.
 // Every warp-tile slot issues its coalesced CSC loads and one 16-byte row-state gather before
@@ -379,7 +380,7 @@ __device__ __forceinline__ void tile_genm(const DevProblem& P, const TileCtx& C,
   __syncthreads();
 }
 
-// last-chunk handshake of a chunked column: returns true in every thread of the last block
+// last-block handshake (the global select): returns true in every thread of the last block
 __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_flag) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -408,14 +409,14 @@ __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_fl
 // scan (in-lane, then a 5-step shuffle scan across lanes), so shared memory only carries the 32
 // finished sums — every random access of the kernel is the row-state gather itself.
 // A chunk of a long binary column (one column, <= kWChunk nonzeros) sums by a warp reduction and
-// adds its partial to the column's accumulator; the last chunk finishes the column.
+// adds its partial to the column's accumulator; k_eval finishes the column.
 struct __align__(16) BinWarp {
   double cs[32];   // column sums
 };
 constexpr size_t kBinSmem = sizeof(BinWarp) * (kBinThreads / 32);
 
 // A warp chunk (<= kWChunk nonzeros) of a long binary column: warp-reduced flip sum added to the
-// column's accumulator; the last chunk (ticket) finishes the column and zeroes the accumulator.
+// column's accumulator (a single-chunk column finishes in place); k_eval finishes the others.
 __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
                                            const int32_t* __restrict__ TB, const WTile& T, int lane,
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   b.init();
   const int nwarps = gridDim.x * (kBinThreads / 32);
   int t = blockIdx.x * (kBinThreads / 32) + wid;
-  // chunks of long columns first (their ticket latency overlaps the packed tiles)
+  // chunks of long columns first (their latency overlaps the packed tiles of other warps)
   for (; t < P.n_bchunks; t += nwarps)
     lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
   t -= P.n_bchunks;
@@ -863,7 +864,7 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
 // chunk first counts into a warp-private shared-memory histogram of 2δ in int32 (exact while the
 // weights are integers <= 2^16: |Σ 2δ| <= 2^27) and then adds each nonzero bucket once; rounds
 // with other weights, or domains above kWarpDom, aggregate per warp instead (lanes with equal
-// buckets: __match_any_sync, the lowest lane adds the group's sum). The last chunk (ticket) scans D
+// buckets: __match_any_sync, the lowest lane adds the group's sum). lbkt_finalize (k_eval) scans D
 // in coalesced rounds of 32 buckets, takes line 16's argmax with R4 and zeroes the accumulators.
 __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
@@ -1067,7 +1068,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   b.init();
   const int nwarps = gridDim.x * (kGenThreads / 32);
   int t = blockIdx.x * (kGenThreads / 32) + wid;
-  // chunks of long columns first (their ticket latency overlaps the packed tiles)
+  // chunks of long columns first (their latency overlaps the packed tiles of other warps)
   for (; t < P.n_gchunks; t += nwarps)
     lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
   __syncwarp();

@@ -105,7 +105,6 @@ struct chap_problem {
   WalkerScalars* e_sc = nullptr;
   Cand* e_part = nullptr;
   unsigned* e_selcnt = nullptr;
-  unsigned* e_lcount = nullptr;
   double* e_lscr = nullptr;
   // host-buffer variant staging (lazy)
   double* h_x = nullptr;
