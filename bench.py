@@ -39,6 +39,11 @@ CONFIGS = {
     "S": dict(desc="S: synthetic set cover 10k rows x 50k binaries, ~500k nnz (BASELINE.json configs[1])", walkers=1),
     "P": dict(desc="P: packing MIP 20k rows x 100k binaries, ~1M nnz, 64 walkers (BASELINE.json configs[3])",
               walkers=64),
+    # BASELINE.json configs[4], the scaling sweep: generator X at a requested nonzero count
+    "X1e5": dict(desc="X: scaling sweep, generator G scaled to ~1e5 nnz (BASELINE.json configs[4])", walkers=1),
+    "X1e6": dict(desc="X: scaling sweep, generator G scaled to ~1e6 nnz (BASELINE.json configs[4])", walkers=1),
+    "X1e7": dict(desc="X: scaling sweep, generator G scaled to ~1e7 nnz (BASELINE.json configs[4])", walkers=1),
+    "X5e7": dict(desc="X: scaling sweep, generator G scaled to ~5e7 nnz (BASELINE.json configs[4])", walkers=1),
     # diagnostic variants of G (not BASELINE configs): same structure, one variable class only
     "Gbin": dict(desc="diagnostic: config G structure with every short variable binary", walkers=1),
     "Gint": dict(desc="diagnostic: config G structure with every short variable bounded integer", walkers=1),
@@ -59,6 +64,8 @@ def make_instance(cfg: str):
         return synth.mixed(p_binary=0.0, p_bounded=1.0)
     if cfg == "Gnl":
         return synth.mixed(n_long=0)
+    if cfg.startswith("X"):
+        return synth.scaled(int(float(cfg[1:])))
     raise ValueError(cfg)
 
 

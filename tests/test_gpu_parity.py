@@ -153,6 +153,30 @@ def test_config_G_full_trajectory(config_G):
     _assert_same(g, o, "G after 40 iterations")
 
 
+def test_config_P_full_eval():
+    """BASELINE configs[3]'s packing instance (10^6 nonzeros) at a walker start point."""
+    inst = synth.packing()
+    P = chap.Problem.from_instance(inst)
+    x = synth.x_bernoulli(inst, (3, 7), 0.5)
+    w = synth.weights_random(P.m_norm, 5, hi=12)
+    g, o = _eval_both(inst, x, w, float(inst.c @ x) - 10.0, P=P)
+    _assert_same(g, o, "P")
+
+
+def test_config_X_largest_eval():
+    """The top of BASELINE configs[4]'s scaling sweep: generator X at 5·10^7 requested nonzeros
+    (46 M nonzeros, 5 M variables, 10^6 rows), every variable at two points."""
+    inst = synth.scaled(50_000_000)
+    P = chap.Problem.from_instance(inst)
+    O = oracle.Problem.from_instance(inst)
+    g, o = _eval_both(inst, synth.x_lower(inst), P=P, O=O)
+    _assert_same(g, o, "X50M x_lower")
+    x = synth.x_random(inst, 8)
+    w = synth.weights_random(P.m_norm, 8, hi=6)
+    g, o = _eval_both(inst, x, w, float(inst.c @ x) - 100.0, P=P, O=O)
+    _assert_same(g, o, "X50M random")
+
+
 def test_host_buffer_variant_equals_device():
     inst = _mixed_small(6)
     P = chap.Problem.from_instance(inst)
