@@ -83,6 +83,9 @@ def lib():
         L.orc_residuals.argtypes = [P, P, ctypes.c_double, P]
         L.orc_best_shift.argtypes = [P, P, P, ctypes.c_double, P, P, P, P, P, ctypes.c_int]
         L.orc_best_shift.restype = ctypes.c_int
+        L.orc_best_shift_range.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P,
+                                           ctypes.c_int]
+        L.orc_best_shift_range.restype = ctypes.c_int
         L.orc_walker_init.argtypes = [P, ctypes.POINTER(Params), P, ctypes.POINTER(Walker)]
         L.orc_walker_init.restype = ctypes.c_int
         L.orc_tabu_run.argtypes = [P, ctypes.POINTER(Params), ctypes.POINTER(Walker), ctypes.c_int64, P,
@@ -175,6 +178,22 @@ class Problem:
         st = lib().orc_best_shift(self.h, x.ctypes.data, wp, float(cutoff_rhs), xhat.ctypes.data,
                                   score.ctypes.data, ctypes.byref(bj), ctypes.byref(bv),
                                   ctypes.byref(bs), int(threads))
+        if st != ORC_OK:
+            raise OracleError(st)
+        return xhat, score, (bj.value, bv.value, bs.value)
+
+    def best_shift_range(self, x, j0, j1, w=None, cutoff_rhs=math.inf, threads=0, out=None):
+        """The same for the variables [j0, j1) only (a bounded sample; activities from scratch)."""
+        x = np.ascontiguousarray(x, np.float64)
+        wp = None
+        if w is not None:
+            w = np.ascontiguousarray(w, np.float32)
+            wp = w.ctypes.data
+        xhat, score = out if out is not None else (np.zeros(self.n), np.zeros(self.n))
+        bj = ctypes.c_int32(); bv = ctypes.c_double(); bs = ctypes.c_double()
+        st = lib().orc_best_shift_range(self.h, x.ctypes.data, wp, float(cutoff_rhs), int(j0), int(j1),
+                                        xhat.ctypes.data, score.ctypes.data, ctypes.byref(bj), ctypes.byref(bv),
+                                        ctypes.byref(bs), int(threads))
         if st != ORC_OK:
             raise OracleError(st)
         return xhat, score, (bj.value, bv.value, bs.value)

@@ -289,10 +289,11 @@ static void best_shift_var(const orc_problem* P, int32_t j, const double* x, con
   *xhat = bv; *score = bs;
 }
 
-int orc_best_shift(const orc_problem* P, const double* x, const float* w, double cutoff_rhs,
-                   double* xhat, double* score, int32_t* best_j, double* best_v, double* best_s,
-                   int n_threads) {
+int orc_best_shift_range(const orc_problem* P, const double* x, const float* w, double cutoff_rhs,
+                         int32_t j0, int32_t j1, double* xhat, double* score, int32_t* best_j,
+                         double* best_v, double* best_s, int n_threads) {
   int32_t n = P->n;
+  if (j0 < 0 || j1 > n || j0 > j1) return ORC_ERR_INVALID_ARG;
   for (int32_t j = 0; j < n; j++)
     if (!(x[j] >= P->lb[j] && x[j] <= P->ub[j])) return ORC_ERR_INVALID_ARG;
   double* y = (double*)malloc(sizeof(double) * P->m_norm);
@@ -302,13 +303,19 @@ int orc_best_shift(const orc_problem* P, const double* x, const float* w, double
   if (n_threads > 0) omp_set_num_threads(n_threads);
 #pragma omp parallel for schedule(dynamic, 256)
 #endif
-  for (int32_t j = 0; j < n; j++) best_shift_var(P, j, x, y, w, cutoff_rhs, &xhat[j], &score[j]);
+  for (int32_t j = j0; j < j1; j++) best_shift_var(P, j, x, y, w, cutoff_rhs, &xhat[j], &score[j]);
   free(y);
   int32_t bj = -1; double bsv = 0.0, bvv = NAN;
-  for (int32_t j = 0; j < n; j++)
+  for (int32_t j = j0; j < j1; j++)
     if (score[j] > 0.0 && (bj < 0 || score[j] > bsv)) { bj = j; bsv = score[j]; bvv = xhat[j]; }
   *best_j = bj; *best_v = bj >= 0 ? bvv : NAN; *best_s = bj >= 0 ? bsv : -INFINITY;
   return ORC_OK;
+}
+
+int orc_best_shift(const orc_problem* P, const double* x, const float* w, double cutoff_rhs,
+                   double* xhat, double* score, int32_t* best_j, double* best_v, double* best_s,
+                   int n_threads) {
+  return orc_best_shift_range(P, x, w, cutoff_rhs, 0, P->n, xhat, score, best_j, best_v, best_s, n_threads);
 }
 
 /* ---------------------------------------------------------------------------------------- */

@@ -67,6 +67,12 @@ int orc_best_shift(const orc_problem* P, const double* x, const float* w, double
                    double* xhat, double* score, int32_t* best_j, double* best_v, double* best_s,
                    int n_threads);
 
+/* The same for the variables [j0, j1) only (activities still from scratch; xhat/score [n] are
+ * written at [j0, j1); the best move is the best within the range). Used for bounded samples. */
+int orc_best_shift_range(const orc_problem* P, const double* x, const float* w, double cutoff_rhs,
+                         int32_t j0, int32_t j1, double* xhat, double* score, int32_t* best_j,
+                         double* best_v, double* best_s, int n_threads);
+
 typedef struct {
   int32_t tenure;        /* T: a moved variable is inadmissible in iterations k+1..k+T (R13)   */
   float weight_cap;      /* w <= cap (R11, R12)                                               */

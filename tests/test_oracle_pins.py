@@ -214,3 +214,22 @@ def test_cutoff_row_scored_like_any_row():
                             np.concatenate([inst.rhs, [cut]]), inst.lb, inst.ub, inst.is_int, inst.c)
         xhat2, score2, _ = P2.best_shift(x, None)
         assert np.array_equal(xhat, xhat2) and np.array_equal(score, score2)
+
+
+def test_best_shift_range_equals_full_slice():
+    """orc_best_shift_range (bench.py's bounded reference sample) is orc_best_shift restricted to
+    [j0, j1): same per-variable values, best move = the best within the slice."""
+    inst = synth.mixed(seed=5, n=3000, m=600, n_long=2, long_lo=200, long_hi=2000)
+    O = oracle.Problem.from_instance(inst)
+    x = synth.x_random(inst, 4)
+    w = synth.weights_random(O.m_norm, 4)
+    fx, fs, _ = O.best_shift(x, w)
+    for j0, j1 in [(0, 3000), (100, 900), (2999, 3000), (500, 500)]:
+        rx, rs, (bj, bv, bs) = O.best_shift_range(x, j0, j1, w)
+        assert np.array_equal(rx[j0:j1], fx[j0:j1]) and np.array_equal(rs[j0:j1], fs[j0:j1])
+        pos = [j for j in range(j0, j1) if fs[j] > 0]
+        if pos:
+            jb = min(pos, key=lambda j: (-fs[j], j))
+            assert (bj, bv, bs) == (jb, fx[jb], fs[jb])
+        else:
+            assert bj == -1
