@@ -304,10 +304,13 @@ def main():
     # CUDA-event timing of the same kernels (event-record nodes between them in a captured graph,
     # same walker state continuing): a conservative cross-check, inflated by the event nodes
     kms = ws.profile(args.profile_iters)
-    mb = [int(info.model_bytes_kernel[i]) for i in range(3)]
+    # batched model: A and the static per-variable data once per pass of the W
+    # walkers, the walker state (x̄, tabu expiry, row state) once per walker
+    mw_ = [int(info.model_bytes_walker_kernel[i]) for i in range(3)]
+    mb = [int(info.model_bytes_kernel[i]) + (W - 1) * mw_[i] for i in range(3)]
     eval_ms = float(ktm[0] + ktm[1] + ktm[2])
     eval_ms_events = float(kms[0] + kms[1] + kms[2])
-    eval_bytes = (mb[0] + mb[1] + mb[2]) * W
+    eval_bytes = mb[0] + mb[1] + mb[2]
     achieved = eval_bytes / (eval_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = None
@@ -320,7 +323,7 @@ def main():
         except Exception:
             traffic = None
     step_ms_profiled = float(kt[4] / n_kt / 1e6)
-    pass_bytes = int(info.model_bytes_pass) * W
+    pass_bytes = int(info.model_bytes_pass) + (W - 1) * sum(mw_)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "kernel": "k_eval_bin + k_eval_gen + k_eval (the best-shift pass of every variable + select)",
@@ -328,8 +331,8 @@ def main():
                 "timing": "per-kernel first-block-start to last-block-end (%globaltimer) inside the timed "
                           "region's CUDA graphs, averaged over its iterations (chap_walkers_timing)",
                 "kernel_ms": {names[i]: float(ktm[i]) for i in (0, 1, 2, 4)},
-                "per_kernel": {names[i]: {"bytes": mb[i] * W, "ms": float(ktm[i]),
-                                          "GBps": (mb[i] * W / (ktm[i] * 1e-3) / 1e9) if ktm[i] > 0 else None}
+                "per_kernel": {names[i]: {"bytes": mb[i], "ms": float(ktm[i]),
+                                          "GBps": (mb[i] / (ktm[i] * 1e-3) / 1e9) if ktm[i] > 0 else None}
                                for i in (0, 1, 2)},
                 "kernel_share_of_step": eval_ms / step_ms_profiled if step_ms_profiled > 0 else None,
                 "events": {"kernel_ms": {names[i]: float(kms[i]) for i in (0, 1, 2, 4)},
@@ -380,8 +383,12 @@ def main():
                            "parallelism": f"walker portfolio x{world}: independent walkers per GPU, "
                                           f"exchange (NCCL allgather) every {K_x} iterations",
                            "exchanges_in_timed_region": n_exchanges,
-                           "l2": "inputs larger than L2: A in CSC alone is "
-                                 f"{info.model_bytes_A / 1e6:.0f} MB vs 126 MB L2; no flush"},
+                           "l2": ("inputs larger than L2: A in CSC alone is "
+                                  f"{info.model_bytes_A / 1e6:.0f} MB vs 126 MB L2; no flush"
+                                  if info.model_bytes_A > 126e6 else
+                                  f"working set L2-resident (A in CSC {info.model_bytes_A / 1e6:.0f} MB + "
+                                  f"{W} walkers' state) and kept so on purpose: consecutive tabu "
+                                  "iterations reuse it, no flush; the HBM fraction is not the bound here")},
                 "tabu_iters_per_s": W * args.steps * world / sec,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_iter * args.steps + 4 + 2 * n_exchanges,

@@ -87,6 +87,10 @@ typedef struct {
   int32_t eval_launches;      /* kernel launches of one best-shift pass (1-3: the eval kernels
                                  with work, k_eval always); a tabu iteration adds the apply   */
   int32_t pad_;
+  int64_t model_bytes_walker_kernel[3]; /* the per-walker part of model_bytes_kernel (x̄, tabu
+                                 expiry, row state); the rest (A in CSC, static per-variable
+                                 data) is read once by a batched pass of W walkers, whose model
+                                 is therefore shared + W x per-walker          */
 } chap_problem_info;
 
 /* Build a problem from HOST CSR data (copied; the caller may free its arrays on return).

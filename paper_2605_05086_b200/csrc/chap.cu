@@ -395,7 +395,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   }
   I.n_long_columns = n_long;
   {  // algorithmic-bytes model
-    int64_t mb[3] = {0, 0, 0}, nz[3] = {0, 0, 0};
+    int64_t mb[3] = {0, 0, 0}, nz[3] = {0, 0, 0}, mw[3] = {0, 0, 0};
     for (int32_t q = 0; q < n; ++q) {
       const int32_t j = perm[q];
       const int k = cls[j];
@@ -404,10 +404,16 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       const bool bin = vclass[j] == 1;
       const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
       mb[kk] += 12LL * deg[j] + (int64_t)std::llround(per_var * 8) / 8;
+      mw[kk] += (int64_t)std::llround(((bin ? 0.125 : 8.0) + 4.0) * 8) / 8;   // x̄, tabu
       nz[kk] += deg[j];
     }
     mb[2] += 12LL * m_norm;   // the row state, read once per pass (attributed to the last kernel)
-    for (int q = 0; q < 3; ++q) { I.model_bytes_kernel[q] = mb[q]; I.nnz_kernel[q] = nz[q]; }
+    mw[2] += 12LL * m_norm;
+    for (int q = 0; q < 3; ++q) {
+      I.model_bytes_kernel[q] = mb[q];
+      I.model_bytes_walker_kernel[q] = mw[q];
+      I.nnz_kernel[q] = nz[q];
+    }
     I.model_bytes_pass = mb[0] + mb[1] + mb[2];
   }
   P->lscr_per_walker = (size_t)std::max<int64_t>(lscr, 1);
@@ -544,9 +550,38 @@ extern "C" chap_status chap_problem_destroy(chap_problem* p) {
 // ------------------------------------------------------------------------------------------
 // eval launches (shared by the eval API and the tabu step)
 // ------------------------------------------------------------------------------------------
+static chap_status launch_bin_wm(const DevProblem& D, const DevWalkers& Wk, int bgrid, cudaStream_t s) {
+  const dim3 grid(bgrid, Wk.n_groups);
+  switch (Wk.rg) {
+    case 2: k_eval_bin_wm<2><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
+    case 4: k_eval_bin_wm<4><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
+    case 8: k_eval_bin_wm<8><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
+    case 16: k_eval_bin_wm<16><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
+    case 32: k_eval_bin_wm<32><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
+    default: return fail(CHAP_ERR_STATE, "row-state group width %d", Wk.rg);
+  }
+  return CHAP_OK;
+}
+
+static int bin_wm_occupancy(int rg) {
+  int occ = 1;
+  cudaError_t e = cudaSuccess;
+  switch (rg) {
+    case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_bin_wm<2>, kBinWmThreads, 0); break;
+    case 4: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_bin_wm<4>, kBinWmThreads, 0); break;
+    case 8: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_bin_wm<8>, kBinWmThreads, 0); break;
+    case 16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_bin_wm<16>, kBinWmThreads, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_bin_wm<32>, kBinWmThreads, 0); break;
+  }
+  return e == cudaSuccess ? std::max(1, occ) : 1;
+}
+
 chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                               double* oxhat, double* oscore, chap_move* best, cudaStream_t s) {
-  if (bgrid > 0) k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
+  if (bgrid > 0) {
+    if (Wk.rg > 1) TRY(launch_bin_wm(P->dp, Wk, bgrid, s));
+    else k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
+  }
   if (ggrid > 0) k_eval_gen<<<dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s>>>(P->dp, Wk, oxhat, oscore, bgrid);
   k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid);
   CUDA_TRY(cudaGetLastError());
@@ -559,6 +594,9 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.xs = (size_t)P->dp.n;
   Wk.rs = P->e_rs;
   Wk.rss = (size_t)P->dp.m_norm + 1;
+  Wk.rg = 1;
+  Wk.n_groups = 1;
+  Wk.xbits = nullptr;
   Wk.tabu = P->e_tabu;
   Wk.ts = (size_t)P->dp.n;
   Wk.best_x = P->e_bx;
@@ -588,9 +626,9 @@ chap_status chap::walker_recompute(const chap_problem* P, DevWalkers& Wk, int w,
   k_acc_zero<<<1, 1, 0, s>>>(Wk.sc, w);
   if (D.n > 0)
     k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, w);
-  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk.x + (size_t)w * Wk.xs, Wk.xs, Wk.rs + (size_t)w * Wk.rss,
-                                                    Wk.rss, Wk.sc + w, 0, nullptr);
-  k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.rs, Wk.rss, Wk.sc, w);
+  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk, 0, nullptr, w);
+  k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk, w);
+  if (Wk.xbits && D.n > 0) k_xbits_build<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(D, Wk, w);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -608,7 +646,7 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, nullptr);
   if (cutoff_rhs < INFINITY && D.n > 0)
     k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1);
-  k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_rs, D.m_norm, p->e_sc, 2, w);
+  k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, Wk, 2, w, 0);
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
@@ -715,12 +753,24 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   DevWalkers& Wk = S->wk;
   DeviceBuffers& B = S->buf;
   TRY(B.alloc(&Wk.x, n * W));
-  TRY(B.alloc(&Wk.rs, (mn + 1) * W));
+  // row-state groups (DevWalkers): walker-minor groups of up to 32 walkers when W > 1
+  int rg = 1;
+  if (W > 1) while (rg < 32 && rg < W) rg <<= 1;
+  Wk.rg = rg;
+  Wk.n_groups = (W + rg - 1) / rg;
+  TRY(B.alloc(&Wk.rs, (mn + 1) * (size_t)rg * Wk.n_groups));
+  Wk.xbits = nullptr;
+  if (rg > 1) TRY(B.alloc(&Wk.xbits, n * (size_t)Wk.n_groups));
   TRY(B.alloc(&Wk.tabu, n * W));
   TRY(B.alloc(&Wk.best_x, n * W));
   TRY(B.alloc(&Wk.sc, W));
   S->eval_grid = std::max(1, std::min(p->eval_grid, (p->eval_occ * p->sm_count + W - 1) / W));
   S->bin_grid = p->bin_grid ? std::max(1, std::min(p->bin_grid, (p->bin_occ * p->sm_count + W - 1) / W)) : 0;
+  if (rg > 1 && p->bin_grid) {   // k_eval_bin_wm: one grid row per group
+    const int items = p->dp.n_btiles + p->dp.n_bchunks, warps = kBinWmThreads / 32;
+    S->bin_grid = std::max(1, std::min((items + warps - 1) / warps,
+                                       (bin_wm_occupancy(rg) * p->sm_count + Wk.n_groups - 1) / Wk.n_groups));
+  }
   S->gen_grid = p->gen_grid ? std::max(1, std::min(p->gen_grid, (p->gen_occ * p->sm_count + W - 1) / W)) : 0;
   Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
@@ -744,13 +794,16 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   CUDA_TRY(cudaMemsetAsync(Wk.lscr, 0, sizeof(double) * Wk.lss * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
+  CUDA_TRY(cudaMemsetAsync(Wk.rs, 0, sizeof(RowState) * (mn + 1) * (size_t)rg * Wk.n_groups, s));
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
   if (D.n > 0)
     k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
   k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1);
   if (D.n > 0) k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, -1);
-  k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.rs, Wk.rss, Wk.sc, 1, nullptr);
-  k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.rs, Wk.rss, Wk.sc, -1);
+  k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk, 1, nullptr, -1);
+  k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk, -1);
+  if (Wk.xbits && D.n > 0)
+    k_xbits_build<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), Wk.n_groups), 256, 0, s>>>(D, Wk, -1);
   k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, -1);
   k_walker_finalize_init<<<W, 1, 0, s>>>(D, Wk, 0, -1);
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, Wk);
@@ -878,8 +931,10 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
   for (int it = 0; it < n_iters; ++it) {
     cudaEvent_t* e = &ev[10 * (size_t)it];
     for (int q = 0; q < 8; ++q) cudaEventRecordWithFlags(e[q], s, cudaEventRecordExternal);
-    if (S->bin_grid > 0)
-      k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(D, S->wk, nullptr, nullptr);
+    if (S->bin_grid > 0) {
+      if (S->wk.rg > 1) TRY(launch_bin_wm(D, S->wk, S->bin_grid, s));
+      else k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(D, S->wk, nullptr, nullptr);
+    }
     cudaEventRecordWithFlags(e[1], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[2], s, cudaEventRecordExternal);
     if (S->gen_grid > 0)

@@ -162,9 +162,16 @@ struct DevProblem {
 };
 
 // Per-walker-set state views; walker w = blockIdx.y.
+// Row state is grouped by walkers: groups of rg consecutive walkers, and inside a group the rg
+// walkers' records of one row are adjacent (walker-minor), so that one row's state for the whole
+// group is one contiguous run (rg x 16 B): record (w, i) is at rs[((w / rg) * rss + i) * rg + w % rg].
+// rg = 1 is the walker-major layout of a single walker.
 struct DevWalkers {
   double* x;            size_t xs;     // [W][n] internal order
-  RowState* rs;         size_t rss;    // [W][m_norm]
+  RowState* rs;         size_t rss;    // [W/rg][rss = m_norm + 1][rg]
+  int32_t rg;                          // walkers per row-state group (1, or a power of two <= 32)
+  int32_t n_groups;                    // ceil(W / rg)
+  uint32_t* xbits;                     // [n_groups][n]: bit (w % rg) = x̄ of binary p for walker w (rg > 1)
   int32_t* tabu;        size_t ts;     // [W][n]
   double* best_x;                      // [W][n]
   WalkerScalars* sc;                   // [W]
@@ -178,5 +185,18 @@ struct DevWalkers {
   double delta;                        // NaN = auto
   unsigned long long* kt;              // [kKtWords] kernel timing, NULL = off
 };
+
+// The row state of one walker: base pointer and stride (in records) between consecutive rows.
+struct RowView {
+  RowState* p;
+  int st;
+  __device__ __forceinline__ RowState& operator[](int i) const { return p[(size_t)i * st]; }
+};
+__host__ __device__ __forceinline__ RowView row_view(const DevWalkers& Wk, int w) {
+  RowView v;
+  v.p = Wk.rs + ((size_t)(w / Wk.rg) * Wk.rss) * Wk.rg + (w % Wk.rg);
+  v.st = Wk.rg;
+  return v;
+}
 
 }  // namespace chap

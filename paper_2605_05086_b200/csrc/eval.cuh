@@ -122,8 +122,8 @@ __device__ __forceinline__ void finish_column(const DevProblem& P, int p, double
 
 // One 16-byte row-state gather (r f64, w f32). The inactive cutoff row holds r = -inf, w = 0,
 // which makes every one of its contributions vanish (no per-nonzero test needed).
-__device__ __forceinline__ void load_row(const RowState* rs, int i, double& r, double& w) {
-  const double2 v = __ldg(reinterpret_cast<const double2*>(rs) + i);
+__device__ __forceinline__ void load_row(const RowView& rs, int i, double& r, double& w) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(rs.p) + (size_t)i * rs.st);
   r = v.x;
   w = (double)__int_as_float((int)__double2loint(v.y));
 }
@@ -194,7 +194,7 @@ constexpr size_t kTileSmem = sizeof(SmemGenM);
 
 struct TileCtx {
   const double* x;
-  const RowState* rs;
+  RowView rs;
   const int32_t* tabu;
   long long k;
   int use_tabu;
@@ -463,7 +463,8 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WalkerScalars* sc = Wk.sc + walker;
   const double* __restrict__ X = Wk.x + (size_t)walker * Wk.xs;
-  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)walker * Wk.rss);
+  // walker-major row state (rg = 1): the walker-minor layout runs k_eval_bin_wm instead
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(row_view(Wk, walker).p);
   const int32_t* __restrict__ TB = Wk.tabu + (size_t)walker * Wk.ts;
   const long long kk = sc->k;
   const int use_tabu = Wk.use_tabu;
@@ -564,6 +565,150 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
 }
 
 // ------------------------------------------------------------------------------------------
+// walker-minor binary kernel (row-state groups of rg > 1 walkers): one lane per walker
+// ------------------------------------------------------------------------------------------
+// With the row state of a group of RG walkers interleaved (DevWalkers), the RG records of one row
+// are one contiguous run, so one warp evaluates a binary column for the whole group: lane =
+// (slot, walker) = (lane / RG, lane % RG), the 32 / RG slots split the column's nonzeros, the CSC
+// entries are read once per group and broadcast, and every row-state gather is a coalesced
+// RG x 16-byte run instead of RG scattered sectors. x̄ comes from the group's
+// bitset word of the column. The flip penalty per nonzero and the column sum are
+// those of k_eval_bin; the sum over slots is a fixed shuffle tree of exact
+// half-integer partials (R11), so the scores are bit-identical to the walker-major kernel's.
+// A chunk of a long binary column adds each walker's partial to that walker's accumulator;
+// k_eval finishes the column.
+constexpr int kBinWmThreads = 256;
+struct BinWmWarp {
+  int id[kBinTile];
+  double a[kBinTile];
+};
+
+template <int RG>
+__global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, DevWalkers Wk) {
+  constexpr int NS = 32 / RG;   // slots per warp
+  __shared__ __align__(16) BinWmWarp sw[kBinWmThreads / 32];
+  __shared__ Best sb[kBinWmThreads / 32][32];
+  const int g = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wl = lane % RG, slot = lane / RG;
+  const int w = g * RG + wl;
+  const bool live = w < Wk.W;
+  const int wr = live ? w : g * RG;   // padding lanes of the last group load a real walker's scalars
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)g * Wk.rss * RG) + wl;
+  const uint32_t* __restrict__ XB = Wk.xbits + (size_t)g * P.n;
+  const int32_t* __restrict__ TB = Wk.tabu + (size_t)wr * Wk.ts;
+  const long long kk = Wk.sc[wr].k;
+  const int use_tabu = Wk.use_tabu;
+  KT_BEGIN(Wk, 0);
+  Best b;
+  b.init();
+  // admissibility (R13) is read only for a column that would become the lane's best
+  auto offer = [&](double sc, int j, int p, double v) {
+    if (better_move(sc, j, b.s, b.j) && (!use_tabu || (long long)__ldg(TB + p) <= kk)) {
+      b.s = sc;
+      b.v = v;
+      b.j = j;
+      b.p = p;
+    }
+  };
+  const int nwarps = gridDim.x * (kBinWmThreads / 32);
+  int t = blockIdx.x * (kBinWmThreads / 32) + wid;
+  for (; t < P.n_bchunks; t += nwarps) {
+    const WTile T = P.bchunks[t];
+    const int p = T.p0, len = T.ncols;
+    const int* __restrict__ ridx = P.row_idx + T.e0;
+    const double* __restrict__ rval = P.val + T.e0;
+    const double xb = (double)((__ldg(XB + p) >> wl) & 1u);
+    const double dir = 1.0 - 2.0 * xb;
+    double acc = 0.0;
+    for (int k0 = slot; k0 < len; k0 += 4 * NS) {
+      int id[4];
+      double av[4];
+      double2 rv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + q * NS;
+        id[q] = k < len ? __ldg(ridx + k) : -1;
+        av[q] = k < len ? __ldg(rval + k) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double r = rv[q].x, wv = (double)__int_as_float((int)__double2loint(rv[q].y));
+        acc += penalty(wv, r, r + av[q] * dir);
+      }
+    }
+#pragma unroll
+    for (int off = RG; off < 32; off <<= 1) acc += __shfl_xor_sync(kFull, acc, off);
+    if (slot == 0 && live) {
+      const LongCol L = P.lcols[T.e1];
+      if (L.nchunks > 1) atomicAdd(Wk.lscr + (size_t)w * Wk.lss + L.scr, acc);
+      else offer(acc, __ldg(P.perm + p), p, 1.0 - xb);
+    }
+  }
+  t -= P.n_bchunks;
+  BinWmWarp& S = sw[wid];
+  for (; t < P.n_btiles; t += nwarps) {
+    const WTile T = P.btiles[t];
+    const int nc = T.ncols, len = T.e1 - T.e0;
+    __syncwarp();
+    if (4 * lane < len) {   // stage the tile's CSC entries (read once for the group)
+      *reinterpret_cast<int4*>(S.id + 4 * lane) = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0) + lane);
+      *reinterpret_cast<double2*>(S.a + 4 * lane) = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane);
+      *reinterpret_cast<double2*>(S.a + 4 * lane + 2) = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane + 1);
+    }
+    int cb = 0, ce = 0, j = 0;
+    uint32_t xw = 0u;
+    if (lane < nc) {   // column data of lane c
+      const int p = T.p0 + lane;
+      cb = __ldg(P.col_ptr + p) - T.e0;
+      ce = min(__ldg(P.col_ptr + p + 1) - T.e0, len);
+      j = __ldg(P.perm + p);
+      xw = __ldg(XB + p);
+    }
+    __syncwarp();
+    for (int c = 0; c < nc; ++c) {
+      const int e0 = __shfl_sync(kFull, cb, c), e1 = __shfl_sync(kFull, ce, c);
+      const int jc = __shfl_sync(kFull, j, c);
+      const double xb = (double)((__shfl_sync(kFull, xw, c) >> wl) & 1u);
+      const double dir = 1.0 - 2.0 * xb;
+      double acc = 0.0;
+      for (int k0 = e0 + slot; k0 < e1; k0 += 4 * NS) {
+        int id[4];
+        double av[4];
+        double2 rv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = k0 + q * NS;
+          id[q] = k < e1 ? S.id[k] : -1;
+          av[q] = k < e1 ? S.a[k] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double r = rv[q].x, wv = (double)__int_as_float((int)__double2loint(rv[q].y));
+          acc += penalty(wv, r, r + av[q] * dir);
+        }
+      }
+#pragma unroll
+      for (int off = RG; off < 32; off <<= 1) acc += __shfl_xor_sync(kFull, acc, off);
+      if (slot == 0 && live) offer(acc, jc, T.p0 + c, 1.0 - xb);
+    }
+  }
+  // per-walker block best: warps in fixed order
+  sb[wid][lane] = b;
+  __syncthreads();
+  if (threadIdx.x < RG) {
+    Best o = sb[0][threadIdx.x];
+    for (int q = 1; q < kBinWmThreads / 32; ++q) o.take(sb[q][threadIdx.x]);
+    const int ww = g * RG + threadIdx.x;
+    if (ww < Wk.W) write_part(Wk.part + (size_t)ww * Wk.ps + blockIdx.x, o);
+  }
+  KT_END(Wk, 0);
+}
+
+// ------------------------------------------------------------------------------------------
 // general-column kernel
 // ------------------------------------------------------------------------------------------
 // k_eval_gen evaluates the packed general columns (and empty columns) with Algorithm 1 per
@@ -616,9 +761,10 @@ __device__ __forceinline__ double next_up(double t) {   // the next double above
 }
 
 __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __restrict__ X,
-                                         const double2* __restrict__ RS, const int32_t* __restrict__ TB,
-                                         const WTile& T, int lane, GenWarp& S, Best& b, double* oxhat,
-                                         double* oscore, long long kk, int use_tabu) {
+                                         const double2* __restrict__ RS, int st,
+                                         const int32_t* __restrict__ TB, const WTile& T, int lane,
+                                         GenWarp& S, Best& b, double* oxhat, double* oscore,
+                                         long long kk, int use_tabu) {
   const int nc = T.ncols, len = T.e1 - T.e0;
   const bool act = 4 * lane < len;
   int4 id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
@@ -643,10 +789,10 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
     cint = __ldg(P.vclass + p) != 3;
   }
   double2 rv[4];
-  rv[0] = __ldg(RS + id.x);
-  rv[1] = __ldg(RS + id.y);
-  rv[2] = __ldg(RS + id.z);
-  rv[3] = __ldg(RS + id.w);
+  rv[0] = __ldg(RS + (size_t)id.x * st);
+  rv[1] = __ldg(RS + (size_t)id.y * st);
+  rv[2] = __ldg(RS + (size_t)id.z * st);
+  rv[3] = __ldg(RS + (size_t)id.w * st);
   if (lane < nc) {
     S.cx[lane] = xb;
     S.cl[lane] = l;
@@ -868,7 +1014,7 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
 // in coalesced rounds of 32 buckets, takes line 16's argmax with R4 and zeroes the accumulators.
 __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
-                                           const int32_t* __restrict__ TB, const WTile& T, int lane,
+                                           int st, const int32_t* __restrict__ TB, const WTile& T, int lane,
                                            unsigned char* wmem, Best& b, double* oxhat, double* oscore,
                                            long long kk, int use_tabu) {
   const LongCol L = P.lcols[T.e1];
@@ -902,7 +1048,7 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
   }
   double2 rv[kWSlotsGen];
 #pragma unroll
-  for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + id[q]);
+  for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + (size_t)id[q] * st);
   bool fast = local;
 #pragma unroll
   for (int q = 0; q < kWSlotsGen; ++q) {
@@ -1050,7 +1196,9 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WalkerScalars* sc = Wk.sc + walker;
   const double* __restrict__ X = Wk.x + (size_t)walker * Wk.xs;
-  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)walker * Wk.rss);
+  const RowView RV = row_view(Wk, walker);
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(RV.p);
+  const int st = RV.st;
   const int32_t* __restrict__ TB = Wk.tabu + (size_t)walker * Wk.ts;
   const long long kk = sc->k;
   const int use_tabu = Wk.use_tabu;
@@ -1058,7 +1206,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   KT_BEGIN(Wk, 1);
   TileCtx C;
   C.x = X;
-  C.rs = Wk.rs + (size_t)walker * Wk.rss;
+  C.rs = RV;
   C.tabu = TB;
   C.k = kk;
   C.use_tabu = use_tabu;
@@ -1070,7 +1218,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   int t = blockIdx.x * (kGenThreads / 32) + wid;
   // chunks of long columns first (their latency overlaps the packed tiles of other warps)
   for (; t < P.n_gchunks; t += nwarps)
-    lbkt_chunk(P, Wk, walker, X, RS, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
+    lbkt_chunk(P, Wk, walker, X, RS, st, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
   __syncwarp();
   t -= P.n_gchunks;
   WTile Tn;
@@ -1078,7 +1226,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   for (; t < P.n_wtiles; t += nwarps) {
     const WTile T = Tn;
     if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];
-    if (T.kind == CC_GEN) gen_tile(P, X, RS, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
+    if (T.kind == CC_GEN) gen_tile(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
     else wtile_empty(P, C, T, lane, b);
   }
   b = block_reduce_best(b, sm_b);
@@ -1103,7 +1251,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   KT_BEGIN(Wk, 2);
   TileCtx C;
   C.x = Wk.x + (size_t)walker * Wk.xs;
-  C.rs = Wk.rs + (size_t)walker * Wk.rss;
+  C.rs = row_view(Wk, walker);
   C.tabu = Wk.tabu + (size_t)walker * Wk.ts;
   C.k = sc->k;
   C.use_tabu = Wk.use_tabu;

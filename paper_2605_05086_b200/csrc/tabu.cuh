@@ -24,14 +24,14 @@ __global__ void k_permute_in(DevProblem P, const double* __restrict__ xu, size_t
 // and w = 0, so that it contributes nothing to any score without a per-nonzero test (its logical
 // weight while inactive is the initial 1: bumps skip inactive rows). init_w: 0 keep weights,
 // 1 set to 1, 2 copy from wsrc (eval API).
-__global__ void k_rows_init(DevProblem P, const double* __restrict__ x, size_t xs, RowState* rs,
-                            size_t rss, const WalkerScalars* sc, int init_w,
-                            const float* __restrict__ wsrc) {
-  const int w = blockIdx.y;
+__global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float* __restrict__ wsrc,
+                            int only_walker) {
+  const int w = only_walker >= 0 ? only_walker : blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const double* xw = x + (size_t)w * xs;
-  RowState* rw = rs + (size_t)w * rss;
+  const double* xw = Wk.x + (size_t)w * Wk.xs;
+  const RowView rw = row_view(Wk, w);
+  const WalkerScalars* sc = Wk.sc;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     RowState d;
     d.r = -INFINITY;
@@ -84,7 +84,7 @@ __device__ __forceinline__ double auto_delta(const DevProblem& P, double delta_p
 // Set the walker's incumbent from its current point (violated == 0): best_obj, cutoff rhs
 // c.x̄ - δ, residual of the cutoff row recomputed as y_cut - rhs.
 __device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWalkers& Wk,
-                                               WalkerScalars* sc, RowState* rw) {
+                                               WalkerScalars* sc, const RowView& rw) {
   const double z = sc->obj;
   sc->best_obj = z;
   sc->has_inc = 1;
@@ -104,7 +104,7 @@ __global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, in
   const int w = (only_walker >= 0) ? only_walker : blockIdx.x;
   const int tid = threadIdx.x;
   WalkerScalars* sc = Wk.sc + w;
-  RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const RowView rw = row_view(Wk, w);
   if (tid == 0) {
     const long long vt = sc->vcount;   // k_viol_count
     const double zt = sc->cdot;        // k_cut_dot
@@ -151,11 +151,11 @@ __global__ void __launch_bounds__(256) k_cut_dot(DevProblem P, const double* __r
 }
 
 // Violated active rows of each walker (r > 0; the inactive cutoff row excluded), grid-wide.
-__global__ void __launch_bounds__(256) k_viol_count(DevProblem P, const RowState* rs, size_t rss,
-                                                     WalkerScalars* sc, int only_walker) {
+__global__ void __launch_bounds__(256) k_viol_count(DevProblem P, DevWalkers Wk, int only_walker) {
   __shared__ unsigned long long sm[8];
   const int w = only_walker >= 0 ? only_walker : blockIdx.y;
-  const RowState* rw = rs + (size_t)w * rss;
+  WalkerScalars* sc = Wk.sc;
+  const RowView rw = row_view(Wk, w);
   const int cut_active = sc[w].cut_active;
   unsigned long long v = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m_norm; i += gridDim.x * blockDim.x)
@@ -167,6 +167,20 @@ __global__ void __launch_bounds__(256) k_viol_count(DevProblem P, const RowState
     unsigned long long t = 0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sm[q];
     if (t) atomicAdd((unsigned long long*)&sc[w].vcount, t);
+  }
+}
+
+// The binary bitset of walker-minor groups from x (all walkers, or walker only_walker).
+__global__ void k_xbits_build(DevProblem P, DevWalkers Wk, int only_walker) {
+  if (!Wk.xbits) return;
+  const int g = only_walker >= 0 ? only_walker / Wk.rg : blockIdx.y;
+  const int w0 = g * Wk.rg, w1 = min(Wk.W, w0 + Wk.rg);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) {
+    if (P.vclass[p] != 1) continue;
+    uint32_t word = 0u;
+    for (int w = w0; w < w1; ++w)
+      if (Wk.x[(size_t)w * Wk.xs + p] != 0.0) word |= 1u << (w - w0);
+    Wk.xbits[(size_t)g * P.n + p] = word;
   }
 }
 
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   const int w = blockIdx.y, tid = threadIdx.x;
   WalkerScalars* sc = Wk.sc + w;
   double* x = Wk.x + (size_t)w * Wk.xs;
-  RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const RowView rw = row_view(Wk, w);
   const Decision d = sc->dec;
   KT_BEGIN(Wk, 3);
   const int cut_active = sc->cut_active;
@@ -232,6 +246,11 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   sc->pending_copy = 0;
   if (d.move) {
     x[d.p] = d.v;
+    if (Wk.xbits && P.vclass[d.p] == 1) {   // the group's binary bitset (walker-minor kernels)
+      uint32_t* word = Wk.xbits + (size_t)(w / Wk.rg) * P.n + d.p;
+      const uint32_t bit = 1u << (w % Wk.rg);
+      if (d.v != 0.0) atomicOr(word, bit); else atomicAnd(word, ~bit);
+    }
     Wk.tabu[(size_t)w * Wk.ts + d.p] = (int32_t)(k + 1 + Wk.tenure);
     sc->obj = vsc->obj + P.c[d.p] * d.delta;
     sc->n_moves = vsc->n_moves + 1;
@@ -302,7 +321,7 @@ __global__ void k_export_vars(DevProblem P, DevWalkers Wk, double* x, int64_t* t
 
 __global__ void k_export_rows(DevProblem P, DevWalkers Wk, double* r, float* wt) {
   const int w = blockIdx.y;
-  const RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const RowView rw = row_view(Wk, w);
   const int cut_active = Wk.sc[w].cut_active;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m_norm; i += gridDim.x * blockDim.x) {
     const RowState s = rw[i];
@@ -333,7 +352,7 @@ __global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= Wk.W) return;
   WalkerScalars* sc = Wk.sc + w;
-  RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const RowView rw = row_view(Wk, w);
   const double rhs = z - auto_delta(P, Wk.delta, z);
   if (sc->cut_active && !(rhs < sc->cutoff_rhs)) return;
   const double r_old = sc->cut_active ? rw[P.cut_row].r : -INFINITY;
@@ -363,7 +382,7 @@ __global__ void __launch_bounds__(256) k_summaries(DevProblem P, DevWalkers Wk, 
                                                    int gid0, int stop) {
   __shared__ double sm[32];
   const int w = blockIdx.x, tid = threadIdx.x;
-  const RowState* rw = Wk.rs + (size_t)w * Wk.rss;
+  const RowView rw = row_view(Wk, w);
   double s = 0.0;
   for (int i = tid; i < P.cut_row; i += blockDim.x) {
     const double r = rw[i].r;

@@ -241,6 +241,31 @@ def test_trajectory_setcover_small():
     _traj_compare(inst, [synth.x_lower(inst)], 400)
 
 
+@pytest.mark.parametrize("W", [3, 17, 33])
+def test_trajectory_walker_groups_packing(W):
+    """Walker-minor row-state groups (rg = 4, 32, 32 + a 1-walker group): every walker's
+    trajectory equals its own oracle run (k_eval_bin_wm, the group bitset, strided apply)."""
+    inst = synth.packing(seed=5, n=3000, m=600)
+    x0s = [synth.x_bernoulli(inst, (3, wi), 0.5) for wi in range(W)]
+    _traj_compare(inst, x0s, 120)
+
+
+def test_trajectory_walker_groups_mixed():
+    """40 walkers (groups of 32 + 8) on a mixed instance with long binary and long bounded-integer
+    columns: binary columns by k_eval_bin_wm, general columns by the strided general kernels."""
+    inst = synth.mixed(seed=9, n=4000, m=800, n_long=4, long_lo=300, long_hi=6000)
+    x0s = [synth.x_lower(inst)] + [synth.x_random(inst, s) for s in range(39)]
+    _traj_compare(inst, x0s, 40)
+
+
+def test_config_P_64_walkers_trajectory():
+    """BASELINE configs[3] in bench.py's launch configuration: 64 walkers on the 10^6-nonzero
+    packing instance (two walker-minor groups of 32), 12 iterations of every walker vs the oracle."""
+    inst = synth.packing()
+    x0s = [synth.x_bernoulli(inst, (3, wi), 0.5) for wi in range(64)]
+    _traj_compare(inst, x0s, 12)
+
+
 def test_invalid_x0_rejected():
     inst = synth.tiny(0)
     P = chap.Problem.from_instance(inst)
