@@ -394,6 +394,128 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     ++p;
   }
   I.n_long_columns = n_long;
+  // row-wise binary blocks (k_eval_binrow): packed binary columns [pb0, pb1) in blocks of <=
+  // kRowVmax columns balanced by nonzeros, a multiple of the resident clusters; each block's
+  // entries sorted by row, cut into kRowCluster slices padded to multiples of 4 with inert entries
+  std::vector<RowBlock> rblocks;
+  std::vector<int32_t> rb_row;
+  std::vector<uint32_t> rb_cv;
+  std::vector<int32_t> rb_perm;
+  {
+    int32_t pb0 = -1, pb1 = -1;
+    for (int32_t q = 0; q < n; ++q)
+      if (cls[perm[q]] == CC_BIN) {
+        if (pb0 < 0) pb0 = q;
+        pb1 = q + 1;
+      }
+    bool ok = pb0 >= 0;
+    int64_t tot = 0;
+    int maxdeg = 0;
+    for (int32_t q = pb0; ok && q < pb1; ++q) {
+      int d = 0;
+      for (int32_t e = col_ptr[q]; e < col_ptr[q + 1]; ++e) {
+        if (row_idx[e] == dummy_row) continue;
+        const double a = cval[e];
+        if (!(a == std::floor(a) && std::fabs(a) <= 32767.0)) ok = false;
+        ++d;
+      }
+      tot += d;
+      maxdeg = std::max(maxdeg, d);
+    }
+    // cluster width: the one that keeps the most SMs busy (clusters live inside a GPC), the wider
+    // on ties (fewer, larger blocks: more entries per row, denser row-state reads)
+    int ncl = 0, C = 0;
+    if (ok) {
+      cudaError_t e1 = cudaFuncSetAttribute(k_eval_binrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem);
+      if (e1 == cudaSuccess) {
+        for (int c = kRowCluster; c >= 4; --c) {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(c * std::max(1, P->sm_count / c));
+          cfg.blockDim = dim3(kRowThreads);
+          cfg.dynamicSmemBytes = kRowSmem;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = c;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          int k = 0;
+          if (cudaOccupancyMaxActiveClusters(&k, k_eval_binrow, &cfg) != cudaSuccess) k = 0;
+          if (k * c > ncl * C) { ncl = k; C = c; }
+        }
+      }
+      cudaGetLastError();
+      if (ncl < 1) ok = false;
+    }
+    if (ok) {
+      // blocks: nb, a multiple of the resident clusters, with <= kRowVmax columns each; column
+      // p = pb0 + b + k nb is column k of block b (round-robin over the degree-sorted columns, so
+      // every block gets an equal mix of long and short columns and about tot / nb entries)
+      const int32_t nbin = pb1 - pb0;
+      int nb = std::max(ncl, (nbin + kRowVmax - 1) / kRowVmax);
+      nb = (nb + ncl - 1) / ncl * ncl;
+      std::vector<int32_t> cnt(m_norm + 2, 0);
+      for (int b = 0; b < nb; ++b) {
+        const int32_t nvb = (nbin - b + nb - 1) / nb;   // columns pb0 + b, pb0 + b + nb, ...
+        // counting sort of the block's entries by row (stable in column order)
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int32_t k = 0; k < nvb; ++k) {
+          const int32_t c = pb0 + b + k * nb;
+          for (int32_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e)
+            if (row_idx[e] != dummy_row) ++cnt[row_idx[e] + 1];
+        }
+        for (int32_t i = 0; i <= m_norm; ++i) cnt[i + 1] += cnt[i];
+        const int64_t E = cnt[m_norm];
+        std::vector<int32_t> er(E);
+        std::vector<uint32_t> ec(E);
+        for (int32_t k = 0; k < nvb; ++k) {
+          const int32_t c = pb0 + b + k * nb;
+          for (int32_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
+            const int32_t i = row_idx[e];
+            if (i == dummy_row) continue;
+            const int32_t at = cnt[i]++;
+            er[at] = i;
+            ec[at] = (uint32_t)k | ((uint32_t)(uint16_t)(int16_t)cval[e] << 16);
+          }
+        }
+        RowBlock R{};
+        R.p0 = pb0 + b;
+        R.nv = nvb;
+        // slice s: the s-th C-th of the entries of rows < cut_row, then the s-th C-th of the
+        // (dense, last) cutoff row's entries, so that every slice carries an equal share of both
+        const int64_t E1 = cut_row > 0 ? cnt[cut_row - 1] : 0;   // (after the scatter cnt[i] = end of row i)
+        const int64_t E2 = E - E1;
+        for (int sl = 0; sl < C; ++sl) {
+          R.es[sl] = (int32_t)rb_row.size();
+          for (int half = 0; half < 2; ++half) {
+            const int64_t base = half ? E1 : 0, len = half ? E2 : E1;
+            for (int64_t k = base + len * sl / C; k < base + len * (sl + 1) / C; ++k) {
+              rb_row.push_back(er[k]);
+              rb_cv.push_back(ec[k]);
+            }
+          }
+          while (rb_row.size() & 3) {   // inert padding (the dummy row)
+            rb_row.push_back(dummy_row);
+            rb_cv.push_back(0u);
+          }
+        }
+        for (int sl = C; sl <= kRowCluster; ++sl) R.es[sl] = (int32_t)rb_row.size();
+        rblocks.push_back(R);
+      }
+      if (getenv("CHAP_DEBUG"))
+        fprintf(stderr, "[chap] binrow: %d clusters x %d CTAs, %zu blocks, %lld entries (%lld stored)\n", ncl, C,
+                rblocks.size(), (long long)tot, (long long)rb_row.size());
+      rb_perm.assign((size_t)nb * kRowVmax, -1);
+      for (int32_t q = 0; q < nbin; ++q) rb_perm[(size_t)(q % nb) * kRowVmax + q / nb] = perm[pb0 + q];
+      P->binrow_grid = ncl * C;
+      P->binrow_pb0 = pb0;
+      P->binrow_nbin = nbin;
+      P->binrow_cluster = C;
+      P->binrow_maxdeg = maxdeg;
+      P->binrow_entries = (int64_t)rb_row.size();
+    }
+  }
   {  // algorithmic-bytes model
     int64_t mb[3] = {0, 0, 0}, nz[3] = {0, 0, 0}, mw[3] = {0, 0, 0};
     for (int32_t q = 0; q < n; ++q) {
@@ -449,7 +571,23 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   int32_t* d_lfin;
   TRY(B.upload(&d_lfin, lfin));
   TRY(B.upload(&d_lcols, lcols));
+  RowBlock* d_rblocks;
+  int32_t* d_rb_row;
+  uint32_t* d_rb_cv;
+  TRY(B.upload(&d_rblocks, rblocks));
+  TRY(B.upload(&d_rb_row, rb_row));
+  TRY(B.upload(&d_rb_cv, rb_cv));
+  int32_t* d_rb_perm;
+  TRY(B.upload(&d_rb_perm, rb_perm));
   DevProblem& D = P->dp;
+  D.rblocks = d_rblocks;
+  D.n_rblocks = (int32_t)rblocks.size();
+  D.rb_cluster = P->binrow_cluster;
+  D.rb_pb0 = P->binrow_pb0;
+  D.rb_perm = d_rb_perm;
+  D.rb_nbin = P->binrow_nbin;
+  D.rb_row = d_rb_row;
+  D.rb_cv = d_rb_cv;
   D.n = n;
   D.m_norm = m_norm;
   D.cut_row = cut_row;
@@ -504,6 +642,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   const int bwarps = kBinThreads / 32;
   const int bwork = D.n_btiles + D.n_bchunks;
   P->bin_grid = bwork ? std::max(1, std::min((bwork + bwarps - 1) / bwarps, P->bin_occ * P->sm_count)) : 0;
+  P->bin_chunk_grid = D.n_bchunks ? std::max(1, std::min((D.n_bchunks + bwarps - 1) / bwarps, P->bin_occ * P->sm_count)) : 0;
   P->info.eval_launches = 1 + (P->bin_grid > 0) + (P->gen_grid > 0);
   P->rows_grid = std::max(1, std::min((m_norm + 7) / 8, 8 * P->sm_count));
   // eval workspace
@@ -576,14 +715,40 @@ static int bin_wm_occupancy(int rg) {
   return e == cudaSuccess ? std::max(1, occ) : 1;
 }
 
+static chap_status launch_binrow(const chap_problem* P, const DevWalkers& Wk, int rgrid, int part_base,
+                                 cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rgrid);
+  cfg.blockDim = dim3(kRowThreads);
+  cfg.dynamicSmemBytes = kRowSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P->binrow_cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_eval_binrow, P->dp, Wk, part_base));
+  return CHAP_OK;
+}
+
+// Part slots of one walker: [k_eval_bin | k_eval_gen | k_eval_binrow | k_eval]; k_eval reduces them.
 chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
-                              double* oxhat, double* oscore, chap_move* best, cudaStream_t s) {
+                              int rgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s) {
   if (bgrid > 0) {
     if (Wk.rg > 1) TRY(launch_bin_wm(P->dp, Wk, bgrid, s));
-    else k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
+    else if (rgrid > 0) {   // packed binary columns row-wise: k_eval_bin takes the long chunks only
+      DevProblem D = P->dp;
+      D.n_btiles = 0;
+      k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(D, Wk, oxhat, oscore);
+    } else {
+      k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
+    }
   }
+  if (rgrid > 0) TRY(launch_binrow(P, Wk, rgrid, bgrid + ggrid, s));
   if (ggrid > 0) k_eval_gen<<<dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s>>>(P->dp, Wk, oxhat, oscore, bgrid);
-  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid);
+  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid + rgrid);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -650,7 +815,7 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, xhat, score, best, s));
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, xhat, score, best, s));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -772,7 +937,15 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
                                        (bin_wm_occupancy(rg) * p->sm_count + Wk.n_groups - 1) / Wk.n_groups));
   }
   S->gen_grid = p->gen_grid ? std::max(1, std::min(p->gen_grid, (p->gen_occ * p->sm_count + W - 1) / W)) : 0;
-  Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid;
+  // one walker with integral weights whose column sums fit int32: packed binary columns row-wise
+  S->binrow_grid = 0;
+  if (W == 1 && p->binrow_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) &&
+      2.0 * (double)prm.weight_cap * (double)std::max(1, p->binrow_maxdeg) < 2147483647.0) {
+    S->binrow_grid = p->binrow_grid;
+    S->bin_grid = p->bin_chunk_grid;
+    TRY(B.alloc(&Wk.xbits, (size_t)p->dp.n_rblocks * kRowWpb));   // block-ordered bitset
+  }
+  Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
   TRY(B.alloc(&Wk.sel_count, W));
   Wk.lss = p->lscr_per_walker;
@@ -821,7 +994,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
-  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, nullptr, nullptr, nullptr, s));
+  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, S->binrow_grid, nullptr, nullptr, nullptr, s));
   k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -932,9 +1105,12 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     cudaEvent_t* e = &ev[10 * (size_t)it];
     for (int q = 0; q < 8; ++q) cudaEventRecordWithFlags(e[q], s, cudaEventRecordExternal);
     if (S->bin_grid > 0) {
+      DevProblem Db = D;
+      if (S->binrow_grid > 0) Db.n_btiles = 0;
       if (S->wk.rg > 1) TRY(launch_bin_wm(D, S->wk, S->bin_grid, s));
-      else k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(D, S->wk, nullptr, nullptr);
+      else k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(Db, S->wk, nullptr, nullptr);
     }
+    if (S->binrow_grid > 0) TRY(launch_binrow(P, S->wk, S->binrow_grid, S->bin_grid + S->gen_grid, s));
     cudaEventRecordWithFlags(e[1], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[2], s, cudaEventRecordExternal);
     if (S->gen_grid > 0)
@@ -942,7 +1118,7 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[4], s, cudaEventRecordExternal);
     k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
-                                                                     S->bin_grid + S->gen_grid);
+                                                                     S->bin_grid + S->gen_grid + S->binrow_grid);
     cudaEventRecordWithFlags(e[5], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[8], s, cudaEventRecordExternal);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);

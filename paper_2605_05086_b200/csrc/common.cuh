@@ -83,6 +83,25 @@ struct Tile {
   int32_t pad;
 };
 
+// Row-wise binary flip evaluation (k_eval_binrow, PAPER.md:347 re-designed): the packed binary
+// columns are cut into variable blocks; the nonzeros of a block are stored sorted by row and cut
+// into kRowCluster equal slices, one per CTA of a thread-block cluster.
+constexpr int kRowCluster = 8;                    // max CTAs per cluster (portable maximum); the
+                                                  // width used is chosen at problem create
+constexpr int kRowThreads = 1024;                 // k_eval_binrow block (one CTA per SM)
+constexpr int kRowVmax = 32768;                   // variables per block: int32 scores in 128 KB of smem
+constexpr int kRowWpb = kRowVmax / 32;            // bitset words per block
+constexpr int kRowConsumers = kRowThreads - 32;   // consumer threads (the last warp produces)
+constexpr int kRowPer = 4;                        // entries per consumer thread per stage
+constexpr int kRowChunk = kRowPer * kRowConsumers;   // entries per TMA stage (7.75 KB rows + 7.75 KB columns)
+constexpr int kRowStages = 3;                     // stages of the entry ring (93 KB)
+struct RowBlock {
+  int32_t p0;                 // first column (internal order): column k of block b is p0 + k nb
+  int32_t nv;                 // columns
+  int32_t es[kRowCluster + 1];   // entry slices [es[s], es[s+1]), multiples of 4
+  int32_t pad;
+};
+
 // Per-column result competing for the global best move.
 struct Cand {
   double s;
@@ -130,6 +149,27 @@ __device__ __forceinline__ unsigned long long kt_now() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// mbarrier / bulk-copy (TMA) helpers (PTX ISA: mbarrier, cp.async.bulk)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+      ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 #define KT_BEGIN(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMin((WK).kt + 2 * (q), chap::kt_now()); } while (0)
 #define KT_END(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMax((WK).kt + 2 * (q) + 1, chap::kt_now()); } while (0)
 constexpr int kKtWords = 16;   // [2q, 2q+1] start/end of kernel q (0 bin, 1 gen, 2 eval, 3 apply); [8..13] sums
@@ -157,6 +197,12 @@ struct DevProblem {
   const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns
   const LongCol* lcols;                                 // [n_long]
   const int32_t* lfin; int32_t n_lfin;                  // long columns k_eval finishes
+  const RowBlock* rblocks; int32_t n_rblocks;           // row-wise binary blocks (0: not built)
+  int32_t rb_cluster;        // CTAs per cluster of k_eval_binrow (= slices per block)
+  int32_t rb_pb0, rb_nbin;   // packed binary columns [rb_pb0, rb_pb0 + rb_nbin), round-robin over blocks
+  const int32_t* rb_perm;    // [n_rblocks][kRowVmax] user index of column k of block b (block order)
+  const int32_t* rb_row;     // [entries] row of each entry (sorted within a slice)
+  const uint32_t* rb_cv;     // [entries] column within the block (low 16 bits) | int16 a_ij (high 16)
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   double auto_delta;
 };
@@ -171,7 +217,11 @@ struct DevWalkers {
   RowState* rs;         size_t rss;    // [W/rg][rss = m_norm + 1][rg]
   int32_t rg;                          // walkers per row-state group (1, or a power of two <= 32)
   int32_t n_groups;                    // ceil(W / rg)
-  uint32_t* xbits;                     // [n_groups][n]: bit (w % rg) = x̄ of binary p for walker w (rg > 1)
+  uint32_t* xbits;                     // rg > 1: [n_groups][n], bit (w % rg) = x̄ of binary p for walker w;
+                                       // rg = 1 (one walker, k_eval_binrow): block-ordered bitset of the
+                                       // packed binaries, [n_rblocks][kRowWpb], column k of block b at
+                                       // bit k % 32 of word b kRowWpb + k / 32 (the bitset incumbent of
+                                       // PAPER.md:349); NULL = not kept
   int32_t* tabu;        size_t ts;     // [W][n]
   double* best_x;                      // [W][n]
   WalkerScalars* sc;                   // [W]

@@ -17,6 +17,8 @@
 // Every warp-tile slot issues its coalesced CSC loads and one 16-byte row-state gather before
 // using any of them.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace chap {
@@ -704,6 +706,162 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
     for (int q = 1; q < kBinWmThreads / 32; ++q) o.take(sb[q][threadIdx.x]);
     const int ww = g * RG + threadIdx.x;
     if (ww < Wk.W) write_part(Wk.part + (size_t)ww * Wk.ps + blockIdx.x, o);
+  }
+  KT_END(Wk, 0);
+}
+
+// ------------------------------------------------------------------------------------------
+// row-wise binary kernel (one walker): PAPER.md:347's row-wise flip scoring, re-designed
+// ------------------------------------------------------------------------------------------
+// The paper scores binary flips row-wise: a warp per row, the row's residual and weight read once,
+// and an atomicAdd of every entry's penalty into a per-variable score array in global memory.
+// Here the packed binary columns are cut into blocks of <= kRowVmax variables whose scores live in
+// shared memory, so the atomics are shared-memory integer adds (2·penalty is an integer for the
+// integral weights of R11; the sums are exact, so their order does not matter). A block's nonzeros
+// are stored sorted by row and cut into kRowCluster slices, one per CTA of a cluster: a CTA streams
+// its slice (8 bytes per nonzero: row, column-in-block | int16 coefficient), reads the row state of
+// consecutive rows (a warp's 32 entries touch a few adjacent 16-byte records instead of 32 random
+// sectors), reads x̄ from the block's slice of the bitset incumbent held in shared
+// memory, and adds 2·p(w_i, r_i, r_i + a_ij (1 - 2x̄_j)) to the column's
+// counter. After a cluster barrier CTA q sums the kRowCluster partial counters of its eighth of the
+// block's columns over distributed shared memory, finishes those columns (tabu R13, R6) and keeps
+// its best; a second barrier frees the counters for the next block (blocks round-robin over the
+// clusters).
+// Each CTA streams its slice of a block in chunks of kRowChunk entries by bulk copies (TMA,
+// cp.async.bulk) into a kRowStages-deep shared-memory ring. The last warp is the producer: its
+// lane 0 refills a stage as soon as the consumers release it (empty barrier: every consumer warp
+// has moved the stage's entries to registers; full barrier: the copy's bytes landed), so the
+// stream's bytes in flight depend neither on registers nor on the consumers' progress.
+struct RowRing {
+  int32_t row[kRowStages][kRowChunk];
+  uint32_t cv[kRowStages][kRowChunk];
+  uint64_t full[kRowStages];
+  uint64_t empty[kRowStages];
+};
+constexpr size_t kRowSmem = sizeof(RowRing) + sizeof(int) * kRowVmax + sizeof(uint32_t) * (kRowWpb + 2);
+
+// Cluster barrier with release/acquire at cluster scope (shared-memory counters become visible to
+// the other CTAs of the cluster).
+__device__ __forceinline__ void cluster_sync_acqrel() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, DevWalkers Wk, int part_base) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Best sb[kRowThreads / 32];
+  KT_BEGIN(Wk, 0);
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), C = P.rb_cluster;
+  const int cid = blockIdx.x / C, ncl = gridDim.x / C;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool producer = tid >= kRowConsumers;
+  RowRing& R = *reinterpret_cast<RowRing*>(smem);
+  int* sc = reinterpret_cast<int*>(smem + sizeof(RowRing));    // [kRowVmax] 2·score partials
+  uint32_t* bits = reinterpret_cast<uint32_t*>(sc + kRowVmax);  // [kRowWpb] the block's x̄ bits
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs);   // rg = 1, walker 0
+  const uint32_t* __restrict__ XB = Wk.xbits;
+  const int32_t* __restrict__ TB = Wk.tabu;
+  const long long kk = Wk.sc[0].k;
+  const int use_tabu = Wk.use_tabu;
+  if (tid == 0) {
+    for (int q = 0; q < kRowStages; ++q) {
+      mbar_init(&R.full[q], 1);
+      mbar_init(&R.empty[q], kRowConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  Best b;
+  b.init();
+  int g = 0;   // chunks of this CTA so far (both roles count the same sequence)
+  for (int vb = cid; vb < P.n_rblocks; vb += ncl) {
+    const RowBlock& B = P.rblocks[vb];
+    const int p0 = B.p0, nv = B.nv, nb = P.n_rblocks;
+    const int s0 = B.es[rank], s1 = B.es[rank + 1];
+    const int nch = (s1 - s0 + kRowChunk - 1) / kRowChunk;
+    for (int i = tid; i < nv; i += kRowThreads) sc[i] = 0;
+    for (int i = tid; i < (nv + 31) / 32; i += kRowThreads) bits[i] = __ldg(XB + (size_t)vb * kRowWpb + i);
+    __syncthreads();
+    if (producer) {
+      if (lane == 0)
+        for (int c = 0; c < nch; ++c) {
+          const int q = g + c, st = q % kRowStages, e = s0 + c * kRowChunk, len = min(kRowChunk, s1 - e);
+          if (q >= kRowStages) mbar_wait(&R.empty[st], (unsigned)((q / kRowStages) - 1) & 1u);
+          mbar_expect_tx(&R.full[st], (unsigned)(8 * len));
+          tma_load_1d(R.row[st], P.rb_row + e, 4u * len, &R.full[st]);
+          tma_load_1d(R.cv[st], P.rb_cv + e, 4u * len, &R.full[st]);
+        }
+      __syncwarp();
+    } else {
+      for (int c = 0; c < nch; ++c) {
+        const int q = g + c, st = q % kRowStages, len = min(kRowChunk, s1 - (s0 + c * kRowChunk));
+        mbar_wait(&R.full[st], (unsigned)(q / kRowStages) & 1u);
+        int id[kRowPer];
+        uint32_t u[kRowPer];
+        double2 rv[kRowPer];
+#pragma unroll
+        for (int k = 0; k < kRowPer; ++k) {
+          const int i = tid + k * kRowConsumers;
+          id[k] = i < len ? R.row[st][i] : -1;
+          u[k] = i < len ? R.cv[st][i] : 0u;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&R.empty[st]);   // the stage's entries are in registers
+#pragma unroll
+        for (int k = 0; k < kRowPer; ++k) rv[k] = id[k] >= 0 ? __ldg(RS + id[k]) : make_double2(-INFINITY, 0.0);
+#pragma unroll
+        for (int k = 0; k < kRowPer; ++k) {
+          // 2·p(w, r, r + d) with d = a (1 - 2x̄), in integers: satisfied
+          // before is r <= 0, after is r <= -d (exact: r + d is exact when it is near 0,
+          // Sterbenz), a violated row gets less violated iff d < 0; w is integral (R11). Inert
+          // rows give 0.
+          const int c2 = (int)(u[k] & 0xffffu);
+          const int ai = (int)(int16_t)(u[k] >> 16);
+          const bool xb = (bits[c2 >> 5] >> (c2 & 31)) & 1u;
+          const int nd = xb ? ai : -ai;   // -d
+          const double r = rv[k].x;
+          const int iw = __float2int_rn(__int_as_float((int)__double2loint(rv[k].y)));
+          const bool z0 = r <= 0.0, z1 = r <= (double)nd;
+          const int p2 = z0 ? (z1 ? 0 : -2 * iw) : (z1 ? 2 * iw : (nd > 0 ? iw : -iw));
+          if (p2 != 0) atomicAdd(sc + c2, p2);
+        }
+      }
+    }
+    g += nch;
+    cluster_sync_acqrel();
+    // columns [v0, v1) of the block: the sum of the cluster's partial counters (all remote loads
+    // in flight together), then the column (x̄ flipped, tabu R13, ties R6)
+    const int per = (nv + C - 1) / C;
+    const int v0 = rank * per, v1 = min(nv, v0 + per);
+    for (int v = v0 + tid; v < v1; v += kRowThreads) {
+      int part[kRowCluster];
+#pragma unroll
+      for (int q = 0; q < kRowCluster; ++q) part[q] = q < C ? cl.map_shared_rank(sc, q)[v] : 0;
+      int tot = 0;
+#pragma unroll
+      for (int q = 0; q < kRowCluster; ++q) tot += part[q];
+      const int p = p0 + v * nb;
+      const double xb = (double)((bits[v >> 5] >> (v & 31)) & 1u);
+      const double s = 0.5 * (double)tot;
+      if (s < b.s) continue;   // cannot become the best: no index or tabu read
+      const int j = __ldg(P.rb_perm + (size_t)vb * kRowVmax + v);
+      if (better_move(s, j, b.s, b.j) && (!use_tabu || (long long)__ldg(TB + p) <= kk)) {
+        b.s = s;
+        b.v = 1.0 - xb;
+        b.j = j;
+        b.p = p;
+      }
+    }
+    cluster_sync_acqrel();
+  }
+  b = warp_reduce_best(b);
+  if (lane == 0) sb[tid >> 5] = b;
+  __syncthreads();
+  if (tid == 0) {
+    Best o = sb[0];
+    for (int q = 1; q < kRowThreads / 32; ++q) o.take(sb[q]);
+    write_part(Wk.part + part_base + blockIdx.x, o);
   }
   KT_END(Wk, 0);
 }

@@ -95,6 +95,12 @@ struct chap_problem {
   int bin_grid = 0;            // k_eval_bin blocks for one walker (0: no binary tiles)
   int gen_occ = 1;
   int gen_grid = 0;            // k_eval_gen blocks for one walker
+  int binrow_grid = 0;         // k_eval_binrow CTAs (clusters x kRowCluster; 0: no row-wise blocks)
+  int binrow_maxdeg = 0;       // longest packed binary column (incl. its cutoff entry)
+  int binrow_cluster = 0;      // CTAs per cluster of k_eval_binrow
+  int binrow_pb0 = 0, binrow_nbin = 0;   // the packed binary columns [pb0, pb0 + nbin)
+  int bin_chunk_grid = 0;      // k_eval_bin blocks for the long binary chunks alone
+  int64_t binrow_entries = 0;  // stored entries (incl. slice padding)
   int rows_grid = 1;
   size_t lscr_per_walker = 1;   // doubles
   // eval workspace (one virtual walker)
@@ -144,6 +150,7 @@ struct chap_walkers {
   int eval_grid = 1;           // k_eval blocks per walker
   int bin_grid = 0;            // k_eval_bin blocks per walker
   int gen_grid = 0;            // k_eval_gen blocks per walker
+  int binrow_grid = 0;         // k_eval_binrow CTAs (one walker, row-wise binary columns), 0 = off
   ~chap_walkers() {
     if (xs) chap_exchange_state_free(xs);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -157,7 +164,7 @@ struct chap_walkers {
 namespace chap {
 // shared launch helpers (chap.cu)
 chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
-                        double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
+                        int rgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
 int grid_for(long long work, int threads, int cap);
 chap_status walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s);
 

@@ -173,6 +173,19 @@ __global__ void __launch_bounds__(256) k_viol_count(DevProblem P, DevWalkers Wk,
 // The binary bitset of walker-minor groups from x (all walkers, or walker only_walker).
 __global__ void k_xbits_build(DevProblem P, DevWalkers Wk, int only_walker) {
   if (!Wk.xbits) return;
+  if (Wk.rg == 1) {   // one walker: the block-ordered bitset of k_eval_binrow
+    const int nb = P.n_rblocks;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nb * kRowWpb; q += gridDim.x * blockDim.x) {
+      const int b = q / kRowWpb, k0 = 32 * (q % kRowWpb);
+      uint32_t word = 0u;
+      for (int t = 0; t < 32; ++t) {
+        const long long pq = (long long)(k0 + t) * nb + b;   // position among the packed binaries
+        if (pq < P.rb_nbin && Wk.x[P.rb_pb0 + pq] != 0.0) word |= 1u << t;
+      }
+      Wk.xbits[q] = word;
+    }
+    return;
+  }
   const int g = only_walker >= 0 ? only_walker / Wk.rg : blockIdx.y;
   const int w0 = g * Wk.rg, w1 = min(Wk.W, w0 + Wk.rg);
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) {
@@ -246,9 +259,14 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   sc->pending_copy = 0;
   if (d.move) {
     x[d.p] = d.v;
-    if (Wk.xbits && P.vclass[d.p] == 1) {   // the group's binary bitset (walker-minor kernels)
+    if (Wk.xbits && Wk.rg > 1 && P.vclass[d.p] == 1) {   // the group's bitset (k_eval_bin_wm)
       uint32_t* word = Wk.xbits + (size_t)(w / Wk.rg) * P.n + d.p;
       const uint32_t bit = 1u << (w % Wk.rg);
+      if (d.v != 0.0) atomicOr(word, bit); else atomicAnd(word, ~bit);
+    } else if (Wk.xbits && Wk.rg == 1 && d.p >= P.rb_pb0 && d.p < P.rb_pb0 + P.rb_nbin) {   // k_eval_binrow
+      const int q = d.p - P.rb_pb0, nb = P.n_rblocks, k = q / nb;
+      uint32_t* word = Wk.xbits + (size_t)(q % nb) * kRowWpb + (k >> 5);
+      const uint32_t bit = 1u << (k & 31);
       if (d.v != 0.0) atomicOr(word, bit); else atomicAnd(word, ~bit);
     }
     Wk.tabu[(size_t)w * Wk.ts + d.p] = (int32_t)(k + 1 + Wk.tenure);
