@@ -247,11 +247,17 @@ chap_status chap_walkers_profile(chap_walkers* ws, int32_t n_iters, double* ms_p
  * the captured graphs without events: every block stamps %globaltimer at its start (atomic min)
  * and end (atomic max) per kernel, and the apply kernel's finalising thread accumulates
  * end - start of each kernel of the iteration. out HOST [6] (may be NULL) first receives the sums:
- * ns of [0] k_eval_bin, [1] k_eval_gen, [2] k_eval, [3] k_apply (its start to the finalisation),
- * [4] first eval kernel start to apply finalisation, [5] iterations timed (synchronous read).
+ * ns of [0] the binary-column kernels (k_eval_bin and k_eval_binrow: first start to last end),
+ * [1] k_eval_gen, [2] k_eval, [3] k_apply (its start to the finalisation), [4] first eval kernel
+ * start to apply finalisation, [5] iterations timed (synchronous read). The eval kernels' device
+ * time is [4] - [3].
  * Then mode 1 turns timing on and zeroes the sums, 0 turns it off, -1 only reads. Turning it on or
  * off re-captures the iteration graph at the next chap_tabu_step. */
 chap_status chap_walkers_timing(chap_walkers* ws, int32_t mode, uint64_t* out, void* cuda_stream);
+
+/* Kernel launches of one tabu iteration of these walkers (the eval kernels with work, the binary
+ * row-wise kernel when used, k_eval and the apply kernel) into *out. */
+chap_status chap_walkers_launches_per_iter(const chap_walkers* ws, int32_t* out);
 
 /* ---------------------------------------------------------------------------------------- */
 /* Multi-GPU portfolio: independent walkers per GPU with an every-K exchange                 */

@@ -102,6 +102,7 @@ _SIGS = {
     "chap_walkers_destroy": (ctypes.c_int, [_P]),
     "chap_walkers_profile": (ctypes.c_int, [_P, c_i32, _P, _P]),
     "chap_walkers_timing": (ctypes.c_int, [_P, c_i32, _P, _P]),
+    "chap_walkers_launches_per_iter": (ctypes.c_int, [_P, _P]),
     "chap_walkers_exchange": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "chap_comm_unique_id": (ctypes.c_int, [_P]),
     "chap_comm_create": (ctypes.c_int, [_P, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
@@ -286,6 +287,12 @@ class Walkers:
         ms = np.zeros(5)
         _check(chap_walkers_profile(self.h, int(n_iters), ms.ctypes.data, _stream(stream)))
         return ms
+
+    def launches_per_iter(self) -> int:
+        """chap_walkers_launches_per_iter: kernel launches of one tabu iteration."""
+        out = ctypes.c_int32()
+        _check(chap_walkers_launches_per_iter(self.h, ctypes.addressof(out)))
+        return int(out.value)
 
     def timing(self, mode: int, stream=None) -> np.ndarray:
         """chap_walkers_timing: the accumulated [bin, gen, eval, apply, span] ns and iteration count;

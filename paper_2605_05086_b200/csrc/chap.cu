@@ -1163,6 +1163,12 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 
 #include "portfolio.cuh"
 
+extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int32_t* out) {
+  if (!S || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or out");
+  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + 2;
+  return CHAP_OK;
+}
+
 extern "C" chap_status chap_walkers_timing(chap_walkers* S, int32_t mode, uint64_t* out, void* cuda_stream) {
   if (!S || mode < -1 || mode > 1) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or mode not in {-1, 0, 1}");
   DeviceGuard g(S->P->device);

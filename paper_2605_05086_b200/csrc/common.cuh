@@ -71,7 +71,7 @@ struct LongCol {
   int32_t p;         // the column (internal order)
   int32_t kind;      // CC_LBIN or CC_LBKT
 };
-constexpr int kWChunk = 128;                      // nonzeros per warp chunk of a long binary column
+constexpr int kWChunk = 256;                      // nonzeros per warp chunk of a long binary column
 constexpr int kBktChunk = 512;                    // nonzeros per warp chunk of a long bounded-integer column
 
 // A block tile (chunk of a long column, or one column sorted by the whole block).

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     const unsigned long long now = kt_now();
     for (int q = 0; q < 3; ++q) kt[8 + q] += kt[2 * q + 1] - kt[2 * q];
     kt[11] += now - kt[6];
-    kt[12] += now - kt[0];
+    kt[12] += now - min(kt[0], min(kt[2], kt[4]));   // the eval kernels may overlap (forked branch)
     kt[13] += 1;
     for (int q = 0; q < 4; ++q) { kt[2 * q] = ~0ull; kt[2 * q + 1] = 0ull; }
   }

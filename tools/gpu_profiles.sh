@@ -9,6 +9,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/launches_$CFG.csv python bench.py --config $CFG --steps 20 --warmup 5 \
   --no-cpu-baseline --profile-iters 5 --e2e-iters 2 > gpurun_out/launches_$CFG.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k 'regex:k_eval|k_apply' \
-  --launch-skip 80 -c 4 -o gpurun_out/full_$CFG python tools/prof_step.py 20 3 $CFG \
+  --launch-skip 100 -c 5 -o gpurun_out/full_$CFG python tools/prof_step.py 20 3 $CFG \
   > gpurun_out/full_$CFG.log 2>&1
 tail -c 600 gpurun_out/bench_$CFG.json

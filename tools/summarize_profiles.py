@@ -30,7 +30,7 @@ for r in rows[1:]:
         continue
     v = float(r[vi]) * (1e-3 if r[ui] == "ns" else 1.0)
     agg[r[ki].split("(")[0]].append(v)
-step = ["k_eval_bin", "k_eval_gen", "k_eval", "k_apply"]
+step = ["k_eval_bin", "k_eval_binrow", "k_eval_gen", "k_eval", "k_apply"]
 tot = sum(sum(agg[k]) / max(1, len(agg[k])) for k in step if k in agg)
 out = [f"ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches) "
        f"of `bench.py --config {cfg} --steps 20 --warmup 5`",
@@ -71,13 +71,13 @@ for v in rr[2:]:
             except ValueError:
                 pass
     txt.append("  stall cycles per issued instruction: " + ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:8]))
-    if name in ("k_eval_bin", "k_eval_gen", "k_eval"):
+    if name in ("k_eval_bin", "k_eval_binrow", "k_eval_gen", "k_eval"):
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             u, c = d[k]
             traffic += float(c) * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}[u]
 open(os.path.join(pr, f"{tag}_ncu_full_{cfg}.txt"), "w").write("\n".join(txt) + "\n")
 json.dump({"config": cfg, "dram_bytes_per_launch": traffic,
            "source": f"profiles/{tag}_ncu_full_{cfg}.txt: dram__bytes_read.sum + dram__bytes_write.sum of "
-                     "k_eval_bin + k_eval_gen + k_eval, one launch each"},
+                     "k_eval_bin + k_eval_binrow + k_eval_gen + k_eval, one launch each"},
           open(os.path.join(pr, "traffic.json"), "w"), indent=1)
 print("traffic", traffic)
