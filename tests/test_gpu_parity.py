@@ -189,16 +189,17 @@ def test_host_buffer_variant_equals_device():
     assert mh.tobytes() == chap.move_from_bytes(md).tobytes()
 
 
-def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16):
+def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10):
     P = chap.Problem.from_instance(inst)
     O = oracle.Problem.from_instance(inst)
-    prm = chap.default_params(graph_iters=graph_iters)
+    prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure)
+    oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap)
     X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
     Wk = chap.Walkers(P, X0, prm)
     log = chap.records(Wk.step(n_iters, log=True)).reshape(n_iters, len(x0s))
     st = Wk.get()
     for wi, x0 in enumerate(x0s):
-        ow = oracle.TabuWalker(O, x0)
+        ow = oracle.TabuWalker(O, x0, oprm)
         olog = ow.run(n_iters)
         glog = log[:, wi]
         for f in ("k", "j", "violated", "obj", "s"):
@@ -264,6 +265,21 @@ def test_config_P_64_walkers_trajectory():
     inst = synth.packing()
     x0s = [synth.x_bernoulli(inst, (3, wi), 0.5) for wi in range(64)]
     _traj_compare(inst, x0s, 12)
+
+
+@pytest.mark.parametrize("cap", [3.0, 3.5])
+def test_trajectory_weight_cap(cap):
+    """Weights reach the cap: an integral cap keeps the row-wise binary kernel (k_eval_binrow), a
+    fractional one (weights 3.5, half-integral penalties) takes the column-wise kernel."""
+    inst = synth.setcover(seed=6, m=400, n=2000)
+    _traj_compare(inst, [synth.x_lower(inst)], 300, weight_cap=cap, tenure=3)
+
+
+def test_trajectory_rowwise_two_rounds():
+    """Generator X at 2·10^7 requested nonzeros: ~1.4 M packed binary columns, more than one round
+    of k_eval_binrow blocks per cluster; 6 iterations of one walker vs the oracle."""
+    inst = synth.scaled(20_000_000)
+    _traj_compare(inst, [synth.x_lower(inst)], 6)
 
 
 def test_invalid_x0_rejected():
