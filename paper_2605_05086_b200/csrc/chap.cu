@@ -424,7 +424,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     }
     // cluster width: the one that keeps the most SMs busy (clusters live inside a GPC), the wider
     // on ties (fewer, larger blocks: more entries per row, denser row-state reads)
-    int ncl = 0, C = 0;
+    int ncl = 0, C = 0, nb = 0;
+    int32_t nbin = 0;
     if (ok) {
       cudaError_t e1 = cudaFuncSetAttribute(k_eval_binrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem);
       if (e1 == cudaSuccess) {
@@ -452,9 +453,17 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       // blocks: nb, a multiple of the resident clusters, with <= kRowVmax columns each; column
       // p = pb0 + b + k nb is column k of block b (round-robin over the degree-sorted columns, so
       // every block gets an equal mix of long and short columns and about tot / nb entries)
-      const int32_t nbin = pb1 - pb0;
-      int nb = std::max(ncl, (nbin + kRowVmax - 1) / kRowVmax);
+      nbin = pb1 - pb0;
+      nb = std::max(ncl, (nbin + kRowVmax - 1) / kRowVmax);
       nb = (nb + ncl - 1) / ncl * ncl;
+      // where the row-wise kernel pays (measured on the X sweep): enough nonzeros to
+      // amortise the cluster launch and the per-block reduction, and enough entries per row of a
+      // block that a warp's consecutive entries share row-state lines; CHAP_BINROW=0/1 overrides
+      const double density = (double)tot / ((double)nb * std::max(1, m_norm));
+      ok = tot >= 3000000 && density >= 0.7;
+      if (const char* ev = getenv("CHAP_BINROW")) ok = ev[0] == '1';
+    }
+    if (ok) {
       std::vector<int32_t> cnt(m_norm + 2, 0);
       for (int b = 0; b < nb; ++b) {
         const int32_t nvb = (nbin - b + nb - 1) / nb;   // columns pb0 + b, pb0 + b + nb, ...

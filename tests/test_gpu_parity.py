@@ -220,8 +220,18 @@ def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e
     return log
 
 
+@pytest.fixture(params=["auto", "1"], ids=["binrow_auto", "binrow_forced"])
+def binrow(request, monkeypatch):
+    """The row-wise binary kernel is chosen by size (chap.cu); "1" forces it on small instances."""
+    if request.param == "1":
+        monkeypatch.setenv("CHAP_BINROW", "1")
+    else:
+        monkeypatch.delenv("CHAP_BINROW", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("seed", range(8))
-def test_trajectory_config_T(seed):
+def test_trajectory_config_T(seed, binrow):
     inst = synth.tiny(seed)
     _traj_compare(inst, [synth.x_lower(inst)], 600, graph_iters=16 if seed % 2 else 0)
 
@@ -232,12 +242,12 @@ def test_trajectory_multi_walker():
     _traj_compare(inst, x0s, 300)
 
 
-def test_trajectory_mixed_small():
+def test_trajectory_mixed_small(binrow):
     inst = synth.mixed(seed=9, n=4000, m=800, n_long=4, long_lo=300, long_hi=6000)
     _traj_compare(inst, [synth.x_lower(inst), synth.x_random(inst, 1)], 60)
 
 
-def test_trajectory_setcover_small():
+def test_trajectory_setcover_small(binrow):
     inst = synth.setcover(seed=4, m=500, n=2500)
     _traj_compare(inst, [synth.x_lower(inst)], 400)
 
@@ -268,16 +278,17 @@ def test_config_P_64_walkers_trajectory():
 
 
 @pytest.mark.parametrize("cap", [3.0, 3.5])
-def test_trajectory_weight_cap(cap):
+def test_trajectory_weight_cap(cap, binrow):
     """Weights reach the cap: an integral cap keeps the row-wise binary kernel (k_eval_binrow), a
     fractional one (weights 3.5, half-integral penalties) takes the column-wise kernel."""
     inst = synth.setcover(seed=6, m=400, n=2000)
     _traj_compare(inst, [synth.x_lower(inst)], 300, weight_cap=cap, tenure=3)
 
 
-def test_trajectory_rowwise_two_rounds():
+def test_trajectory_rowwise_two_rounds(monkeypatch):
     """Generator X at 2·10^7 requested nonzeros: ~1.4 M packed binary columns, more than one round
-    of k_eval_binrow blocks per cluster; 6 iterations of one walker vs the oracle."""
+    of k_eval_binrow blocks per cluster (forced on); 6 iterations of one walker vs the oracle."""
+    monkeypatch.setenv("CHAP_BINROW", "1")
     inst = synth.scaled(20_000_000)
     _traj_compare(inst, [synth.x_lower(inst)], 6)
 
