@@ -331,6 +331,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     W.e1 = col_ptr[r.second];
     W.ncols = (int16_t)(r.second - r.first);
     W.kind = (int8_t)CC_GEN;
+    for (int32_t q = r.first; q < r.second; ++q) {   // pad = 1: the tile holds a continuous column
+      if (vclass[perm[q]] == 3) W.pad = 1;
+      P->gen_kmax = std::max(P->gen_kmax, col_ptr[q + 1] - col_ptr[q]);
+    }
     wtiles.push_back(W);
   }
   int32_t n_long = 0;
@@ -591,6 +595,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   DevProblem& D = P->dp;
   D.rblocks = d_rblocks;
   D.n_rblocks = (int32_t)rblocks.size();
+  D.n_cont_wtiles = 0;
+  for (const WTile& T : wtiles) D.n_cont_wtiles += (T.kind == CC_GEN && T.pad) ? 1 : 0;
   D.rb_cluster = P->binrow_cluster;
   D.rb_pb0 = P->binrow_pb0;
   D.rb_perm = d_rb_perm;
@@ -711,6 +717,40 @@ static chap_status launch_bin_wm(const DevProblem& D, const DevWalkers& Wk, int 
   return CHAP_OK;
 }
 
+static chap_status launch_gen_wm(const chap_problem* P, const DevWalkers& Wk, int wgrid, int part_base, cudaStream_t s) {
+  const dim3 grid(wgrid, Wk.n_groups);
+  const int kmax = std::max(1, P->gen_kmax);
+  const size_t sm = gen_wm_smem(kmax);
+  switch (Wk.rg) {
+    case 2: k_eval_gen_wm<2><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
+    case 4: k_eval_gen_wm<4><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
+    case 8: k_eval_gen_wm<8><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
+    case 16: k_eval_gen_wm<16><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
+    case 32: k_eval_gen_wm<32><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
+    default: return fail(CHAP_ERR_STATE, "row-state group width %d", Wk.rg);
+  }
+  return CHAP_OK;
+}
+
+template <int RG>
+static int gen_wm_occ_one(size_t sm) {
+  int occ = 0;
+  if (cudaFuncSetAttribute(k_eval_gen_wm<RG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_gen_wm<RG>, kGenWmThreads, sm) != cudaSuccess)
+    occ = 0;
+  cudaGetLastError();
+  return occ;
+}
+static int gen_wm_occupancy(int rg, size_t sm) {
+  switch (rg) {
+    case 2: return gen_wm_occ_one<2>(sm);
+    case 4: return gen_wm_occ_one<4>(sm);
+    case 8: return gen_wm_occ_one<8>(sm);
+    case 16: return gen_wm_occ_one<16>(sm);
+    default: return gen_wm_occ_one<32>(sm);
+  }
+}
+
 static int bin_wm_occupancy(int rg) {
   int occ = 1;
   cudaError_t e = cudaSuccess;
@@ -744,7 +784,8 @@ static chap_status launch_binrow(const chap_problem* P, const DevWalkers& Wk, in
 
 // Part slots of one walker: [k_eval_bin | k_eval_gen | k_eval_binrow | k_eval]; k_eval reduces them.
 chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
-                              int rgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s) {
+                              int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best,
+                              cudaStream_t s) {
   if (bgrid > 0) {
     if (Wk.rg > 1) TRY(launch_bin_wm(P->dp, Wk, bgrid, s));
     else if (rgrid > 0) {   // packed binary columns row-wise: k_eval_bin takes the long chunks only
@@ -756,8 +797,10 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
     }
   }
   if (rgrid > 0) TRY(launch_binrow(P, Wk, rgrid, bgrid + ggrid, s));
-  if (ggrid > 0) k_eval_gen<<<dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s>>>(P->dp, Wk, oxhat, oscore, bgrid);
-  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid + rgrid);
+  if (ggrid > 0)
+    k_eval_gen<<<dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s>>>(P->dp, Wk, oxhat, oscore, bgrid, wgrid > 0 ? 1 : 0);
+  if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s));
+  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid + rgrid + wgrid);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -824,7 +867,7 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, xhat, score, best, s));
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -954,7 +997,16 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
     S->bin_grid = p->bin_chunk_grid;
     TRY(B.alloc(&Wk.xbits, (size_t)p->dp.n_rblocks * kRowWpb));   // block-ordered bitset
   }
-  Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid;
+  S->genwm_grid = 0;   // walker groups: integer general tiles and empty columns per group (k_eval_gen_wm)
+  if (rg > 1 && p->dp.n_wtiles > 0) {
+    const int occ = gen_wm_occupancy(rg, gen_wm_smem(std::max(1, p->gen_kmax)));
+    if (occ > 0) {
+      const int warps = kGenWmThreads / 32;
+      S->genwm_grid = std::max(1, std::min((p->dp.n_wtiles + warps - 1) / warps,
+                                           (occ * p->sm_count + Wk.n_groups - 1) / Wk.n_groups));
+    }
+  }
+  Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid + S->genwm_grid;
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
   TRY(B.alloc(&Wk.sel_count, W));
   Wk.lss = p->lscr_per_walker;
@@ -1003,7 +1055,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
-  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, S->binrow_grid, nullptr, nullptr, nullptr, s));
+  TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, S->binrow_grid, S->genwm_grid, nullptr, nullptr,
+                  nullptr, s));
   k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -1123,11 +1176,14 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     cudaEventRecordWithFlags(e[1], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[2], s, cudaEventRecordExternal);
     if (S->gen_grid > 0)
-      k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid);
+      k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid,
+                                                                       S->genwm_grid > 0 ? 1 : 0);
+    if (S->genwm_grid > 0) TRY(launch_gen_wm(P, S->wk, S->genwm_grid, S->bin_grid + S->gen_grid + S->binrow_grid, s));
     cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[4], s, cudaEventRecordExternal);
     k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
-                                                                     S->bin_grid + S->gen_grid + S->binrow_grid);
+                                                                     S->bin_grid + S->gen_grid + S->binrow_grid +
+                                                                         S->genwm_grid);
     cudaEventRecordWithFlags(e[5], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[8], s, cudaEventRecordExternal);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
@@ -1174,7 +1230,7 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 
 extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int32_t* out) {
   if (!S || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or out");
-  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + 2;
+  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + 2;
   return CHAP_OK;
 }
 

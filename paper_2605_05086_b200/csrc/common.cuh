@@ -61,7 +61,7 @@ struct WTile {
   int32_t e1;        // nonzero range [e0, e1); a chunk of a long column: the long-column index
   int16_t ncols;     // columns; a chunk of a long column: its nonzeros (<= kWChunk)
   int8_t kind;       // CC_BIN, CC_GEN, CC_EMPTY, or a warp chunk of a long column: CC_LBIN, CC_LBKT
-  int8_t pad;
+  int8_t pad;        // CC_GEN: 1 if the tile holds a continuous column
 };
 // A long column split into warp chunks: where its accumulators live in walker scratch.
 struct LongCol {
@@ -192,6 +192,7 @@ struct DevProblem {
   const int32_t* perm;       // internal p -> user j
   const Tile* tiles; int32_t n_tiles; int32_t n_long;   // block tiles
   const WTile* wtiles; int32_t n_wtiles;                // warp tiles (general, empty)
+  int32_t n_cont_wtiles;                                // general tiles holding a continuous column
   const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles
   const WTile* bchunks; int32_t n_bchunks;              // warp chunks of long binary columns
   const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns

@@ -1346,8 +1346,10 @@ __device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalk
                   1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
 }
 
+// wm_mode 1 (walker groups): the integer general tiles and the empty columns are k_eval_gen_wm's;
+// this kernel takes the long bounded-integer chunks and the tiles holding a continuous column.
 __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
-                                                              double* oscore, int part_base) {
+                                                              double* oscore, int part_base, int wm_mode) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
   const int walker = blockIdx.y;
@@ -1379,17 +1381,152 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     lbkt_chunk(P, Wk, walker, X, RS, st, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
   __syncwarp();
   t -= P.n_gchunks;
+  if (wm_mode && P.n_cont_wtiles == 0) t = P.n_wtiles;   // nothing left for this kernel
   WTile Tn;
   if (t < P.n_wtiles) Tn = P.wtiles[t];
   for (; t < P.n_wtiles; t += nwarps) {
     const WTile T = Tn;
     if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];
-    if (T.kind == CC_GEN) gen_tile(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
-    else wtile_empty(P, C, T, lane, b);
+    if (T.kind == CC_GEN) {
+      if (!wm_mode || T.pad) gen_tile(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
+    } else if (!wm_mode) {
+      wtile_empty(P, C, T, lane, b);
+    }
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
   KT_END(Wk, 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// walker-minor general kernel (row-state groups of rg > 1 walkers)
+// ------------------------------------------------------------------------------------------
+// One warp evaluates a packed integer general column for a whole walker group: lane = (slot,
+// walker), the 32 / RG slots take different columns of the tile. Every lane runs Algorithm 1 for
+// its own walker serially: lines 3-11 per entry (the CSC entry is read once for the group, the
+// row-state read is a coalesced RG x 16-byte run) into its own shared-memory column of (key, δ),
+// then lines 13-16 sort-free: σ(v) = β + α [v > x̄] + Σ_e δ_e [key_e <= v] for every
+// candidate v (emitted breakpoints in [l, u] other than x̄, and the finite bounds; R2, R3, R5),
+// argmax with R4. No cross-lane coordination: the lanes of a slot do identical control flow on
+// different walkers. Sums of ±w, ±w/2 in double are exact (R11), so the scores equal the per-walker
+// kernels' bit for bit.
+constexpr int kGenWmThreads = 128;
+template <int RG>
+__global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, DevWalkers Wk, int part_base, int kmax) {
+  constexpr int NS = 32 / RG;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Best sb[kGenWmThreads / 32][32];
+  const int g = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wl = lane % RG, slot = lane / RG;
+  const int w = g * RG + wl;
+  const bool live = w < Wk.W;
+  const int wr = live ? w : g * RG;
+  double* skey = reinterpret_cast<double*>(smem) + (size_t)wid * kmax * 32;                 // [kmax][32]
+  float* sD = reinterpret_cast<float*>(reinterpret_cast<double*>(smem) + (size_t)(kGenWmThreads / 32) * kmax * 32) +
+              (size_t)wid * kmax * 32;                                                       // [kmax][32]
+  const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)g * Wk.rss * RG) + wl;
+  const double* __restrict__ X = Wk.x + (size_t)wr * Wk.xs;
+  const int32_t* __restrict__ TB = Wk.tabu + (size_t)wr * Wk.ts;
+  const long long kk = Wk.sc[wr].k;
+  const int use_tabu = Wk.use_tabu;
+  KT_BEGIN(Wk, 1);
+  Best b;
+  b.init();
+  auto offer = [&](double sc, double v, int j, int p) {
+    if (better_move(sc, j, b.s, b.j) && (!use_tabu || (long long)__ldg(TB + p) <= kk)) {
+      b.s = sc;
+      b.v = v;
+      b.j = j;
+      b.p = p;
+    }
+  };
+  const int nwarps = gridDim.x * (kGenWmThreads / 32);
+  for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < P.n_wtiles; t += nwarps) {
+    const WTile T = P.wtiles[t];
+    if (T.kind == CC_GEN && T.pad) continue;   // a continuous column: k_eval_gen (wm_mode 1)
+    for (int c = slot; c < T.ncols; c += NS) {
+      const int p = T.p0 + c;
+      const double xb = __ldg(X + p), l = __ldg(P.lb + p), u = __ldg(P.ub + p);
+      const int j = __ldg(P.perm + p);
+      double bs = -INFINITY, bv = xb;
+      if (T.kind != CC_GEN) {   // a column without nonzeros (R2, R4, R5)
+        if (__ldg(P.vclass + p) == 1) {
+          bs = 0.0;
+          bv = 1.0 - xb;
+        } else {
+          if (isfinite(l) && l != xb) { bs = 0.0; bv = l; }
+          if (isfinite(u) && u != xb && better_shift(0.0, u, bs, bv, xb)) { bs = 0.0; bv = u; }
+        }
+        if (live) offer(bs, bv, j, p);
+        continue;
+      }
+      const int cb = __ldg(P.col_ptr + p), k = __ldg(P.col_ptr + p + 1) - cb;
+      // lines 3-11 per entry into the lane's (key, δ) column
+      double beta = 0.0, alpha = 0.0, pl = 0.0, pu = 0.0;
+      unsigned long long cm = 0ull;   // candidate entries
+      for (int e0 = 0; e0 < k; e0 += 4) {
+        int id[4];
+        double av[4];
+        double2 rv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          id[q] = e0 + q < k ? __ldg(P.row_idx + cb + e0 + q) : -1;
+          av[q] = e0 + q < k ? __ldg(P.val + cb + e0 + q) : 1.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = e0 + q;
+          if (e >= k) break;
+          const double wv = (double)__int_as_float((int)__double2loint(rv[q].y));
+          const Elem el = emit(xb, rv[q].x, av[q], wv, 1);   // inert rows emit nothing
+          beta += el.beta;
+          alpha += el.alpha;
+          double key = INFINITY;
+          float D = 0.f;
+          if (el.valid && isfinite(el.t)) {
+            D = (float)el.delta;
+            key = el.delta > 0.0 ? el.t : el.t + 1.0;   // integer column: nothing lies in (t, t+1)
+            if (el.t >= l && el.t <= u && el.t != xb) cm |= 1ull << e;
+          }
+          skey[e * 32 + lane] = key;
+          sD[e * 32 + lane] = D;
+          if (key <= l) pl += (double)D;   // the bounds' prefix sums (lines 13-14 at l and u)
+          if (key <= u) pu += (double)D;
+        }
+      }
+      // lines 13-16 without the sort: each candidate's prefix sum over the column
+      for (unsigned long long m = cm; m; m &= m - 1) {
+        const int c2 = __ffsll((long long)m) - 1;
+        const double kc = skey[c2 * 32 + lane];
+        const double v = sD[c2 * 32 + lane] > 0.f ? kc : kc - 1.0;
+        double acc = 0.0;
+        for (int e = 0; e < k; ++e)
+          if (skey[e * 32 + lane] <= v) acc += (double)sD[e * 32 + lane];
+        const double sig = beta + acc + (v > xb ? alpha : 0.0);
+        if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
+      }
+      if (isfinite(l) && l != xb && better_shift(beta + pl, l, bs, bv, xb)) { bs = beta + pl; bv = l; }   // l < x̄
+      if (isfinite(u) && u != xb && better_shift(beta + alpha + pu, u, bs, bv, xb)) { bs = beta + alpha + pu; bv = u; }
+      if (live) offer(bs, bs == -INFINITY ? xb : bv, j, p);
+    }
+  }
+  // per-walker block best: slots, then warps, in fixed order
+  sb[wid][lane] = b;
+  __syncthreads();
+  if (threadIdx.x < RG) {
+    Best o;
+    o.init();
+    for (int q = 0; q < kGenWmThreads / 32; ++q)
+      for (int sl = 0; sl < NS; ++sl) o.take(sb[q][sl * RG + threadIdx.x]);
+    const int ww = g * RG + threadIdx.x;
+    if (ww < Wk.W) write_part(Wk.part + (size_t)ww * Wk.ps + part_base + blockIdx.x, o);
+  }
+  KT_END(Wk, 1);
+}
+__host__ __device__ constexpr size_t gen_wm_smem(int kmax) {
+  return (size_t)(kGenWmThreads / 32) * kmax * 32 * (sizeof(double) + sizeof(float));
 }
 
 // ------------------------------------------------------------------------------------------

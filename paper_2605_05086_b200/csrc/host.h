@@ -96,6 +96,7 @@ struct chap_problem {
   int gen_occ = 1;
   int gen_grid = 0;            // k_eval_gen blocks for one walker
   int binrow_grid = 0;         // k_eval_binrow CTAs (clusters x kRowCluster; 0: no row-wise blocks)
+  int gen_kmax = 0;            // longest packed general column (entries incl. padding)
   int binrow_maxdeg = 0;       // longest packed binary column (incl. its cutoff entry)
   int binrow_cluster = 0;      // CTAs per cluster of k_eval_binrow
   int binrow_pb0 = 0, binrow_nbin = 0;   // the packed binary columns [pb0, pb0 + nbin)
@@ -151,6 +152,8 @@ struct chap_walkers {
   int bin_grid = 0;            // k_eval_bin blocks per walker
   int gen_grid = 0;            // k_eval_gen blocks per walker
   int binrow_grid = 0;         // k_eval_binrow CTAs (one walker, row-wise binary columns), 0 = off
+  int genwm_grid = 0;          // k_eval_gen_wm blocks per walker group (walker groups), 0 = off
+  size_t genwm_smem = 0;
   ~chap_walkers() {
     if (xs) chap_exchange_state_free(xs);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -164,7 +167,7 @@ struct chap_walkers {
 namespace chap {
 // shared launch helpers (chap.cu)
 chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
-                        int rgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
+                        int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
 int grid_for(long long work, int threads, int cap);
 chap_status walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s);
 

@@ -17,7 +17,7 @@ inst = {"G": synth.mixed, "S": synth.setcover, "P": synth.packing,
         "Gbin": lambda: synth.mixed(p_binary=1.0, p_bounded=0.0),
         "Gnl": lambda: synth.mixed(n_long=0), "Gint": lambda: synth.mixed(p_binary=0.0, p_bounded=1.0)}[cfg]()
 P = chap.Problem.from_instance(inst)
-W = 64 if cfg == "P" else 1
+W = int(sys.argv[4]) if len(sys.argv) > 4 else (64 if cfg == "P" else 1)
 x0 = np.stack([synth.x_lower(inst)] * W) if cfg != "P" else \
     np.stack([synth.x_bernoulli(inst, (3, w), 0.5) for w in range(W)])
 ws = chap.Walkers(P, torch.from_numpy(x0).cuda(), chap.default_params(graph_iters=0))
