@@ -704,29 +704,61 @@ extern "C" chap_status chap_problem_destroy(chap_problem* p) {
 // ------------------------------------------------------------------------------------------
 // eval launches (shared by the eval API and the tabu step)
 // ------------------------------------------------------------------------------------------
-static chap_status launch_bin_wm(const DevProblem& D, const DevWalkers& Wk, int bgrid, cudaStream_t s) {
+// Kernel launch through cudaLaunchKernelEx: optional cluster shape and, for the kernels of a tabu
+// iteration, programmatic dependent launch (each kernel starts with pdl_wait_trigger()).
+template <typename... KArgs, typename... Args>
+static chap_status lk(void (*kern)(KArgs...), dim3 grid, int block, size_t smem, cudaStream_t s, bool pdl,
+                      int cluster, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return CHAP_OK;
+}
+
+static chap_status launch_bin_wm(const DevProblem& D, const DevWalkers& Wk, int bgrid, cudaStream_t s, bool pdl) {
   const dim3 grid(bgrid, Wk.n_groups);
   switch (Wk.rg) {
-    case 2: k_eval_bin_wm<2><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
-    case 4: k_eval_bin_wm<4><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
-    case 8: k_eval_bin_wm<8><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
-    case 16: k_eval_bin_wm<16><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
-    case 32: k_eval_bin_wm<32><<<grid, kBinWmThreads, 0, s>>>(D, Wk); break;
+    case 2: TRY(lk(k_eval_bin_wm<2>, grid, kBinWmThreads, 0, s, pdl, 1, D, Wk)); break;
+    case 4: TRY(lk(k_eval_bin_wm<4>, grid, kBinWmThreads, 0, s, pdl, 1, D, Wk)); break;
+    case 8: TRY(lk(k_eval_bin_wm<8>, grid, kBinWmThreads, 0, s, pdl, 1, D, Wk)); break;
+    case 16: TRY(lk(k_eval_bin_wm<16>, grid, kBinWmThreads, 0, s, pdl, 1, D, Wk)); break;
+    case 32: TRY(lk(k_eval_bin_wm<32>, grid, kBinWmThreads, 0, s, pdl, 1, D, Wk)); break;
     default: return fail(CHAP_ERR_STATE, "row-state group width %d", Wk.rg);
   }
   return CHAP_OK;
 }
 
-static chap_status launch_gen_wm(const chap_problem* P, const DevWalkers& Wk, int wgrid, int part_base, cudaStream_t s) {
+static chap_status launch_gen_wm(const chap_problem* P, const DevWalkers& Wk, int wgrid, int part_base, cudaStream_t s,
+                                 bool pdl) {
   const dim3 grid(wgrid, Wk.n_groups);
   const int kmax = std::max(1, P->gen_kmax);
   const size_t sm = gen_wm_smem(kmax);
   switch (Wk.rg) {
-    case 2: k_eval_gen_wm<2><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
-    case 4: k_eval_gen_wm<4><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
-    case 8: k_eval_gen_wm<8><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
-    case 16: k_eval_gen_wm<16><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
-    case 32: k_eval_gen_wm<32><<<grid, kGenWmThreads, sm, s>>>(P->dp, Wk, part_base, kmax); break;
+    case 1: TRY(lk(k_eval_gen_wm<1>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
+    case 2: TRY(lk(k_eval_gen_wm<2>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
+    case 4: TRY(lk(k_eval_gen_wm<4>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
+    case 8: TRY(lk(k_eval_gen_wm<8>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
+    case 16: TRY(lk(k_eval_gen_wm<16>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
+    case 32: TRY(lk(k_eval_gen_wm<32>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
     default: return fail(CHAP_ERR_STATE, "row-state group width %d", Wk.rg);
   }
   return CHAP_OK;
@@ -743,6 +775,7 @@ static int gen_wm_occ_one(size_t sm) {
 }
 static int gen_wm_occupancy(int rg, size_t sm) {
   switch (rg) {
+    case 1: return gen_wm_occ_one<1>(sm);
     case 2: return gen_wm_occ_one<2>(sm);
     case 4: return gen_wm_occ_one<4>(sm);
     case 8: return gen_wm_occ_one<8>(sm);
@@ -765,43 +798,30 @@ static int bin_wm_occupancy(int rg) {
 }
 
 static chap_status launch_binrow(const chap_problem* P, const DevWalkers& Wk, int rgrid, int part_base,
-                                 cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(rgrid);
-  cfg.blockDim = dim3(kRowThreads);
-  cfg.dynamicSmemBytes = kRowSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = P->binrow_cluster;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_eval_binrow, P->dp, Wk, part_base));
-  return CHAP_OK;
+                                 cudaStream_t s, bool pdl) {
+  return lk(k_eval_binrow, dim3(rgrid), kRowThreads, kRowSmem, s, pdl, P->binrow_cluster, P->dp, Wk, part_base);
 }
 
 // Part slots of one walker: [k_eval_bin | k_eval_gen | k_eval_binrow | k_eval]; k_eval reduces them.
 chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                               int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool pdl) {
   if (bgrid > 0) {
-    if (Wk.rg > 1) TRY(launch_bin_wm(P->dp, Wk, bgrid, s));
-    else if (rgrid > 0) {   // packed binary columns row-wise: k_eval_bin takes the long chunks only
-      DevProblem D = P->dp;
-      D.n_btiles = 0;
-      k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(D, Wk, oxhat, oscore);
+    if (Wk.rg > 1) {
+      TRY(launch_bin_wm(P->dp, Wk, bgrid, s, pdl));
     } else {
-      k_eval_bin<<<dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s>>>(P->dp, Wk, oxhat, oscore);
+      DevProblem D = P->dp;
+      if (rgrid > 0) D.n_btiles = 0;   // packed binary columns row-wise: k_eval_bin takes the long chunks only
+      TRY(lk(k_eval_bin, dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s, pdl, 1, D, Wk, oxhat, oscore));
     }
   }
-  if (rgrid > 0) TRY(launch_binrow(P, Wk, rgrid, bgrid + ggrid, s));
+  if (rgrid > 0) TRY(launch_binrow(P, Wk, rgrid, bgrid + ggrid, s, pdl));
   if (ggrid > 0)
-    k_eval_gen<<<dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s>>>(P->dp, Wk, oxhat, oscore, bgrid, wgrid > 0 ? 1 : 0);
-  if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s));
-  k_eval<<<dim3(grid, Wk.W), kTileThreads, kTileSmem, s>>>(P->dp, Wk, oxhat, oscore, best, bgrid + ggrid + rgrid + wgrid);
-  CUDA_TRY(cudaGetLastError());
+    TRY(lk(k_eval_gen, dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, bgrid,
+           wgrid > 0 ? 1 : 0));
+  if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s, pdl));
+  TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
+         bgrid + ggrid + rgrid + wgrid));
   return CHAP_OK;
 }
 
@@ -867,7 +887,7 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s));
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s, false));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -997,8 +1017,13 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
     S->bin_grid = p->bin_chunk_grid;
     TRY(B.alloc(&Wk.xbits, (size_t)p->dp.n_rblocks * kRowWpb));   // block-ordered bitset
   }
+  // programmatic dependent launch between the iteration's kernels: measured slower on config G
+  // (0.1344 vs 0.1273 ms; early-scheduled k_eval_gen blocks disturb its persistent grid), so off
+  // unless CHAP_PDL=1
+  { const char* ev = getenv("CHAP_PDL"); S->pdl = ev && ev[0] == '1'; }
   S->genwm_grid = 0;   // walker groups: integer general tiles and empty columns per group (k_eval_gen_wm)
-  if (rg > 1 && p->dp.n_wtiles > 0) {
+  const char* gw = getenv("CHAP_GENWM");   // experiment: lane-per-column general tiles for one walker
+  if ((rg > 1 || (gw && gw[0] == '1')) && p->dp.n_wtiles > 0) {
     const int occ = gen_wm_occupancy(rg, gen_wm_smem(std::max(1, p->gen_kmax)));
     if (occ > 0) {
       const int warps = kGenWmThreads / 32;
@@ -1056,8 +1081,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
   TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, S->binrow_grid, S->genwm_grid, nullptr, nullptr,
-                  nullptr, s));
-  k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(P->dp, S->wk);
+                  nullptr, s, S->pdl));
+  TRY(lk(k_apply, dim3(S->apply_grid, S->W), kApplyThreads, 0, s, S->pdl, 1, P->dp, S->wk));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -1169,16 +1194,17 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     if (S->bin_grid > 0) {
       DevProblem Db = D;
       if (S->binrow_grid > 0) Db.n_btiles = 0;
-      if (S->wk.rg > 1) TRY(launch_bin_wm(D, S->wk, S->bin_grid, s));
+      if (S->wk.rg > 1) TRY(launch_bin_wm(D, S->wk, S->bin_grid, s, false));
       else k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(Db, S->wk, nullptr, nullptr);
     }
-    if (S->binrow_grid > 0) TRY(launch_binrow(P, S->wk, S->binrow_grid, S->bin_grid + S->gen_grid, s));
+    if (S->binrow_grid > 0) TRY(launch_binrow(P, S->wk, S->binrow_grid, S->bin_grid + S->gen_grid, s, false));
     cudaEventRecordWithFlags(e[1], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[2], s, cudaEventRecordExternal);
     if (S->gen_grid > 0)
       k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid,
                                                                        S->genwm_grid > 0 ? 1 : 0);
-    if (S->genwm_grid > 0) TRY(launch_gen_wm(P, S->wk, S->genwm_grid, S->bin_grid + S->gen_grid + S->binrow_grid, s));
+    if (S->genwm_grid > 0)
+      TRY(launch_gen_wm(P, S->wk, S->genwm_grid, S->bin_grid + S->gen_grid + S->binrow_grid, s, false));
     cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[4], s, cudaEventRecordExternal);
     k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,

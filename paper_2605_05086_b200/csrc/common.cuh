@@ -170,6 +170,14 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// Programmatic dependent launch (the tabu iteration's kernels are launched with the PDL
+// attribute): wait for the preceding grid to complete and its writes to be visible, then let the
+// next grid be scheduled onto SMs as this one's blocks retire. Both are no-ops for plain launches.
+__device__ __forceinline__ void pdl_wait_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 #define KT_BEGIN(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMin((WK).kt + 2 * (q), chap::kt_now()); } while (0)
 #define KT_END(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMax((WK).kt + 2 * (q) + 1, chap::kt_now()); } while (0)
 constexpr int kKtWords = 16;   // [2q, 2q+1] start/end of kernel q (0 bin, 1 gen, 2 eval, 3 apply); [8..13] sums

@@ -459,6 +459,7 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
 
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
                                                               double* oscore) {
+  pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
   const int walker = blockIdx.y;
@@ -587,6 +588,7 @@ struct BinWmWarp {
 
 template <int RG>
 __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, DevWalkers Wk) {
+  pdl_wait_trigger();
   constexpr int NS = 32 / RG;   // slots per warp
   __shared__ __align__(16) BinWmWarp sw[kBinWmThreads / 32];
   __shared__ Best sb[kBinWmThreads / 32][32];
@@ -747,6 +749,7 @@ __device__ __forceinline__ void cluster_sync_acqrel() {
 }
 
 __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, DevWalkers Wk, int part_base) {
+  pdl_wait_trigger();
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sb[kRowThreads / 32];
@@ -1350,6 +1353,7 @@ __device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalk
 // this kernel takes the long bounded-integer chunks and the tiles holding a continuous column.
 __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
                                                               double* oscore, int part_base, int wm_mode) {
+  pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
   const int walker = blockIdx.y;
@@ -1413,6 +1417,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
 constexpr int kGenWmThreads = 128;
 template <int RG>
 __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, DevWalkers Wk, int part_base, int kmax) {
+  pdl_wait_trigger();
   constexpr int NS = 32 / RG;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sb[kGenWmThreads / 32][32];
@@ -1537,6 +1542,7 @@ __host__ __device__ constexpr size_t gen_wm_smem(int kmax) {
 __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalkers Wk, double* oxhat,
                                                           double* oscore, chap_move* best_out,
                                                           int part_base) {
+  pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double sm_red[32];
   __shared__ Best sm_b[32];

@@ -153,6 +153,7 @@ struct chap_walkers {
   int gen_grid = 0;            // k_eval_gen blocks per walker
   int binrow_grid = 0;         // k_eval_binrow CTAs (one walker, row-wise binary columns), 0 = off
   int genwm_grid = 0;          // k_eval_gen_wm blocks per walker group (walker groups), 0 = off
+  bool pdl = false;            // tabu iterations launched with programmatic dependent launch (CHAP_PDL=1)
   size_t genwm_smem = 0;
   ~chap_walkers() {
     if (xs) chap_exchange_state_free(xs);
@@ -167,7 +168,8 @@ struct chap_walkers {
 namespace chap {
 // shared launch helpers (chap.cu)
 chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
-                        int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s);
+                        int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s,
+                        bool pdl);
 int grid_for(long long work, int threads, int cap);
 chap_status walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s);
 

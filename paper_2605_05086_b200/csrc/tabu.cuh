@@ -206,6 +206,7 @@ __global__ void k_tabu_clear(int32_t* tabu, size_t ts, int n, int only_walker) {
 
 // Apply the selected move or bump weights, then (last block) finalise the iteration.
 __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalkers Wk) {
+  pdl_wait_trigger();
   __shared__ long long smv[32];
   __shared__ int s_last;
   const int w = blockIdx.y, tid = threadIdx.x;
