@@ -837,22 +837,34 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
     // in flight together), then the column (x̄ flipped, tabu R13, ties R6)
     const int per = (nv + C - 1) / C;
     const int v0 = rank * per, v1 = min(nv, v0 + per);
-    for (int v = v0 + tid; v < v1; v += kRowThreads) {
-      int part[kRowCluster];
+    // four columns per thread at a time: their remote counters and user indices are all loaded
+    // before any is used; the tabu expiry only for a column that would become the thread's best
+    const int32_t* __restrict__ bperm = P.rb_perm + (size_t)vb * kRowVmax;
+    for (int vq = v0 + tid; vq < v1; vq += 4 * kRowThreads) {
+      int tot[4], jq[4];
 #pragma unroll
-      for (int q = 0; q < kRowCluster; ++q) part[q] = q < C ? cl.map_shared_rank(sc, q)[v] : 0;
-      int tot = 0;
+      for (int i = 0; i < 4; ++i) {
+        const int v = vq + i * kRowThreads;
+        tot[i] = 0;
+        jq[i] = 0;
+        if (v < v1) {
 #pragma unroll
-      for (int q = 0; q < kRowCluster; ++q) tot += part[q];
-      const int p = p0 + v * nb;
-      const double xb = (double)((bits[v >> 5] >> (v & 31)) & 1u);
-      const double s = 0.5 * (double)tot;
-      if (s < b.s) continue;   // cannot become the best: no index or tabu read
-      const int j = __ldg(P.rb_perm + (size_t)vb * kRowVmax + v);
-      if (better_move(s, j, b.s, b.j) && (!use_tabu || (long long)__ldg(TB + p) <= kk)) {
+          for (int q = 0; q < kRowCluster; ++q)
+            if (q < C) tot[i] += cl.map_shared_rank(sc, q)[v];
+          jq[i] = __ldg(bperm + v);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int v = vq + i * kRowThreads;
+        if (v >= v1) break;
+        const double s = 0.5 * (double)tot[i];
+        if (!better_move(s, jq[i], b.s, b.j)) continue;
+        const int p = p0 + v * nb;
+        if (use_tabu && (long long)__ldg(TB + p) > kk) continue;
         b.s = s;
-        b.v = 1.0 - xb;
-        b.j = j;
+        b.v = 1.0 - (double)((bits[v >> 5] >> (v & 31)) & 1u);
+        b.j = jq[i];
         b.p = p;
       }
     }
