@@ -24,7 +24,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _deps():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-o", SO + ".tmp"]
+    extra = os.environ.get("CHAP_NVCC_FLAGS", "").split()   # experiments (e.g. -DCHAP_GEN_MINB=4)
+    cmd = [nvcc] + NVCC_FLAGS + extra + ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-o", SO + ".tmp"]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
     cmd += ["-ldl"]   # NCCL is dlopen'ed at run time (csrc/portfolio.cuh)
     if verbose:

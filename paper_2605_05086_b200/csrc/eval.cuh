@@ -146,7 +146,11 @@ struct Elem {
 // exactly; the guard also keeps zero/inf numerators off the IEEE division's slow path.
 __device__ __forceinline__ double breakpoint(double xb, double r, double a) {
   const bool plain = r != 0.0 && isfinite(r);
+#ifdef CHAP_EXP_NODIV
+  const double q = (plain ? r : 1.0) * a;
+#else
   const double q = (plain ? r : 1.0) / a;
+#endif
   return plain ? xb - q : xb;
 }
 
@@ -1063,7 +1067,11 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
   }
   __syncwarp();
   // (2) one work item per lane
+#ifdef CHAP_EXP_SKIP2
+  for (int i0 = 0; i0 < 0; i0 += 32) {
+#else
   for (int i0 = 0; i0 < n_items; i0 += 32) {
+#endif
     const int I = i0 + lane;
     // the item's column: the last column c with ip_c <= I (ip is nondecreasing over the lanes)
     int c = 0;
@@ -1130,7 +1138,11 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
     if (fast) {
       const float lf = isfinite(l) ? (float)l : -INFINITY, uf = isfinite(u) ? (float)u : INFINITY;
       float bf = 0.f, af = 0.f, plf = 0.f, puf = 0.f;
+#ifdef CHAP_EXP_SKIP3
+      for (int e = cb; e < cb; ++e) {
+#else
       for (int e = cb; e < ce; ++e) {
+#endif
         const float2 ab = S.AB[e];
         const float ke = S.kf[e], de = S.D[e];
         bf += ab.x;
@@ -1393,7 +1405,12 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   const int nwarps = gridDim.x * (kGenThreads / 32);
   int t = blockIdx.x * (kGenThreads / 32) + wid;
   // chunks of long columns first (their latency overlaps the packed tiles of other warps)
+#ifdef CHAP_EXP_SKIPLBKT
+  for (; t < P.n_gchunks; t += nwarps) continue;
+  for (; false;)
+#else
   for (; t < P.n_gchunks; t += nwarps)
+#endif
     lbkt_chunk(P, Wk, walker, X, RS, st, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
   __syncwarp();
   t -= P.n_gchunks;
@@ -1404,6 +1421,9 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     const WTile T = Tn;
     if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];
     if (T.kind == CC_GEN) {
+#ifdef CHAP_EXP_SKIPTILES
+      continue;
+#endif
       if (!wm_mode || T.pad) gen_tile(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
     } else if (!wm_mode) {
       wtile_empty(P, C, T, lane, b);
