@@ -72,7 +72,10 @@ struct LongCol {
   int32_t kind;      // CC_LBIN or CC_LBKT
 };
 constexpr int kWChunk = 256;                      // nonzeros per warp chunk of a long binary column
-constexpr int kBktChunk = 512;                    // nonzeros per warp chunk of a long bounded-integer column
+#ifndef CHAP_BKT_CHUNK
+#define CHAP_BKT_CHUNK 512
+#endif
+constexpr int kBktChunk = CHAP_BKT_CHUNK;         // nonzeros per warp chunk of a long bounded-integer column
 
 // A block tile (chunk of a long column, or one column sorted by the whole block).
 struct Tile {

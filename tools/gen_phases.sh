@@ -1,7 +1,7 @@
 #!/bin/bash
 # Timing-only variants of k_eval_gen (results wrong on purpose): which phase of gen_tile costs what.
 mkdir -p gpurun_out; : > gpurun_out/gen_phases.txt
-for v in "" "-DCHAP_EXP_SKIPLBKT"; do
+for v in "-DCHAP_BKT_CHUNK=256" "-DCHAP_BKT_CHUNK=1024" "-DCHAP_BKT_CHUNK=2048"; do
   CHAP_NVCC_FLAGS="$v" python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || { echo "build fail $v" >> gpurun_out/gen_phases.txt; continue; }
   touch paper_2605_05086_b200/csrc/chap.cu
   timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/gp.csv python tools/prof_step.py 20 5 G > /dev/null 2>&1
