@@ -67,3 +67,31 @@ def test_oracle_and_cuda_path_share_nothing():
                         pat = (r'^\s*(#\s*include\s*[<"][^>"]*' + re.escape(bad) + r'|import\s+' + re.escape(bad) +
                                r'|from\s+' + re.escape(bad) + r')')
                         assert not re.search(pat, txt, flags=re.M), (f, bad)
+
+
+def test_binding_structs_match_header_layout(tmp_path):
+    """Every ABI struct of include/chap.h: size and field offsets as gcc lays them out equal the
+    ctypes binding's (catches header/binding drift without a GPU)."""
+    import ctypes
+    import paper_2605_05086_b200 as chap
+    structs = ["chap_problem_info", "chap_move", "chap_params", "chap_step_record", "chap_walker_stats",
+               "chap_result", "chap_walker_summary"]
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "chap.h"', "int main(void) {"]
+    for sname in structs:
+        src.append(f'  printf("{sname} size %zu\\n", sizeof({sname}));')
+        for fname, _ in getattr(chap, sname)._fields_:
+            src.append(f'  printf("{sname} {fname} %zu\\n", offsetof({sname}, {fname}));')
+    src += ["  return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(c)])
+    got = {}
+    for line in subprocess.check_output([str(exe)]).decode().splitlines():
+        sname, field, val = line.split()
+        got[(sname, field)] = int(val)
+    for sname in structs:
+        cls = getattr(chap, sname)
+        assert got[(sname, "size")] == ctypes.sizeof(cls), sname
+        for fname, _ in cls._fields_:
+            assert got[(sname, fname)] == getattr(cls, fname).offset, (sname, fname)
