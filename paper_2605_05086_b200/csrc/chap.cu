@@ -818,7 +818,7 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
   if (rgrid > 0) TRY(launch_binrow(P, Wk, rgrid, bgrid + ggrid, s, pdl));
   if (ggrid > 0)
     TRY(lk(k_eval_gen, dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, bgrid,
-           wgrid > 0 ? 1 : 0));
+           wgrid > 0 ? 1 : 0, (rgrid > 0 && bgrid == 0) ? 1 : 0));
   if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s, pdl));
   TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
          bgrid + ggrid + rgrid + wgrid));
@@ -1014,7 +1014,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   if (W == 1 && p->binrow_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) &&
       2.0 * (double)prm.weight_cap * (double)std::max(1, p->binrow_maxdeg) < 2147483647.0) {
     S->binrow_grid = p->binrow_grid;
-    S->bin_grid = p->bin_chunk_grid;
+    // the long binary chunks ride in k_eval_gen when it runs (with_lbin), else in k_eval_bin
+    S->bin_grid = (S->gen_grid > 0) ? 0 : p->bin_chunk_grid;
     TRY(B.alloc(&Wk.xbits, (size_t)p->dp.n_rblocks * kRowWpb));   // block-ordered bitset
   }
   // programmatic dependent launch between the iteration's kernels: measured slower on config G
@@ -1202,7 +1203,8 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     cudaEventRecordWithFlags(e[2], s, cudaEventRecordExternal);
     if (S->gen_grid > 0)
       k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid,
-                                                                       S->genwm_grid > 0 ? 1 : 0);
+                                                                       S->genwm_grid > 0 ? 1 : 0,
+                                                                       (S->binrow_grid > 0 && S->bin_grid == 0) ? 1 : 0);
     if (S->genwm_grid > 0)
       TRY(launch_gen_wm(P, S->wk, S->genwm_grid, S->bin_grid + S->gen_grid + S->binrow_grid, s, false));
     cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);

@@ -1375,8 +1375,11 @@ __device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalk
 
 // wm_mode 1 (walker groups): the integer general tiles and the empty columns are k_eval_gen_wm's;
 // this kernel takes the long bounded-integer chunks and the tiles holding a continuous column.
+// with_lbin (one walker, row-wise binary mode): this kernel also takes the long binary chunks,
+// whose gather latency then overlaps the general tiles' arithmetic
 __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
-                                                              double* oscore, int part_base, int wm_mode) {
+                                                              double* oscore, int part_base, int wm_mode,
+                                                              int with_lbin) {
   pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
@@ -1405,6 +1408,11 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   const int nwarps = gridDim.x * (kGenThreads / 32);
   int t = blockIdx.x * (kGenThreads / 32) + wid;
   // chunks of long columns first (their latency overlaps the packed tiles of other warps)
+  if (with_lbin) {
+    for (; t < P.n_bchunks; t += nwarps)
+      lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
+    t -= P.n_bchunks;
+  }
 #ifdef CHAP_EXP_SKIPLBKT
   for (; t < P.n_gchunks; t += nwarps) continue;
   for (; false;)
