@@ -30,7 +30,11 @@ for r in rows[1:]:
         continue
     v = float(r[vi]) * (1e-3 if r[ui] == "ns" else 1.0)
     agg[r[ki].split("(")[0]].append(v)
-step = ["k_eval_bin", "k_eval_binrow", "k_eval_gen", "k_eval", "k_apply"]
+# the tabu iteration's kernels: the eval/apply kernels launched about once per iteration (the
+# eval API's few e2e launches of k_eval_bin are not part of the step)
+nit = max(len(v) for k, v in agg.items() if k == "k_apply") if "k_apply" in agg else 0
+step = [k for k in ("k_eval_bin", "k_eval_binrow", "k_eval_gen", "k_eval", "k_apply")
+        if k in agg and len(agg[k]) >= max(1, nit // 2)]
 tot = sum(sum(agg[k]) / max(1, len(agg[k])) for k in step if k in agg)
 out = [f"ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches) "
        f"of `bench.py --config {cfg} --steps 20 --warmup 5`",

@@ -1,12 +1,16 @@
 #!/bin/bash
 # Bench lines for the non-default configurations (run on the GPU box): P (64 walkers), G with walker
-# groups, S, and the X scaling sweep; one JSON line each into gpurun_out/sweep.jsonl.
+# groups, S, and the X scaling sweep; one JSON line each into gpurun_out/sweep.jsonl. Step counts
+# keep every timed region >= ~0.5 s (short regions read launch and clock-ramp jitter).
 set -u
 mkdir -p gpurun_out
 : > gpurun_out/sweep.jsonl
 run() { timeout 300 python bench.py --no-cpu-baseline --e2e-iters 2 --profile-iters 20 "$@" 2>>gpurun_out/sweep.err | tail -1 >> gpurun_out/sweep.jsonl; }
-run --config P --steps 1000 --warmup 20
-run --config G --walkers 8 --steps 200 --warmup 5
-run --config G --walkers 32 --steps 50 --warmup 5
-run --config S --steps 4000 --warmup 50
-for c in X1e5 X1e6 X1e7 X5e7; do run --config $c --steps 500 --warmup 10; done
+run --config P --steps 4000 --warmup 50
+run --config G --walkers 8 --steps 800 --warmup 10
+run --config G --walkers 32 --steps 250 --warmup 5
+run --config S --steps 30000 --warmup 200
+run --config X1e5 --steps 20000 --warmup 200
+run --config X1e6 --steps 15000 --warmup 200
+run --config X1e7 --steps 4000 --warmup 50
+run --config X5e7 --steps 1000 --warmup 20
