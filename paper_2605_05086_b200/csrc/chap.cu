@@ -806,22 +806,28 @@ static chap_status launch_binrow(const chap_problem* P, const DevWalkers& Wk, in
 chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                               int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best,
                               cudaStream_t s, bool pdl) {
+  // k_eval only selects when there are no long columns and no sort tiles: then the last eval kernel
+  // (k_eval_gen, else k_eval_bin) selects in its last block and k_eval is not launched
+  const bool sel_only = Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && P->dp.n_lfin == 0 && wgrid == 0;
+  const int gen_sel = (sel_only && ggrid > 0) ? bgrid + ggrid + rgrid : 0;
+  const int bin_sel = (sel_only && ggrid == 0 && rgrid == 0 && bgrid > 0) ? bgrid : 0;
   if (bgrid > 0) {
     if (Wk.rg > 1) {
       TRY(launch_bin_wm(P->dp, Wk, bgrid, s, pdl));
     } else {
       DevProblem D = P->dp;
       if (rgrid > 0) D.n_btiles = 0;   // packed binary columns row-wise: k_eval_bin takes the long chunks only
-      TRY(lk(k_eval_bin, dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s, pdl, 1, D, Wk, oxhat, oscore));
+      TRY(lk(k_eval_bin, dim3(bgrid, Wk.W), kBinThreads, kBinSmem, s, pdl, 1, D, Wk, oxhat, oscore, bin_sel, best));
     }
   }
   if (rgrid > 0) TRY(launch_binrow(P, Wk, rgrid, bgrid + ggrid, s, pdl));
   if (ggrid > 0)
     TRY(lk(k_eval_gen, dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, bgrid,
-           wgrid > 0 ? 1 : 0, (rgrid > 0 && bgrid == 0) ? 1 : 0));
+           wgrid > 0 ? 1 : 0, (rgrid > 0 && bgrid == 0) ? 1 : 0, gen_sel, best));
   if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s, pdl));
-  TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
-         bgrid + ggrid + rgrid + wgrid));
+  if (!gen_sel && !bin_sel)
+    TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
+           bgrid + ggrid + rgrid + wgrid));
   return CHAP_OK;
 }
 
@@ -1196,7 +1202,7 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
       DevProblem Db = D;
       if (S->binrow_grid > 0) Db.n_btiles = 0;
       if (S->wk.rg > 1) TRY(launch_bin_wm(D, S->wk, S->bin_grid, s, false));
-      else k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(Db, S->wk, nullptr, nullptr);
+      else k_eval_bin<<<dim3(S->bin_grid, S->W), kBinThreads, kBinSmem, s>>>(Db, S->wk, nullptr, nullptr, 0, nullptr);
     }
     if (S->binrow_grid > 0) TRY(launch_binrow(P, S->wk, S->binrow_grid, S->bin_grid + S->gen_grid, s, false));
     cudaEventRecordWithFlags(e[1], s, cudaEventRecordExternal);
@@ -1204,7 +1210,8 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     if (S->gen_grid > 0)
       k_eval_gen<<<dim3(S->gen_grid, S->W), kGenThreads, kGenSmem, s>>>(D, S->wk, nullptr, nullptr, S->bin_grid,
                                                                        S->genwm_grid > 0 ? 1 : 0,
-                                                                       (S->binrow_grid > 0 && S->bin_grid == 0) ? 1 : 0);
+                                                                       (S->binrow_grid > 0 && S->bin_grid == 0) ? 1 : 0,
+                                                                       0, nullptr);
     if (S->genwm_grid > 0)
       TRY(launch_gen_wm(P, S->wk, S->genwm_grid, S->bin_grid + S->gen_grid + S->binrow_grid, s, false));
     cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);
@@ -1258,7 +1265,10 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 
 extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int32_t* out) {
   if (!S || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or out");
-  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + 2;
+  const DevProblem& D = S->P->dp;
+  const bool sel_only = S->W == 1 && S->wk.rg == 1 && D.n_tiles == 0 && D.n_lfin == 0 && S->genwm_grid == 0;
+  const bool fused = sel_only && (S->gen_grid > 0 || (S->binrow_grid == 0 && S->bin_grid > 0));
+  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + (fused ? 0 : 1) + 1;
   return CHAP_OK;
 }
 

@@ -399,6 +399,47 @@ __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_fl
   return last;
 }
 
+// The global select (R6), run by the last block of a walker's final eval kernel: the
+// best admissible move over the walker's nparts block parts, written as the walker's decision (and
+// to best_out for the eval API).
+__device__ __forceinline__ void select_walker(const DevWalkers& Wk, int walker, int nparts, Best* sm_b,
+                                              chap_move* best_out, const double* x) {
+  const Cand* part = Wk.part + (size_t)walker * Wk.ps;
+  Best g;
+  g.init();
+  for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
+    Best o;
+    o.s = __ldcg(&part[q].s);
+    o.v = __ldcg(&part[q].v);
+    o.j = __ldcg(&part[q].j);
+    o.p = __ldcg(&part[q].p);
+    g.take(o);
+  }
+  g = block_reduce_best(g, sm_b);
+  if (threadIdx.x == 0) {
+    WalkerScalars* scw = Wk.sc + walker;
+    const bool found = g.p >= 0;
+    Decision d;
+    d.move = (found && g.s > 0.0) ? 1 : 0;
+    d.p = g.p;
+    d.j = found ? g.j : -1;
+    d.pad = 0;
+    d.v = g.v;
+    d.s = found ? g.s : -INFINITY;
+    d.delta = d.move ? (g.v - x[g.p]) : 0.0;
+    scw->dec = d;
+    if (best_out) {
+      chap_move mv;
+      mv.j = d.move ? d.j : -1;
+      mv.pad = 0;
+      mv.v = d.move ? d.v : NAN;
+      mv.s = d.move ? d.s : -INFINITY;
+      best_out[walker] = mv;
+    }
+    Wk.sel_count[walker] = 0u;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // the kernel
 // ------------------------------------------------------------------------------------------
@@ -461,8 +502,11 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
                   oscore, kk, use_tabu);
 }
 
+// select_parts > 0: this is the walker's only and last eval kernel and k_eval has nothing but the
+// select to do (no long columns, no sort tiles): the last block to finish selects over
+// select_parts block parts and k_eval is not launched.
 __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProblem P, DevWalkers Wk, double* oxhat,
-                                                              double* oscore) {
+                                                              double* oscore, int select_parts, chap_move* best_out) {
   pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
@@ -568,6 +612,11 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + blockIdx.x, b);
+  KT_END(Wk, 0);
+  if (select_parts <= 0) return;
+  __shared__ int s_flag;
+  if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
+  select_walker(Wk, walker, select_parts, sm_b, best_out, X);
   KT_END(Wk, 0);
 }
 
@@ -1379,7 +1428,7 @@ __device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalk
 // whose gather latency then overlaps the general tiles' arithmetic
 __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
                                                               double* oscore, int part_base, int wm_mode,
-                                                              int with_lbin) {
+                                                              int with_lbin, int select_parts, chap_move* best_out) {
   pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Best sm_b[32];
@@ -1439,6 +1488,11 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
+  KT_END(Wk, 1);
+  if (select_parts <= 0) return;   // as in k_eval_bin: the last eval kernel selects
+  __shared__ int s_flag;
+  if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
+  select_walker(Wk, walker, select_parts, sm_b, best_out, X);
   KT_END(Wk, 1);
 }
 
@@ -1620,39 +1674,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
   KT_END(Wk, 2);
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
-  Best g;
-  g.init();
-  for (int q = threadIdx.x; q < part_base + (int)gridDim.x; q += blockDim.x) {
-    Best o;
-    o.s = __ldcg(&part[q].s);
-    o.v = __ldcg(&part[q].v);
-    o.j = __ldcg(&part[q].j);
-    o.p = __ldcg(&part[q].p);
-    g.take(o);
-  }
-  g = block_reduce_best(g, sm_b);
-  if (threadIdx.x == 0) {
-    WalkerScalars* scw = Wk.sc + walker;
-    const bool found = g.p >= 0;
-    Decision d;
-    d.move = (found && g.s > 0.0) ? 1 : 0;
-    d.p = g.p;
-    d.j = found ? g.j : -1;
-    d.pad = 0;
-    d.v = g.v;
-    d.s = found ? g.s : -INFINITY;
-    d.delta = d.move ? (g.v - C.x[g.p]) : 0.0;
-    scw->dec = d;
-    if (best_out) {
-      chap_move mv;
-      mv.j = d.move ? d.j : -1;
-      mv.pad = 0;
-      mv.v = d.move ? d.v : NAN;
-      mv.s = d.move ? d.s : -INFINITY;
-      best_out[walker] = mv;
-    }
-    Wk.sel_count[walker] = 0u;
-  }
+  select_walker(Wk, walker, part_base + (int)gridDim.x, sm_b, best_out, C.x);
   KT_END(Wk, 2);
 }
 

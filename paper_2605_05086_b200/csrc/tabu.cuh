@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   if (Wk.kt && w == 0) {   // kernel timing: accumulate this iteration's spans, re-arm
     unsigned long long* kt = Wk.kt;
     const unsigned long long now = kt_now();
-    for (int q = 0; q < 3; ++q) kt[8 + q] += kt[2 * q + 1] - kt[2 * q];
+    for (int q = 0; q < 3; ++q)
+      if (kt[2 * q + 1] > kt[2 * q]) kt[8 + q] += kt[2 * q + 1] - kt[2 * q];   // a kernel not launched: 0
     kt[11] += now - kt[6];
     kt[12] += now - min(kt[0], min(kt[2], kt[4]));   // the eval kernels may overlap (forked branch)
     kt[13] += 1;
