@@ -432,6 +432,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     int32_t nbin = 0;
     if (ok) {
       cudaError_t e1 = cudaFuncSetAttribute(k_eval_binrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem);
+      if (cudaFuncSetAttribute(k_eval_binrow, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        cudaGetLastError();
       if (e1 == cudaSuccess) {
         for (int c = kRowCluster; c >= 4; --c) {
           cudaLaunchConfig_t cfg = {};
@@ -447,7 +449,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
           cfg.numAttrs = 1;
           int k = 0;
           if (cudaOccupancyMaxActiveClusters(&k, k_eval_binrow, &cfg) != cudaSuccess) k = 0;
-          if (k * c > ncl * C) { ncl = k; C = c; }
+          if (k < 1) continue;
+          // fewest rounds of blocks first (a block holds <= kRowVmax columns), then the most SMs
+          auto rounds = [&](int kc) { return (int)(((int64_t)(pb1 - pb0) + (int64_t)kc * kRowVmax - 1) / ((int64_t)kc * kRowVmax)); };
+          if (ncl == 0 || rounds(k) < rounds(ncl) || (rounds(k) == rounds(ncl) && k * c > ncl * C)) { ncl = k; C = c; }
         }
       }
       cudaGetLastError();

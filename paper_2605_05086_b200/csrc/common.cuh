@@ -89,7 +89,7 @@ struct Tile {
 // Row-wise binary flip evaluation (k_eval_binrow, PAPER.md:347 re-designed): the packed binary
 // columns are cut into variable blocks; the nonzeros of a block are stored sorted by row and cut
 // into kRowCluster equal slices, one per CTA of a thread-block cluster.
-constexpr int kRowCluster = 8;                    // max CTAs per cluster (portable maximum); the
+constexpr int kRowCluster = 12;                   // max CTAs per cluster (above 8: non-portable); the
                                                   // width used is chosen at problem create
 constexpr int kRowThreads = 1024;                 // k_eval_binrow block (one CTA per SM)
 constexpr int kRowVmax = 32768;                   // variables per block: int32 scores in 128 KB of smem
