@@ -392,6 +392,8 @@ def main():
                                   f"{W} walkers' state) and kept so on purpose: consecutive tabu "
                                   "iterations reuse it, no flush; the HBM fraction is not the bound here")},
                 "tabu_iters_per_s": W * args.steps * world / sec,
+                # nonzeros visited per second (every nonzero incl. cutoff-row entries, per walker)
+                "nnz_visits_per_s": float(info.nnz_norm + info.nnz_cut) * W * args.steps * world / sec,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_iter * args.steps + 4 + 2 * n_exchanges,
                 "clocks": clk.summary(),
