@@ -315,12 +315,14 @@ def main():
     achieved = eval_bytes / (eval_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = None
+    winstr = {}
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
             if tj.get("config") == cfg:
                 traffic = tj.get("dram_bytes_per_launch")
+                winstr = tj.get("warp_instructions_per_launch", {}) or {}
         except Exception:
             traffic = None
     step_ms_profiled = float(kt[4] / n_kt / 1e6)
@@ -342,6 +344,15 @@ def main():
                            "frac": eval_bytes / (eval_ms_events * 1e-3) / 1e9 / peak,
                            "how": "CUDA-event pairs around each kernel node of a captured graph "
                                   f"({args.profile_iters} iterations right after the timed region)"},
+                # the dominant kernel is issue-bound, not bandwidth-bound: its warp instructions per
+                # launch (ncu capture of the same configuration, profiles/traffic.json) over its
+                # in-graph time, against the issue peak 148 SMs x 4 schedulers x the SM clock
+                "issue": ({"kernel": "k_eval_gen", "bound": "issue",
+                           "warp_instructions_per_launch": winstr["k_eval_gen"],
+                           "achieved": winstr["k_eval_gen"] / (ktm[1] * 1e-3),
+                           "peak": 148 * 4 * 1.965e9, "unit": "warp instructions/s",
+                           "frac": winstr["k_eval_gen"] / (ktm[1] * 1e-3) / (148 * 4 * 1.965e9)}
+                          if winstr.get("k_eval_gen") and ktm[1] > 0 else None),
                 "whole_step": {"model_bytes": pass_bytes, "ms": ms_max / args.steps,
                                "achieved": pass_bytes / (ms_max / args.steps * 1e-3) / 1e9,
                                "frac": pass_bytes / (ms_max / args.steps * 1e-3) / 1e9 / peak}}

@@ -48,6 +48,8 @@ print("\n".join(out))
 
 # full capture
 rep = os.path.join(go, f"full_{cfg}.ncu-rep")
+if not os.path.exists(rep):
+    sys.exit(f"no capture {rep}: rerun tools/gpu_profiles.sh")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(raw.splitlines()))
 H, U = rr[0], rr[1]
@@ -59,8 +61,13 @@ keys = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg", "smsp__inst_executed
         "launch__block_size", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 txt = [f"ncu --set full --clock-control none, one launch each (tools/prof_step.py {cfg}, after 20 iterations)"]
 traffic = 0.0
+warp_instr = {}
+seen = set()
 for v in rr[2:]:
     name = v[H.index("Kernel Name")].split("(")[0]
+    if name in seen:   # the capture may run into the next iteration: one launch per kernel
+        continue
+    seen.add(name)
     txt.append(f"== {name}")
     d = {}
     for a, u, c in zip(H, U, v):
@@ -75,12 +82,14 @@ for v in rr[2:]:
             except ValueError:
                 pass
     txt.append("  stall cycles per issued instruction: " + ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:8]))
+    if "smsp__inst_executed.sum" in d:
+        warp_instr[name] = float(d["smsp__inst_executed.sum"][1])
     if name in ("k_eval_bin", "k_eval_binrow", "k_eval_gen", "k_eval"):
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             u, c = d[k]
             traffic += float(c) * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}[u]
 open(os.path.join(pr, f"{tag}_ncu_full_{cfg}.txt"), "w").write("\n".join(txt) + "\n")
-json.dump({"config": cfg, "dram_bytes_per_launch": traffic,
+json.dump({"config": cfg, "dram_bytes_per_launch": traffic, "warp_instructions_per_launch": warp_instr,
            "source": f"profiles/{tag}_ncu_full_{cfg}.txt: dram__bytes_read.sum + dram__bytes_write.sum of "
                      "k_eval_bin + k_eval_binrow + k_eval_gen + k_eval, one launch each"},
           open(os.path.join(pr, "traffic.json"), "w"), indent=1)
