@@ -95,9 +95,15 @@ constexpr int kRowThreads = 1024;                 // k_eval_binrow block (one CT
 constexpr int kRowVmax = 32768;                   // variables per block: int32 scores in 128 KB of smem
 constexpr int kRowWpb = kRowVmax / 32;            // bitset words per block
 constexpr int kRowConsumers = kRowThreads - 32;   // consumer threads (the last warp produces)
-constexpr int kRowPer = 4;                        // entries per consumer thread per stage
+#ifndef CHAP_ROW_PER
+#define CHAP_ROW_PER 4
+#endif
+#ifndef CHAP_ROW_STAGES
+#define CHAP_ROW_STAGES 3
+#endif
+constexpr int kRowPer = CHAP_ROW_PER;             // entries per consumer thread per stage
 constexpr int kRowChunk = kRowPer * kRowConsumers;   // entries per TMA stage (7.75 KB rows + 7.75 KB columns)
-constexpr int kRowStages = 3;                     // stages of the entry ring (93 KB)
+constexpr int kRowStages = CHAP_ROW_STAGES;       // stages of the entry ring (93 KB at 4 x 3)
 struct RowBlock {
   int32_t p0;                 // first column (internal order): column k of block b is p0 + k nb
   int32_t nv;                 // columns
