@@ -138,11 +138,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def planted_objective(inst):
+    """The objective of the instance's planted feasible point: the walkers search with the cutoff
+    c.x <= z* - delta active from the start, as CHAP's tabu workers do with the pool's best-known
+    objective (SURVEY 8(d) 'G, 1 walker, tabu step (cutoff active)')."""
+    xs = getattr(inst, "x_star", None)
+    return None if xs is None else float(np.asarray(inst.c, np.float64) @ np.asarray(xs, np.float64))
+
+
 def oracle_baseline(inst, x0, seconds_target: float = 15.0, max_iters: int = 400):
     """The oracle as it stands, on the host cores: tabu iterations of one walker (bounded sample)."""
     import oracle
     O = oracle.Problem.from_instance(inst)
     ow = oracle.TabuWalker(O, x0)
+    z = planted_objective(inst)
+    if z is not None:
+        ow.set_cutoff(z)
     n_eval = int(np.sum(O.vars()[2] != 0))
     t0 = time.perf_counter()
     ow.run(1)
@@ -173,6 +184,9 @@ def run_reference(args):
     import oracle
     O = oracle.Problem.from_instance(inst)
     ow = oracle.TabuWalker(O, x0)
+    z = planted_objective(inst)
+    if z is not None:
+        ow.set_cutoff(z)
     n_eval = int(np.sum(O.vars()[2] != 0))
     t0 = time.perf_counter()
     ow.run(1)   # one full iteration sizes the run
@@ -210,7 +224,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator synth/, no dataset)",
-            "config": {"workload": CONFIGS[cfg]["desc"], "walkers": 1, "n": inst.n, "m": inst.m, "nnz": inst.nnz},
+            "config": {"workload": CONFIGS[cfg]["desc"], "walkers": 1, "n": inst.n, "m": inst.m, "nnz": inst.nnz,
+                       "cutoff": "active from the start (z* of the planted point)" if z is not None else "none"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -255,6 +270,9 @@ def main():
     x0 = torch.from_numpy(start_points(inst, cfg, W, rank)).to(dev)
     prm = chap.default_params(graph_iters=32)
     ws = chap.Walkers(P, x0, prm)
+    z_star = planted_objective(inst)
+    if z_star is not None:
+        ws.set_cutoff(z_star)   # the cutoff row is active from the start
     ws.timing(1)   # per-kernel %globaltimer spans inside the graphs (no events), on before the warm-up
     comm = None    # the portfolio exchange every exchange_K iterations: NCCL across ranks
     if world > 1:
@@ -365,11 +383,15 @@ def main():
     wh = pinned(P.m_norm, torch.float32)
     wh[:] = 1.0
     outs = (pinned(inst.n, torch.float64), pinned(inst.n, torch.float64))
-    P.eval_best_shift_host(xh, wh, out=outs)
+    cut_rhs = math.inf
+    if z_star is not None:   # the same active cutoff: rhs = z* - delta (R14)
+        dlt = float(info.auto_cutoff_delta)
+        cut_rhs = z_star - (dlt if math.isfinite(dlt) else 1e-6 * max(1.0, abs(z_star)))
+    P.eval_best_shift_host(xh, wh, cut_rhs, out=outs)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_iters):
-        P.eval_best_shift_host(xh, wh, out=outs)
+        P.eval_best_shift_host(xh, wh, cut_rhs, out=outs)
     e2e_s = time.perf_counter() - t0
     et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -396,6 +418,8 @@ def main():
                            "parallelism": f"walker portfolio x{world}: independent walkers per GPU, "
                                           f"exchange (NCCL allgather) every {K_x} iterations",
                            "exchanges_in_timed_region": n_exchanges,
+                           "cutoff": ("active from the start: c.x <= z* - delta, z* = c.x* of the instance's "
+                                      "planted feasible point (PAPER.md:373)" if z_star is not None else "none"),
                            "l2": ("inputs larger than L2: A in CSC alone is "
                                   f"{info.model_bytes_A / 1e6:.0f} MB vs 126 MB L2; no flush"
                                   if info.model_bytes_A > 126e6 else
