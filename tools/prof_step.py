@@ -21,6 +21,8 @@ W = int(sys.argv[4]) if len(sys.argv) > 4 else (64 if cfg == "P" else 1)
 x0 = np.stack([synth.x_lower(inst)] * W) if cfg != "P" else \
     np.stack([synth.x_bernoulli(inst, (3, w), 0.5) for w in range(W)])
 ws = chap.Walkers(P, torch.from_numpy(x0).cuda(), chap.default_params(graph_iters=0))
+if getattr(inst, "x_star", None) is not None:   # as bench.py: the cutoff row active from the start
+    ws.set_cutoff(float(inst.c @ inst.x_star))
 ws.step(warm)
 torch.cuda.synchronize()
 ws.step(iters)
