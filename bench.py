@@ -36,6 +36,8 @@ UNIT = "move_evals/s"
 CONFIGS = {
     "G": dict(desc="G: synthetic mixed general-integer MIP 200k rows x 1M vars, ~10.4M nnz, 100 long columns "
                    "(BASELINE.json configs[2])", walkers=1),
+    "T": dict(desc="T: tiny synthetic MIP, 40 vars x 25 rows (knapsack + cover + general; BASELINE.json "
+                   "configs[0], a test configuration)", walkers=1),
     "S": dict(desc="S: synthetic set cover 10k rows x 50k binaries, ~500k nnz (BASELINE.json configs[1])", walkers=1),
     "P": dict(desc="P: packing MIP 20k rows x 100k binaries, ~1M nnz, 64 walkers (BASELINE.json configs[3])",
               walkers=64),
@@ -52,6 +54,8 @@ CONFIGS = {
 
 
 def make_instance(cfg: str):
+    if cfg == "T":
+        return synth.tiny(0)
     if cfg == "G":
         return synth.mixed()
     if cfg == "S":
@@ -70,10 +74,44 @@ def make_instance(cfg: str):
 
 
 def start_points(inst, cfg: str, W: int, rank: int):
+    """x0 of the W walkers of a rank. Config P: Bernoulli(0.5) keyed (3, global walker id) (SURVEY
+    8(d)). Otherwise walker 0 of rank 0 starts at x_lower (0); every other walker (global id g > 0)
+    at x_lower with 1 % of its variables raised by one step (keyed by g), so that weak-scaling
+    replicas walk different trajectories over the same amount of work per iteration."""
     if cfg == "P":
         return np.stack([synth.x_bernoulli(inst, (3, rank * W + w), 0.5) for w in range(W)])
-    x = synth.x_lower(inst)
-    return np.stack([x] * W)
+    return np.stack([synth.x_lower(inst) if rank * W + w == 0 else synth.x_perturbed(inst, (5, rank * W + w), 0.01)
+                     for w in range(W)])
+
+
+def config_dict(cfg: str, inst, W: int, world: int, z_star):
+    """The `config` object of the JSON line: identical for both arms (--impl chap / reference)."""
+    a_bytes = 12 * (inst.nnz + int(np.count_nonzero(inst.c))) + 4 * (inst.n + 1)   # SURVEY 8(d) model of A
+    l2 = (f"inputs larger than L2: A in CSC alone is {a_bytes / 1e6:.0f} MB vs 126 MB L2; no flush"
+          if a_bytes > 126e6 else
+          f"working set L2-resident (A in CSC {a_bytes / 1e6:.0f} MB + {W} walkers' state) and kept so on "
+          "purpose: consecutive tabu iterations reuse it, no flush; the HBM fraction is not the bound here")
+    return {"workload": CONFIGS[cfg]["desc"], "walkers_per_gpu": W, "n": inst.n, "m": inst.m, "nnz": inst.nnz,
+            "l2": l2,
+            "parallelism": f"walker portfolio x{world}: independent walkers per GPU (weak scaling, distinct start "
+                           f"points), exchange every 1000 iterations",
+            "cutoff": ("active from the start: c.x <= z* - delta, z* = c.x* of the instance's planted feasible "
+                       "point (PAPER.md:373)" if z_star is not None else "none")}
+
+
+def maybe_spawn(args):
+    """--gpus N with no torchrun environment: re-launch this command under torch.distributed.run with
+    N ranks (one process per GPU, rendezvous on 127.0.0.1); returns only in the child ranks or at N=1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execvp(sys.executable, cmd)
 
 
 def measured_peak_hbm():
@@ -146,26 +184,45 @@ def planted_objective(inst):
     return None if xs is None else float(np.asarray(inst.c, np.float64) @ np.asarray(xs, np.float64))
 
 
-def oracle_baseline(inst, x0, seconds_target: float = 15.0, max_iters: int = 400):
-    """The oracle as it stands, on the host cores: tabu iterations of one walker (bounded sample)."""
+def cpu_model() -> str:
+    try:
+        for line in subprocess.check_output(["lscpu"], text=True).splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_baseline(inst, x0, seconds_target: float = 12.0, max_iters: int = 400):
+    """The oracle as it stands, on the host cores: tabu iterations of one walker (bounded sample),
+    timed with all cores and with one thread."""
     import oracle
     O = oracle.Problem.from_instance(inst)
-    ow = oracle.TabuWalker(O, x0)
     z = planted_objective(inst)
-    if z is not None:
-        ow.set_cutoff(z)
     n_eval = int(np.sum(O.vars()[2] != 0))
-    t0 = time.perf_counter()
-    ow.run(1)
-    t1 = time.perf_counter() - t0
-    iters = int(max(1, min(max_iters, seconds_target / max(t1, 1e-6))))
-    t0 = time.perf_counter()
-    ow.run(iters)
-    dt = time.perf_counter() - t0
-    return {"value": n_eval * iters / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{iters} tabu iterations of 1 walker (after 1 warm-up iteration), all "
-                      f"{n_eval} non-fixed variables evaluated per iteration, OpenMP over variables",
-            "seconds": dt, "iters_per_s": iters / dt}
+    cores = os.cpu_count() or 1
+    out = {}
+    for threads in (cores, 1):
+        ow = oracle.TabuWalker(O, x0)
+        if z is not None:
+            ow.set_cutoff(z)
+        t0 = time.perf_counter()
+        ow.run(1, threads=threads)
+        t1 = time.perf_counter() - t0
+        budget = seconds_target if threads == cores else seconds_target / 2
+        iters = int(max(1, min(max_iters, budget / max(t1, 1e-6))))
+        t0 = time.perf_counter()
+        ow.run(iters, threads=threads)
+        dt = time.perf_counter() - t0
+        out[threads] = (n_eval * iters / dt, iters, dt)
+    v, iters, dt = out[cores]
+    v1, iters1, dt1 = out[1]
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{iters} tabu iterations of 1 walker (after 1 warm-up iteration), all {n_eval} non-fixed "
+                      f"variables evaluated per iteration, OpenMP over variables on {cores} threads",
+            "seconds": dt, "iters_per_s": iters / dt, "cpu_model": cpu_model(),
+            "one_thread": {"value": v1, "unit": UNIT, "cores": 1, "iters": iters1, "seconds": dt1}}
 
 
 def run_reference(args):
@@ -176,7 +233,7 @@ def run_reference(args):
     budget."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        return
+        return   # under torchrun (N > 1) rank 0 alone runs the oracle; the other ranks exit 0
     budget_s = float(os.environ.get("CHAP_REF_BUDGET_S", "150"))
     cfg = args.config
     inst = make_instance(cfg)
@@ -224,11 +281,11 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator synth/, no dataset)",
-            "config": {"workload": CONFIGS[cfg]["desc"], "walkers": 1, "n": inst.n, "m": inst.m, "nnz": inst.nnz,
-                       "cutoff": "active from the start (z* of the planted point)" if z is not None else "none"},
+            "config": config_dict(cfg, inst, 1, args.gpus, z),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": sample, "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "launcher": {"world_size": int(os.environ.get("WORLD_SIZE", "1")), "rank": rank}}
     print(json.dumps(line), flush=True)
 
 
@@ -245,6 +302,7 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    maybe_spawn(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -316,6 +374,8 @@ def main():
     kt = ws.timing(0).astype(np.float64)   # sums over the timed region, then timing off
     st = ws.get()["stats"]
     names = ["binary (k_eval_binrow / k_eval_bin)", "k_eval_gen", "k_eval", "-", "k_apply"]
+    classes = ["packed binary columns", "long binary, general, empty, long bounded-integer columns",
+               "sorted general columns + row state"]
     n_kt = max(1.0, kt[5])
     ktm = [kt[0] / n_kt / 1e6, kt[1] / n_kt / 1e6, kt[2] / n_kt / 1e6, 0.0, kt[3] / n_kt / 1e6]
 
@@ -349,13 +409,14 @@ def main():
                 "traffic": traffic,
                 "kernel": "the best-shift pass of every variable + select: binary columns (k_eval_binrow "
                           "row-wise, long ones k_eval_bin), k_eval_gen, then k_eval",
+                "model": "SURVEY 8(d): 12 B per original nonzero and cutoff entry + 4 B col_ptr per var + static "
+                         "per var (1 B binary / 17 B other) + walker state (x̄ 1 bit / 8 B, 4 B tabu per var, "
+                         "12 B per normalised row)",
                 "peak_kind": peak_kind, "algorithmic_bytes_per_launch": eval_bytes,
                 "timing": "per-kernel first-block-start to last-block-end (%globaltimer) inside the timed "
                           "region's CUDA graphs, averaged over its iterations (chap_walkers_timing)",
                 "kernel_ms": {names[i]: float(ktm[i]) for i in (0, 1, 2, 4)},
-                "per_kernel": {names[i]: {"bytes": mb[i], "ms": float(ktm[i]),
-                                          "GBps": (mb[i] / (ktm[i] * 1e-3) / 1e9) if ktm[i] > 0 else None}
-                               for i in (0, 1, 2)},
+                "model_bytes_by_class": {classes[i]: mb[i] for i in (0, 1, 2)},
                 "kernel_share_of_step": eval_ms / step_ms_profiled if step_ms_profiled > 0 else None,
                 "events": {"kernel_ms": {names[i]: float(kms[i]) for i in (0, 1, 2, 4)},
                            "achieved": eval_bytes / (eval_ms_events * 1e-3) / 1e9,
@@ -412,20 +473,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded generator synth/, no dataset or weights)",
-                "config": {"workload": CONFIGS[cfg]["desc"], "walkers_per_gpu": W, "n": inst.n, "m": inst.m,
-                           "nnz": inst.nnz, "m_norm": P.m_norm, "nnz_with_cutoff": int(info.nnz_norm + info.nnz_cut),
-                           "non_fixed_vars": n_eval,
-                           "parallelism": f"walker portfolio x{world}: independent walkers per GPU, "
-                                          f"exchange (NCCL allgather) every {K_x} iterations",
-                           "exchanges_in_timed_region": n_exchanges,
-                           "cutoff": ("active from the start: c.x <= z* - delta, z* = c.x* of the instance's "
-                                      "planted feasible point (PAPER.md:373)" if z_star is not None else "none"),
-                           "l2": ("inputs larger than L2: A in CSC alone is "
-                                  f"{info.model_bytes_A / 1e6:.0f} MB vs 126 MB L2; no flush"
-                                  if info.model_bytes_A > 126e6 else
-                                  f"working set L2-resident (A in CSC {info.model_bytes_A / 1e6:.0f} MB + "
-                                  f"{W} walkers' state) and kept so on purpose: consecutive tabu "
-                                  "iterations reuse it, no flush; the HBM fraction is not the bound here")},
+                "config": config_dict(cfg, inst, W, world, z_star),
+                "workload_detail": {"m_norm": P.m_norm, "nnz_norm_with_cutoff": int(info.nnz_norm + info.nnz_cut),
+                           "non_fixed_vars": n_eval, "exchanges_in_timed_region": n_exchanges},
                 "tabu_iters_per_s": W * args.steps * world / sec,
                 # nonzeros visited per second (every nonzero incl. cutoff-row entries, per walker)
                 "nnz_visits_per_s": float(info.nnz_norm + info.nnz_cut) * W * args.steps * world / sec,

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CHAP_ABI_VERSION 1
+#define CHAP_ABI_VERSION 2
 
 typedef enum {
   CHAP_OK = 0,
@@ -73,17 +73,19 @@ typedef struct {
   double auto_cutoff_delta;   /* 1 if every c_j != 0 is integral on an integer variable, else
                                  NaN (= 1e-6 max(1,|z|) when the cutoff is set) (R14)         */
   int64_t device_bytes;       /* device memory held by the problem                            */
-  int64_t model_bytes_A;      /* algorithmic bytes of one pass over A in CSC:
-                                 12 (nnz_norm + nnz_cut) + 4 (n + 1)            */
-  int64_t model_bytes_pass;   /* algorithmic bytes of one best-shift pass of one walker: A in CSC,
-                                 static per-variable data (1 B binary, 17 B other), walker state
-                                 per variable (x̄: 1 bit binary / 8 B other; 4 B tabu expiry) and
-                                 12 B per normalised row (r f64 + w f32), each read once (§6)  */
-  int64_t model_bytes_kernel[3]; /* the same model split by eval kernel: [0] k_eval_bin (binary
-                                 columns), [1] k_eval_gen (general, empty and long bounded-
-                                 integer columns), [2] k_eval (sorted general columns and the
-                                 12 B/row row state)                                          */
-  int64_t nnz_kernel[3];      /* nonzeros (incl. cutoff entries) evaluated by each kernel      */
+  int64_t model_bytes_A;      /* algorithmic bytes of one pass over A in CSC (SURVEY §8(d)):
+                                 12 (nnz + nnz_cut) + 4 (n + 1), nnz = the ORIGINAL nonzeros
+                                 (a two-sided row's entry counts once)          */
+  int64_t model_bytes_pass;   /* algorithmic bytes of one best-shift pass of one walker (SURVEY
+                                 §8(d)): A in CSC as above, static per-variable data (1 B binary,
+                                 17 B other), walker state per variable (x̄: 1 bit binary / 8 B
+                                 other; 4 B tabu expiry) and 12 B per normalised row (r f64 +
+                                 w f32), each read once (§6)                                  */
+  int64_t model_bytes_kernel[3]; /* the same model split by column class: [0] packed binary
+                                 columns (k_eval_binrow / k_eval_bin), [1] long binary, general,
+                                 empty and long bounded-integer columns, [2] sorted general
+                                 columns and the 12 B/row row state                           */
+  int64_t nnz_kernel[3];      /* original nonzeros (incl. cutoff entries) of each class split  */
   int32_t eval_launches;      /* kernel launches of one best-shift pass (1-3: the eval kernels
                                  with work, k_eval always); a tabu iteration adds the apply   */
   int32_t pad_;
@@ -170,7 +172,13 @@ typedef struct {
   int32_t n_elite;       /* elite points exchanged per kind per rank (default 4)               */
   int32_t n_restart;     /* walkers restarted from the elite per exchange (default W_total/8)  */
   int32_t graph_iters;   /* iterations per captured CUDA graph in chap_tabu_step (default 16;
-                            0 = plain launches)                                               */
+                            0 = plain launches); a call's remainder runs as one more graph    */
+  int32_t binary_kernel; /* packed binary columns of a single walker: 0 = auto (row-wise kernel
+                            when the problem has >= 3e6 binary nonzeros and >= 0.7 entries per
+                            row per block), 1 = column-wise, 2 = row-wise (when the
+                            coefficients allow it: integers of magnitude <= 32767)            */
+  int32_t pdl;           /* 1 = launch the iteration's kernels with programmatic dependent launch
+                            (default 0: measured slower on config G)               */
 } chap_params;
 
 /* Fill *out with the defaults above (n_restart = -1 meaning W_total/8). */
@@ -209,7 +217,7 @@ chap_status chap_walkers_create(const chap_problem* p, int32_t W, const double* 
                                 const chap_params* params, void* cuda_stream, chap_walkers** out);
 
 /* n_iters tabu iterations of every walker, entirely on the device (CUDA graphs of
- * params.graph_iters iterations). One iteration: best shift of every variable (Alg. 1);
+ * params.graph_iters iterations, the remainder of n_iters as one more graph, kept for reuse). One iteration: best shift of every variable (Alg. 1);
  * select the admissible (tabu_until_j <= k) argmax s_j, ties lowest j (R6); if s* > 0 apply it
  * (x̄_j* <- x̂_j*, r_i += a_ij Δ over column j* — PAPER.md:343 — and tabu_until_j* = k+1+T),
  * else bump w_i <- min(w_i + 1, cap) on every active row with r_i > 0 (R12); then if no active

@@ -467,10 +467,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       nb = (nb + ncl - 1) / ncl * ncl;
       // where the row-wise kernel pays (measured on the X sweep): enough nonzeros to
       // amortise the cluster launch and the per-block reduction, and enough entries per row of a
-      // block that a warp's consecutive entries share row-state lines; CHAP_BINROW=0/1 overrides
+      // block that a warp's consecutive entries share row-state lines (chap_params.binary_kernel
+      // overrides the rule per walkers object)
       const double density = (double)tot / ((double)nb * std::max(1, m_norm));
-      ok = tot >= 3000000 && density >= 0.7;
-      if (const char* ev = getenv("CHAP_BINROW")) ok = ev[0] == '1';
+      P->binrow_auto = tot >= 3000000 && density >= 0.7;
     }
     if (ok) {
       std::vector<int32_t> cnt(m_norm + 2, 0);
@@ -534,18 +534,24 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       P->binrow_entries = (int64_t)rb_row.size();
     }
   }
-  {  // algorithmic-bytes model
+  {  // algorithmic-bytes model: 12 B per ORIGINAL nonzero (a two-sided
+     // row's entry counts once, R17) and per cutoff entry, whatever the kernels store or gather
+    std::vector<int32_t> odeg(n, 0);
+    for (int64_t e = 0; e < nnz; ++e) odeg[col_idx[e]] += (val[e] != 0.0);
+    for (int32_t j = 0; j < n; ++j) odeg[j] += (cc[j] != 0.0);
     int64_t mb[3] = {0, 0, 0}, nz[3] = {0, 0, 0}, mw[3] = {0, 0, 0};
     for (int32_t q = 0; q < n; ++q) {
       const int32_t j = perm[q];
       const int k = cls[j];
       if (k == CC_FIXED) continue;
-      const int kk = (k == CC_BIN || k == CC_LBIN) ? 0 : (k == CC_GENM ? 2 : 1);
+      // [0] packed binary columns, [1] long binary, general, empty and long bounded-integer
+      // columns, [2] sorted general columns and the row state
+      const int kk = (k == CC_BIN) ? 0 : (k == CC_GENM ? 2 : 1);
       const bool bin = vclass[j] == 1;
       const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
-      mb[kk] += 12LL * deg[j] + (int64_t)std::llround(per_var * 8) / 8;
+      mb[kk] += 12LL * odeg[j] + (int64_t)std::llround(per_var * 8) / 8;
       mw[kk] += (int64_t)std::llround(((bin ? 0.125 : 8.0) + 4.0) * 8) / 8;   // x̄, tabu
-      nz[kk] += deg[j];
+      nz[kk] += odeg[j];
     }
     mb[2] += 12LL * m_norm;   // the row state, read once per pass (attributed to the last kernel)
     mw[2] += 12LL * m_norm;
@@ -680,7 +686,11 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   CUDA_TRY(cudaMemset(P->e_tabu, 0, sizeof(int32_t) * std::max(n, 1)));
   CUDA_TRY(cudaDeviceSynchronize());
   I.device_bytes = (int64_t)B.bytes_total;
-  I.model_bytes_A = 12LL * nnz_total + 4LL * (n + 1);
+  {
+    int64_t nnz_orig = 0;
+    for (int64_t e = 0; e < nnz; ++e) nnz_orig += (val[e] != 0.0);
+    I.model_bytes_A = 12LL * (nnz_orig + nnz_cut) + 4LL * (n + 1);
+  }
   *out = holder.release();
   return CHAP_OK;
 }
@@ -969,6 +979,8 @@ extern "C" chap_status chap_params_default(chap_params* out) {
   out->n_elite = 4;
   out->n_restart = -1;
   out->graph_iters = 16;
+  out->binary_kernel = 0;
+  out->pdl = 0;
   return CHAP_OK;
 }
 
@@ -978,6 +990,8 @@ static chap_status check_params(const chap_params& q) {
   if (!std::isnan(q.cutoff_delta) && !(q.cutoff_delta >= 0.0 && std::isfinite(q.cutoff_delta)))
     return fail(CHAP_ERR_INVALID_ARG, "cutoff_delta must be NaN (auto) or finite >= 0");
   if (q.graph_iters < 0) return fail(CHAP_ERR_INVALID_ARG, "graph_iters < 0");
+  if (q.binary_kernel < 0 || q.binary_kernel > 2) return fail(CHAP_ERR_INVALID_ARG, "binary_kernel not in {0, 1, 2}");
+  if (q.pdl < 0 || q.pdl > 1) return fail(CHAP_ERR_INVALID_ARG, "pdl not in {0, 1}");
   return CHAP_OK;
 }
 
@@ -1022,20 +1036,20 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   S->gen_grid = p->gen_grid ? std::max(1, std::min(p->gen_grid, (p->gen_occ * p->sm_count + W - 1) / W)) : 0;
   // one walker with integral weights whose column sums fit int32: packed binary columns row-wise
   S->binrow_grid = 0;
-  if (W == 1 && p->binrow_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) &&
+  const bool want_row = prm.binary_kernel == 2 || (prm.binary_kernel == 0 && p->binrow_auto);
+  if (W == 1 && want_row && p->binrow_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) &&
       2.0 * (double)prm.weight_cap * (double)std::max(1, p->binrow_maxdeg) < 2147483647.0) {
     S->binrow_grid = p->binrow_grid;
     // the long binary chunks ride in k_eval_gen when it runs (with_lbin), else in k_eval_bin
     S->bin_grid = (S->gen_grid > 0) ? 0 : p->bin_chunk_grid;
     TRY(B.alloc(&Wk.xbits, (size_t)p->dp.n_rblocks * kRowWpb));   // block-ordered bitset
   }
-  // programmatic dependent launch between the iteration's kernels: measured slower on config G
-  // (0.1344 vs 0.1273 ms; early-scheduled k_eval_gen blocks disturb its persistent grid), so off
-  // unless CHAP_PDL=1
-  { const char* ev = getenv("CHAP_PDL"); S->pdl = ev && ev[0] == '1'; }
+  // programmatic dependent launch between the iteration's kernels (chap_params.pdl): measured
+  // slower on config G (0.1344 vs 0.1273 ms; early-scheduled k_eval_gen blocks disturb its
+  // persistent grid), so off by default
+  S->pdl = prm.pdl != 0;
   S->genwm_grid = 0;   // walker groups: integer general tiles and empty columns per group (k_eval_gen_wm)
-  const char* gw = getenv("CHAP_GENWM");   // experiment: lane-per-column general tiles for one walker
-  if ((rg > 1 || (gw && gw[0] == '1')) && p->dp.n_wtiles > 0) {
+  if (rg > 1 && p->dp.n_wtiles > 0) {
     const int occ = gen_wm_occupancy(rg, gen_wm_smem(std::max(1, p->gen_kmax)));
     if (occ > 0) {
       const int warps = kGenWmThreads / 32;
@@ -1099,6 +1113,21 @@ static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   return CHAP_OK;
 }
 
+// Capture `iters` tabu iterations of the walkers as one instantiated CUDA graph.
+static chap_status capture_iterations(chap_walkers* S, cudaStream_t s, int iters, cudaGraphExec_t* out) {
+  cudaGraph_t graph;
+  CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  chap_status st = CHAP_OK;
+  for (int it = 0; it < iters && st == CHAP_OK; ++it) st = launch_iteration(S, s);
+  cudaError_t ce = cudaStreamEndCapture(s, &graph);
+  if (st != CHAP_OK) return st;
+  if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+  return CHAP_OK;
+}
+
 extern "C" chap_status chap_tabu_step(chap_walkers* S, int32_t n_iters, chap_step_record* log,
                                       void* cuda_stream) {
   if (!S || n_iters < 0) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or n_iters < 0");
@@ -1112,23 +1141,31 @@ extern "C" chap_status chap_tabu_step(chap_walkers* S, int32_t n_iters, chap_ste
   CUDA_TRY(cudaGetLastError());
   const int gi = S->prm.graph_iters;
   int done = 0;
-  if (gi > 0 && n_iters >= gi) {
-    if (!S->gexec) {
-      cudaGraph_t graph;
-      CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      chap_status st = CHAP_OK;
-      for (int it = 0; it < gi && st == CHAP_OK; ++it) st = launch_iteration(S, s);
-      cudaError_t ce = cudaStreamEndCapture(s, &graph);
-      if (st != CHAP_OK) return st;
-      if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
-      ce = cudaGraphInstantiate(&S->gexec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
-      S->g_iters = gi;
+  if (gi > 0) {
+    // every iteration runs inside a CUDA graph: graphs of gi iterations, then one
+    // graph of the remainder (captured once per distinct remainder length and kept)
+    if (n_iters >= gi) {
+      if (!S->gexec) {
+        TRY(capture_iterations(S, s, gi, &S->gexec));
+        S->g_iters = gi;
+      }
+      while (n_iters - done >= S->g_iters) {
+        CUDA_TRY(cudaGraphLaunch(S->gexec, s));
+        done += S->g_iters;
+      }
     }
-    while (n_iters - done >= S->g_iters) {
-      CUDA_TRY(cudaGraphLaunch(S->gexec, s));
-      done += S->g_iters;
+    const int rem = n_iters - done;
+    if (rem > 0) {
+      if (S->gexec_rem && S->g_rem != rem) {
+        cudaGraphExecDestroy(S->gexec_rem);
+        S->gexec_rem = nullptr;
+      }
+      if (!S->gexec_rem) {
+        TRY(capture_iterations(S, s, rem, &S->gexec_rem));
+        S->g_rem = rem;
+      }
+      CUDA_TRY(cudaGraphLaunch(S->gexec_rem, s));
+      done += rem;
     }
   }
   for (; done < n_iters; ++done) TRY(launch_iteration(S, s));
@@ -1305,6 +1342,10 @@ extern "C" chap_status chap_walkers_timing(chap_walkers* S, int32_t mode, uint64
     if (S->gexec) {
       cudaGraphExecDestroy(S->gexec);
       S->gexec = nullptr;
+    }
+    if (S->gexec_rem) {
+      cudaGraphExecDestroy(S->gexec_rem);
+      S->gexec_rem = nullptr;
     }
   }
   return CHAP_OK;

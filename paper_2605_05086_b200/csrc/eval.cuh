@@ -146,11 +146,7 @@ struct Elem {
 // exactly; the guard also keeps zero/inf numerators off the IEEE division's slow path.
 __device__ __forceinline__ double breakpoint(double xb, double r, double a) {
   const bool plain = r != 0.0 && isfinite(r);
-#ifdef CHAP_EXP_NODIV
-  const double q = (plain ? r : 1.0) * a;
-#else
   const double q = (plain ? r : 1.0) / a;
-#endif
   return plain ? xb - q : xb;
 }
 
@@ -1116,11 +1112,7 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
   }
   __syncwarp();
   // (2) one work item per lane
-#ifdef CHAP_EXP_SKIP2
-  for (int i0 = 0; i0 < 0; i0 += 32) {
-#else
   for (int i0 = 0; i0 < n_items; i0 += 32) {
-#endif
     const int I = i0 + lane;
     // the item's column: the last column c with ip_c <= I (ip is nondecreasing over the lanes)
     int c = 0;
@@ -1187,11 +1179,7 @@ __device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __re
     if (fast) {
       const float lf = isfinite(l) ? (float)l : -INFINITY, uf = isfinite(u) ? (float)u : INFINITY;
       float bf = 0.f, af = 0.f, plf = 0.f, puf = 0.f;
-#ifdef CHAP_EXP_SKIP3
-      for (int e = cb; e < cb; ++e) {
-#else
       for (int e = cb; e < ce; ++e) {
-#endif
         const float2 ab = S.AB[e];
         const float ke = S.kf[e], de = S.D[e];
         bf += ab.x;
@@ -1462,12 +1450,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
       lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
     t -= P.n_bchunks;
   }
-#ifdef CHAP_EXP_SKIPLBKT
-  for (; t < P.n_gchunks; t += nwarps) continue;
-  for (; false;)
-#else
   for (; t < P.n_gchunks; t += nwarps)
-#endif
     lbkt_chunk(P, Wk, walker, X, RS, st, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
   __syncwarp();
   t -= P.n_gchunks;
@@ -1478,9 +1461,6 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     const WTile T = Tn;
     if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];
     if (T.kind == CC_GEN) {
-#ifdef CHAP_EXP_SKIPTILES
-      continue;
-#endif
       if (!wm_mode || T.pad) gen_tile(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
     } else if (!wm_mode) {
       wtile_empty(P, C, T, lane, b);

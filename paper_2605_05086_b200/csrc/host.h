@@ -96,6 +96,7 @@ struct chap_problem {
   int gen_occ = 1;
   int gen_grid = 0;            // k_eval_gen blocks for one walker
   int binrow_grid = 0;         // k_eval_binrow CTAs (clusters x kRowCluster; 0: no row-wise blocks)
+  bool binrow_auto = false;    // the size rule chooses the row-wise binary kernel (chap_params.binary_kernel 0)
   int gen_kmax = 0;            // longest packed general column (entries incl. padding)
   int binrow_maxdeg = 0;       // longest packed binary column (incl. its cutoff entry)
   int binrow_cluster = 0;      // CTAs per cluster of k_eval_binrow
@@ -145,8 +146,10 @@ struct chap_walkers {
   chap_exchange_state* xs = nullptr;   // portfolio exchange buffers and state (portfolio.cuh)
   cudaStream_t stream = nullptr;       // internal stream (graph capture / launch)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t gexec = nullptr;      // graph of g_iters iterations
   int g_iters = 0;
+  cudaGraphExec_t gexec_rem = nullptr;  // graph of g_rem iterations (the remainder of a call)
+  int g_rem = 0;
   int apply_grid = 1;
   int eval_grid = 1;           // k_eval blocks per walker
   int bin_grid = 0;            // k_eval_bin blocks per walker
@@ -158,6 +161,7 @@ struct chap_walkers {
   ~chap_walkers() {
     if (xs) chap_exchange_state_free(xs);
     if (gexec) cudaGraphExecDestroy(gexec);
+    if (gexec_rem) cudaGraphExecDestroy(gexec_rem);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (stream) cudaStreamDestroy(stream);

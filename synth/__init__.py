@@ -287,6 +287,16 @@ def x_bernoulli(inst: Instance, key, p: float = 0.5) -> np.ndarray:
     return np.clip(x, inst.lb, inst.ub)
 
 
+def x_perturbed(inst: Instance, key, frac: float = 0.01) -> np.ndarray:
+    """x_lower with a fraction `frac` of the variables (chosen keyed by `key`) raised by one unit
+    where the upper bound allows it: a start point per weak-scaling replica."""
+    rng = np.random.default_rng(list(key))
+    x = x_lower(inst)
+    up = (rng.random(inst.n) < frac) & (x + 1.0 <= inst.ub)
+    x[up] += 1.0
+    return x
+
+
 def x_random(inst: Instance, seed: int, spread: int = 10) -> np.ndarray:
     """Random in-bounds point, integral on integer variables (an evaluation point for parity)."""
     rng = np.random.default_rng([0xE7, seed])

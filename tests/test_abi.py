@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     import paper_2605_05086_b200 as chap
     assert set(declared) <= set(chap.EXPORTED)
-    assert chap.chap_abi_version() == 1
+    assert chap.chap_abi_version() == 2
     assert chap.chap_status_string(7) == b"CHAP_ERR_UNSUPPORTED"
 
 
@@ -39,6 +39,7 @@ def test_struct_sizes_match_header():
     assert ctypes.sizeof(chap.chap_walker_stats) == 64
     p = chap.default_params()
     assert (p.tenure, p.weight_cap, p.exchange_K, p.n_elite, p.n_restart) == (10, 1e6, 1000, 4, -1)
+    assert (p.graph_iters, p.binary_kernel, p.pdl) == (16, 0, 0)
 
 
 def test_invalid_args_fail_loudly_without_gpu():

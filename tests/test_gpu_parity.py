@@ -189,10 +189,11 @@ def test_host_buffer_variant_equals_device():
     assert mh.tobytes() == chap.move_from_bytes(md).tobytes()
 
 
-def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10):
+def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10, binary_kernel=0):
     P = chap.Problem.from_instance(inst)
     O = oracle.Problem.from_instance(inst)
-    prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure)
+    prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure,
+                              binary_kernel=binary_kernel)
     oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap)
     X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
     Wk = chap.Walkers(P, X0, prm)
@@ -220,20 +221,17 @@ def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e
     return log
 
 
-@pytest.fixture(params=["auto", "1"], ids=["binrow_auto", "binrow_forced"])
-def binrow(request, monkeypatch):
-    """The row-wise binary kernel is chosen by size (chap.cu); "1" forces it on small instances."""
-    if request.param == "1":
-        monkeypatch.setenv("CHAP_BINROW", "1")
-    else:
-        monkeypatch.delenv("CHAP_BINROW", raising=False)
+@pytest.fixture(params=[0, 2, 1], ids=["binrow_auto", "binrow_forced", "colwise_forced"])
+def binrow(request):
+    """chap_params.binary_kernel: 0 = the size rule (chap.cu), 2 = the row-wise kernel forced on
+    small instances, 1 = the column-wise kernel forced."""
     return request.param
 
 
 @pytest.mark.parametrize("seed", range(8))
 def test_trajectory_config_T(seed, binrow):
     inst = synth.tiny(seed)
-    _traj_compare(inst, [synth.x_lower(inst)], 600, graph_iters=16 if seed % 2 else 0)
+    _traj_compare(inst, [synth.x_lower(inst)], 600, graph_iters=16 if seed % 2 else 0, binary_kernel=binrow)
 
 
 def test_trajectory_multi_walker():
@@ -244,12 +242,12 @@ def test_trajectory_multi_walker():
 
 def test_trajectory_mixed_small(binrow):
     inst = synth.mixed(seed=9, n=4000, m=800, n_long=4, long_lo=300, long_hi=6000)
-    _traj_compare(inst, [synth.x_lower(inst), synth.x_random(inst, 1)], 60)
+    _traj_compare(inst, [synth.x_lower(inst), synth.x_random(inst, 1)], 60, binary_kernel=binrow)
 
 
 def test_trajectory_setcover_small(binrow):
     inst = synth.setcover(seed=4, m=500, n=2500)
-    _traj_compare(inst, [synth.x_lower(inst)], 400)
+    _traj_compare(inst, [synth.x_lower(inst)], 400, binary_kernel=binrow)
 
 
 @pytest.mark.parametrize("W", [3, 17, 33])
@@ -282,15 +280,14 @@ def test_trajectory_weight_cap(cap, binrow):
     """Weights reach the cap: an integral cap keeps the row-wise binary kernel (k_eval_binrow), a
     fractional one (weights 3.5, half-integral penalties) takes the column-wise kernel."""
     inst = synth.setcover(seed=6, m=400, n=2000)
-    _traj_compare(inst, [synth.x_lower(inst)], 300, weight_cap=cap, tenure=3)
+    _traj_compare(inst, [synth.x_lower(inst)], 300, weight_cap=cap, tenure=3, binary_kernel=binrow)
 
 
-def test_trajectory_rowwise_two_rounds(monkeypatch):
+def test_trajectory_rowwise_two_rounds():
     """Generator X at 2·10^7 requested nonzeros: ~1.4 M packed binary columns, more than one round
     of k_eval_binrow blocks per cluster (forced on); 6 iterations of one walker vs the oracle."""
-    monkeypatch.setenv("CHAP_BINROW", "1")
     inst = synth.scaled(20_000_000)
-    _traj_compare(inst, [synth.x_lower(inst)], 6)
+    _traj_compare(inst, [synth.x_lower(inst)], 6, binary_kernel=2)
 
 
 def test_invalid_x0_rejected():
@@ -312,7 +309,8 @@ def test_single_walker_restart_matches_oracle(binrow):
     O = oracle.Problem.from_instance(inst)
     x0 = synth.x_lower(inst)
     x1 = synth.x_bernoulli(inst, (8, 1), 0.3)
-    Wk = chap.Walkers(P, torch.from_numpy(x0[None, :]).cuda(), chap.default_params(graph_iters=16))
+    Wk = chap.Walkers(P, torch.from_numpy(x0[None, :]).cuda(),
+                      chap.default_params(graph_iters=16, binary_kernel=binrow))
     ow = oracle.TabuWalker(O, x0)
     for step in range(2):
         log = chap.records(Wk.step(60, log=True))

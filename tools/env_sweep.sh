@@ -1,5 +1,5 @@
 #!/bin/bash
-# bench ms/step of alternative libchap builds (swapped in place) or env settings:
+# bench ms/step of alternative libchap builds (swapped in place):
 #   tools/env_sweep.sh CFG lib1.so lib2.so ...
 CFG=$1; shift
 cp paper_2605_05086_b200/libchap.so /tmp/libchap_keep.so
