@@ -88,7 +88,9 @@ typedef struct {
   int64_t nnz_kernel[3];      /* original nonzeros (incl. cutoff entries) of each class split  */
   int32_t eval_launches;      /* kernel launches of one best-shift pass (1-3: the eval kernels
                                  with work, k_eval always); a tabu iteration adds the apply   */
-  int32_t pad_;
+  int32_t n_sorted_columns;   /* general columns whose breakpoints are sorted (line 13) rather
+                                 than prefix-summed or bucket-counted: non-bucketable columns
+                                 with more than 62 nonzeros                     */
   int64_t model_bytes_walker_kernel[3]; /* the per-walker part of model_bytes_kernel (x̄, tabu
                                  expiry, row state); the rest (A in CSC, static per-variable
                                  data) is read once by a batched pass of W walkers, whose model
@@ -135,10 +137,13 @@ typedef struct {
 } chap_move;   /* 24 bytes */
 
 /* Eq. (1) for every variable at the point x, by Algorithm 1:
- *   x      DEVICE [n] float64: within bounds, integral on integer variables (not checked here;
- *          a violating x gives unspecified scores)
+ *   x      DEVICE [n] float64: within bounds, integral on integer variables
  *   w      DEVICE [m_norm] float32 weights >= 0 (NULL = all 1); w[m_norm-1] is the cutoff
  *          row's weight. Scores are exact when weights are integers <= 2^24 (R11).
+ *          x and w are validated on the device during the call: an x out of bounds or
+ *          fractional on an integer variable, or a negative or NaN weight (negative weights break
+ *          Algorithm 1's monotone prefixes), returns CHAP_ERR_INVALID_ARG after the
+ *          stream is synchronised (the outputs are then unspecified).
  *   cutoff_rhs  +INF = cutoff row inactive; finite = the row c.x <= cutoff_rhs is scored
  *   xhat, score DEVICE [n] float64 outputs (either may be NULL): the best shift x̂_j and its raw
  *          maximum score s_j over the candidate set {finite bounds} ∪ {breakpoints} within
@@ -146,8 +151,8 @@ typedef struct {
  *          A variable without candidates (fixed) reports (x̄_j, -INF). s_j may be <= 0 (R7).
  *   best   DEVICE [1] chap_move out (may be NULL): argmax of s_j over s_j > 0, ties -> lowest j
  *          (R6); j = -1 if none.
- * Stream-ordered on cuda_stream; uses the problem's internal workspace, so calls on one
- * problem must not overlap. */
+ * Runs on cuda_stream and synchronises it before returning (to report the validation); uses the
+ * problem's internal workspace, so calls on one problem must not overlap. */
 chap_status chap_eval_best_shift(const chap_problem* p, const double* x, const float* w,
                                  double cutoff_rhs, double* xhat, double* score, chap_move* best,
                                  void* cuda_stream);
@@ -237,7 +242,9 @@ chap_status chap_walkers_get(const chap_walkers* ws, double* x, double* r, float
  * above z_best - delta gets rhs = z_best - delta (residual recomputed). Stream-ordered. */
 chap_status chap_walkers_set_cutoff(chap_walkers* ws, double z_best, void* cuda_stream);
 /* Restart walker `walker` from x DEVICE [n] (user order): residuals recomputed from scratch,
- * weights kept, tabu cleared (SURVEY §8(e) restart rule). Stream-ordered. */
+ * weights kept, tabu cleared (SURVEY §8(e) restart rule). x is validated first (synchronising the
+ * stream): out of bounds or fractional on an integer variable -> CHAP_ERR_INVALID_ARG with the
+ * walker untouched. */
 chap_status chap_walkers_restart(chap_walkers* ws, int32_t walker, const double* x,
                                  void* cuda_stream);
 chap_status chap_walkers_destroy(chap_walkers* ws);

@@ -398,6 +398,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     ++p;
   }
   I.n_long_columns = n_long;
+  I.n_sorted_columns = 0;
+  for (int32_t j = 0; j < n; ++j) I.n_sorted_columns += (cls[j] == CC_GENM);
   // row-wise binary blocks (k_eval_binrow): packed binary columns [pb0, pb1) in blocks of <=
   // kRowVmax columns balanced by nonzeros, a multiple of the resident clusters; each block's
   // entries sorted by row, cut into kRowCluster slices padded to multiples of 4 with inert entries
@@ -679,6 +681,9 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.alloc(&P->e_sc, 1));
   TRY(B.alloc(&P->e_part, P->eval_grid + P->bin_grid + P->gen_grid));
   TRY(B.alloc(&P->e_selcnt, 1));
+  TRY(B.alloc(&P->e_bad, 1));
+  CUDA_TRY(cudaMallocHost(&P->h_bad, sizeof(int)));
+  *P->h_bad = 0;
   CUDA_TRY(cudaMemset(P->e_selcnt, 0, sizeof(unsigned)));
   TRY(B.alloc(&P->e_lscr, P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_sc, 0, sizeof(WalkerScalars)));
@@ -884,10 +889,39 @@ chap_status chap::walker_recompute(const chap_problem* P, DevWalkers& Wk, int w,
   k_acc_zero<<<1, 1, 0, s>>>(Wk.sc, w);
   if (D.n > 0)
     k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, w);
-  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk, 0, nullptr, w);
+  k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk, 0, nullptr, w, nullptr);
   k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk, w);
   if (Wk.xbits && D.n > 0) k_xbits_build<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(D, Wk, w);
   CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+// The launches of one eval call; the validation flag (x out of bounds or fractional on an integer
+// variable, a negative or NaN weight) is copied to the problem's pinned h_bad, to be read after
+// the stream is synchronised.
+static chap_status eval_launch(const chap_problem* p, const double* x, const float* w, double cutoff_rhs,
+                               double* xhat, double* score, chap_move* best, cudaStream_t s) {
+  const DevProblem& D = p->dp;
+  DevWalkers Wk = eval_walkers(p);
+  CUDA_TRY(cudaMemsetAsync(p->e_bad, 0, sizeof(int), s));
+  k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs);
+  if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, p->e_bad);
+  if (cutoff_rhs < INFINITY && D.n > 0)
+    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1);
+  k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, Wk, 2, w, 0, p->e_bad);
+  CUDA_TRY(cudaGetLastError());
+  if (D.n_fixed > 0 && (xhat || score))
+    k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s, false));
+  CUDA_TRY(cudaMemcpyAsync(p->h_bad, p->e_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+static chap_status eval_check(const chap_problem* p) {
+  if (*p->h_bad)
+    return fail(CHAP_ERR_INVALID_ARG, "x out of bounds or fractional on an integer variable, or a weight < 0 / NaN "
+                                      "(outputs unspecified)");
   return CHAP_OK;
 }
 
@@ -898,25 +932,16 @@ extern "C" chap_status chap_eval_best_shift(const chap_problem* p, const double*
   if (std::isnan(cutoff_rhs) || cutoff_rhs == -INFINITY) return fail(CHAP_ERR_INVALID_ARG, "cutoff_rhs must be finite or +INF");
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  const DevProblem& D = p->dp;
-  DevWalkers Wk = eval_walkers(p);
-  k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs);
-  if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, nullptr);
-  if (cutoff_rhs < INFINITY && D.n > 0)
-    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1);
-  k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, Wk, 2, w, 0);
-  CUDA_TRY(cudaGetLastError());
-  if (D.n_fixed > 0 && (xhat || score))
-    k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s, false));
-  CUDA_TRY(cudaGetLastError());
-  return CHAP_OK;
+  TRY(eval_launch(p, x, w, cutoff_rhs, xhat, score, best, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return eval_check(p);
 }
 
 extern "C" chap_status chap_eval_best_shift_host(chap_problem* p, const double* x, const float* w,
                                                  double cutoff_rhs, double* xhat, double* score,
                                                  chap_move* best, void* cuda_stream) {
   if (!p || (!x && p->dp.n > 0)) return fail(CHAP_ERR_INVALID_ARG, "NULL problem or x");
+  if (std::isnan(cutoff_rhs) || cutoff_rhs == -INFINITY) return fail(CHAP_ERR_INVALID_ARG, "cutoff_rhs must be finite or +INF");
   DeviceGuard g(p->device);
   const int n = p->dp.n, mn = p->dp.m_norm;
   cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -953,14 +978,15 @@ extern "C" chap_status chap_eval_best_shift_host(chap_problem* p, const double* 
     }
     CUDA_TRY(cudaMemcpyAsync(p->d_wu, hw, sizeof(float) * mn, cudaMemcpyHostToDevice, s));
   }
-  TRY(chap_eval_best_shift(p, p->d_xu, w ? p->d_wu : nullptr, cutoff_rhs, xhat ? p->d_out : nullptr,
-                           score ? p->d_out + n : nullptr, best ? p->d_best : nullptr, cuda_stream));
+  TRY(eval_launch(p, p->d_xu, w ? p->d_wu : nullptr, cutoff_rhs, xhat ? p->d_out : nullptr,
+                  score ? p->d_out + n : nullptr, best ? p->d_best : nullptr, s));
   const bool px = pinned(xhat), ps = pinned(score);
   if (xhat) CUDA_TRY(cudaMemcpyAsync(px ? xhat : p->h_out, p->d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   if (score)
     CUDA_TRY(cudaMemcpyAsync(ps ? score : p->h_out + n, p->d_out + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   if (best) CUDA_TRY(cudaMemcpyAsync(p->h_best, p->d_best, sizeof(chap_move), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  TRY(eval_check(p));
   if (xhat && !px) memcpy(xhat, p->h_out, sizeof(double) * n);
   if (score && !ps) memcpy(score, p->h_out + n, sizeof(double) * n);
   if (best) *best = *p->h_best;
@@ -1085,7 +1111,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
     k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
   k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1);
   if (D.n > 0) k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, -1);
-  k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk, 1, nullptr, -1);
+  k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk, 1, nullptr, -1, nullptr);
   k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk, -1);
   if (Wk.xbits && D.n > 0)
     k_xbits_build<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), Wk.n_groups), 256, 0, s>>>(D, Wk, -1);
@@ -1212,6 +1238,14 @@ extern "C" chap_status chap_walkers_restart(chap_walkers* S, int32_t walker, con
   DevWalkers& Wk = S->wk;
   const int gx = grid_for(D.n, 256, 4 * S->P->sm_count);
   // write into walker `walker` only: offset the destinations
+  // the point is validated first (in bounds, integral on integer variables): an invalid x leaves the
+  // walker untouched
+  CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
+  if (D.n > 0) k_check_point<<<dim3(gx, 1), 256, 0, s>>>(D, x, S->d_bad);
+  int bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, S->d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (bad) return fail(CHAP_ERR_INVALID_ARG, "restart point out of bounds or fractional on an integer variable");
   if (D.n > 0) k_permute_in<<<dim3(gx, 1), 256, 0, s>>>(D, x, D.n, Wk.x + (size_t)walker * Wk.xs, Wk.xs, nullptr);
   TRY(chap::walker_recompute(S->P, Wk, walker, s));
   k_tabu_clear<<<dim3(gx, 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, walker);

@@ -113,6 +113,8 @@ struct chap_problem {
   WalkerScalars* e_sc = nullptr;
   Cand* e_part = nullptr;
   unsigned* e_selcnt = nullptr;
+  int* e_bad = nullptr;         // eval-call validation flag (device) and its pinned host copy
+  int* h_bad = nullptr;
   double* e_lscr = nullptr;
   // host-buffer variant staging (lazy)
   double* h_x = nullptr;
@@ -128,6 +130,7 @@ struct chap_problem {
     if (h_w) cudaFreeHost(h_w);
     if (h_out) cudaFreeHost(h_out);
     if (h_best) cudaFreeHost(h_best);
+    if (h_bad) cudaFreeHost(h_bad);
   }
 };
 

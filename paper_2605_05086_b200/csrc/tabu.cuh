@@ -19,13 +19,22 @@ __global__ void k_permute_in(DevProblem P, const double* __restrict__ xu, size_t
   }
 }
 
+// Flags a user-order point that is out of bounds or fractional on an integer variable.
+__global__ void k_check_point(DevProblem P, const double* __restrict__ xu, int* bad) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) {
+    const double v = xu[P.perm[p]];
+    const bool ok = (v >= P.lb[p]) && (v <= P.ub[p]) && (P.vclass[p] == 3 || v == floor(v));
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+
 // r_i = Σ_k a_ik x̄_k - b_i from scratch (warp per row, CSR). The cutoff row (last) is active
 // iff sc[w].cut_active (rhs sc[w].cutoff_rhs); an inactive cutoff row is stored inert, r = -inf
 // and w = 0, so that it contributes nothing to any score without a per-nonzero test (its logical
 // weight while inactive is the initial 1: bumps skip inactive rows). init_w: 0 keep weights,
 // 1 set to 1, 2 copy from wsrc (eval API).
 __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float* __restrict__ wsrc,
-                            int only_walker) {
+                            int only_walker, int* bad) {
   const int w = only_walker >= 0 ? only_walker : blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -46,6 +55,7 @@ __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float
         s.r = sc[w].cut_active ? sc[w].cdot - sc[w].cutoff_rhs : -INFINITY;
         if (init_w == 1) s.w = 1.0f;
         else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
+        if (init_w == 2 && bad && !(s.w >= 0.0f)) atomicOr(bad, 1);   // weights must be >= 0 (R11)
         if (!sc[w].cut_active) s.w = 0.0f;
         s.pad = 0;
         rw[i] = s;
@@ -68,6 +78,7 @@ __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float
       s.r = r;
       if (init_w == 1) s.w = 1.0f;
       else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
+      if (init_w == 2 && bad && !(s.w >= 0.0f)) atomicOr(bad, 1);
       if (i == P.cut_row && !sc[w].cut_active) s.w = 0.0f;
       s.pad = 0;
       rw[i] = s;

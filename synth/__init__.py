@@ -169,9 +169,20 @@ def setcover(seed: int = 1, m: int = 10_000, n: int = 50_000) -> Instance:
 # --------------------------------------------------------------------------------------
 # Config G (configs[2]): mixed general-integer MIP, 2e5 rows x 1e6 vars, ~1e7 nnz, 100 long columns
 # --------------------------------------------------------------------------------------
+LONG_KINDS = {
+    "bin": "binary",
+    "bkt": "integer [0, 64] (bounded domain: counting sort)",
+    "unb": "integer [0, inf) (unbounded: sorted)",
+    "big": "integer [0, 10000] (domain > 4096: sorted)",
+    "cont": "continuous [0, 50] (sorted; tolerance mode)",
+}
+
+
 def mixed(seed: int = 2, n: int = 1_000_000, m: int = 200_000, n_long: int = 100,
           long_lo: float = 1e3, long_hi: float = 1e5, short_mean: float = 7.0,
-          p_binary: float = 0.70, p_bounded: float = 0.25) -> Instance:
+          p_binary: float = 0.70, p_bounded: float = 0.25, long_kinds=("bin", "bkt")) -> Instance:
+    """Config G's generator. The long columns are split into equal consecutive groups, one per
+    entry of `long_kinds` (LONG_KINDS); the default (50 binary + 50 integer [0, 64]) is config G."""
     rng = np.random.default_rng([0x6E, seed])
     # variable classes: 70% binary, 25% integer [0, U] with U log-uniform{2..1000}, 5% integer [0, inf)
     u = rng.random(n)
@@ -181,12 +192,13 @@ def mixed(seed: int = 2, n: int = 1_000_000, m: int = 200_000, n_long: int = 100
     ub = np.where(vclass == 0, 1.0, np.where(vclass == 1, U, INF))
     # long columns: 50 binary + 50 integer [0, 64]; unbounded integers only on short columns
     long_idx = rng.choice(n, size=n_long, replace=False)
-    half = n_long // 2
-    vclass[long_idx[:half]] = 0
-    ub[long_idx[:half]] = 1.0
-    vclass[long_idx[half:]] = 1
-    ub[long_idx[half:]] = 64.0
     is_int = np.ones(n, dtype=np.uint8)
+    for q, j in enumerate(long_idx):
+        kind = long_kinds[q * len(long_kinds) // n_long]
+        vclass[j], ub[j] = {"bin": (0, 1.0), "bkt": (1, 64.0), "unb": (2, INF), "big": (1, 10000.0),
+                            "cont": (1, 50.0)}[kind]
+        if kind == "cont":
+            is_int[j] = 0
     deg = 1 + rng.poisson(short_mean, n)
     deg[long_idx] = 0
     rows, cols = _columns_to_coo(rng, m, deg)

@@ -375,3 +375,102 @@ def test_continuous_columns_tolerance_mode():
             n_cmp += 1
         n_ok += 1
     assert n_ok > 100 and n_cmp > 200
+
+
+def _sorted_mix(seed=7, kinds=("unb", "big", "bkt", "bin"), n_long=16, hi=2000):
+    """Long general columns that are neither binary nor a bounded domain of <= 4096 values:
+    unbounded integers [0, inf) and large-domain integers [0, 10000] with 100..2000 nonzeros
+    (the sorted class), beside long binary and bounded-integer columns."""
+    return synth.mixed(seed=seed, n=20_000, m=4_000, n_long=n_long, long_lo=100, long_hi=hi, long_kinds=kinds)
+
+
+def test_sorted_columns_eval():
+    inst = _sorted_mix()
+    P = chap.Problem.from_instance(inst)
+    assert P.info.n_sorted_columns >= 6, P.info.n_sorted_columns
+    for s in range(4):
+        x = synth.x_random(inst, 20 + s, spread=40)
+        w = synth.weights_random(P.m_norm, s, hi=7)
+        cut = math.inf if s == 0 else float(inst.c @ x) - 50.0
+        g, o = _eval_both(inst, x, w, cut, P=P)
+        _assert_same(g, o, f"sorted s={s}")
+
+
+def test_sorted_columns_trajectory(binrow):
+    inst = _sorted_mix(seed=8)
+    assert chap.Problem.from_instance(inst).info.n_sorted_columns >= 6
+    _traj_compare(inst, [synth.x_lower(inst), synth.x_random(inst, 3, spread=30)], 80, binary_kernel=binrow)
+
+
+def test_sorted_continuous_columns_tolerance_mode():
+    """Long continuous columns (sorted class) in tolerance mode: each long continuous column and a
+    sample of the others against Algorithm 1 in exact rational arithmetic (tests/exact.alg1) on the
+    same double inputs, scores and values within 1e-9 relative."""
+    inst = _sorted_mix(seed=9, kinds=("cont", "unb"), n_long=8)
+    P = chap.Problem.from_instance(inst)
+    assert P.info.n_sorted_columns >= 4 and P.info.n_continuous >= 4
+    x = synth.x_random(inst, 5, spread=20)
+    w = synth.weights_random(P.m_norm, 5, hi=5)
+    cut = float(inst.c @ x) - 20.0
+    gx, gs, _ = P.eval_best_shift(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), cut)
+    torch.cuda.synchronize()
+    gx, gs = gx.cpu().numpy(), gs.cpu().numpy()
+    from fractions import Fraction as Fr
+    rows = exact.normalized_rows(inst)
+    rows.append(({j: Fr(float(inst.c[j])) for j in range(inst.n) if inst.c[j] != 0}, Fr(cut), -1, +1))
+    assert len(rows) == P.m_norm
+    lb, ub = exact.bounds(inst)
+    deg = np.bincount(inst.col_idx, minlength=inst.n)
+    long_cols = np.nonzero(deg > 62)[0]
+    rng = np.random.default_rng(0)
+    sample = np.concatenate([long_cols, rng.choice(inst.n, 150, replace=False)])
+    cols = {j: [] for j in sample}
+    for i, (a, _, _, _) in enumerate(rows):
+        for j in a:
+            if j in cols:
+                cols[j].append(i)
+    r = exact.residuals(rows, x)
+    for j in sample:
+        if lb[j] == ub[j]:
+            continue
+        sub = [rows[i] for i in cols[j]]
+        v, sc = exact.alg1(sub, [r[i] for i in cols[j]], x, w[cols[j]], j, lb[j], ub[j], bool(inst.is_int[j]))
+        if sc is None:
+            assert gs[j] == -math.inf, j
+            continue
+        assert abs(gs[j] - float(sc)) <= 1e-9 * max(1.0, abs(float(sc))), (j, gs[j], float(sc))
+        assert abs(gx[j] - float(v)) <= 1e-9 * max(1.0, abs(float(v))), (j, gx[j], float(v))
+
+
+def test_eval_rejects_negative_weights_and_bad_x():
+    """chap_eval_best_shift returns CHAP_ERR_INVALID_ARG for w < 0 (negative weights
+    break Algorithm 1) and for an x out of bounds or fractional on an integer variable; the restart
+    entry point rejects such a point and leaves the walker untouched."""
+    inst = synth.tiny(2)
+    P = chap.Problem.from_instance(inst)
+    x = synth.x_lower(inst)
+    w = np.ones(P.m_norm, np.float32)
+    P.eval_best_shift(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda())
+    w[3] = -1.0
+    with pytest.raises(chap.ChapError) as e:
+        P.eval_best_shift(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda())
+    assert e.value.status == 1
+    with pytest.raises(chap.ChapError) as e:
+        P.eval_best_shift_host(x, w)
+    assert e.value.status == 1
+    for bad in (0.5, -1.0, 99.0):
+        xb = x.copy()
+        xb[35] = bad   # integer variable in [0, 7]
+        with pytest.raises(chap.ChapError) as e:
+            P.eval_best_shift(torch.from_numpy(xb).cuda())
+        assert e.value.status == 1
+    Wk = chap.Walkers(P, torch.from_numpy(x[None, :]).cuda())
+    Wk.step(5)
+    before = Wk.get()
+    xb = x.copy()
+    xb[35] = 0.5
+    with pytest.raises(chap.ChapError) as e:
+        Wk.restart(0, torch.from_numpy(xb).cuda())
+    assert e.value.status == 1
+    after = Wk.get()
+    assert np.array_equal(before["x"], after["x"]) and np.array_equal(before["r"], after["r"])

@@ -162,3 +162,72 @@ def test_tabu_never_beats_highs_optimum():
             assert all(v <= 0 for v in exact.residuals(rows, list(W.best_x)))
             assert float(inst.c @ W.best_x) == W.best_obj
     assert found >= 6
+
+
+def _check_records(log, exp_records):
+    for rec, exp in zip(log, exp_records):
+        assert rec["k"] == exp["k"] and rec["j"] == exp["j"], (rec, exp)
+        if exp["j"] >= 0:
+            assert rec["v"] == exp["v"]
+        else:
+            assert math.isnan(rec["v"])
+        s = -math.inf if exp["s"] == "-inf" else exp["s"]
+        assert rec["s"] == s and rec["violated"] == exp["violated"] and rec["obj"] == exp["obj"], (rec, exp)
+
+
+def test_trajectory_2var_weight_cap_golden():
+    """The weight-cap clamp w <- min(w + 1, cap) (R12): a hand-worked 16-step trajectory with cap 3
+    in which the cutoff row's weight (k = 3) and then the row's weight (k = 14) reach the cap."""
+    g = json.load(open(os.path.join(GOLD, "trajectory_2var_cap3.json")))
+    inst = exact.rows_from_json(g)
+    P = oracle.Problem.from_instance(inst)
+    W = oracle.TabuWalker(P, np.array(g["x0"], float),
+                          oracle.TabuParams(tenure=g["tenure"], weight_cap=g["weight_cap"]))
+    recs = g["records"]
+    log = W.run(4)
+    _check_records(log, recs[:4])
+    assert list(W.w) == [1.0, 3.0]          # cutoff weight at the cap after k = 3
+    log = np.concatenate([log, W.run(len(recs) - 4)])
+    _check_records(log, recs)
+    assert list(W.w) == g["final_w"] and W.best_obj == g["best_obj"]
+
+
+def test_cutoff_delta_fractional_objective_golden():
+    """The non-integral cutoff delta (R14): 1e-6 * max(1, |z|), both branches of the max (z = 0 at
+    the start, z = -2.5 after the first move), hand-derived."""
+    g = json.load(open(os.path.join(GOLD, "cutoff_delta_fractional.json")))
+    inst = exact.rows_from_json(g)
+    P = oracle.Problem.from_instance(inst)
+    assert math.isnan(P.auto_delta)
+    W = oracle.TabuWalker(P, np.array(g["x0"], float), oracle.TabuParams(tenure=g["tenure"]))
+    st = g["steps"]
+    assert W.has_incumbent and W.best_obj == 0.0
+    assert abs(W.cutoff_rhs - st[0]["cutoff_rhs"]) <= 1e-15
+    for exp in st[1:]:
+        rec = W.run(1)[0]
+        _check_records([rec], [dict(exp, k=int(exp["after"][2:]))])
+        assert abs(W.cutoff_rhs - exp["cutoff_rhs"]) <= 1e-15 * abs(exp["cutoff_rhs"])
+        if "w_cut" in exp:
+            assert W.w[-1] == exp["w_cut"]
+    assert W.best_obj == -2.5
+
+
+def test_summary_and_restart_golden():
+    """orc_walker_summary / orc_walker_restart against hand-derived values: violated counts (cutoff
+    included), the violation sum over non-cutoff rows, and the incumbent taken by a restart to a
+    feasible point; the restart keeps the weights and k and clears the tabu list."""
+    g = json.load(open(os.path.join(GOLD, "summary_restart.json")))
+    inst = exact.rows_from_json(g)
+    P = oracle.Problem.from_instance(inst)
+    W = oracle.TabuWalker(P, np.array(g["x0"], float), oracle.TabuParams(tenure=g["tenure"]))
+    for exp in g["steps"]:
+        if exp["op"] == "restart":
+            w_before, k_before = W.w.copy(), W.k
+            W.tabu_until[:] = 7
+            W.restart(np.array(exp["x"], float))
+            assert np.array_equal(W.w, w_before) and W.k == k_before
+            assert not W.tabu_until[: inst.n].any()
+        assert W.summary() == (exp["violated"], exp["sumviol"]), exp
+        assert W.has_incumbent == bool(exp["has_incumbent"])
+        if exp["has_incumbent"]:
+            assert W.best_obj == exp["best_obj"] and W.cutoff_rhs == exp["cutoff_rhs"]
