@@ -197,7 +197,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     } else if (vclass[j] == 1) {
       cls[j] = (d <= kShortDeg) ? CC_BIN : CC_LBIN;
     } else if (d + 2 <= kShortDeg) {
-      cls[j] = CC_GEN;
+      cls[j] = vclass[j] == 3 ? CC_GENC : CC_GEN;
     } else if (vclass[j] == 2 && std::isfinite(l[j]) && std::isfinite(u[j]) && u[j] - l[j] + 1.0 <= kBucketMax) {
       cls[j] = CC_LBKT;
     } else if (d + 2 + 3 <= kGenmMax) {   // + up to 3 padding entries
@@ -223,7 +223,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   // columns) and long columns start on a multiple of 4 nonzeros (16-byte vector loads): inert
   // padding entries (the dummy row) are appended to the column before such a start
   std::vector<int32_t> pad(n, 0);
-  std::vector<std::pair<int32_t, int32_t>> bin_ranges, gen_ranges;   // [p0, p1)
+  std::vector<std::pair<int32_t, int32_t>> bin_ranges, gen_ranges, cont_ranges;   // [p0, p1)
   {
     int64_t off = 0;
     auto align_at = [&](int32_t p) {
@@ -236,9 +236,14 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     int32_t p = 0;
     while (p < n) {
       const int k = cls[perm[p]];
-      if (k == CC_BIN || k == CC_GEN) {
+      if (k == CC_GENC) {   // a lane per column: no alignment, no entry cap
+        int cnt = 0;
+        while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k) off += deg[perm[p + cnt++]];
+        cont_ranges.push_back({p, p + cnt});
+        p += cnt;
+      } else if (k == CC_BIN || k == CC_GEN) {
         align_at(p);
-        const int cap = (k == CC_BIN ? kBinTile : kWTileGen) - 3;
+        const int cap = (k == CC_BIN ? kBinTile : kG32Max) - 3;
         int cnt = 0, tot = 0;
         while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k &&
                tot + deg[perm[p + cnt]] <= cap) {
@@ -331,12 +336,20 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     W.e1 = col_ptr[r.second];
     W.ncols = (int16_t)(r.second - r.first);
     W.kind = (int8_t)CC_GEN;
-    for (int32_t q = r.first; q < r.second; ++q) {   // pad = 1: the tile holds a continuous column
-      if (vclass[perm[q]] == 3) W.pad = 1;
-      P->gen_kmax = std::max(P->gen_kmax, col_ptr[q + 1] - col_ptr[q]);
-    }
+    for (int32_t q = r.first; q < r.second; ++q) P->gen_kmax = std::max(P->gen_kmax, col_ptr[q + 1] - col_ptr[q]);
     wtiles.push_back(W);
   }
+  const int32_t n_gtiles = (int32_t)wtiles.size();
+  for (const auto& r : cont_ranges) {
+    WTile W{};
+    W.p0 = r.first;
+    W.e0 = col_ptr[r.first];
+    W.e1 = col_ptr[r.second];
+    W.ncols = (int16_t)(r.second - r.first);
+    W.kind = (int8_t)CC_GENC;
+    wtiles.push_back(W);
+  }
+  const int32_t n_ctiles = (int32_t)wtiles.size() - n_gtiles;
   int32_t n_long = 0;
   int64_t lscr = 0;
   int32_t p = 0;
@@ -344,7 +357,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     const int32_t j = perm[p];
     const int k = cls[j];
     if (k == CC_FIXED || k == CC_BIN) { ++p; continue; }
-    if (k == CC_GEN) { ++p; continue; }   // packed in gen_ranges
+    if (k == CC_GEN || k == CC_GENC) { ++p; continue; }   // packed in gen_ranges / cont_ranges
     if (k == CC_EMPTY) {
       int cnt = 0;
       while (p + cnt < n && cnt < kWTileCols && cls[perm[p + cnt]] == k) ++cnt;
@@ -608,8 +621,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   DevProblem& D = P->dp;
   D.rblocks = d_rblocks;
   D.n_rblocks = (int32_t)rblocks.size();
-  D.n_cont_wtiles = 0;
-  for (const WTile& T : wtiles) D.n_cont_wtiles += (T.kind == CC_GEN && T.pad) ? 1 : 0;
+  D.n_gtiles = n_gtiles;
+  D.n_ctiles = n_ctiles;
   D.rb_cluster = P->binrow_cluster;
   D.rb_pb0 = P->binrow_pb0;
   D.rb_perm = d_rb_perm;

@@ -49,9 +49,10 @@ enum ColClass : int {
                  // over kBktChunk-nonzero warp chunks, finished by k_eval
   CC_LBIN = 2,   // binary, deg > kShortDeg: flip partial sums over kWChunk-nonzero warp chunks
   CC_GENM = 3,   // general, kShortDeg < deg+2 <= kGenmMax, other domains: one tile, bitonic sort
-  CC_GEN = 4,    // general, deg+2 <= kShortDeg: packed warp tiles, sort-free prefix per candidate
+  CC_GEN = 4,    // general integer, deg+2 <= kShortDeg: packed warp tiles (gen32_tile), sort-free
   CC_BIN = 5,    // binary, deg <= kShortDeg: packed tiles, flip sums
   CC_EMPTY = 6,  // a column without nonzeros (and c_j = 0)
+  CC_GENC = 7,   // continuous, deg+2 <= kShortDeg: a lane per column (gen_column_serial)
 };
 
 // A warp tile: ncols consecutive packed columns (CC_BIN or CC_GEN) of one warp.
@@ -61,7 +62,7 @@ struct WTile {
   int32_t e1;        // nonzero range [e0, e1); a chunk of a long column: the long-column index
   int16_t ncols;     // columns; a chunk of a long column: its nonzeros (<= kWChunk)
   int8_t kind;       // CC_BIN, CC_GEN, CC_EMPTY, or a warp chunk of a long column: CC_LBIN, CC_LBKT
-  int8_t pad;        // CC_GEN: 1 if the tile holds a continuous column
+  int8_t pad;
 };
 // A long column split into warp chunks: where its accumulators live in walker scratch.
 struct LongCol {
@@ -149,6 +150,8 @@ struct WalkerScalars {
   chap_step_record* log;      // current log base (NULL = no log)
   double cdot;                // c.x of the current point (k_cut_dot), for the cutoff row and obj
   long long vcount;           // violated active rows (k_viol_count)
+  int wint;                   // every weight is an integer <= 2^20 (the int path of gen32_tile)
+  int pad2;
 };
 
 // Per-kernel device time (chap_walkers_timing): %globaltimer at every block's start (atomic min)
@@ -208,8 +211,8 @@ struct DevProblem {
   const uint8_t* vclass;     // [n] 0 fixed 1 binary 2 integer 3 continuous
   const int32_t* perm;       // internal p -> user j
   const Tile* tiles; int32_t n_tiles; int32_t n_long;   // block tiles
-  const WTile* wtiles; int32_t n_wtiles;                // warp tiles (general, empty)
-  int32_t n_cont_wtiles;                                // general tiles holding a continuous column
+  const WTile* wtiles; int32_t n_wtiles;                // warp tiles: n_gtiles CC_GEN, n_ctiles CC_GENC, then
+  int32_t n_gtiles, n_ctiles;                           // CC_EMPTY
   const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles
   const WTile* bchunks; int32_t n_bchunks;              // warp chunks of long binary columns
   const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns

@@ -17,7 +17,9 @@
 // Every warp-tile slot issues its coalesced CSC loads and one 16-byte row-state gather before
 // using any of them.
 #pragma once
+#include <climits>
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -933,41 +935,50 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 // ------------------------------------------------------------------------------------------
 // general-column kernel
 // ------------------------------------------------------------------------------------------
-// k_eval_gen evaluates the packed general columns (and empty columns) with Algorithm 1 per
-// column, sort-free. For a candidate value v the score Algorithm 1 reports (the largest sigma of
-// the entries at v, R3) is sigma(v) = β + α [v > x̄] + Σ_{entries e: t_e < v, or t_e = v with
-// marker -1} δ_e. A marker +1 entry has δ <= 0 and a marker -1 entry δ >= 0, and an
-// entry with δ = 0 adds nothing, so "marker -1" is δ > 0, and the condition is the single compare
-// key_e <= v with key_e = t_e if δ_e > 0 and otherwise key_e = the next value above t_e (t_e + 1
-// on an integer column, the next double on a continuous one): nothing lies strictly between them,
-// so key_e <= v <=> t_e < v exactly.
-// A tile holds whole columns (<= 32) with <= kWTileGen nonzeros, starting on a multiple of 4;
-// lane l owns slots 4l..4l+3 (vector CSC loads, four row-state gathers in flight).
-// Phases: (1) slots: lines 3-11 per entry (key, δ, β/α parts, candidate flag) into shared memory,
-// and the candidate slots compacted in slot (= column) order; (2) work items of up to 4 candidates
-// of one column, one item per lane: one pass over the column's entries sums Σ_{key_e <= v} δ_e
-// for the item's candidates (lines 13-15 as direct prefix sums), and keeps the best candidate
-// above and the best below x̄ apart, so that α, known only at the end, is added once; (3) lane c:
-// β, α and the two bound candidates l, u (R2), then line 16's argmax with R4.
-// Every δ, β and α part is ±w or ±w/2 of a float weight, exact in float. When a tile's weights are
-// integers <= 2^16 and its keys and candidates integers of magnitude <= 2^22 (the common case of
-// the tabu dynamics on integer columns), every partial sum is a multiple of 1/2 below 2^23 in
-// magnitude and every key exact in float, so phases 2 and 3 run in exact float arithmetic;
-// otherwise in double.
-constexpr float kFastMag = 4194304.0f;   // 2^22
+// k_eval_gen evaluates the packed general integer columns (deg + 2 <= kShortDeg) with
+// Algorithm 1 per column, sort-free, in offsets relative to x̄.
+//
+// Lines 3-11 in offsets. For an integer column and a row with residual r and coefficient a, the
+// breakpoint of line 3-4 is t = floor(x̄ - r/a) (a > 0) or ceil(x̄ - r/a) (a < 0), so its offset
+// d = t - x̄ = -ceil(r/a) (a > 0) or -floor(r/a) (a < 0) needs neither x̄ nor the column: it is
+// computed per entry, slot-parallel, from the gathered row state alone. The six cases of lines
+// 5-11 are the sign of a and of d (d > 0 <=> x̄ < t). With w the row weight they give, in units
+// of half a weight (F = 2δ, β2 = 2β, α2 = 2α, integers for the integral weights of R11):
+//   code  case                 key     F      β2     α2     side   positive step
+//   6     a<0, d>0 (violated)  d       w      -w     2w     up     yes (σ rises at d)
+//   0     a<0, d<0 (slack)     d       2w     -2w    0      down   no
+//   5     a>0, d<0 (violated)  d+1     -w     2w     -2w    down   yes (σ rises below d+1)
+//   3     a>0, d>0 (slack)     d+1     -2w    0      0      up     no
+//   2     a<0, d=0 (tight)     MAX     0      -2w    2w     -      -
+//   2     a>0, d=0 (tight)     MAX     0      0      -2w    -      -
+// (an a>0 row's (t,-1,0) entry of line 10-11 carries no delta; its value is the candidate v = d,
+// scored before its +1 entry, R3), so that σ(v) = β + α [v > 0] + Σ_{key_e <= v} δ_e exactly
+// (DESIGN §2.3). Code bit 0: key = v + 1; bit 1: up side (v > 0); bit 2: positive step.
+//
+// Lines 13-16 without a sort. Candidates (R2, R5) are the entries with v in [l - x̄, u - x̄] and the
+// finite bounds other than x̄. On the up side (v > 0) σ changes only at keys, rising at the
+// positive steps (code 6) and falling elsewhere, so a candidate that is not a positive step scores
+// at most the nearest positive step below it, or the smallest up candidate if there is none; on
+// the down side symmetrically. Since R4 prefers the smaller |v| on ties, the argmax of Algorithm 1
+// over all candidates is always among {the positive steps, the smallest up candidate, the largest
+// down candidate} (DESIGN §2.3 gives the proof): only those are scored, each by one pass over
+// the column's entries. The number of positive steps is the number of violated rows of the
+// column (cutoff row included), a few in a tabu walk.
+//
+// A tile holds <= 32 whole columns, <= kG32Max entries, starting on a multiple of 4. Phase 1
+// (slot-parallel, coalesced CSC loads, four gathers in flight per lane): every entry into shared
+// memory as {key << 3 | code, F, β2, α2}. Phase 2 (lane c = column c): one pass for β, α, the
+// nearest candidates and the positive steps, then one pass per four candidates. The columns of
+// a tile have nearly equal lengths (internal order is by degree), so lanes stay balanced.
+// The int path needs weights that are integers <= 2^20 (WalkerScalars::wint; |Σ F| < 2^27) and
+// offsets |d| < 2^28; with other weights the F, β2, α2 words are floats summed in double (same
+// candidates, scores up to summation order), and a tile with a larger offset is
+// evaluated column by column by gen_column_serial.
+constexpr int kG32Max = 512;                    // entries per general tile
+constexpr int kKeyMax = (1 << 28) - 1;          // key of entries that are never in a prefix
+constexpr int kKeyLim = kKeyMax - 2;            // |offset| limit of the int path (bounds clamp here)
 struct __align__(16) GenWarp {
-  union {
-    double kd[kWTileGen];  // key (double path)
-    float kf[kWTileGen];   // key clamped to ±(2^22 + 1) (float path)
-  };
-  float D[kWTileGen];      // δ
-  float2 AB[kWTileGen];    // β, α parts of the entry
-  double v[kWTileGen];     // the candidate value t_e
-  double it[2 * 32][4];    // per item: best below x̄ (σ', v), best above x̄ (σ', v)
-  double cx[32], cl[32], cu[32];
-  int cb[32], ce[32], cr[32], cn[32];   // slot range, first candidate rank, candidates
-  int cj[32], ctb[32];     // user index and tabu expiry of column c (read at the finish)
-  uint8_t cidx[kWTileGen]; // candidate slots, compacted
+  int4 ent[kG32Max];
 };
 constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
 // a long bounded-integer chunk uses the warp's GenWarp area: int32 histogram, candidate words, stage
@@ -982,244 +993,232 @@ __device__ __forceinline__ double next_up(double t) {   // the next double above
   return __longlong_as_double(t > 0.0 ? bits + 1 : bits - 1);
 }
 
-__device__ __forceinline__ void gen_tile(const DevProblem& P, const double* __restrict__ X,
-                                         const double2* __restrict__ RS, int st,
-                                         const int32_t* __restrict__ TB, const WTile& T, int lane,
-                                         GenWarp& S, Best& b, double* oxhat, double* oscore,
-                                         long long kk, int use_tabu) {
-  const int nc = T.ncols, len = T.e1 - T.e0;
-  const bool act = 4 * lane < len;
-  int4 id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
-  double2 a01 = make_double2(1.0, 1.0), a23 = a01;
-  if (act) {
-    id = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0) + lane);
-    a01 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane);
-    a23 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0) + 2 * lane + 1);
+// Within one variable on offsets (R4): higher score, then smaller |v|, then smaller v.
+template <class S>
+__device__ __forceinline__ bool better_off(S s1, int v1, S s0, int v0) {
+  if (s1 != s0) return s1 > s0;
+  const int a1 = abs(v1), a0 = abs(v0);
+  if (a1 != a0) return a1 < a0;
+  return v1 < v0;
+}
+
+// The admissible-best update of a column (R6, R13); the tabu expiry is read only for a column
+// that would become the lane's best.
+__device__ __forceinline__ void offer_column(int p, int j, const int32_t* __restrict__ TB, double xb, double v,
+                                             double s, Best& b, double* oxhat, double* oscore, long long k,
+                                             int use_tabu) {
+  if (s == -INFINITY) v = xb;
+  if (oxhat) oxhat[j] = v;
+  if (oscore) oscore[j] = s;
+  if (!better_move(s, j, b.s, b.j)) return;
+  if (use_tabu && (long long)__ldg(TB + p) > k) return;
+  b.s = s;
+  b.v = v;
+  b.j = j;
+  b.p = p;
+}
+
+// One general column by one lane, in double: continuous columns (their breakpoints are not
+// integers), and integer columns of a tile whose offsets exceed the int path. Lines 3-11 per
+// entry (emit), the reduced candidate set of the tile path (positive steps, nearest up and down
+// candidates), and for each candidate the line-14 prefix as a direct sum over the column's
+// entries (re-gathered: L1/L2 hits). Returns (x̂, s); s = -inf without a candidate.
+__device__ void gen_column_serial(const DevProblem& P, const double* __restrict__ X, const double2* __restrict__ RS,
+                                  int st, int p, double& v_out, double& s_out) {
+  const int cb = __ldg(P.col_ptr + p), ce = __ldg(P.col_ptr + p + 1);
+  const double xb = __ldg(X + p), l = __ldg(P.lb + p), u = __ldg(P.ub + p);
+  const int is_int = __ldg(P.vclass + p) != 3;
+  auto entry = [&](int e) {
+    const double2 rv = __ldg(RS + (size_t)__ldg(P.row_idx + e) * st);
+    const double w = (double)__int_as_float((int)__double2loint(rv.y));
+    return emit(xb, rv.x, __ldg(P.val + e), w, is_int);
+  };
+  auto key_of = [&](const Elem& el) { return el.delta > 0.0 ? el.t : (is_int ? el.t + 1.0 : next_up(el.t)); };
+  double beta = 0.0, alpha = 0.0, vup = INFINITY, vdn = -INFINITY;
+  unsigned long long pm = 0ull;   // positive steps (deg <= 62)
+  for (int e = cb; e < ce; ++e) {
+    const Elem el = entry(e);
+    beta += el.beta;
+    alpha += el.alpha;
+    if (!el.valid || !isfinite(el.t) || !(el.t >= l && el.t <= u)) continue;   // R5; valid => t != x̄
+    if (el.t > xb) vup = fmin(vup, el.t); else vdn = fmax(vdn, el.t);
+    if ((el.t > xb) != (el.plus != 0)) pm |= 1ull << (e - cb);
   }
-  // column data of lane c
+  if (isfinite(u) && u != xb) vup = fmin(vup, u);
+  if (isfinite(l) && l != xb) vdn = fmax(vdn, l);
+  double bs = -INFINITY, bv = xb;
+  auto score = [&](double v) {
+    double acc = 0.0;
+    for (int e = cb; e < ce; ++e) {
+      const Elem el = entry(e);
+      if (el.valid && isfinite(el.t) && key_of(el) <= v) acc += el.delta;
+    }
+    const double sg = beta + acc + (v > xb ? alpha : 0.0);
+    if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
+  };
+  if (vup < INFINITY) score(vup);
+  if (vdn > -INFINITY) score(vdn);
+  for (unsigned long long m = pm; m; m &= m - 1) score(entry(cb + __ffsll((long long)m) - 1).t);
+  v_out = bv;
+  s_out = bs;
+}
+
+// One tile of packed general integer columns (see above). INTW: integral weights <= 2^20.
+template <bool INTW>
+__device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __restrict__ X,
+                                           const double2* __restrict__ RS, int st,
+                                           const int32_t* __restrict__ TB, const WTile& T, int lane,
+                                           GenWarp& S, Best& b, double* oxhat, double* oscore,
+                                           long long kk, int use_tabu) {
+  const int nc = T.ncols, len = T.e1 - T.e0;
+  // column data of lane c (loads in flight during phase 1)
   const int p = T.p0 + lane;
-  int cb = 0x7fffffff, ce = 0, cint = 1;
+  int cb = 0, ce = 0, j = 0;
   double xb = 0.0, l = 0.0, u = 0.0;
   if (lane < nc) {
     cb = __ldg(P.col_ptr + p) - T.e0;
     ce = __ldg(P.col_ptr + p + 1) - T.e0;
-    S.cj[lane] = __ldg(P.perm + p);
-    S.ctb[lane] = use_tabu ? __ldg(TB + p) : 0;
+    j = __ldg(P.perm + p);
     xb = __ldg(X + p);
     l = __ldg(P.lb + p);
     u = __ldg(P.ub + p);
-    cint = __ldg(P.vclass + p) != 3;
   }
-  double2 rv[4];
-  rv[0] = __ldg(RS + (size_t)id.x * st);
-  rv[1] = __ldg(RS + (size_t)id.y * st);
-  rv[2] = __ldg(RS + (size_t)id.z * st);
-  rv[3] = __ldg(RS + (size_t)id.w * st);
-  if (lane < nc) {
-    S.cx[lane] = xb;
-    S.cl[lane] = l;
-    S.cu[lane] = u;
-    S.cb[lane] = cb;
-    S.ce[lane] = ce;
-  }
-  const unsigned im = __ballot_sync(kFull, cint != 0);
-  // float path: integer columns, finite bounds within ±2^22 (as candidates)
-  bool fast = lane >= nc || (cint && (!isfinite(l) || fabs(l) <= (double)kFastMag) &&
-                             (!isfinite(u) || fabs(u) <= (double)kFastMag));
-  const int hwi = lane >> 3, sh = 4 * (lane & 7);
-  const unsigned h0 = __reduce_or_sync(kFull, (cb >> 5) == 0 ? (1u << (cb & 31)) : 0u);
-  const unsigned h1 = __reduce_or_sync(kFull, (cb >> 5) == 1 ? (1u << (cb & 31)) : 0u);
-  const unsigned h2 = __reduce_or_sync(kFull, (cb >> 5) == 2 ? (1u << (cb & 31)) : 0u);
-  const unsigned h3 = __reduce_or_sync(kFull, (cb >> 5) == 3 ? (1u << (cb & 31)) : 0u);
-  const unsigned hw = hwi == 0 ? h0 : (hwi == 1 ? h1 : (hwi == 2 ? h2 : h3));
-  const int base = (hwi > 0 ? __popc(h0) : 0) + (hwi > 1 ? __popc(h1) : 0) + (hwi > 2 ? __popc(h2) : 0) - 1;
-  __syncwarp();
-  // (1) lines 3-11 per entry
-  unsigned cmask = 0u;
-  double kq[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int k = 4 * lane + q;
-    const int c = base + __popc(hw & ((2u << (sh + q)) - 1u));
-    const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
-    const double x = S.cx[c], lc = S.cl[c], uc = S.cu[c];
-    const double r = rv[q].x;
-    const float wf = __int_as_float((int)__double2loint(rv[q].y));
-    const bool ci = (im >> c) & 1u;
-    double t = breakpoint(x, r, a);                                  // line 3
-    if (ci) t = (a > 0.0) ? floor(t) : ceil(t);                      // line 4
-    const bool pos = a > 0.0, lt = x < t, gt = x > t;                // lines 5-11
-    const float hw2 = 0.5f * wf;
-    float D = pos ? (gt ? -hw2 : (lt ? -wf : 0.f)) : (lt ? hw2 : (gt ? wf : 0.f));
-    float Bp = pos ? (gt ? wf : 0.f) : (lt ? -hw2 : -wf);            // β part
-    float Ap = pos ? (lt ? 0.f : -wf) : (gt ? 0.f : wf);             // α part
-    const bool fin = isfinite(r) && k < len;                         // inert rows (cutoff, padding)
-    if (!fin) { D = 0.f; Ap = Bp = 0.f; }
-    const bool cand = fin && x != t && t >= lc && t <= uc;           // R2, R5
-    if (cand) cmask |= 1u << q;
-    if (fin && !(wf == truncf(wf) && wf <= 65536.f)) fast = false;
-    if (cand && !(fabs(t) <= (double)kFastMag)) fast = false;
-    kq[q] = D > 0.f ? t : (ci ? t + 1.0 : next_up(t));
-    S.D[k] = D;
-    S.v[k] = t;
-    S.AB[k] = make_float2(Bp, Ap);
-  }
-  fast = __all_sync(kFull, fast);
-  if (fast) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      S.kf[4 * lane + q] = fminf(fmaxf((float)kq[q], -kFastMag - 1.0f), kFastMag + 1.0f);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) S.kd[4 * lane + q] = kq[q];
-  }
-  // compaction of the candidate slots (slot order = column order)
-  const int cnt = __popc(cmask);
-  int incl = cnt;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y = __shfl_up_sync(kFull, incl, off);
-    if (lane >= off) incl += y;
-  }
-  {
-    int rk = incl - cnt;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if ((cmask >> q) & 1u) S.cidx[rk++] = (uint8_t)(4 * lane + q);
-  }
-  const int n_cand = __shfl_sync(kFull, incl, 31);
-  auto rank_before = [&](int slot) -> int {   // candidates in slots < slot (all lanes call)
-    const int ln = min(slot >> 2, 31);
-    const int ex = __shfl_sync(kFull, incl - cnt, ln);
-    const unsigned cm = __shfl_sync(kFull, cmask, ln);
-    return slot >= 128 ? n_cand : ex + __popc(cm & ((1u << (slot & 3)) - 1u));
-  };
-  const int r0 = rank_before(lane < nc ? cb : 0);
-  const int r1 = rank_before(lane < nc ? ce : 0);
-  const int ncand = r1 - r0;
-  const int nit = lane < nc ? (ncand + 3) >> 2 : 0;   // work items of column `lane`
-  int ip = nit;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y = __shfl_up_sync(kFull, ip, off);
-    if (lane >= off) ip += y;
-  }
-  const int n_items = __shfl_sync(kFull, ip, 31);
-  ip -= nit;   // first item of column `lane`
-  if (lane < nc) {
-    S.cr[lane] = r0;
-    S.cn[lane] = ncand;
-  }
-  __syncwarp();
-  // (2) one work item per lane
-  for (int i0 = 0; i0 < n_items; i0 += 32) {
-    const int I = i0 + lane;
-    // the item's column: the last column c with ip_c <= I (ip is nondecreasing over the lanes)
-    int c = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int ct = c + step;
-      const int ipt = __shfl_sync(kFull, ip, ct & 31);
-      if (ct < 32 && ipt <= I) c = ct;
+  // phase 1: lines 3-11 per entry (slots 4 lane .. 4 lane + 3 of each round of 128)
+  bool ovf = false;
+  for (int r0 = 0; r0 < len; r0 += 4 * 32) {
+    const int k0 = r0 + 4 * lane;
+    int4 id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
+    double2 a01 = make_double2(1.0, 1.0), a23 = a01;
+    if (k0 < len) {
+      id = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0 + k0));
+      a01 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0 + k0));
+      a23 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0 + k0) + 1);
     }
-    const int g = I - __shfl_sync(kFull, ip, c);   // item of the column
-    if (I < n_items) {
-      const int e0 = S.cb[c], e1 = S.ce[c], r0c = S.cr[c] + 4 * g, r1c = min(S.cr[c] + S.cn[c], r0c + 4);
-      const double x = S.cx[c];
-      double vq[4], acc[4];
+    double2 rv[4];
+    rv[0] = __ldg(RS + (size_t)id.x * st);
+    rv[1] = __ldg(RS + (size_t)id.y * st);
+    rv[2] = __ldg(RS + (size_t)id.z * st);
+    rv[3] = __ldg(RS + (size_t)id.w * st);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) vq[q] = (r0c + q < r1c) ? S.v[S.cidx[r0c + q]] : -INFINITY;
-      if (fast) {
-        float vf[4], af[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          vf[q] = (r0c + q < r1c) ? (float)vq[q] : -INFINITY;
-          af[q] = 0.f;
-        }
-        for (int e = e0; e < e1; ++e) {
-          const float ke = S.kf[e], de = S.D[e];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (ke <= vf[q]) af[q] += de;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = (double)af[q];
+    for (int q = 0; q < 4; ++q) {
+      const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
+      const double r = rv[q].x;
+      const float wf = __int_as_float((int)__double2loint(rv[q].y));
+      const bool live = r > -INFINITY;                 // inert rows: the inactive cutoff row, padding
+      const bool pos = a > 0.0;
+      const double qd = (live && r != 0.0) ? r / a : 0.0;
+      const double dd = pos ? -ceil(qd) : -floor(qd);   // t - x̄ of lines 3-4
+      const bool big = !(fabs(dd) <= (double)(kKeyLim - 1));
+      ovf |= live && big;
+      const int d = (live && !big) ? (int)dd : 0;
+      int code, key;
+      if (!live || d == 0) { code = 2; key = kKeyMax; }
+      else if (pos) { code = d < 0 ? 5 : 3; key = d + 1; }
+      else { code = d > 0 ? 6 : 0; key = d; }
+      int4 ent;
+      ent.x = (key << 3) | code;
+      if (INTW) {
+        const int w1 = live ? __float2int_rn(wf) : 0, w2 = 2 * w1;
+        ent.y = d == 0 ? 0 : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2));
+        ent.z = pos ? (d < 0 ? w2 : 0) : (d > 0 ? -w1 : -w2);
+        ent.w = pos ? (d <= 0 ? -w2 : 0) : (d >= 0 ? w2 : 0);
       } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = 0.0;
-        for (int e = e0; e < e1; ++e) {
-          const double ke = S.kd[e], de = (double)S.D[e];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (ke <= vq[q]) acc[q] += de;
-        }
+        const float w1 = live ? wf : 0.f, w2 = 2.f * w1;
+        const float F = d == 0 ? 0.f : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2));
+        const float B = pos ? (d < 0 ? w2 : 0.f) : (d > 0 ? -w1 : -w2);
+        const float A = pos ? (d <= 0 ? -w2 : 0.f) : (d >= 0 ? w2 : 0.f);
+        ent.y = __float_as_int(F);
+        ent.z = __float_as_int(B);
+        ent.w = __float_as_int(A);
       }
-      double slt = -INFINITY, vlt = x, sgt = -INFINITY, vgt = x;
+      S.ent[k0 + q] = ent;
+    }
+  }
+  ovf = __any_sync(kFull, ovf);
+  __syncwarp();
+  if (ovf) {   // an offset beyond the int path: every column of the tile in double
+    if (lane < nc) {
+      double v, s;
+      gen_column_serial(P, X, RS, st, p, v, s);
+      offer_column(p, j, TB, xb, v, s, b, oxhat, oscore, kk, use_tabu);
+    }
+    __syncwarp();
+    return;
+  }
+  if (lane < nc) {
+    // phase 2, pass 0: β, α, nearest candidates (bounds included), positive steps
+    const bool ufin = isfinite(u), lfin = isfinite(l);
+    const double hid = u - xb, lod = l - xb;
+    const int hi = ufin ? (int)fmin(hid, (double)kKeyLim) : kKeyLim;
+    const int lo = lfin ? (int)fmax(lod, -(double)kKeyLim) : -kKeyLim;
+    int vup = (ufin && hi > 0) ? hi : INT_MAX;
+    int vdn = (lfin && lo < 0) ? lo : INT_MIN;
+    using Acc = typename std::conditional<INTW, int, double>::type;
+    Acc b2 = 0, a2 = 0;
+    unsigned long long pm = 0ull;
+    for (int e = cb; e < ce; ++e) {
+      const int4 E = S.ent[e];
+      if (INTW) {
+        b2 += E.z;
+        a2 += E.w;
+      } else {
+        b2 += (double)__int_as_float(E.z);
+        a2 += (double)__int_as_float(E.w);
+      }
+      const int code = E.x & 7, v = (E.x >> 3) - (code & 1);
+      const bool up = code & 2;
+      if (up ? v > hi : v < lo) continue;   // outside [l, u] (and every tight / inert entry)
+      if (up) vup = min(vup, v); else vdn = max(vdn, v);
+      if (code & 4) pm |= 1ull << (e - cb);
+    }
+    // pass 1..: σ2 at up to four candidates per pass over the entries
+    Acc bs2 = 0;
+    int bv = 0;
+    bool have = false;
+    int cq[4];
+    int nq = 0;
+    auto flush = [&]() {
+      Acc acc[4];
+      int lim[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (r0c + q >= r1c) continue;
-        if (vq[q] > x) {
-          if (better_shift(acc[q], vq[q], sgt, vgt, x)) { sgt = acc[q]; vgt = vq[q]; }
-        } else if (better_shift(acc[q], vq[q], slt, vlt, x)) {
-          slt = acc[q]; vlt = vq[q];
+        acc[q] = 0;
+        lim[q] = q < nq ? ((cq[q] << 3) | 7) : INT_MIN;   // key <= v  <=>  key << 3 | code <= v << 3 | 7
+      }
+      for (int e = cb; e < ce; ++e) {
+        const int2 E = *reinterpret_cast<const int2*>(&S.ent[e]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (E.x <= lim[q]) {
+            if (INTW) acc[q] += E.y; else acc[q] += (double)__int_as_float(E.y);
+          }
         }
       }
-      S.it[I][0] = slt;
-      S.it[I][1] = vlt;
-      S.it[I][2] = sgt;
-      S.it[I][3] = vgt;
-    }
-  }
-  __syncwarp();
-  // (3) lane c: β, α, the bounds (R2), line 16 over the column's items and bounds (R4)
-  if (lane < nc) {
-    const double xb = S.cx[lane], l = S.cl[lane], u = S.cu[lane];
-    const int cb = S.cb[lane], ce = S.ce[lane];
-    double beta, alpha, pl, pu;
-    if (fast) {
-      const float lf = isfinite(l) ? (float)l : -INFINITY, uf = isfinite(u) ? (float)u : INFINITY;
-      float bf = 0.f, af = 0.f, plf = 0.f, puf = 0.f;
-      for (int e = cb; e < ce; ++e) {
-        const float2 ab = S.AB[e];
-        const float ke = S.kf[e], de = S.D[e];
-        bf += ab.x;
-        af += ab.y;
-        if (ke <= lf) plf += de;
-        if (ke <= uf) puf += de;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q >= nq) break;
+        const Acc sg = b2 + acc[q] + (cq[q] > 0 ? a2 : (Acc)0);
+        if (!have || better_off(sg, cq[q], bs2, bv)) { bs2 = sg; bv = cq[q]; have = true; }
       }
-      beta = bf; alpha = af; pl = plf; pu = puf;
-    } else {
-      beta = alpha = pl = pu = 0.0;
-      for (int e = cb; e < ce; ++e) {
-        const float2 ab = S.AB[e];
-        const double ke = S.kd[e], de = (double)S.D[e];
-        beta += (double)ab.x;
-        alpha += (double)ab.y;
-        if (ke <= l) pl += de;
-        if (ke <= u) pu += de;
-      }
+      nq = 0;
+    };
+    if (vup != INT_MAX) cq[nq++] = vup;
+    if (vdn != INT_MIN) cq[nq++] = vdn;
+    for (unsigned long long m = pm; m; m &= m - 1) {
+      const int e = cb + __ffsll((long long)m) - 1;
+      const int x3 = S.ent[e].x;
+      const int v = (x3 >> 3) - (x3 & 1);
+      if (v != vup && v != vdn) cq[nq++] = v;
+      if (nq == 4) flush();
     }
-    double bs = -INFINITY, bv = xb;
-    for (int i = ip; i < ip + nit; ++i) {
-      const double s0 = S.it[i][0], s1 = S.it[i][2];
-      if (s0 != -INFINITY) {
-        const double sg = beta + s0, v = S.it[i][1];
-        if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
-      }
-      if (s1 != -INFINITY) {
-        const double sg = beta + alpha + s1, v = S.it[i][3];
-        if (better_shift(sg, v, bs, bv, xb)) { bs = sg; bv = v; }
-      }
+    if (nq > 0) flush();
+    double v = xb, s = -INFINITY;
+    if (have) {
+      s = 0.5 * (double)bs2;
+      // a bound beyond the clamp is the farthest candidate of its side: report its exact value
+      v = (bv == hi && ufin && hid > (double)kKeyLim) ? u : ((bv == lo && lfin && lod < -(double)kKeyLim) ? l : xb + (double)bv);
     }
-    if (isfinite(l) && l != xb) {   // l < x̄: no α
-      const double sg = beta + pl;
-      if (better_shift(sg, l, bs, bv, xb)) { bs = sg; bv = l; }
-    }
-    if (isfinite(u) && u != xb) {   // u > x̄
-      const double sg = beta + alpha + pu;
-      if (better_shift(sg, u, bs, bv, xb)) { bs = sg; bv = u; }
-    }
-    finish_column_j(p, S.cj[lane], S.ctb[lane], xb, bv, bs, b, oxhat, oscore, kk, use_tabu);
+    offer_column(p, j, TB, xb, v, s, b, oxhat, oscore, kk, use_tabu);
   }
   __syncwarp();
 }
@@ -1454,15 +1453,25 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     lbkt_chunk(P, Wk, walker, X, RS, st, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
   __syncwarp();
   t -= P.n_gchunks;
-  if (wm_mode && P.n_cont_wtiles == 0) t = P.n_wtiles;   // nothing left for this kernel
-  WTile Tn;
-  if (t < P.n_wtiles) Tn = P.wtiles[t];
-  for (; t < P.n_wtiles; t += nwarps) {
-    const WTile T = Tn;
-    if (t + nwarps < P.n_wtiles) Tn = P.wtiles[t + nwarps];
+  // tiles: [0, n_gtiles) packed integer columns (gen32_tile), then [n_gtiles, n_gtiles + n_ctiles)
+  // continuous columns (gen_column_serial, a lane per column), then empty columns; with walker
+  // groups (wm_mode) the integer and empty tiles are k_eval_gen_wm's
+  const int tb = wm_mode ? P.n_gtiles : 0;
+  const int te = wm_mode ? P.n_gtiles + P.n_ctiles : P.n_wtiles;
+  const bool wint = sc->wint != 0;   // integral weights <= 2^20: the int path of gen32_tile
+  for (t += tb; t < te; t += nwarps) {
+    const WTile T = P.wtiles[t];
     if (T.kind == CC_GEN) {
-      if (!wm_mode || T.pad) gen_tile(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
-    } else if (!wm_mode) {
+      if (wint) gen32_tile<true>(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
+      else gen32_tile<false>(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
+    } else if (T.kind == CC_GENC) {
+      if (lane < T.ncols) {
+        const int p = T.p0 + lane;
+        double v, s;
+        gen_column_serial(P, X, RS, st, p, v, s);
+        offer_column(p, __ldg(P.perm + p), TB, __ldg(X + p), v, s, b, oxhat, oscore, kk, use_tabu);
+      }
+    } else {
       wtile_empty(P, C, T, lane, b);
     }
   }
@@ -1522,7 +1531,7 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
   const int nwarps = gridDim.x * (kGenWmThreads / 32);
   for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < P.n_wtiles; t += nwarps) {
     const WTile T = P.wtiles[t];
-    if (T.kind == CC_GEN && T.pad) continue;   // a continuous column: k_eval_gen (wm_mode 1)
+    if (T.kind == CC_GENC) continue;   // continuous columns: k_eval_gen (wm_mode 1)
     for (int c = slot; c < T.ncols; c += NS) {
       const int p = T.p0 + c;
       const double xb = __ldg(X + p), l = __ldg(P.lb + p), u = __ldg(P.ub + p);

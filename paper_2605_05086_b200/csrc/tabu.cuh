@@ -56,6 +56,7 @@ __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float
         if (init_w == 1) s.w = 1.0f;
         else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
         if (init_w == 2 && bad && !(s.w >= 0.0f)) atomicOr(bad, 1);   // weights must be >= 0 (R11)
+        if (init_w == 2 && !(s.w == truncf(s.w) && s.w <= 1048576.0f)) atomicAnd(&Wk.sc[w].wint, 0);
         if (!sc[w].cut_active) s.w = 0.0f;
         s.pad = 0;
         rw[i] = s;
@@ -79,6 +80,7 @@ __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float
       if (init_w == 1) s.w = 1.0f;
       else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
       if (init_w == 2 && bad && !(s.w >= 0.0f)) atomicOr(bad, 1);
+      if (init_w == 2 && !(s.w == truncf(s.w) && s.w <= 1048576.0f)) atomicAnd(&Wk.sc[w].wint, 0);
       if (i == P.cut_row && !sc[w].cut_active) s.w = 0.0f;
       s.pad = 0;
       rw[i] = s;
@@ -122,6 +124,8 @@ __global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, in
     sc->violated = vt;
     sc->obj = zt;
     if (mode == 0) {
+      // weights start at 1 and grow by +1 up to the cap (R12): integers <= 2^20 when the cap is one
+      sc->wint = Wk.wcap == floorf(Wk.wcap) && Wk.wcap <= 1048576.0f;
       sc->k = 0;
       sc->n_moves = 0;
       sc->n_stuck = 0;
@@ -398,6 +402,7 @@ __global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
 // Scalars of the eval API's single virtual walker: k = 0, cutoff from the call.
 __global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs) {
   sc->k = 0;
+  sc->wint = 1;   // cleared by k_rows_init on a non-integral weight or one above 2^20
   sc->cut_active = cutoff_rhs < INFINITY;
   sc->cutoff_rhs = cutoff_rhs;
   sc->cdot = 0.0;
