@@ -1063,6 +1063,40 @@ __device__ void gen_column_serial(const DevProblem& P, const double* __restrict_
   s_out = bs;
 }
 
+// Lines 3-11 of Algorithm 1 for one entry of an integer column in offsets (table above): the
+// entry word key << 3 | code and F, β2, α2 (ints for INTW, else float bits). Sets ovf for an offset
+// beyond the int path.
+template <bool INTW>
+__device__ __forceinline__ int4 off_entry(double r, float wf, double a, bool& ovf) {
+  const bool live = r > -INFINITY;                 // inert rows: the inactive cutoff row, padding
+  const bool pos = a > 0.0;
+  const double qd = (live && r != 0.0) ? r / a : 0.0;
+  const double dd = pos ? -ceil(qd) : -floor(qd);   // t - x̄ of lines 3-4
+  const bool big = !(fabs(dd) <= (double)(kKeyLim - 1));
+  ovf |= live && big;
+  // an offset beyond the int path is clamped (its sign, hence its case, is kept): the general tile
+  // then re-evaluates in double (ovf); for a bounded domain it lies outside [l, u] either way
+  const int d = !live ? 0 : (big ? (dd > 0.0 ? kKeyLim - 1 : 1 - kKeyLim) : (int)dd);
+  int code, key;
+  if (!live || d == 0) { code = 2; key = kKeyMax; }
+  else if (pos) { code = d < 0 ? 5 : 3; key = d + 1; }
+  else { code = d > 0 ? 6 : 0; key = d; }
+  int4 ent;
+  ent.x = (key << 3) | code;
+  if (INTW) {
+    const int w1 = live ? __float2int_rn(wf) : 0, w2 = 2 * w1;
+    ent.y = d == 0 ? 0 : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2));
+    ent.z = pos ? (d < 0 ? w2 : 0) : (d > 0 ? -w1 : -w2);
+    ent.w = pos ? (d <= 0 ? -w2 : 0) : (d >= 0 ? w2 : 0);
+  } else {
+    const float w1 = live ? wf : 0.f, w2 = 2.f * w1;
+    ent.y = __float_as_int(d == 0 ? 0.f : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2)));
+    ent.z = __float_as_int(pos ? (d < 0 ? w2 : 0.f) : (d > 0 ? -w1 : -w2));
+    ent.w = __float_as_int(pos ? (d <= 0 ? -w2 : 0.f) : (d >= 0 ? w2 : 0.f));
+  }
+  return ent;
+}
+
 // One tile of packed general integer columns (see above). INTW: integral weights <= 2^20.
 template <bool INTW>
 __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __restrict__ X,
@@ -1102,35 +1136,7 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
-      const double r = rv[q].x;
-      const float wf = __int_as_float((int)__double2loint(rv[q].y));
-      const bool live = r > -INFINITY;                 // inert rows: the inactive cutoff row, padding
-      const bool pos = a > 0.0;
-      const double qd = (live && r != 0.0) ? r / a : 0.0;
-      const double dd = pos ? -ceil(qd) : -floor(qd);   // t - x̄ of lines 3-4
-      const bool big = !(fabs(dd) <= (double)(kKeyLim - 1));
-      ovf |= live && big;
-      const int d = (live && !big) ? (int)dd : 0;
-      int code, key;
-      if (!live || d == 0) { code = 2; key = kKeyMax; }
-      else if (pos) { code = d < 0 ? 5 : 3; key = d + 1; }
-      else { code = d > 0 ? 6 : 0; key = d; }
-      int4 ent;
-      ent.x = (key << 3) | code;
-      if (INTW) {
-        const int w1 = live ? __float2int_rn(wf) : 0, w2 = 2 * w1;
-        ent.y = d == 0 ? 0 : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2));
-        ent.z = pos ? (d < 0 ? w2 : 0) : (d > 0 ? -w1 : -w2);
-        ent.w = pos ? (d <= 0 ? -w2 : 0) : (d >= 0 ? w2 : 0);
-      } else {
-        const float w1 = live ? wf : 0.f, w2 = 2.f * w1;
-        const float F = d == 0 ? 0.f : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2));
-        const float B = pos ? (d < 0 ? w2 : 0.f) : (d > 0 ? -w1 : -w2);
-        const float A = pos ? (d <= 0 ? -w2 : 0.f) : (d >= 0 ? w2 : 0.f);
-        ent.y = __float_as_int(F);
-        ent.z = __float_as_int(B);
-        ent.w = __float_as_int(A);
-      }
+      const int4 ent = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), a, ovf);
       S.ent[k0 + q] = ent;
     }
   }
@@ -1224,32 +1230,33 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
 }
 
 // A warp chunk (<= kBktChunk nonzeros) of a long general integer column with domain [l, u],
-// dom = u - l + 1 <= kBucketMax: the sort of line 13 becomes a counting pass. D[v-l] collects the
-// marker -1 deltas at v and the marker +1 deltas at v-1, so sigma(v) = β + Σ_{v' <= v} D[v'] +
-// α [v > x̄]. Every chunk adds its entries into the column's accumulators (D, β, α,
-// candidate bits) in walker scratch. Breakpoints of a long column crowd onto few values, so a
-// chunk first counts into a warp-private shared-memory histogram of 2δ in int32 (exact while the
-// weights are integers <= 2^16: |Σ 2δ| <= 2^27) and then adds each nonzero bucket once; rounds
-// with other weights, or domains above kWarpDom, aggregate per warp instead (lanes with equal
-// buckets: __match_any_sync, the lowest lane adds the group's sum). lbkt_finalize (k_eval) scans D
-// in coalesced rounds of 32 buckets, takes line 16's argmax with R4 and zeroes the accumulators.
+// dom = u - l + 1 <= kBucketMax: the sort of line 13 becomes a counting pass. With the entries of
+// off_entry (gen32_tile's table), D[x̄ + key - l] collects δ = F/2 of every emitted entry, so that
+// sigma(v) = β + Σ_{v' <= v} D[v' - l] + α [v > x̄]; an entry whose key is below l is in
+// every prefix (folded into β), one above u in none (dropped), and the candidates (R2, R5) are the
+// emitted values in [l, u]. Every chunk adds its entries into the column's accumulators (D, β, α,
+// candidate bits) in walker scratch. Breakpoints of a long column crowd onto few values, so with
+// integral weights <= 2^20 (INTW) a chunk first counts F into a warp-private int32 shared-memory
+// histogram (|Σ| <= kBktChunk 2^21 < 2^31) and then adds each nonzero bucket once; other weights, or
+// domains above kWarpDom, aggregate per warp instead (lanes with equal buckets: __match_any_sync,
+// the lowest lane adds the group's sum). lbkt_finalize (k_eval) scans D in coalesced rounds of 32
+// buckets, takes line 16's argmax with R4 and zeroes the accumulators.
+template <bool INTW>
 __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
-                                           int st, const int32_t* __restrict__ TB, const WTile& T, int lane,
-                                           unsigned char* wmem, Best& b, double* oxhat, double* oscore,
-                                           long long kk, int use_tabu) {
+                                           int st, const WTile& T, int lane, unsigned char* wmem) {
   const LongCol L = P.lcols[T.e1];
   const int p = T.p0, dom = L.dom, len = T.ncols;
   const int* __restrict__ ridx = P.row_idx + T.e0;
   const double* __restrict__ rval = P.val + T.e0;
-  const double xb = __ldg(X + p), l = __ldg(P.lb + p), u = __ldg(P.ub + p);
+  const int xl = (int)(__ldg(X + p) - __ldg(P.lb + p));      // x̄ - l, in [0, dom)
   double* Dg = Wk.lscr + (size_t)walker * Wk.lss + L.scr;   // [dom + 1]
   double* BA = Dg + dom + 1;                                 // β, α
   unsigned* Cw = reinterpret_cast<unsigned*>(BA + 2);        // candidate bits
   int* hist = reinterpret_cast<int*>(wmem);                              // [kWarpDom + 1]
   unsigned* hcw = reinterpret_cast<unsigned*>(wmem + kLbktHistBytes);    // [kWarpDom / 32]
   double* stage = reinterpret_cast<double*>(wmem + kLbktHistBytes + kWarpDom / 8);   // [32]
-  const bool local = dom <= kWarpDom;
+  const bool local = INTW && dom <= kWarpDom;
   const int nwords = (dom + 31) >> 5;
   if (local) {
     for (int q = lane; q <= dom; q += 32) hist[q] = 0;
@@ -1257,62 +1264,58 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     __syncwarp();
   }
   const unsigned lt_mask = (1u << lane) - 1u;
-  double beta = 0.0, alpha = 0.0;
+  using Acc = typename std::conditional<INTW, int, double>::type;
+  Acc b2 = 0, a2 = 0;
+  bool ovf = false;   // irrelevant here: a clamped offset lies outside [l, u]
   for (int r0 = 0; r0 < len; r0 += 32 * kWSlotsGen) {
-  int id[kWSlotsGen];
-  double av[kWSlotsGen];
+    int id[kWSlotsGen];
+    double av[kWSlotsGen];
 #pragma unroll
-  for (int q = 0; q < kWSlotsGen; ++q) {
-    const int k = r0 + lane + 32 * q;
-    id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
-    av[q] = k < len ? __ldcs(rval + k) : 1.0;
-  }
-  double2 rv[kWSlotsGen];
-#pragma unroll
-  for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + (size_t)id[q] * st);
-  bool fast = local;
-#pragma unroll
-  for (int q = 0; q < kWSlotsGen; ++q) {
-    const float wf = __int_as_float((int)__double2loint(rv[q].y));
-    if (isfinite(rv[q].x) && !(wf == truncf(wf) && wf <= 65536.f)) fast = false;
-  }
-  fast = __all_sync(kFull, fast);
-#pragma unroll
-  for (int q = 0; q < kWSlotsGen; ++q) {
-    const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
-    const Elem el = emit(xb, r, av[q], w, 1);   // inert rows emit nothing
-    beta += el.beta;
-    alpha += el.alpha;
-    const double t = el.t;
-    int bq = -1, cq = -1;
-    double dq = 0.0;
-    if (el.valid) {
-      if (t >= l && t <= u && t != xb) cq = (int)(t - l);
-      if (t < l) beta += el.delta;
-      else if (!el.plus) { if (t <= u) { bq = (int)(t - l); dq = el.delta; } }
-      else if (t < u) { bq = (int)(t - l) + 1; dq = el.delta; }
+    for (int q = 0; q < kWSlotsGen; ++q) {
+      const int k = r0 + lane + 32 * q;
+      id[q] = k < len ? __ldcs(ridx + k) : P.dummy_row;
+      av[q] = k < len ? __ldcs(rval + k) : 1.0;
     }
-    if (fast) {
-      if (bq >= 0) atomicAdd(hist + bq, (int)(2.0 * dq));
-      if (cq >= 0) atomicOr(hcw + (cq >> 5), 1u << (cq & 31));
-      continue;
+    double2 rv[kWSlotsGen];
+#pragma unroll
+    for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + (size_t)id[q] * st);
+#pragma unroll
+    for (int q = 0; q < kWSlotsGen; ++q) {
+      const int4 E = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), av[q], ovf);
+      if (INTW) { b2 += E.z; a2 += E.w; } else { b2 += (double)__int_as_float(E.z); a2 += (double)__int_as_float(E.w); }
+      const int code = E.x & 7, key = E.x >> 3;
+      int bq = -1, cq = -1;
+      if (code != 2) {
+        const int bk = key + xl, cv = key - (code & 1) + xl;
+        if (bk < 0) {   // below l: in every prefix
+          if (INTW) b2 += E.y; else b2 += (double)__int_as_float(E.y);
+        } else if (bk < dom) {
+          bq = bk;
+        }
+        if (cv >= 0 && cv < dom) cq = cv;
+      }
+      if (local) {
+        if (bq >= 0 && E.y != 0) atomicAdd(hist + bq, E.y);
+        if (cq >= 0) atomicOr(hcw + (cq >> 5), 1u << (cq & 31));
+        continue;
+      }
+      // bucket deltas: one atomic per distinct bucket of the 32 entries
+      const double dq = bq >= 0 ? 0.5 * (INTW ? (double)E.y : (double)__int_as_float(E.y)) : 0.0;
+      const unsigned mD = __match_any_sync(kFull, bq);
+      stage[lane] = dq;
+      __syncwarp();
+      if (bq >= 0 && (mD & lt_mask) == 0) {
+        double sum = dq;
+        for (unsigned mm = mD & (mD - 1); mm; mm &= mm - 1) sum += stage[__ffs(mm) - 1];
+        if (sum != 0.0) atomicAdd(Dg + bq, sum);
+      }
+      __syncwarp();
+      // candidate bits: one OR per distinct word, skipped once the bits are set
+      const int wq = cq >= 0 ? (cq >> 5) : -1;
+      const unsigned mC = __match_any_sync(kFull, wq);
+      const unsigned bits = __reduce_or_sync(mC, cq >= 0 ? (1u << (cq & 31)) : 0u);
+      if (wq >= 0 && (mC & lt_mask) == 0 && (__ldcg(Cw + wq) & bits) != bits) atomicOr(Cw + wq, bits);
     }
-    // bucket deltas: one atomic per distinct bucket of the 32 entries
-    const unsigned mD = __match_any_sync(kFull, bq);
-    stage[lane] = dq;
-    __syncwarp();
-    if (bq >= 0 && (mD & lt_mask) == 0) {
-      double sum = dq;
-      for (unsigned mm = mD & (mD - 1); mm; mm &= mm - 1) sum += stage[__ffs(mm) - 1];
-      atomicAdd(Dg + bq, sum);
-    }
-    __syncwarp();
-    // candidate bits: one OR per distinct word, skipped once the bits are set
-    const int wq = cq >= 0 ? (cq >> 5) : -1;
-    const unsigned mC = __match_any_sync(kFull, wq);
-    const unsigned bits = __reduce_or_sync(mC, cq >= 0 ? (1u << (cq & 31)) : 0u);
-    if (wq >= 0 && (mC & lt_mask) == 0 && (__ldcg(Cw + wq) & bits) != bits) atomicOr(Cw + wq, bits);
-  }
   }
   if (local) {   // one addition per nonzero bucket and candidate word
     __syncwarp();
@@ -1327,12 +1330,12 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    beta += __shfl_xor_sync(kFull, beta, off);
-    alpha += __shfl_xor_sync(kFull, alpha, off);
+    b2 += __shfl_xor_sync(kFull, b2, off);
+    a2 += __shfl_xor_sync(kFull, a2, off);
   }
   if (lane == 0) {   // k_eval scans and finishes the column after this kernel
-    if (beta != 0.0) atomicAdd(BA, beta);
-    if (alpha != 0.0) atomicAdd(BA + 1, alpha);
+    if (b2 != 0) atomicAdd(BA, 0.5 * (double)b2);
+    if (a2 != 0) atomicAdd(BA + 1, 0.5 * (double)a2);
   }
 }
 
@@ -1443,6 +1446,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   b.init();
   const int nwarps = gridDim.x * (kGenThreads / 32);
   int t = blockIdx.x * (kGenThreads / 32) + wid;
+  const bool wint = sc->wint != 0;   // integral weights <= 2^20: the int paths
   // chunks of long columns first (their latency overlaps the packed tiles of other warps)
   if (with_lbin) {
     for (; t < P.n_bchunks; t += nwarps)
@@ -1450,7 +1454,10 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     t -= P.n_bchunks;
   }
   for (; t < P.n_gchunks; t += nwarps)
-    lbkt_chunk(P, Wk, walker, X, RS, st, TB, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S), b, oxhat, oscore, kk, use_tabu);
+  {
+    if (wint) lbkt_chunk<true>(P, Wk, walker, X, RS, st, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S));
+    else lbkt_chunk<false>(P, Wk, walker, X, RS, st, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S));
+  }
   __syncwarp();
   t -= P.n_gchunks;
   // tiles: [0, n_gtiles) packed integer columns (gen32_tile), then [n_gtiles, n_gtiles + n_ctiles)
@@ -1458,7 +1465,6 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   // groups (wm_mode) the integer and empty tiles are k_eval_gen_wm's
   const int tb = wm_mode ? P.n_gtiles : 0;
   const int te = wm_mode ? P.n_gtiles + P.n_ctiles : P.n_wtiles;
-  const bool wint = sc->wint != 0;   // integral weights <= 2^20: the int path of gen32_tile
   for (t += tb; t < te; t += nwarps) {
     const WTile T = P.wtiles[t];
     if (T.kind == CC_GEN) {
