@@ -419,6 +419,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   std::vector<RowBlock> rblocks;
   std::vector<int32_t> rb_row;
   std::vector<uint32_t> rb_cv;
+  std::vector<RowStage> rb_stage;
   std::vector<int32_t> rb_perm;
   {
     int32_t pb0 = -1, pb1 = -1;
@@ -534,6 +535,30 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
           }
         }
         for (int sl = C; sl <= kRowCluster; ++sl) R.es[sl] = (int32_t)rb_row.size();
+        // stages of each slice: <= kRowChunk entries (whole groups of 4) whose rows span <= kRowSpan
+        // rows (padding entries, rb_cv = 0, take no row); a single group wider than that gathers
+        for (int sl = 0; sl <= kRowCluster; ++sl) {
+          R.st[sl] = (int32_t)rb_stage.size();
+          if (sl >= C) continue;
+          for (int64_t e = R.es[sl], e1; e < R.es[sl + 1]; e = e1) {
+            int32_t lo = INT32_MAX, hi = -1;
+            for (e1 = e; e1 < R.es[sl + 1] && e1 - e + 4 <= kRowChunk; e1 += 4) {
+              int32_t glo = lo, ghi = hi;
+              for (int64_t k = e1; k < e1 + 4; ++k)
+                if (rb_cv[k] != 0u) { glo = std::min(glo, rb_row[k]); ghi = std::max(ghi, rb_row[k]); }
+              if (e1 > e && ghi >= 0 && ghi - glo + 1 > kRowSpan) break;
+              lo = glo;
+              hi = ghi;
+            }
+            RowStage G{};
+            G.e0 = (int32_t)e;
+            G.ne = (int32_t)(e1 - e);
+            const bool fits = hi >= 0 && hi - lo + 1 <= kRowSpan;
+            G.r0 = fits ? lo : 0;
+            G.nr = fits ? hi - lo + 1 : 0;
+            rb_stage.push_back(G);
+          }
+        }
         rblocks.push_back(R);
       }
       if (getenv("CHAP_DEBUG"))
@@ -616,9 +641,12 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_rblocks, rblocks));
   TRY(B.upload(&d_rb_row, rb_row));
   TRY(B.upload(&d_rb_cv, rb_cv));
+  RowStage* d_rb_stage;
+  TRY(B.upload(&d_rb_stage, rb_stage));
   int32_t* d_rb_perm;
   TRY(B.upload(&d_rb_perm, rb_perm));
   DevProblem& D = P->dp;
+  D.rb_stage = d_rb_stage;
   D.rblocks = d_rblocks;
   D.n_rblocks = (int32_t)rblocks.size();
   D.n_gtiles = n_gtiles;

@@ -97,19 +97,31 @@ constexpr int kRowVmax = 32768;                   // variables per block: int32 
 constexpr int kRowWpb = kRowVmax / 32;            // bitset words per block
 constexpr int kRowConsumers = kRowThreads - 32;   // consumer threads (the last warp produces)
 #ifndef CHAP_ROW_PER
-#define CHAP_ROW_PER 4
+#define CHAP_ROW_PER 2
 #endif
 #ifndef CHAP_ROW_STAGES
-#define CHAP_ROW_STAGES 3
+#define CHAP_ROW_STAGES 2
+#endif
+#ifndef CHAP_ROW_SPAN
+#define CHAP_ROW_SPAN 2000
 #endif
 constexpr int kRowPer = CHAP_ROW_PER;             // entries per consumer thread per stage
-constexpr int kRowChunk = kRowPer * kRowConsumers;   // entries per TMA stage (7.75 KB rows + 7.75 KB columns)
-constexpr int kRowStages = CHAP_ROW_STAGES;       // stages of the entry ring (93 KB at 4 x 3)
+constexpr int kRowChunk = kRowPer * kRowConsumers;   // max entries per stage (a multiple of 4)
+constexpr int kRowSpan = CHAP_ROW_SPAN;           // max rows of row state per stage
+constexpr int kRowStages = CHAP_ROW_STAGES;       // stages of the ring (entries + row state)
+static_assert(kRowChunk % 4 == 0, "stages start on 16-byte boundaries");
 struct RowBlock {
   int32_t p0;                 // first column (internal order): column k of block b is p0 + k nb
   int32_t nv;                 // columns
   int32_t es[kRowCluster + 1];   // entry slices [es[s], es[s+1]), multiples of 4
-  int32_t pad;
+  int32_t st[kRowCluster + 1];   // the stages of slice s: [st[s], st[s+1]) in DevProblem::rb_stage
+  int32_t pad[2];
+};
+// One stage of a slice: entries [e0, e0 + ne) (a multiple of 4 each) whose rows lie in [r0, r0 + nr):
+// the row state of those rows comes with the entries by one bulk copy; nr = 0: the stage's rows span
+// more than kRowSpan rows and its row state is gathered instead.
+struct RowStage {
+  int32_t e0, ne, r0, nr;
 };
 
 // Per-column result competing for the global best move.
@@ -224,6 +236,7 @@ struct DevProblem {
   const int32_t* rb_perm;    // [n_rblocks][kRowVmax] user index of column k of block b (block order)
   const int32_t* rb_row;     // [entries] row of each entry (sorted within a slice)
   const uint32_t* rb_cv;     // [entries] column within the block (low 16 bits) | int16 a_ij (high 16)
+  const RowStage* rb_stage;  // stages of the slices (RowBlock::st)
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   double auto_delta;
 };

@@ -780,14 +780,18 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
 // block's columns over distributed shared memory, finishes those columns (tabu R13, R6) and keeps
 // its best; a second barrier frees the counters for the next block (blocks round-robin over the
 // clusters).
-// Each CTA streams its slice of a block in chunks of kRowChunk entries by bulk copies (TMA,
-// cp.async.bulk) into a kRowStages-deep shared-memory ring. The last warp is the producer: its
-// lane 0 refills a stage as soon as the consumers release it (empty barrier: every consumer warp
-// has moved the stage's entries to registers; full barrier: the copy's bytes landed), so the
-// stream's bytes in flight depend neither on registers nor on the consumers' progress.
+// Each CTA streams its slice of a block in stages (RowStage, cut on the host): a stage's entries
+// (row, column | coefficient; <= kRowChunk) and the row state of the rows they span (<= kRowSpan
+// consecutive 16-byte records, one bulk copy: the entries are sorted by row) arrive together by
+// bulk copies (TMA, cp.async.bulk) into a kRowStages-deep shared-memory ring, so that no consumer
+// waits on a row-state gather: the kernel streams. The last warp is the producer: its lane 0
+// refills a stage as soon as the consumers release it (empty barrier: every consumer warp has
+// finished with the stage; full barrier: the copies' bytes landed). A stage whose rows span more
+// than kRowSpan rows (very sparse slices) gathers its row state instead (nr = 0).
 struct RowRing {
   int32_t row[kRowStages][kRowChunk];
   uint32_t cv[kRowStages][kRowChunk];
+  double2 rs[kRowStages][kRowSpan];
   uint64_t full[kRowStages];
   uint64_t empty[kRowStages];
 };
@@ -832,24 +836,26 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
   for (int vb = cid; vb < P.n_rblocks; vb += ncl) {
     const RowBlock& B = P.rblocks[vb];
     const int p0 = B.p0, nv = B.nv, nb = P.n_rblocks;
-    const int s0 = B.es[rank], s1 = B.es[rank + 1];
-    const int nch = (s1 - s0 + kRowChunk - 1) / kRowChunk;
+    const int st0 = B.st[rank], nch = B.st[rank + 1] - st0;
     for (int i = tid; i < nv; i += kRowThreads) sc[i] = 0;
     for (int i = tid; i < (nv + 31) / 32; i += kRowThreads) bits[i] = __ldg(XB + (size_t)vb * kRowWpb + i);
     __syncthreads();
     if (producer) {
       if (lane == 0)
         for (int c = 0; c < nch; ++c) {
-          const int q = g + c, st = q % kRowStages, e = s0 + c * kRowChunk, len = min(kRowChunk, s1 - e);
+          const int q = g + c, st = q % kRowStages;
+          const RowStage G = P.rb_stage[st0 + c];
           if (q >= kRowStages) mbar_wait(&R.empty[st], (unsigned)((q / kRowStages) - 1) & 1u);
-          mbar_expect_tx(&R.full[st], (unsigned)(8 * len));
-          tma_load_1d(R.row[st], P.rb_row + e, 4u * len, &R.full[st]);
-          tma_load_1d(R.cv[st], P.rb_cv + e, 4u * len, &R.full[st]);
+          mbar_expect_tx(&R.full[st], (unsigned)(8 * G.ne + 16 * G.nr));
+          tma_load_1d(R.row[st], P.rb_row + G.e0, 4u * G.ne, &R.full[st]);
+          tma_load_1d(R.cv[st], P.rb_cv + G.e0, 4u * G.ne, &R.full[st]);
+          if (G.nr > 0) tma_load_1d(R.rs[st], RS + G.r0, 16u * G.nr, &R.full[st]);
         }
       __syncwarp();
     } else {
       for (int c = 0; c < nch; ++c) {
-        const int q = g + c, st = q % kRowStages, len = min(kRowChunk, s1 - (s0 + c * kRowChunk));
+        const int q = g + c, st = q % kRowStages;
+        const RowStage G = P.rb_stage[st0 + c];
         mbar_wait(&R.full[st], (unsigned)(q / kRowStages) & 1u);
         int id[kRowPer];
         uint32_t u[kRowPer];
@@ -857,13 +863,12 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 #pragma unroll
         for (int k = 0; k < kRowPer; ++k) {
           const int i = tid + k * kRowConsumers;
-          id[k] = i < len ? R.row[st][i] : -1;
-          u[k] = i < len ? R.cv[st][i] : 0u;
+          id[k] = i < G.ne ? R.row[st][i] : 0;
+          u[k] = i < G.ne ? R.cv[st][i] : 0u;   // 0: no entry, or inert padding (a coefficient is never 0)
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[st]);   // the stage's entries are in registers
 #pragma unroll
-        for (int k = 0; k < kRowPer; ++k) rv[k] = id[k] >= 0 ? __ldg(RS + id[k]) : make_double2(-INFINITY, 0.0);
+        for (int k = 0; k < kRowPer; ++k)
+          rv[k] = u[k] == 0u ? make_double2(-INFINITY, 0.0) : (G.nr > 0 ? R.rs[st][id[k] - G.r0] : __ldg(RS + id[k]));
 #pragma unroll
         for (int k = 0; k < kRowPer; ++k) {
           // 2·p(w, r, r + d) with d = a (1 - 2x̄), in integers: satisfied
@@ -880,6 +885,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
           const int p2 = z0 ? (z1 ? 0 : -2 * iw) : (z1 ? 2 * iw : (nd > 0 ? iw : -iw));
           if (p2 != 0) atomicAdd(sc + c2, p2);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&R.empty[st]);   // the stage's entries and row state are consumed
       }
     }
     g += nch;
@@ -974,7 +981,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 // offsets |d| < 2^28; with other weights the F, β2, α2 words are floats summed in double (same
 // candidates, scores up to summation order), and a tile with a larger offset is
 // evaluated column by column by gen_column_serial.
-constexpr int kG32Max = 512;                    // entries per general tile
+#ifndef CHAP_G32_MAX
+#define CHAP_G32_MAX 512
+#endif
+constexpr int kG32Max = CHAP_G32_MAX;           // entries per general tile
 constexpr int kKeyMax = (1 << 28) - 1;          // key of entries that are never in a prefix
 constexpr int kKeyLim = kKeyMax - 2;            // |offset| limit of the int path (bounds clamp here)
 struct __align__(16) GenWarp {
