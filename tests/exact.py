@@ -143,3 +143,39 @@ def alg1(rows, r, x, w, j, l, u, is_integer):
     if best is None:
         return xb, None
     return best[1], best[2]
+
+
+def rounding_ambiguous(rows, r, x, j, col_rows, values, is_integer, l, u, eps=1e-9):
+    """True when Algorithm 1's result for column j is decided by a quantity within rounding distance
+    of a threshold, so that an fp64 evaluation (residuals summed in any order) may legitimately take
+    the other branch of a `r <= 0` test or merge two distinct breakpoints (tolerance
+    mode). Checked, per row i of the column whose terms are not all integers (an all-integer row is
+    exact in fp64): |r_i| and |r_i + a_ij (v - x̄_j)| for the given candidate values v against
+    eps * (|b_i| + Σ_k |a_ik x̄_k|); on a continuous column also two distinct breakpoints, or a
+    breakpoint and a finite bound, closer than eps * (1 + |t|)."""
+    xb = F(x[j])
+    ts = []
+    for i in col_rows:
+        a_row, b, _, _ = rows[i]
+        terms = [a_row[k] * F(x[k]) for k in a_row]
+        exact_row = b.denominator == 1 and all(t.denominator == 1 for t in terms)
+        scale = abs(b) + sum(abs(t) for t in terms)
+        a = a_row[j]
+        if not is_integer:
+            ts.append(xb - r[i] / a)
+        if exact_row:
+            continue
+        if abs(r[i]) <= eps * scale:
+            return True
+        for v in values:
+            q = r[i] + a * (F(v) - xb)
+            # on a continuous column a row whose own breakpoint is v is tight there by construction
+            # (Algorithm 1 orders it by its marker, not by a residual test)
+            if abs(q) <= eps * scale and (is_integer or q != 0):
+                return True
+    if not is_integer:
+        pts = sorted(set(ts) | {F(q) for q in (l, u) if math.isfinite(q)})
+        for p0, p1 in zip(pts, pts[1:]):
+            if p1 - p0 <= eps * (1 + abs(p1)):
+                return True
+    return False

@@ -430,6 +430,7 @@ def test_sorted_continuous_columns_tolerance_mode():
             if j in cols:
                 cols[j].append(i)
     r = exact.residuals(rows, x)
+    n_cols = n_amb = 0
     for j in sample:
         if lb[j] == ub[j]:
             continue
@@ -438,8 +439,15 @@ def test_sorted_continuous_columns_tolerance_mode():
         if sc is None:
             assert gs[j] == -math.inf, j
             continue
+        n_cols += 1
+        # a column whose result hinges on a residual within rounding of 0 (here typically
+        # the cutoff row, c.x - cut nearly 0 after the move) is outside the tolerance contract
+        if exact.rounding_ambiguous(rows, r, x, j, cols[j], (v, gx[j]), bool(inst.is_int[j]), lb[j], ub[j]):
+            n_amb += 1
+            continue
         assert abs(gs[j] - float(sc)) <= 1e-9 * max(1.0, abs(float(sc))), (j, gs[j], float(sc))
         assert abs(gx[j] - float(v)) <= 1e-9 * max(1.0, abs(float(v))), (j, gx[j], float(v))
+    assert n_cols > 100 and n_amb <= 0.1 * n_cols, (n_cols, n_amb)
 
 
 def test_eval_rejects_negative_weights_and_bad_x():
