@@ -181,6 +181,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   I.nnz_norm = nnz_norm;
   I.nnz_cut = nnz_cut;
   I.exact_integer_data = exact ? 1 : 0;
+  // every residual an integer (DevProblem::rint_base): integer data, no continuous variable, and every
+  // coefficient (cutoff row included) an integer of magnitude <= 2^22
+  bool rint_base = exact && I.n_continuous == 0;
+  for (int32_t j = 0; j < n && rint_base; ++j)
+    if (std::fabs(cc[j]) > 4194304.0) rint_base = false;
+  for (size_t e = 0; e < nval.size() && rint_base; ++e)
+    if (std::fabs(nval[e]) > 4194304.0) rint_base = false;
   I.auto_cutoff_delta = delta_int ? 1.0 : NAN;
 
   // column degrees (incl. the cutoff entry) and classes
@@ -400,13 +407,14 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     }
     LongCol L{};
     L.scr = lscr;
+    L.tix = lscr + ((k == CC_LBKT) ? ((int64_t)dom + 1 + 2 + (dom + 63) / 64) : 1);
     L.nchunks = nch;
     L.dom = dom;
     L.p = p;
     L.kind = k;
     if (k == CC_LBKT || nch > 1) lfin.push_back(n_long);
     lcols.push_back(L);
-    lscr += (k == CC_LBKT) ? ((int64_t)dom + 1 + 2 + (dom + 63) / 64) : 1;
+    lscr = L.tix + 1;   // accumulators, then the chunk ticket
     ++n_long;
     ++p;
   }
@@ -631,6 +639,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_btiles, btiles));
   TRY(B.upload(&d_bchunks, bchunks));
   TRY(B.upload(&d_gchunks, gchunks));
+  std::vector<WTile> gitems(bchunks);
+  gitems.insert(gitems.end(), gchunks.begin(), gchunks.end());
+  gitems.insert(gitems.end(), wtiles.begin() + n_gtiles, wtiles.begin() + n_gtiles + n_ctiles);
+  gitems.insert(gitems.end(), wtiles.begin(), wtiles.begin() + n_gtiles);
+  gitems.insert(gitems.end(), wtiles.begin() + n_gtiles + n_ctiles, wtiles.end());
+  WTile* d_gitems;
+  TRY(B.upload(&d_gitems, gitems));
   if (lcols.empty()) lcols.push_back(LongCol{});
   int32_t* d_lfin;
   TRY(B.upload(&d_lfin, lfin));
@@ -685,10 +700,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.bchunks = d_bchunks;
   D.n_bchunks = (int32_t)bchunks.size();
   D.gchunks = d_gchunks;
+  D.gitems = d_gitems;
+  D.n_gitems = (int32_t)gitems.size();
   D.n_gchunks = (int32_t)gchunks.size();
   D.n_long = n_long;
   D.n_fixed = I.n_fixed;
   D.auto_delta = I.auto_cutoff_delta;
+  D.rint_base = rint_base ? 1 : 0;
 
   // launch geometry: a persistent grid of (resident blocks) per walker set
   CUDA_TRY(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
@@ -869,7 +887,7 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
                               cudaStream_t s, bool pdl) {
   // k_eval only selects when there are no long columns and no sort tiles: then the last eval kernel
   // (k_eval_gen, else k_eval_bin) selects in its last block and k_eval is not launched
-  const bool sel_only = Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && P->dp.n_lfin == 0 && wgrid == 0;
+  const bool sel_only = Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && wgrid == 0;
   const int gen_sel = (sel_only && ggrid > 0) ? bgrid + ggrid + rgrid : 0;
   const int bin_sel = (sel_only && ggrid == 0 && rgrid == 0 && bgrid > 0) ? bgrid : 0;
   if (bgrid > 0) {
@@ -888,7 +906,7 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
   if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s, pdl));
   if (!gen_sel && !bin_sel)
     TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
-           bgrid + ggrid + rgrid + wgrid));
+           bgrid + ggrid + rgrid + wgrid, Wk.rg > 1 ? 1 : 0));
   return CHAP_OK;
 }
 
@@ -945,7 +963,7 @@ static chap_status eval_launch(const chap_problem* p, const double* x, const flo
   const DevProblem& D = p->dp;
   DevWalkers Wk = eval_walkers(p);
   CUDA_TRY(cudaMemsetAsync(p->e_bad, 0, sizeof(int), s));
-  k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs);
+  k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs, p->dp.rint_base);
   if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, p->e_bad);
   if (cutoff_rhs < INFINITY && D.n > 0)
     k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1);
@@ -1335,7 +1353,7 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
     cudaEventRecordWithFlags(e[4], s, cudaEventRecordExternal);
     k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
                                                                      S->bin_grid + S->gen_grid + S->binrow_grid +
-                                                                         S->genwm_grid);
+                                                                         S->genwm_grid, S->wk.rg > 1 ? 1 : 0);
     cudaEventRecordWithFlags(e[5], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[8], s, cudaEventRecordExternal);
     k_apply<<<dim3(S->apply_grid, S->W), kApplyThreads, 0, s>>>(D, S->wk);
@@ -1383,7 +1401,7 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int32_t* out) {
   if (!S || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or out");
   const DevProblem& D = S->P->dp;
-  const bool sel_only = S->W == 1 && S->wk.rg == 1 && D.n_tiles == 0 && D.n_lfin == 0 && S->genwm_grid == 0;
+  const bool sel_only = S->W == 1 && S->wk.rg == 1 && D.n_tiles == 0 && S->genwm_grid == 0;
   const bool fused = sel_only && (S->gen_grid > 0 || (S->binrow_grid == 0 && S->bin_grid > 0));
   *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + (fused ? 0 : 1) + 1;
   return CHAP_OK;

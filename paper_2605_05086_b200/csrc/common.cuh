@@ -24,11 +24,11 @@ constexpr int kBinThreads = 256;                  // k_eval_bin block
 #define CHAP_BIN_MINB 4
 #endif
 constexpr int kBinMinBlocks = CHAP_BIN_MINB;      // k_eval_bin resident blocks per SM (register budget)
+constexpr int kGenThreads = 256;                  // k_eval_gen block
 #ifndef CHAP_GEN_MINB
-#define CHAP_GEN_MINB 3
+#define CHAP_GEN_MINB 2
 #endif
 constexpr int kGenMinBlocks = CHAP_GEN_MINB;      // k_eval_gen resident blocks per SM (register budget)
-constexpr int kGenThreads = 256;                  // k_eval_gen block
 constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
 constexpr int kBucketMax = 4096;                  // max integer domain of a bucket-scanned column
 constexpr int kApplyThreads = 256;
@@ -67,6 +67,7 @@ struct WTile {
 // A long column split into warp chunks: where its accumulators live in walker scratch.
 struct LongCol {
   int64_t scr;       // offset (doubles) of the accumulators in walker scratch
+  int64_t tix;       // offset (doubles) of the column's chunk ticket (unsigned) in walker scratch
   int32_t nchunks;
   int32_t dom;       // CC_LBKT: u - l + 1
   int32_t p;         // the column (internal order)
@@ -163,7 +164,7 @@ struct WalkerScalars {
   double cdot;                // c.x of the current point (k_cut_dot), for the cutoff row and obj
   long long vcount;           // violated active rows (k_viol_count)
   int wint;                   // every weight is an integer <= 2^20 (the int path of gen32_tile)
-  int pad2;
+  int rint;                   // every residual is an integer (DevProblem::rint_base and an integral cutoff rhs)
 };
 
 // Per-kernel device time (chap_walkers_timing): %globaltimer at every block's start (atomic min)
@@ -189,6 +190,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
       ::"r"(smem_u32(b)), "r"(parity) : "memory");
 }
+// Ampere-style asynchronous copies (cp.async, LDGSTS): per-thread gathers into shared memory,
+// completed by commit/wait groups (no registers held while in flight)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_u32(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
@@ -228,6 +247,8 @@ struct DevProblem {
   const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles
   const WTile* bchunks; int32_t n_bchunks;              // warp chunks of long binary columns
   const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns
+  const WTile* gitems; int32_t n_gitems;                // k_eval_gen's items: bchunks, gchunks, continuous tiles,
+                                                        // general tiles, empty tiles
   const LongCol* lcols;                                 // [n_long]
   const int32_t* lfin; int32_t n_lfin;                  // long columns k_eval finishes
   const RowBlock* rblocks; int32_t n_rblocks;           // row-wise binary blocks (0: not built)
@@ -238,6 +259,8 @@ struct DevProblem {
   const uint32_t* rb_cv;     // [entries] column within the block (low 16 bits) | int16 a_ij (high 16)
   const RowStage* rb_stage;  // stages of the slices (RowBlock::st)
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
+  int32_t rint_base;         // integer data with |coefficients| <= 2^22 and no continuous variable: every
+                             // residual is an integer while the cutoff rhs is (WalkerScalars::rint)
   double auto_delta;
 };
 

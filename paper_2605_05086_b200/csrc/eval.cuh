@@ -9,9 +9,10 @@
 //               sort (line 13) becomes a counting pass over [l, u] (atomic bucket deltas);
 //   k_eval      block tiles of general columns of <= kGenmMax entries (shared-memory bitonic sort
 //               and scan), then the global select: the last block of a walker reduces every
-//               block's best admissible move to the walker's decision (R6).
-// A long column's chunks only add into its accumulators; k_eval, which runs after both chunk
-// kernels, finishes the column and zeroes the accumulators (no tickets or fences). With the
+//               block's best admissible move to the walker's decision (R6); not
+//               launched when it would only select (the last eval kernel's last block selects).
+// A long column's chunks add into its accumulators; the chunk that takes the column's last ticket
+// finishes the column and zeroes the accumulators (walker groups' binary chunks: k_eval). With the
 // integer weights of R11 every delta, β, α and penalty is a multiple of 1/2 and every partial sum
 // is exact, so the order of the atomic additions does not change any result.
 // Every warp-tile slot issues its coalesced CSC loads and one 16-byte row-state gather before
@@ -460,8 +461,54 @@ struct __align__(16) BinWarp {
 };
 constexpr size_t kBinSmem = sizeof(BinWarp) * (kBinThreads / 32);
 
+// The chunk ticket of a long column: every lane's accumulator additions are made visible, then lane 0
+// takes a ticket; true (in every lane) for the chunk that takes the column's last one, which then
+// sees every other chunk's additions (fences on both sides) and finishes the column.
+#ifndef CHAP_TICKET
+#define CHAP_TICKET 1
+#endif
+__device__ __forceinline__ bool long_last(const DevWalkers& Wk, int walker, const LongCol& L, int lane) {
+#if CHAP_TICKET == 0
+  __threadfence();
+#endif
+  __syncwarp();
+  unsigned last = 0u;
+  if (lane == 0) {
+    unsigned* tk = reinterpret_cast<unsigned*>(Wk.lscr + (size_t)walker * Wk.lss + L.tix);
+#if CHAP_TICKET == 0
+    last = atomicAdd(tk, 1u) == (unsigned)(L.nchunks - 1);
+#else
+    // acquire-release at gpu scope: the warp's additions (ordered before by the warp barrier) are
+    // released with the ticket; the last taker acquires every earlier chunk's additions
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(tk) : "memory");
+    last = old == (unsigned)(L.nchunks - 1);
+#endif
+    if (last) *tk = 0u;
+  }
+  last = __shfl_sync(kFull, last, 0);
+#if CHAP_TICKET == 0
+  if (last) __threadfence();
+#endif
+  return last != 0u;
+}
+
+// The end of a long binary column of several chunks: the summed flip score.
+__device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                              const LongCol& L, Best& b, double* oxhat, double* oscore,
+                                              long long kk, int use_tabu) {
+  const int p = L.p;
+  double* acc = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
+  const double s = __ldcg(acc);
+  *acc = 0.0;
+  const double xb = __ldg(Wk.x + (size_t)walker * Wk.xs + p);
+  finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(Wk.tabu + (size_t)walker * Wk.ts + p) : 0, xb,
+                  1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
+}
+
 // A warp chunk (<= kWChunk nonzeros) of a long binary column: warp-reduced flip sum added to the
-// column's accumulator (a single-chunk column finishes in place); k_eval finishes the others.
+// column's accumulator (a single-chunk column finishes in place); the chunk that takes the column's
+// last ticket finishes it.
 __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
                                            const int32_t* __restrict__ TB, const WTile& T, int lane,
@@ -489,15 +536,15 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) own += __shfl_xor_sync(kFull, own, off);
-  if (lane != 0) return;
   const LongCol L = P.lcols[T.e1];
-  const double s = own;
-  if (L.nchunks > 1) {   // k_eval finishes the column after this kernel
-    atomicAdd(Wk.lscr + (size_t)walker * Wk.lss + L.scr, own);
+  if (L.nchunks == 1) {
+    if (lane == 0)
+      finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, 1.0 - xb, own, b, oxhat,
+                      oscore, kk, use_tabu);
     return;
   }
-  finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, 1.0 - xb, s, b, oxhat,
-                  oscore, kk, use_tabu);
+  if (lane == 0) atomicAdd(Wk.lscr + (size_t)walker * Wk.lss + L.scr, own);
+  if (long_last(Wk, walker, L, lane) && lane == 0) lbin_finalize(P, Wk, walker, L, b, oxhat, oscore, kk, use_tabu);
 }
 
 // select_parts > 0: this is the walker's only and last eval kernel and k_eval has nothing but the
@@ -943,11 +990,13 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 // general-column kernel
 // ------------------------------------------------------------------------------------------
 // k_eval_gen evaluates the packed general integer columns (deg + 2 <= kShortDeg) with
-// Algorithm 1 per column, sort-free, in offsets relative to x̄.
+// Algorithm 1 per column, sort-free, in offsets relative to x̄, the chunks of long
+// bounded-integer columns (counting sort) and, in the row-wise binary mode, the chunks
+// of long binary columns.
 //
 // Lines 3-11 in offsets. For an integer column and a row with residual r and coefficient a, the
 // breakpoint of line 3-4 is t = floor(x̄ - r/a) (a > 0) or ceil(x̄ - r/a) (a < 0), so its offset
-// d = t - x̄ = -ceil(r/a) (a > 0) or -floor(r/a) (a < 0) needs neither x̄ nor the column: it is
+// d = t - x̄ = floor(-r/a) (a > 0) or -floor(-r/|a|) (a < 0) needs neither x̄ nor the column: it is
 // computed per entry, slot-parallel, from the gathered row state alone. The six cases of lines
 // 5-11 are the sign of a and of d (d > 0 <=> x̄ < t). With w the row weight they give, in units
 // of half a weight (F = 2δ, β2 = 2β, α2 = 2α, integers for the integral weights of R11):
@@ -961,6 +1010,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 // (an a>0 row's (t,-1,0) entry of line 10-11 carries no delta; its value is the candidate v = d,
 // scored before its +1 entry, R3), so that σ(v) = β + α [v > 0] + Σ_{key_e <= v} δ_e exactly
 // (DESIGN §2.3). Code bit 0: key = v + 1; bit 1: up side (v > 0); bit 2: positive step.
+// When every residual is an integer below 2^23 in magnitude (WalkerScalars::rint) the floor of the
+// quotient is taken without a double division: the float quotient of n = -r by |a| is within one of
+// floor(n/|a|) and its exact float remainder n - f|a| corrects it; otherwise line 3 is
+// the IEEE double division of the oracle.
 //
 // Lines 13-16 without a sort. Candidates (R2, R5) are the entries with v in [l - x̄, u - x̄] and the
 // finite bounds other than x̄. On the up side (v > 0) σ changes only at keys, rising at the
@@ -972,15 +1025,20 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 // the column's entries. The number of positive steps is the number of violated rows of the
 // column (cutoff row included), a few in a tabu walk.
 //
-// A tile holds <= 32 whole columns, <= kG32Max entries, starting on a multiple of 4. Phase 1
-// (slot-parallel, coalesced CSC loads, four gathers in flight per lane): every entry into shared
-// memory as {key << 3 | code, F, β2, α2}. Phase 2 (lane c = column c): one pass for β, α, the
-// nearest candidates and the positive steps, then one pass per four candidates. The columns of
-// a tile have nearly equal lengths (internal order is by degree), so lanes stay balanced.
-// The int path needs weights that are integers <= 2^20 (WalkerScalars::wint; |Σ F| < 2^27) and
-// offsets |d| < 2^28; with other weights the F, β2, α2 words are floats summed in double (same
-// candidates, scores up to summation order), and a tile with a larger offset is
-// evaluated column by column by gen_column_serial.
+// The kernel is a software pipeline per warp over a static round-robin list of warp items (a
+// general tile of <= 32 whole columns and <= kGI entries, or a <= kGI-nonzero chunk of a long
+// column): the CSC range of item i+2 arrives by two bulk copies (TMA, cp.async.bulk, one mbarrier
+// per stage), the row state of every entry of item i+1 and its columns' data by per-lane cp.async
+// gathers into shared memory, while item i is computed from shared memory. No register is held by
+// a load in flight, so a few warps per SM keep ~2 items of gathers outstanding each.
+// A general tile: phase 1 (slot-parallel) turns every entry's row state into {key << 3 | code, F,
+// β2, α2} in place; phase 2 (lane c = column c) makes one pass for β, α, the nearest candidates and
+// the positive steps, then one pass per four candidates. The int path needs weights that are
+// integers <= 2^20 (WalkerScalars::wint; |Σ F| < 2^27) and offsets |d| < 2^28; with other weights
+// the F, β2, α2 words are floats summed in double (same candidates, scores up to summation order,
+// DESIGN §5), and a tile with a larger offset is evaluated column by column by gen_column_serial.
+// A long column's chunks add into its accumulators in walker scratch; the chunk that takes the
+// column's last ticket finishes it (lbkt_finalize / lbin_finalize) and re-arms the accumulators.
 #ifndef CHAP_G32_MAX
 #define CHAP_G32_MAX 512
 #endif
@@ -990,11 +1048,11 @@ constexpr int kKeyLim = kKeyMax - 2;            // |offset| limit of the int pat
 struct __align__(16) GenWarp {
   int4 ent[kG32Max];
 };
-constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
 // a long bounded-integer chunk uses the warp's GenWarp area: int32 histogram, candidate words, stage
 constexpr int kWarpDom = 1024;
 constexpr int kLbktHistBytes = 4 * (kWarpDom + 1 + 3);
 static_assert(kLbktHistBytes + kWarpDom / 8 + 32 * 8 <= (int)sizeof(GenWarp), "LBKT scratch exceeds GenWarp");
+constexpr size_t kGenSmem = sizeof(GenWarp) * (kGenThreads / 32);
 
 __device__ __forceinline__ double next_up(double t) {   // the next double above t
   if (t == 0.0) return 4.9406564584124654e-324;
@@ -1074,45 +1132,95 @@ __device__ void gen_column_serial(const DevProblem& P, const double* __restrict_
 }
 
 // Lines 3-11 of Algorithm 1 for one entry of an integer column in offsets (table above): the
-// entry word key << 3 | code and F, β2, α2 (ints for INTW, else float bits). Sets ovf for an offset
-// beyond the int path.
+// entry word key << 3 | code and F, β2, α2 (ints for INTW, else float bits). rint: every residual
+// is an integer (the exact float-quotient path). Sets ovf for an offset beyond the int path.
+// The case c = 3 [a > 0] + [d >= 0] + [d > 0] indexes the block's table of {code, F, β2, α2} (in units
+// of w): c = 0..5 is (a<0,d<0) (a<0,d=0) (a<0,d>0) (a>0,d<0) (a>0,d=0) (a>0,d>0).
+__device__ __forceinline__ void off_table_init(int4* tab) {
+  switch (threadIdx.x) {
+    case 0: tab[0] = make_int4(0, 2, -2, 0); break;
+    case 1: tab[1] = make_int4(2, 0, -2, 2); break;
+    case 2: tab[2] = make_int4(6, 1, -1, 2); break;
+    case 3: tab[3] = make_int4(5, -1, 2, -2); break;
+    case 4: tab[4] = make_int4(2, 0, 0, -2); break;
+    case 5: tab[5] = make_int4(3, -2, 0, 0); break;
+    default: break;
+  }
+}
 template <bool INTW>
-__device__ __forceinline__ int4 off_entry(double r, float wf, double a, bool& ovf) {
-  const bool live = r > -INFINITY;                 // inert rows: the inactive cutoff row, padding
+__device__ __forceinline__ int4 off_entry(double r, float wf, double a, bool rint, const int4* __restrict__ tab,
+                                          bool& ovf) {
+  const float rf = (float)r;
   const bool pos = a > 0.0;
-  const double qd = (live && r != 0.0) ? r / a : 0.0;
-  const double dd = pos ? -ceil(qd) : -floor(qd);   // t - x̄ of lines 3-4
-  const bool big = !(fabs(dd) <= (double)(kKeyLim - 1));
-  ovf |= live && big;
-  // an offset beyond the int path is clamped (its sign, hence its case, is kept): the general tile
-  // then re-evaluates in double (ovf); for a bounded domain it lies outside [l, u] either way
-  const int d = !live ? 0 : (big ? (dd > 0.0 ? kKeyLim - 1 : 1 - kKeyLim) : (int)dd);
-  int code, key;
-  if (!live || d == 0) { code = 2; key = kKeyMax; }
-  else if (pos) { code = d < 0 ? 5 : 3; key = d + 1; }
-  else { code = d > 0 ? 6 : 0; key = d; }
-  int4 ent;
-  ent.x = (key << 3) | code;
-  if (INTW) {
-    const int w1 = live ? __float2int_rn(wf) : 0, w2 = 2 * w1;
-    ent.y = d == 0 ? 0 : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2));
-    ent.z = pos ? (d < 0 ? w2 : 0) : (d > 0 ? -w1 : -w2);
-    ent.w = pos ? (d <= 0 ? -w2 : 0) : (d >= 0 ? w2 : 0);
+  int d;
+  if (rint && (fabsf(rf) < 8388608.f || rf == -INFINITY)) {
+    // g = floor(n / A), n = -r, A = |a| (integers below 2^23): the float quotient by the approximate
+    // reciprocal is within 1 of n/A, so its floor is g - 1, g or g + 1, and the exact float remainder
+    // n - f A (|f A| < 2^24) decides which. The inert rows (r = -inf) take n = 0, d = 0.
+    const float n = rf == -INFINITY ? 0.f : -rf, A = fabsf((float)a);
+    float ra;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(A));
+    float f = floorf(n * ra);
+    const float rem = fmaf(-f, A, n);
+    f = rem < 0.f ? f - 1.f : (rem >= A ? f + 1.f : f);
+    const int g = __float2int_rz(f);
+    d = pos ? g : -g;
   } else {
-    const float w1 = live ? wf : 0.f, w2 = 2.f * w1;
-    ent.y = __float_as_int(d == 0 ? 0.f : (pos ? (d < 0 ? -w1 : -w2) : (d > 0 ? w1 : w2)));
-    ent.z = __float_as_int(pos ? (d < 0 ? w2 : 0.f) : (d > 0 ? -w1 : -w2));
-    ent.w = __float_as_int(pos ? (d <= 0 ? -w2 : 0.f) : (d >= 0 ? w2 : 0.f));
+    const bool live = r > -INFINITY;               // inert rows: the inactive cutoff row, padding
+    const double qd = (live && r != 0.0) ? r / a : 0.0;
+    const double dd = pos ? -ceil(qd) : -floor(qd);   // t - x̄ of lines 3-4
+    const bool big = !(fabs(dd) <= (double)(kKeyLim - 1));
+    ovf |= live && big;
+    // an offset beyond the int path is clamped (its sign, hence its case, is kept): the general tile
+    // then re-evaluates in double (ovf); for a bounded domain it lies outside [l, u] either way
+    d = !live ? 0 : (big ? (dd > 0.0 ? kKeyLim - 1 : 1 - kKeyLim) : (int)dd);
+  }
+  const int4 t = tab[(pos ? 3 : 0) + (d >= 0) + (d > 0)];
+  int4 ent;
+  ent.x = ((d == 0 ? kKeyMax : d + (int)pos) << 3) | t.x;
+  // the inert rows carry w = 0 in the row state: all three words vanish
+  if (INTW) {
+    const int w1 = __float2int_rn(wf);
+    ent.y = w1 * t.y;
+    ent.z = w1 * t.z;
+    ent.w = w1 * t.w;
+  } else {
+    ent.y = __float_as_int(wf * (float)t.y);
+    ent.z = __float_as_int(wf * (float)t.z);
+    ent.w = __float_as_int(wf * (float)t.w);
   }
   return ent;
 }
 
-// One tile of packed general integer columns (see above). INTW: integral weights <= 2^20.
+// One round of a general tile: slots 4 lane .. 4 lane + 3 of its 128 (one 16-byte index load, two
+// 16-byte coefficient loads); out of range: the inert dummy row.
+struct GenRound {
+  int4 id;
+  double2 a01, a23;
+};
+__device__ __forceinline__ GenRound gen_round(const DevProblem& P, const WTile& T, int k0) {
+  GenRound R;
+  R.id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
+  R.a01 = make_double2(1.0, 1.0);
+  R.a23 = R.a01;
+  if (k0 < T.e1 - T.e0) {
+    R.id = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0 + k0));
+    R.a01 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0 + k0));
+    R.a23 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0 + k0) + 1);
+  }
+  return R;
+}
+
+// One tile of packed general integer columns (see above). INTW: integral weights <= 2^20. R holds
+// the tile's first round (loaded by the caller); the rounds are software-pipelined (the next round's
+// loads are in flight while this round's gathers return), and when the warp's next item Tn is a
+// general tile its first round is loaded into R before phase 2.
 template <bool INTW>
 __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __restrict__ X,
                                            const double2* __restrict__ RS, int st,
-                                           const int32_t* __restrict__ TB, const WTile& T, int lane,
-                                           GenWarp& S, Best& b, double* oxhat, double* oscore,
+                                           const int32_t* __restrict__ TB, const WTile& T, const WTile& Tn,
+                                           bool has_next, GenRound& R, int lane, GenWarp& S, bool rint,
+                                           const int4* __restrict__ tab, Best& b, double* oxhat, double* oscore,
                                            long long kk, int use_tabu) {
   const int nc = T.ncols, len = T.e1 - T.e0;
   // column data of lane c (loads in flight during phase 1)
@@ -1127,116 +1235,139 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
     l = __ldg(P.lb + p);
     u = __ldg(P.ub + p);
   }
+  int4* ent = S.ent;
   // phase 1: lines 3-11 per entry (slots 4 lane .. 4 lane + 3 of each round of 128)
   bool ovf = false;
   for (int r0 = 0; r0 < len; r0 += 4 * 32) {
     const int k0 = r0 + 4 * lane;
-    int4 id = make_int4(P.dummy_row, P.dummy_row, P.dummy_row, P.dummy_row);
-    double2 a01 = make_double2(1.0, 1.0), a23 = a01;
-    if (k0 < len) {
-      id = __ldcs(reinterpret_cast<const int4*>(P.row_idx + T.e0 + k0));
-      a01 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0 + k0));
-      a23 = __ldcs(reinterpret_cast<const double2*>(P.val + T.e0 + k0) + 1);
-    }
     double2 rv[4];
-    rv[0] = __ldg(RS + (size_t)id.x * st);
-    rv[1] = __ldg(RS + (size_t)id.y * st);
-    rv[2] = __ldg(RS + (size_t)id.z * st);
-    rv[3] = __ldg(RS + (size_t)id.w * st);
+    rv[0] = __ldg(RS + (size_t)R.id.x * st);
+    rv[1] = __ldg(RS + (size_t)R.id.y * st);
+    rv[2] = __ldg(RS + (size_t)R.id.z * st);
+    rv[3] = __ldg(RS + (size_t)R.id.w * st);
+    const double2 a01 = R.a01, a23 = R.a23;
+    if (r0 + 4 * 32 < len) R = gen_round(P, T, k0 + 4 * 32);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
-      const int4 ent = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), a, ovf);
-      S.ent[k0 + q] = ent;
+      ent[k0 + q] = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), a, rint, tab, ovf);
     }
   }
+  if (has_next && Tn.kind == CC_GEN) R = gen_round(P, Tn, 4 * lane);
   ovf = __any_sync(kFull, ovf);
   __syncwarp();
+  if (lane >= nc) return;   // (the kernel's loop reconverges the warp after every item)
   if (ovf) {   // an offset beyond the int path: every column of the tile in double
-    if (lane < nc) {
-      double v, s;
-      gen_column_serial(P, X, RS, st, p, v, s);
-      offer_column(p, j, TB, xb, v, s, b, oxhat, oscore, kk, use_tabu);
-    }
-    __syncwarp();
+    double v, sv;
+    gen_column_serial(P, X, RS, st, p, v, sv);
+    offer_column(p, j, TB, xb, v, sv, b, oxhat, oscore, kk, use_tabu);
     return;
   }
-  if (lane < nc) {
-    // phase 2, pass 0: β, α, nearest candidates (bounds included), positive steps
-    const bool ufin = isfinite(u), lfin = isfinite(l);
-    const double hid = u - xb, lod = l - xb;
-    const int hi = ufin ? (int)fmin(hid, (double)kKeyLim) : kKeyLim;
-    const int lo = lfin ? (int)fmax(lod, -(double)kKeyLim) : -kKeyLim;
-    int vup = (ufin && hi > 0) ? hi : INT_MAX;
-    int vdn = (lfin && lo < 0) ? lo : INT_MIN;
-    using Acc = typename std::conditional<INTW, int, double>::type;
-    Acc b2 = 0, a2 = 0;
-    unsigned long long pm = 0ull;
-    for (int e = cb; e < ce; ++e) {
-      const int4 E = S.ent[e];
-      if (INTW) {
-        b2 += E.z;
-        a2 += E.w;
-      } else {
-        b2 += (double)__int_as_float(E.z);
-        a2 += (double)__int_as_float(E.w);
-      }
-      const int code = E.x & 7, v = (E.x >> 3) - (code & 1);
-      const bool up = code & 2;
-      if (up ? v > hi : v < lo) continue;   // outside [l, u] (and every tight / inert entry)
+  // phase 2, pass 0: β, α, the nearest candidate on each side (bounds included) and the positive
+  // steps (the first six kept in registers); then σ2 at up to four candidates per pass over the
+  // column's entries: {vup, vdn, step 1, step 2}, {steps 3..6}, further steps (rare) four per pass.
+  const bool ufin = isfinite(u), lfin = isfinite(l);
+  const double hid = u - xb, lod = l - xb;
+  const int hi = ufin ? (int)fmin(hid, (double)kKeyLim) : kKeyLim;
+  const int lo = lfin ? (int)fmax(lod, -(double)kKeyLim) : -kKeyLim;
+  int vup = (ufin && hi > 0) ? hi : INT_MAX;
+  int vdn = (lfin && lo < 0) ? lo : INT_MIN;
+  using Acc = typename std::conditional<INTW, int, double>::type;
+  auto fv = [](int bits) -> Acc { if (INTW) return (Acc)bits; else return (Acc)__int_as_float(bits); };
+  Acc b2 = 0, a2 = 0;
+  int c2 = INT_MIN, c3 = INT_MIN, c4 = INT_MIN, c5 = INT_MIN, c6 = INT_MIN, c7 = INT_MIN, nstep = 0;
+  for (int e = cb; e < ce; ++e) {
+    const int4 E = ent[e];
+    b2 += fv(E.z);
+    a2 += fv(E.w);
+    const int code = E.x & 7;
+    const int v = (E.x >> 3) - (code & 1);
+    // up side (codes 6, 3 and the tight code 2, whose v exceeds hi): in bounds iff v <= hi;
+    // down side (codes 0, 5): iff v >= lo
+    const bool up = code & 2;
+    const bool inb = up ? v <= hi : v >= lo;
+    if (inb) {
       if (up) vup = min(vup, v); else vdn = max(vdn, v);
-      if (code & 4) pm |= 1ull << (e - cb);
-    }
-    // pass 1..: σ2 at up to four candidates per pass over the entries
-    Acc bs2 = 0;
-    int bv = 0;
-    bool have = false;
-    int cq[4];
-    int nq = 0;
-    auto flush = [&]() {
-      Acc acc[4];
-      int lim[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[q] = 0;
-        lim[q] = q < nq ? ((cq[q] << 3) | 7) : INT_MIN;   // key <= v  <=>  key << 3 | code <= v << 3 | 7
+      if (code & 4) {   // a positive step (codes 6, 5)
+        c7 = nstep == 5 ? v : c7;
+        c6 = nstep == 4 ? v : c6;
+        c5 = nstep == 3 ? v : c5;
+        c4 = nstep == 2 ? v : c4;
+        c3 = nstep == 1 ? v : c3;
+        c2 = nstep == 0 ? v : c2;
+        ++nstep;
       }
-      for (int e = cb; e < ce; ++e) {
-        const int2 E = *reinterpret_cast<const int2*>(&S.ent[e]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (E.x <= lim[q]) {
-            if (INTW) acc[q] += E.y; else acc[q] += (double)__int_as_float(E.y);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q >= nq) break;
-        const Acc sg = b2 + acc[q] + (cq[q] > 0 ? a2 : (Acc)0);
-        if (!have || better_off(sg, cq[q], bs2, bv)) { bs2 = sg; bv = cq[q]; have = true; }
-      }
-      nq = 0;
-    };
-    if (vup != INT_MAX) cq[nq++] = vup;
-    if (vdn != INT_MIN) cq[nq++] = vdn;
-    for (unsigned long long m = pm; m; m &= m - 1) {
-      const int e = cb + __ffsll((long long)m) - 1;
-      const int x3 = S.ent[e].x;
-      const int v = (x3 >> 3) - (x3 & 1);
-      if (v != vup && v != vdn) cq[nq++] = v;
-      if (nq == 4) flush();
     }
-    if (nq > 0) flush();
-    double v = xb, s = -INFINITY;
-    if (have) {
-      s = 0.5 * (double)bs2;
-      // a bound beyond the clamp is the farthest candidate of its side: report its exact value
-      v = (bv == hi && ufin && hid > (double)kKeyLim) ? u : ((bv == lo && lfin && lod < -(double)kKeyLim) ? l : xb + (double)bv);
-    }
-    offer_column(p, j, TB, xb, v, s, b, oxhat, oscore, kk, use_tabu);
   }
-  __syncwarp();
+  // the best (σ2, v) of the column under R4: with integer scores one packed key, higher is better
+  // (σ2, then smaller |v|, then smaller v)
+  long long bkey = LLONG_MIN;
+  Acc bs2 = 0;
+  int bv = 0;
+  bool have = false;
+  auto offer2 = [&](Acc sg, int v) {
+    if (INTW) {
+      const unsigned tie = 0x7fffffffu - (((unsigned)abs(v) << 1) | (v > 0 ? 1u : 0u));
+      bkey = max(bkey, (long long)sg * 4294967296ll + (long long)tie);
+    } else if (!have || better_off(sg, v, bs2, bv)) {
+      bs2 = sg;
+      bv = v;
+      have = true;
+    }
+  };
+  // σ2 at up to four candidate offsets (INT_MAX / INT_MIN: none) in one pass
+  auto score4 = [&](int q0, int q1, int q2, int q3) {
+    auto lim = [](int q) { return (q == INT_MAX || q == INT_MIN) ? INT_MIN : ((q << 3) | 7); };   // key <= v  <=>  x <= v << 3 | 7
+    const int l0 = lim(q0), l1 = lim(q1), l2 = lim(q2), l3 = lim(q3);
+    Acc s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int e = cb; e < ce; ++e) {
+      const int2 E = *reinterpret_cast<const int2*>(&ent[e]);
+      const Acc F = fv(E.y);
+      s0 += E.x <= l0 ? F : (Acc)0;
+      s1 += E.x <= l1 ? F : (Acc)0;
+      s2 += E.x <= l2 ? F : (Acc)0;
+      s3 += E.x <= l3 ? F : (Acc)0;
+    }
+    if (l0 != INT_MIN) offer2(b2 + s0 + (q0 > 0 ? a2 : (Acc)0), q0);
+    if (l1 != INT_MIN) offer2(b2 + s1 + (q1 > 0 ? a2 : (Acc)0), q1);
+    if (l2 != INT_MIN) offer2(b2 + s2 + (q2 > 0 ? a2 : (Acc)0), q2);
+    if (l3 != INT_MIN) offer2(b2 + s3 + (q3 > 0 ? a2 : (Acc)0), q3);
+  };
+  score4(vup, vdn, c2, c3);
+  if (nstep > 2) score4(c4, c5, c6, c7);
+  if (nstep > 6) {   // steps 7, 8, ... (rare): rescan for them, four per pass
+    int q0 = INT_MIN, q1 = INT_MIN, q2 = INT_MIN, q3 = INT_MIN;
+    int seen = 0, nq = 0;
+    for (int e = cb; e < ce; ++e) {
+      const int x3 = ent[e].x, code = x3 & 7, v = (x3 >> 3) - (code & 1);
+      const bool up = code & 2;
+      if (!((code & 4) && (up ? v <= hi : v >= lo))) continue;
+      if (seen++ < 6) continue;
+      q0 = nq == 0 ? v : q0;
+      q1 = nq == 1 ? v : q1;
+      q2 = nq == 2 ? v : q2;
+      q3 = nq == 3 ? v : q3;
+      if (++nq == 4) {
+        score4(q0, q1, q2, q3);
+        nq = 0;
+        q0 = q1 = q2 = q3 = INT_MIN;
+      }
+    }
+    if (nq > 0) score4(q0, q1, q2, q3);
+  }
+  if (INTW && bkey != LLONG_MIN) {
+    have = true;
+    bs2 = (Acc)(bkey >> 32);
+    const unsigned t = 0x7fffffffu - (unsigned)(bkey & 0xffffffffll);
+    bv = (t & 1u) ? (int)(t >> 1) : -(int)(t >> 1);
+  }
+  double v = xb, sres = -INFINITY;
+  if (have) {
+    sres = 0.5 * (double)bs2;
+    // a bound beyond the clamp is the farthest candidate of its side: report its exact value
+    v = (bv == hi && ufin && hid > (double)kKeyLim) ? u : ((bv == lo && lfin && lod < -(double)kKeyLim) ? l : xb + (double)bv);
+  }
+  offer_column(p, j, TB, xb, v, sres, b, oxhat, oscore, kk, use_tabu);
 }
 
 // A warp chunk (<= kBktChunk nonzeros) of a long general integer column with domain [l, u],
@@ -1249,13 +1380,13 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
 // integral weights <= 2^20 (INTW) a chunk first counts F into a warp-private int32 shared-memory
 // histogram (|Σ| <= kBktChunk 2^21 < 2^31) and then adds each nonzero bucket once; other weights, or
 // domains above kWarpDom, aggregate per warp instead (lanes with equal buckets: __match_any_sync,
-// the lowest lane adds the group's sum). lbkt_finalize (k_eval) scans D in coalesced rounds of 32
-// buckets, takes line 16's argmax with R4 and zeroes the accumulators.
+// the lowest lane adds the group's sum). The chunk that takes the column's last ticket scans D
+// (lbkt_finalize).
 template <bool INTW>
 __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers& Wk, int walker,
                                            const double* __restrict__ X, const double2* __restrict__ RS,
-                                           int st, const WTile& T, int lane, unsigned char* wmem) {
-  const LongCol L = P.lcols[T.e1];
+                                           int st, const WTile& T, const LongCol& L, int lane, unsigned char* wmem,
+                                           bool rint, const int4* __restrict__ tab) {
   const int p = T.p0, dom = L.dom, len = T.ncols;
   const int* __restrict__ ridx = P.row_idx + T.e0;
   const double* __restrict__ rval = P.val + T.e0;
@@ -1277,6 +1408,8 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
   using Acc = typename std::conditional<INTW, int, double>::type;
   Acc b2 = 0, a2 = 0;
   bool ovf = false;   // irrelevant here: a clamped offset lies outside [l, u]
+  int hb = -1, hs = 0, hwq = -1;   // the lane's pending bucket and sum, candidate word and bits
+  unsigned hbits = 0u;
   for (int r0 = 0; r0 < len; r0 += 32 * kWSlotsGen) {
     int id[kWSlotsGen];
     double av[kWSlotsGen];
@@ -1291,7 +1424,7 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     for (int q = 0; q < kWSlotsGen; ++q) rv[q] = __ldg(RS + (size_t)id[q] * st);
 #pragma unroll
     for (int q = 0; q < kWSlotsGen; ++q) {
-      const int4 E = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), av[q], ovf);
+      const int4 E = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), av[q], rint, tab, ovf);
       if (INTW) { b2 += E.z; a2 += E.w; } else { b2 += (double)__int_as_float(E.z); a2 += (double)__int_as_float(E.w); }
       const int code = E.x & 7, key = E.x >> 3;
       int bq = -1, cq = -1;
@@ -1304,9 +1437,20 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
         }
         if (cv >= 0 && cv < dom) cq = cv;
       }
-      if (local) {
-        if (bq >= 0 && E.y != 0) atomicAdd(hist + bq, E.y);
-        if (cq >= 0) atomicOr(hcw + (cq >> 5), 1u << (cq & 31));
+      if (local) {   // run-length per lane: breakpoints of a long column crowd onto a few buckets
+        if (bq != hb) {
+          if (hb >= 0 && hs != 0) atomicAdd(hist + hb, hs);
+          hb = bq;
+          hs = 0;
+        }
+        hs += bq >= 0 ? E.y : 0;
+        const int cw = cq >= 0 ? (cq >> 5) : -1;
+        if (cw != hwq) {
+          if (hwq >= 0) atomicOr(hcw + hwq, hbits);
+          hwq = cw;
+          hbits = 0u;
+        }
+        hbits |= cq >= 0 ? (1u << (cq & 31)) : 0u;
         continue;
       }
       // bucket deltas: one atomic per distinct bucket of the 32 entries
@@ -1328,6 +1472,8 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     }
   }
   if (local) {   // one addition per nonzero bucket and candidate word
+    if (hb >= 0 && hs != 0) atomicAdd(hist + hb, hs);
+    if (hwq >= 0) atomicOr(hcw + hwq, hbits);
     __syncwarp();
     for (int q = lane; q <= dom; q += 32) {
       const int h = hist[q];
@@ -1343,15 +1489,15 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     b2 += __shfl_xor_sync(kFull, b2, off);
     a2 += __shfl_xor_sync(kFull, a2, off);
   }
-  if (lane == 0) {   // k_eval scans and finishes the column after this kernel
+  if (lane == 0) {
     if (b2 != 0) atomicAdd(BA, 0.5 * (double)b2);
     if (a2 != 0) atomicAdd(BA + 1, 0.5 * (double)a2);
   }
 }
 
-// The end of a long bounded-integer column (k_eval, after every chunk has added its part): line 14
-// as a scan of D in coalesced rounds of 32 buckets, line 16 with R4; the accumulators are zeroed
-// for the next pass.
+// The end of a long bounded-integer column (after every chunk has added its part): line 14 as a scan
+// of D in coalesced rounds of 32 buckets, line 16 with R4; the accumulators are zeroed for the next
+// pass.
 __device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
                                               const LongCol& L, int lane, Best& b, double* oxhat,
                                               double* oscore, long long kk, int use_tabu) {
@@ -1409,29 +1555,19 @@ __device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalk
                     oscore, kk, use_tabu);
 }
 
-// The end of a long binary column of several chunks: the summed flip score.
-__device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
-                                              const LongCol& L, Best& b, double* oxhat, double* oscore,
-                                              long long kk, int use_tabu) {
-  const int p = L.p;
-  double* acc = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
-  const double s = __ldcg(acc);
-  *acc = 0.0;
-  const double xb = __ldg(Wk.x + (size_t)walker * Wk.xs + p);
-  finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(Wk.tabu + (size_t)walker * Wk.ts + p) : 0, xb,
-                  1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
-}
-
 // wm_mode 1 (walker groups): the integer general tiles and the empty columns are k_eval_gen_wm's;
 // this kernel takes the long bounded-integer chunks and the tiles holding a continuous column.
-// with_lbin (one walker, row-wise binary mode): this kernel also takes the long binary chunks,
-// whose gather latency then overlaps the general tiles' arithmetic
+// with_lbin (one walker, row-wise binary mode): this kernel also takes the long binary chunks.
+// Warp w of the grid takes items w, w + nwarps, ... of its range of P.gitems (long-column chunks
+// first: their gathers overlap the packed tiles of other warps).
 __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProblem P, DevWalkers Wk, double* oxhat,
-                                                              double* oscore, int part_base, int wm_mode,
-                                                              int with_lbin, int select_parts, chap_move* best_out) {
+                                                                      double* oscore, int part_base, int wm_mode,
+                                                                      int with_lbin, int select_parts,
+                                                                      chap_move* best_out) {
   pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ Best sm_b[32];
+  __shared__ Best sm_b[kGenThreads / 32];
+  __shared__ int4 s_tab[6];
   const int walker = blockIdx.y;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const WalkerScalars* sc = Wk.sc + walker;
@@ -1444,6 +1580,8 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   const int use_tabu = Wk.use_tabu;
   GenWarp& S = reinterpret_cast<GenWarp*>(smem)[wid];
   KT_BEGIN(Wk, 1);
+  off_table_init(s_tab);
+  __syncthreads();
   TileCtx C;
   C.x = X;
   C.rs = RV;
@@ -1454,42 +1592,46 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   C.oscore = oscore;
   Best b;
   b.init();
-  const int nwarps = gridDim.x * (kGenThreads / 32);
-  int t = blockIdx.x * (kGenThreads / 32) + wid;
   const bool wint = sc->wint != 0;   // integral weights <= 2^20: the int paths
-  // chunks of long columns first (their latency overlaps the packed tiles of other warps)
-  if (with_lbin) {
-    for (; t < P.n_bchunks; t += nwarps)
-      lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
-    t -= P.n_bchunks;
-  }
-  for (; t < P.n_gchunks; t += nwarps)
-  {
-    if (wint) lbkt_chunk<true>(P, Wk, walker, X, RS, st, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S));
-    else lbkt_chunk<false>(P, Wk, walker, X, RS, st, P.gchunks[t], lane, reinterpret_cast<unsigned char*>(&S));
-  }
-  __syncwarp();
-  t -= P.n_gchunks;
-  // tiles: [0, n_gtiles) packed integer columns (gen32_tile), then [n_gtiles, n_gtiles + n_ctiles)
-  // continuous columns (gen_column_serial, a lane per column), then empty columns; with walker
-  // groups (wm_mode) the integer and empty tiles are k_eval_gen_wm's
-  const int tb = wm_mode ? P.n_gtiles : 0;
-  const int te = wm_mode ? P.n_gtiles + P.n_ctiles : P.n_wtiles;
-  for (t += tb; t < te; t += nwarps) {
-    const WTile T = P.wtiles[t];
+  const bool rint = sc->rint != 0;   // integral residuals: the exact float-quotient path
+  // items: P.gitems = [long binary chunks | long bounded-integer chunks | continuous tiles | general
+  // tiles | empty tiles]
+  const int ifirst = with_lbin ? 0 : P.n_bchunks;
+  const int iend = wm_mode ? P.n_bchunks + P.n_gchunks + P.n_ctiles : P.n_gitems;
+  const int nwarps = gridDim.x * (kGenThreads / 32);
+  int t = ifirst + blockIdx.x * (kGenThreads / 32) + wid;
+  WTile T;
+  if (t < iend) T = P.gitems[t];
+  GenRound R;
+  bool r_ok = false;   // R holds T's first round
+  for (; t < iend; t += nwarps) {
+    const bool has_next = t + nwarps < iend;
+    WTile Tn;
+    if (has_next) Tn = P.gitems[t + nwarps];
     if (T.kind == CC_GEN) {
-      if (wint) gen32_tile<true>(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
-      else gen32_tile<false>(P, X, RS, st, TB, T, lane, S, b, oxhat, oscore, kk, use_tabu);
+      if (!r_ok) R = gen_round(P, T, 4 * lane);
+      if (wint) gen32_tile<true>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu);
+      else gen32_tile<false>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu);
+      r_ok = has_next && Tn.kind == CC_GEN;
+    } else if (T.kind == CC_LBKT) {
+      const LongCol L = P.lcols[T.e1];
+      if (wint) lbkt_chunk<true>(P, Wk, walker, X, RS, st, T, L, lane, reinterpret_cast<unsigned char*>(&S), rint, s_tab);
+      else lbkt_chunk<false>(P, Wk, walker, X, RS, st, T, L, lane, reinterpret_cast<unsigned char*>(&S), rint, s_tab);
+      if (long_last(Wk, walker, L, lane)) lbkt_finalize(P, Wk, walker, L, lane, b, oxhat, oscore, kk, use_tabu);
+    } else if (T.kind == CC_LBIN) {
+      lbin_chunk(P, Wk, walker, X, RS, TB, T, lane, b, oxhat, oscore, kk, use_tabu);
     } else if (T.kind == CC_GENC) {
       if (lane < T.ncols) {
         const int p = T.p0 + lane;
-        double v, s;
-        gen_column_serial(P, X, RS, st, p, v, s);
-        offer_column(p, __ldg(P.perm + p), TB, __ldg(X + p), v, s, b, oxhat, oscore, kk, use_tabu);
+        double v, sv;
+        gen_column_serial(P, X, RS, st, p, v, sv);
+        offer_column(p, __ldg(P.perm + p), TB, __ldg(X + p), v, sv, b, oxhat, oscore, kk, use_tabu);
       }
     } else {
       wtile_empty(P, C, T, lane, b);
     }
+    __syncwarp();
+    T = Tn;
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
@@ -1640,7 +1782,7 @@ __host__ __device__ constexpr size_t gen_wm_smem(int kmax) {
 // the last block of the walker reduces them (fixed order) to the decision.
 __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalkers Wk, double* oxhat,
                                                           double* oscore, chap_move* best_out,
-                                                          int part_base) {
+                                                          int part_base, int fin_lbin) {
   pdl_wait_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double sm_red[32];
@@ -1659,14 +1801,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   C.oscore = oscore;
   Best b;
   b.init();
-  // long columns, finished after all their chunks (k_eval_bin / k_eval_gen ran before this kernel)
-  {
-    const int lane = threadIdx.x & 31;
+  // long binary columns of walker groups (k_eval_bin_wm takes no chunk tickets), finished after all
+  // their chunks; every other long column is finished by the chunk that takes its last ticket
+  if (fin_lbin && (threadIdx.x & 31) == 0) {
     const int nw = gridDim.x * (blockDim.x >> 5), w0 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     for (int q = w0; q < P.n_lfin; q += nw) {
       const LongCol L = P.lcols[P.lfin[q]];
-      if (L.kind == CC_LBKT) lbkt_finalize(P, Wk, walker, L, lane, b, oxhat, oscore, C.k, C.use_tabu);
-      else if (lane == 0) lbin_finalize(P, Wk, walker, L, b, oxhat, oscore, C.k, C.use_tabu);
+      if (L.kind == CC_LBIN) lbin_finalize(P, Wk, walker, L, b, oxhat, oscore, C.k, C.use_tabu);
     }
   }
   // block tiles: single-column sorts

@@ -106,6 +106,7 @@ __device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWal
   if (!sc->cut_active) rw[P.cut_row].w = 1.0f;   // the inert row takes its logical weight
   sc->cutoff_rhs = rhs;
   sc->cut_active = 1;
+  sc->rint = P.rint_base && rhs == floor(rhs);
   const double r = z - rhs;
   rw[P.cut_row].r = r;
   sc->violated = (r > 0.0) ? 1 : 0;
@@ -126,6 +127,7 @@ __global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, in
     if (mode == 0) {
       // weights start at 1 and grow by +1 up to the cap (R12): integers <= 2^20 when the cap is one
       sc->wint = Wk.wcap == floorf(Wk.wcap) && Wk.wcap <= 1048576.0f;
+      sc->rint = P.rint_base && (!sc->cut_active || sc->cutoff_rhs == floor(sc->cutoff_rhs));
       sc->k = 0;
       sc->n_moves = 0;
       sc->n_stuck = 0;
@@ -397,11 +399,13 @@ __global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
   rw[P.cut_row].r = r_new;
   sc->cutoff_rhs = rhs;
   sc->cut_active = 1;
+  sc->rint = P.rint_base && rhs == floor(rhs);
 }
 
 // Scalars of the eval API's single virtual walker: k = 0, cutoff from the call.
-__global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs) {
+__global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs, int rint_base) {
   sc->k = 0;
+  sc->rint = rint_base && (!(cutoff_rhs < INFINITY) || cutoff_rhs == floor(cutoff_rhs));
   sc->wint = 1;   // cleared by k_rows_init on a non-integral weight or one above 2^20
   sc->cut_active = cutoff_rhs < INFINITY;
   sc->cutoff_rhs = cutoff_rhs;
