@@ -43,7 +43,7 @@ typedef enum {
   CHAP_ERR_OOM = 4,               /* device or host allocation failed                            */
   CHAP_ERR_NCCL = 5,              /* an NCCL call failed                                         */
   CHAP_ERR_STATE = 6,             /* call not valid in the handle's current state                */
-  CHAP_ERR_UNSUPPORTED = 7        /* a column shape this build cannot evaluate (see message)     */
+  CHAP_ERR_UNSUPPORTED = 7        /* reserved (no column shape is rejected since the grid-wide sort) */
 } chap_status;
 
 /* Message for the last non-OK status returned on this thread ("" if none). */
@@ -95,6 +95,10 @@ typedef struct {
                                  expiry, row state); the rest (A in CSC, static per-variable
                                  data) is read once by a batched pass of W walkers, whose model
                                  is therefore shared + W x per-walker          */
+  int32_t n_gridsort_columns; /* of n_sorted_columns, those longer than one block's sort (more
+                                 than 2043 nonzeros): chunk sorts plus co-ranking across blocks
+                                 ("grid-wide primitives")           */
+  int32_t pad_info;
 } chap_problem_info;
 
 /* Build a problem from HOST CSR data (copied; the caller may free its arrays on return).

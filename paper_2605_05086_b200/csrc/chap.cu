@@ -210,9 +210,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     } else if (d + 2 + 3 <= kGenmMax) {   // + up to 3 padding entries
       cls[j] = CC_GENM;
     } else {
-      return fail(CHAP_ERR_UNSUPPORTED,
-                  "variable %d: non-binary column with %d nonzeros and domain [%g, %g] (needs the "
-                  "multi-block merge sort, not in this build)", j, d, l[j], u[j]);
+      cls[j] = CC_GENL;   // grid-wide sort
     }
   }
   // internal order: fixed columns, then packed binary columns (so that the binary CSC region starts
@@ -327,6 +325,8 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   std::vector<WTile> wtiles, btiles, bchunks, gchunks;
   std::vector<LongCol> lcols;
   std::vector<int32_t> lfin;
+  std::vector<Tile> schunks;
+  std::vector<SortCol> scols;
   for (const auto& r : bin_ranges) {
     WTile W{};
     W.p0 = r.first;
@@ -382,6 +382,27 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     T.kind = k;
     T.p0 = p;
     T.ncols = 1;
+    if (k == CC_GENL) {   // chunks of <= kSortChunk entries, sorted per block, co-ranked
+      SortCol S{};
+      S.scr = lscr;
+      S.p = p;
+      const int d = col_ptr[p + 1] - col_ptr[p];   // incl. any padding (inert: emits nothing)
+      S.nchunks = (d + kSortChunk - 1) / kSortChunk;
+      for (int c = 0; c < S.nchunks; ++c) {
+        Tile C{};
+        C.kind = CC_GENL;
+        C.p0 = p;
+        C.ncols = c;
+        C.e0 = col_ptr[p] + c * kSortChunk;
+        C.e1 = std::min(col_ptr[p + 1], C.e0 + kSortChunk);
+        C.pad = (int32_t)scols.size();
+        schunks.push_back(C);
+      }
+      lscr += (int64_t)S.nchunks * kSortStride;
+      scols.push_back(S);
+      ++p;
+      continue;
+    }
     if (k == CC_GENM) {
       T.e0 = col_ptr[p];
       T.e1 = col_ptr[p + 1];
@@ -420,7 +441,11 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   }
   I.n_long_columns = n_long;
   I.n_sorted_columns = 0;
-  for (int32_t j = 0; j < n; ++j) I.n_sorted_columns += (cls[j] == CC_GENM);
+  I.n_gridsort_columns = 0;
+  for (int32_t j = 0; j < n; ++j) {
+    I.n_sorted_columns += (cls[j] == CC_GENM || cls[j] == CC_GENL);
+    I.n_gridsort_columns += (cls[j] == CC_GENL);
+  }
   // row-wise binary blocks (k_eval_binrow): packed binary columns [pb0, pb1) in blocks of <=
   // kRowVmax columns balanced by nonzeros, a multiple of the resident clusters; each block's
   // entries sorted by row, cut into kRowCluster slices padded to multiples of 4 with inert entries
@@ -594,7 +619,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       if (k == CC_FIXED) continue;
       // [0] packed binary columns, [1] long binary, general, empty and long bounded-integer
       // columns, [2] sorted general columns and the row state
-      const int kk = (k == CC_BIN) ? 0 : (k == CC_GENM ? 2 : 1);
+      const int kk = (k == CC_BIN) ? 0 : ((k == CC_GENM || k == CC_GENL) ? 2 : 1);
       const bool bin = vclass[j] == 1;
       const double per_var = 4.0 + (bin ? 1.0 + 0.125 : 17.0 + 8.0) + 4.0;   // col_ptr, static, x̄, tabu
       mb[kk] += 12LL * odeg[j] + (int64_t)std::llround(per_var * 8) / 8;
@@ -650,6 +675,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   int32_t* d_lfin;
   TRY(B.upload(&d_lfin, lfin));
   TRY(B.upload(&d_lcols, lcols));
+  Tile* d_schunks;
+  SortCol* d_scols;
+  TRY(B.upload(&d_schunks, schunks));
+  TRY(B.upload(&d_scols, scols));
   RowBlock* d_rblocks;
   int32_t* d_rb_row;
   uint32_t* d_rb_cv;
@@ -695,6 +724,10 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.btiles = d_btiles;
   D.n_btiles = (int32_t)btiles.size();
   D.lcols = d_lcols;
+  D.schunks = d_schunks;
+  D.n_schunks = (int32_t)schunks.size();
+  D.scols = d_scols;
+  D.n_scols = (int32_t)scols.size();
   D.lfin = d_lfin;
   D.n_lfin = (int32_t)lfin.size();
   D.bchunks = d_bchunks;
@@ -710,10 +743,12 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
 
   // launch geometry: a persistent grid of (resident blocks) per walker set
   CUDA_TRY(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+  CUDA_TRY(cudaFuncSetAttribute(k_sort_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval, kTileThreads, kTileSmem));
   P->eval_occ = std::max(1, occ);
-  const int ework = std::max(std::max(D.n_tiles, (D.n_lfin + kTileWarps - 1) / kTileWarps), 1);
+  const int ework = std::max(std::max(D.n_tiles, (D.n_lfin + kTileWarps - 1) / kTileWarps),
+                             std::max(1, (D.n_scols + kTileThreads - 1) / kTileThreads));
   P->eval_grid = std::max(1, std::min(ework, P->eval_occ * P->sm_count));
   CUDA_TRY(cudaFuncSetAttribute(k_eval_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGenSmem));
   int gocc = 1;
@@ -887,7 +922,7 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
                               cudaStream_t s, bool pdl) {
   // k_eval only selects when there are no long columns and no sort tiles: then the last eval kernel
   // (k_eval_gen, else k_eval_bin) selects in its last block and k_eval is not launched
-  const bool sel_only = Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && wgrid == 0;
+  const bool sel_only = Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && P->dp.n_scols == 0 && wgrid == 0;
   const int gen_sel = (sel_only && ggrid > 0) ? bgrid + ggrid + rgrid : 0;
   const int bin_sel = (sel_only && ggrid == 0 && rgrid == 0 && bgrid > 0) ? bgrid : 0;
   if (bgrid > 0) {
@@ -904,6 +939,10 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
     TRY(lk(k_eval_gen, dim3(ggrid, Wk.W), kGenThreads, kGenSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, bgrid,
            wgrid > 0 ? 1 : 0, (rgrid > 0 && bgrid == 0) ? 1 : 0, gen_sel, best));
   if (wgrid > 0) TRY(launch_gen_wm(P, Wk, wgrid, bgrid + ggrid + rgrid, s, pdl));
+  if (P->dp.n_schunks > 0) {   // long general columns: chunk sorts, then co-ranking (k_eval finishes them)
+    TRY(lk(k_sort_chunks, dim3(P->dp.n_schunks, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk));
+    TRY(lk(k_sort_rank, dim3(P->dp.n_schunks, Wk.W), kTileThreads, 0, s, pdl, 1, P->dp, Wk));
+  }
   if (!gen_sel && !bin_sel)
     TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
            bgrid + ggrid + rgrid + wgrid, Wk.rg > 1 ? 1 : 0));
@@ -1349,6 +1388,10 @@ extern "C" chap_status chap_walkers_profile(chap_walkers* S, int32_t n_iters, do
                                                                        0, nullptr);
     if (S->genwm_grid > 0)
       TRY(launch_gen_wm(P, S->wk, S->genwm_grid, S->bin_grid + S->gen_grid + S->binrow_grid, s, false));
+    if (D.n_schunks > 0) {
+      k_sort_chunks<<<dim3(D.n_schunks, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk);
+      k_sort_rank<<<dim3(D.n_schunks, S->W), kTileThreads, 0, s>>>(D, S->wk);
+    }
     cudaEventRecordWithFlags(e[3], s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(e[4], s, cudaEventRecordExternal);
     k_eval<<<dim3(S->eval_grid, S->W), kTileThreads, kTileSmem, s>>>(D, S->wk, nullptr, nullptr, nullptr,
@@ -1401,9 +1444,10 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int32_t* out) {
   if (!S || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or out");
   const DevProblem& D = S->P->dp;
-  const bool sel_only = S->W == 1 && S->wk.rg == 1 && D.n_tiles == 0 && S->genwm_grid == 0;
+  const bool sel_only = S->W == 1 && S->wk.rg == 1 && D.n_tiles == 0 && D.n_scols == 0 && S->genwm_grid == 0;
   const bool fused = sel_only && (S->gen_grid > 0 || (S->binrow_grid == 0 && S->bin_grid > 0));
-  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + (fused ? 0 : 1) + 1;
+  *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + (fused ? 0 : 1) + 1 +
+         (D.n_schunks > 0 ? 2 : 0);
   return CHAP_OK;
 }
 

@@ -53,6 +53,7 @@ enum ColClass : int {
   CC_BIN = 5,    // binary, deg <= kShortDeg: packed tiles, flip sums
   CC_EMPTY = 6,  // a column without nonzeros (and c_j = 0)
   CC_GENC = 7,   // continuous, deg+2 <= kShortDeg: a lane per column (gen_column_serial)
+  CC_GENL = 8,   // general, deg+2 > kGenmMax, not bucketable: grid-wide sort (chunk sorts + co-ranking)
 };
 
 // A warp tile: ncols consecutive packed columns (CC_BIN or CC_GEN) of one warp.
@@ -123,6 +124,19 @@ struct RowBlock {
 // more than kRowSpan rows and its row state is gathered instead.
 struct RowStage {
   int32_t e0, ne, r0, nr;
+};
+
+// A general column longer than one block sort (CC_GENL, "grid-wide primitives"): its
+// entries are cut into chunks of <= kSortChunk (chunk 0 also holds the two bounds), each sorted by
+// one block; every candidate is then co-ranked against every other chunk by binary search.
+constexpr int kSortChunk = kGenmMax - 2;
+// walker scratch of one chunk (doubles): t[kGenmMax], P[kGenmMax] (prefix of δ in sorted order),
+// mk[kGenmMax] (u32), then n (entries), β, α, best s, best v of the chunk's candidates
+constexpr int kSortStride = 2 * kGenmMax + kGenmMax / 2 + 8;
+struct SortCol {
+  int64_t scr;       // offset (doubles) of chunk 0 in walker scratch
+  int32_t p;         // the column (internal order)
+  int32_t nchunks;
 };
 
 // Per-column result competing for the global best move.
@@ -242,6 +256,9 @@ struct DevProblem {
   const uint8_t* vclass;     // [n] 0 fixed 1 binary 2 integer 3 continuous
   const int32_t* perm;       // internal p -> user j
   const Tile* tiles; int32_t n_tiles; int32_t n_long;   // block tiles
+  const Tile* schunks; int32_t n_schunks;               // chunks of CC_GENL columns (e0, e1: entries;
+                                                        // ncols: chunk index; pad: the SortCol)
+  const SortCol* scols; int32_t n_scols;                // CC_GENL columns
   const WTile* wtiles; int32_t n_wtiles;                // warp tiles: n_gtiles CC_GEN, n_ctiles CC_GENC, then
   int32_t n_gtiles, n_ctiles;                           // CC_EMPTY
   const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles

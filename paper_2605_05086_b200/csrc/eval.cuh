@@ -385,6 +385,180 @@ __device__ __forceinline__ void tile_genm(const DevProblem& P, const TileCtx& C,
   __syncthreads();
 }
 
+// ------------------------------------------------------------------------------------------
+// grid-wide sort of long general columns (CC_GENL)
+// ------------------------------------------------------------------------------------------
+// k_sort_chunks: one block per chunk and walker. Lines 3-11 per entry (emit) as in tile_genm, the
+// chunk's (value, marker) pairs sorted by a shared-memory bitonic network, the inclusive prefix P of
+// the deltas in sorted order (line 14 within the chunk), written to walker scratch with the keys and
+// the chunk's parts of β and α. The sort key is (t, +1 marker, candidate flag, chunk << 11 | slot):
+// a total order in which every (t, -1) entry precedes every (t, +1) entry (line 13, R3).
+__global__ void __launch_bounds__(kTileThreads) k_sort_chunks(DevProblem P, DevWalkers Wk) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double sm_red[32];
+  SmemGenM& S = *reinterpret_cast<SmemGenM*>(smem);
+  const int walker = blockIdx.y, tid = threadIdx.x;
+  const Tile T = P.schunks[blockIdx.x];
+  const int p = T.p0, ch = T.ncols, d = T.e1 - T.e0;
+  const double* X = Wk.x + (size_t)walker * Wk.xs;
+  const RowView rs = row_view(Wk, walker);
+  const double xb = X[p], l = P.lb[p], u = P.ub[p];
+  const int is_int = P.vclass[p] != 3;
+  const int nb = ch == 0 ? 2 : 0;   // the bounds ride in chunk 0
+  int Lp = 1;
+  while (Lp < d + nb) Lp <<= 1;
+  const uint32_t tag = (uint32_t)ch << 11;
+  double beta = 0.0, alpha = 0.0;
+  for (int e = tid; e < Lp; e += blockDim.x) {
+    double t = INFINITY, del = 0.0;
+    uint32_t mk = 0xffffffffu;
+    if (e < d) {
+      double r, w;
+      load_row(rs, P.row_idx[T.e0 + e], r, w);
+      const Elem el = emit(xb, r, P.val[T.e0 + e], w, is_int);
+      beta += el.beta;
+      alpha += el.alpha;
+      if (el.valid && isfinite(el.t)) {
+        const bool cand = el.t >= l && el.t <= u && el.t != xb;
+        t = el.t;
+        del = el.delta;
+        mk = ((uint32_t)el.plus << 31) | ((uint32_t)cand << 30) | tag | (uint32_t)e;
+      }
+    } else if (e < d + nb) {
+      const double bv = e == d ? l : u;
+      if (isfinite(bv)) { t = bv; mk = ((uint32_t)(bv != xb) << 30) | tag | (uint32_t)e; }
+    }
+    S.t[e] = t;
+    S.mk[e] = mk;
+    S.del[e] = del;
+  }
+  beta = block_sum(beta, sm_red);
+  alpha = block_sum(alpha, sm_red);
+  for (int size = 2; size <= Lp; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int q = tid; q < (Lp >> 1); q += blockDim.x) {
+        const int lo = 2 * q - (q & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const double t0 = S.t[lo], t1 = S.t[hi];
+        const uint32_t m0 = S.mk[lo], m1 = S.mk[hi];
+        const bool gt = (t0 > t1) || (t0 == t1 && m0 > m1);
+        if (gt == asc) {
+          S.t[lo] = t1; S.t[hi] = t0;
+          S.mk[lo] = m1; S.mk[hi] = m0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < Lp; q += blockDim.x) {
+    const uint32_t mk = S.mk[q];
+    S.P[q] = (mk == 0xffffffffu) ? 0.0 : S.del[mk & 0x7ffu];
+  }
+  __syncthreads();
+  block_scan_inclusive(S.P, Lp, sm_red);
+  // write the chunk (valid entries sort first: the others carry t = +inf and the largest key)
+  const SortCol C = P.scols[T.pad];
+  double* base = Wk.lscr + (size_t)walker * Wk.lss + C.scr + (size_t)ch * kSortStride;
+  double* gt = base;
+  double* gP = base + kGenmMax;
+  uint32_t* gmk = reinterpret_cast<uint32_t*>(base + 2 * kGenmMax);
+  double* meta = base + 2 * kGenmMax + kGenmMax / 2;
+  int nv = 0;
+  for (int q = tid; q < Lp; q += blockDim.x) {
+    const uint32_t mk = S.mk[q];
+    if (mk == 0xffffffffu) continue;
+    gt[q] = S.t[q];
+    gP[q] = S.P[q];
+    gmk[q] = mk;
+    ++nv;
+  }
+  nv = (int)block_sum((double)nv, sm_red);
+  if (tid == 0) {
+    meta[0] = (double)nv;
+    meta[1] = beta;
+    meta[2] = alpha;
+  }
+}
+
+// k_sort_rank: one block per chunk and walker. Every candidate entry of the chunk (R2, R3, R5) gets
+// its σ of line 15 from the global prefix of line 14: its own chunk's prefix (through a -1 entry,
+// strictly before a +1 entry) plus, for every other chunk of the column, the prefix of the entries
+// that precede it in the total order (binary search, co-ranking); β and α are the sums of the chunks'
+// parts. The chunk's best (σ, value) under R4 goes to its scratch; k_eval takes the column's best.
+__global__ void __launch_bounds__(kTileThreads) k_sort_rank(DevProblem P, DevWalkers Wk) {
+  __shared__ Best sm_b[32];
+  __shared__ double s_ba[2];
+  const int walker = blockIdx.y, tid = threadIdx.x;
+  const Tile T = P.schunks[blockIdx.x];
+  const int p = T.p0, ch = T.ncols;
+  const SortCol C = P.scols[T.pad];
+  const double* X = Wk.x + (size_t)walker * Wk.xs;
+  const double xb = X[p];
+  double* col = Wk.lscr + (size_t)walker * Wk.lss + C.scr;
+  auto chunk = [&](int c) { return col + (size_t)c * kSortStride; };
+  constexpr int kMeta = 2 * kGenmMax + kGenmMax / 2;
+  if (tid == 0) {
+    double B = 0.0, A = 0.0;
+    for (int c = 0; c < C.nchunks; ++c) {
+      B += __ldcg(chunk(c) + kMeta + 1);
+      A += __ldcg(chunk(c) + kMeta + 2);
+    }
+    s_ba[0] = B;
+    s_ba[1] = A;
+  }
+  __syncthreads();
+  const double B = s_ba[0], A = s_ba[1];
+  const double* me = chunk(ch);
+  const int n = (int)__ldcg(me + kMeta);
+  const uint32_t* mmk = reinterpret_cast<const uint32_t*>(me + 2 * kGenmMax);
+  double bs = -INFINITY, bv = xb;
+  for (int q = tid; q < n; q += blockDim.x) {
+    const uint32_t mk = __ldcg(mmk + q);
+    if (!((mk >> 30) & 1u)) continue;
+    const double t = __ldcg(me + q);
+    const bool plus = mk >> 31;
+    double pre = plus ? (q > 0 ? __ldcg(me + kGenmMax + q - 1) : 0.0) : __ldcg(me + kGenmMax + q);
+    for (int c = 0; c < C.nchunks; ++c) {
+      if (c == ch) continue;
+      const double* o = chunk(c);
+      const uint32_t* omk = reinterpret_cast<const uint32_t*>(o + 2 * kGenmMax);
+      int lo = 0, hi = (int)__ldcg(o + kMeta);   // count of entries before (t, mk): first not-less
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const double tm = __ldcg(o + mid);
+        const bool less = tm < t || (tm == t && __ldcg(omk + mid) < mk);
+        if (less) lo = mid + 1; else hi = mid;
+      }
+      if (lo > 0) pre += __ldcg(o + kGenmMax + lo - 1);
+    }
+    const double sig = B + pre + (t > xb ? A : 0.0);
+    if (better_shift(sig, t, bs, bv, xb)) { bs = sig; bv = t; }
+  }
+  block_best_shift(bs, bv, xb, sm_b);
+  if (tid == 0) {
+    double* meta = const_cast<double*>(me) + kMeta;
+    meta[3] = bs;
+    meta[4] = bv;
+  }
+}
+
+// The column's result from its chunks' bests (R4), in k_eval after k_sort_rank.
+__device__ __forceinline__ void sortcol_finish(const DevProblem& P, const DevWalkers& Wk, int walker, const SortCol& C,
+                                               Best& b, double* oxhat, double* oscore, long long kk, int use_tabu) {
+  const double* col = Wk.lscr + (size_t)walker * Wk.lss + C.scr;
+  const double xb = Wk.x[(size_t)walker * Wk.xs + C.p];
+  constexpr int kMeta = 2 * kGenmMax + kGenmMax / 2;
+  double bs = -INFINITY, bv = xb;
+  for (int c = 0; c < C.nchunks; ++c) {
+    const double s = __ldcg(col + (size_t)c * kSortStride + kMeta + 3), v = __ldcg(col + (size_t)c * kSortStride + kMeta + 4);
+    if (s > -INFINITY && better_shift(s, v, bs, bv, xb)) { bs = s; bv = v; }
+  }
+  finish_column_j(C.p, P.perm[C.p], use_tabu ? Wk.tabu[(size_t)walker * Wk.ts + C.p] : 0, xb, bv, bs, b, oxhat, oscore,
+                  kk, use_tabu);
+}
+
 // last-block handshake (the global select): returns true in every thread of the last block
 __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_flag) {
   __syncthreads();
@@ -1810,6 +1984,9 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
       if (L.kind == CC_LBIN) lbin_finalize(P, Wk, walker, L, b, oxhat, oscore, C.k, C.use_tabu);
     }
   }
+  // long general columns sorted grid-wide (k_sort_chunks, k_sort_rank ran before this kernel)
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < P.n_scols; q += gridDim.x * blockDim.x)
+    sortcol_finish(P, Wk, walker, P.scols[q], b, oxhat, oscore, C.k, C.use_tabu);
   // block tiles: single-column sorts
   for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x)
     tile_genm(P, C, P.tiles[t], *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b);

@@ -482,3 +482,65 @@ def test_eval_rejects_negative_weights_and_bad_x():
     assert e.value.status == 1
     after = Wk.get()
     assert np.array_equal(before["x"], after["x"]) and np.array_equal(before["r"], after["r"])
+
+
+def _gridsort_mix(seed=13):
+    """Long general columns beyond one block's sort (2100..9000 nonzeros, unbounded and large-domain
+    integers): the grid-wide sort of DESIGN §2.5, 2..5 chunks each."""
+    return synth.mixed(seed=seed, n=20_000, m=12_000, n_long=6, long_lo=2100, long_hi=9000, long_kinds=("unb", "big"))
+
+
+def test_gridsort_columns_eval():
+    """PAPER.md:355 (grid-wide primitives for vectors longer than a block): per-variable results and
+    the best move bit-exact against the oracle, with and without the cutoff row."""
+    inst = _gridsort_mix()
+    P = chap.Problem.from_instance(inst)
+    assert P.info.n_gridsort_columns >= 4, P.info.n_gridsort_columns
+    O = oracle.Problem.from_instance(inst)
+    for s in range(3):
+        x = synth.x_random(inst, 40 + s, spread=60)
+        w = synth.weights_random(P.m_norm, 10 + s, hi=9)
+        cut = math.inf if s == 0 else float(inst.c @ x) - 40.0
+        g, o = _eval_both(inst, x, w, cut, P=P, O=O)
+        _assert_same(g, o, f"gridsort s={s}")
+
+
+def test_gridsort_columns_trajectory(binrow):
+    inst = _gridsort_mix(seed=14)
+    assert chap.Problem.from_instance(inst).info.n_gridsort_columns >= 4
+    _traj_compare(inst, [synth.x_lower(inst), synth.x_random(inst, 5, spread=30)], 25, binary_kernel=binrow)
+
+
+def test_gridsort_1e5_column():
+    """An unbounded integer column with 10^5 nonzeros (49+ chunks): its (x̂, s) bit-exact against
+    Algorithm 1 run verbatim in exact rationals (tests/exact.alg1; the oracle's brute force would
+    take O(deg^2)), every other variable against the oracle."""
+    from fractions import Fraction as Fr
+    inst = synth.mixed(seed=15, n=200_000, m=110_000, n_long=1, long_lo=1e5, long_hi=1e5, long_kinds=("unb",))
+    P = chap.Problem.from_instance(inst)
+    assert P.info.n_gridsort_columns == 1
+    deg = np.bincount(inst.col_idx, minlength=inst.n)
+    jl = int(np.argmax(deg))
+    assert deg[jl] == 100_000
+    x = synth.x_random(inst, 7, spread=40)
+    w = synth.weights_random(P.m_norm, 7, hi=9)
+    xt = torch.from_numpy(x).cuda()
+    gx, gs, _ = P.eval_best_shift(xt, torch.from_numpy(w).cuda())
+    torch.cuda.synchronize()
+    gx, gs = gx.cpu().numpy(), gs.cpu().numpy()
+    O = oracle.Problem.from_instance(inst)
+    ox, os_ = np.zeros(inst.n), np.zeros(inst.n)
+    O.best_shift_range(x, 0, jl, w, out=(ox, os_))
+    O.best_shift_range(x, jl + 1, inst.n, w, out=(ox, os_))
+    others = np.arange(inst.n) != jl
+    assert np.array_equal(gx[others], ox[others]) and np.array_equal(gs[others], os_[others])
+    rows = exact.normalized_rows(inst)
+    rows.append(({}, Fr(0), -1, +1))   # the inactive cutoff row
+    assert len(rows) == P.m_norm
+    col = [i for i, (a, _, _, _) in enumerate(rows) if jl in a]
+    sub = [rows[i] for i in col]
+    r = exact.residuals(sub, x)
+    lb, ub = exact.bounds(inst)
+    v, sc = exact.alg1(sub, r, x, w[col], jl, lb[jl], ub[jl], True)
+    assert sc is not None
+    assert gs[jl] == float(sc) and gx[jl] == float(v), (gx[jl], gs[jl], float(v), float(sc))
