@@ -300,6 +300,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=200)
     ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--param", action="append", default=[],
+                    help="chap_params field override NAME=VALUE (A/B runs, e.g. l2_persist=0)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     maybe_spawn(args)
@@ -327,6 +329,9 @@ def main():
     n_eval = info.n - info.n_fixed
     x0 = torch.from_numpy(start_points(inst, cfg, W, rank)).to(dev)
     prm = chap.default_params(graph_iters=32)
+    for kv in args.param:
+        k, v = kv.split("=", 1)
+        setattr(prm, k, type(getattr(prm, k))(float(v)) if isinstance(getattr(prm, k), float) else int(v))
     ws = chap.Walkers(P, x0, prm)
     z_star = planted_objective(inst)
     if z_star is not None:

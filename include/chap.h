@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CHAP_ABI_VERSION 2
+#define CHAP_ABI_VERSION 3
 
 typedef enum {
   CHAP_OK = 0,
@@ -188,6 +188,12 @@ typedef struct {
                             coefficients allow it: integers of magnitude <= 32767)            */
   int32_t pdl;           /* 1 = launch the iteration's kernels with programmatic dependent launch
                             (default 0: measured slower on config G)               */
+  int32_t l2_persist;    /* 1 (default) = the walkers' row state (residuals and weights, the
+                            target of every gather) is an L2 access-policy window with hits
+                            persisting ("pin it to the L2 cache"); 0 = off        */
+  int32_t aspiration;    /* 1 = incumbent aspiration (NEXT f1, DESIGN R18): a tabu variable is
+                            admissible when its best shift makes the point feasible (a new
+                            incumbent, the cutoff row included); 0 (default) = off           */
 } chap_params;
 
 /* Fill *out with the defaults above (n_restart = -1 meaning W_total/8). */

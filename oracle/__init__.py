@@ -46,7 +46,7 @@ RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("pad", "<i4"), ("v", "<f8"
 
 class Params(ctypes.Structure):
     _fields_ = [("tenure", ctypes.c_int32), ("weight_cap", ctypes.c_float),
-                ("cutoff_delta", ctypes.c_double)]
+                ("cutoff_delta", ctypes.c_double), ("aspiration", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class Walker(ctypes.Structure):
@@ -204,9 +204,10 @@ class TabuParams:
     tenure: int = 10
     weight_cap: float = 1e6
     cutoff_delta: float = math.nan
+    aspiration: int = 0
 
     def c(self):
-        return Params(self.tenure, self.weight_cap, self.cutoff_delta)
+        return Params(self.tenure, self.weight_cap, self.cutoff_delta, self.aspiration, 0)
 
 
 class TabuWalker:

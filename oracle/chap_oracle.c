@@ -365,6 +365,15 @@ int orc_walker_init(const orc_problem* P, const orc_params* prm, const double* x
   return ORC_OK;
 }
 
+/* Aspiration test (R18): would x_j <- v leave every active row (cutoff row included) satisfied?
+ * The point after the move and its residuals recomputed from scratch (plain definition). */
+static int feasible_after(const orc_problem* P, const orc_walker* S, int32_t j, double v, double* xt, double* r) {
+  memcpy(xt, S->x, sizeof(double) * P->n);
+  xt[j] = v;
+  orc_residuals(P, xt, S->cutoff_rhs, r);
+  return count_violated(P, r, S->cutoff_rhs < INFINITY) == 0;
+}
+
 int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int64_t n_iters,
                  orc_record* log, int n_threads) {
   if (!S->initialised) return ORC_ERR_INVALID_ARG;
@@ -373,7 +382,12 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
   double* y = (double*)malloc(sizeof(double) * mn);
   double* xhat = (double*)malloc(sizeof(double) * (n + 1));
   double* score = (double*)malloc(sizeof(double) * (n + 1));
-  if (!r || !y || !xhat || !score) { free(r); free(y); free(xhat); free(score); return ORC_ERR_OOM; }
+  double* xt = (double*)malloc(sizeof(double) * (n + 1));   /* aspiration: the point after a move */
+  double* r2 = (double*)malloc(sizeof(double) * mn);
+  if (!r || !y || !xhat || !score || !xt || !r2) {
+    free(r); free(y); free(xhat); free(score); free(xt); free(r2);
+    return ORC_ERR_OOM;
+  }
 #ifdef _OPENMP
   if (n_threads > 0) omp_set_num_threads(n_threads);
 #endif
@@ -386,10 +400,13 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
 #endif
     for (int32_t j = 0; j < n; j++) best_shift_var(P, j, S->x, y, S->w, S->cutoff_rhs, &xhat[j], &score[j]);
     orc_residuals(P, S->x, S->cutoff_rhs, r);
-    /* selection: admissible = not tabu; max s_j, ties lowest j (R6) */
+    /* selection: admissible = not tabu, or (aspiration, R18) tabu with s_j > 0
+     * and a feasible point after the move; max s_j, ties lowest j (R6) */
     int32_t js = -1; double ss = -INFINITY;
     for (int32_t j = 0; j < n; j++) {
-      if (P->vclass[j] == 0 || S->tabu_until[j] > k) continue;
+      if (P->vclass[j] == 0) continue;
+      if (S->tabu_until[j] > k && !(prm->aspiration && score[j] > 0.0 && feasible_after(P, S, j, xhat[j], xt, r2)))
+        continue;
       if (js < 0 || score[j] > ss) { js = j; ss = score[j]; }
     }
     orc_record rec;
@@ -416,7 +433,7 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
     if (log) log[it] = rec;
     S->k = k + 1;
   }
-  free(r); free(y); free(xhat); free(score);
+  free(r); free(y); free(xhat); free(score); free(xt); free(r2);
   return ORC_OK;
 }
 

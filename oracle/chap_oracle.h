@@ -77,6 +77,9 @@ typedef struct {
   int32_t tenure;        /* T: a moved variable is inadmissible in iterations k+1..k+T (R13)   */
   float weight_cap;      /* w <= cap (R11, R12)                                               */
   double cutoff_delta;   /* NaN = auto (R14)                                                  */
+  int32_t aspiration;    /* 1: a tabu variable is admissible when moving it to its best shift
+                            makes the point feasible, i.e. gives a new incumbent (R18, NEXT f1) */
+  int32_t pad;
 } orc_params;
 
 typedef struct {
@@ -95,8 +98,9 @@ int orc_walker_init(const orc_problem* P, const orc_params* prm, const double* x
 
 /* n_iters tabu iterations ("the best admissible move is selected and applied";
  * PAPER.md:361 own solution, tabu list and weights). Each iteration: residuals from scratch;
- * best shift of every variable; select the admissible (tabu_until_j <= k) argmax s_j, ties
- * lowest j; if s* > 0 move x_j* <- xhat_j*, tabu_until_j* = k+1+T; else (stuck) bump
+ * best shift of every variable; select the admissible (tabu_until_j <= k, or with
+ * prm->aspiration a tabu j with s_j > 0 whose move to xhat_j leaves no active row violated, R18)
+ * argmax s_j, ties lowest j; if s* > 0 move x_j* <- xhat_j*, tabu_until_j* = k+1+T; else (stuck) bump
  * w_i <- min(w_i + 1, cap) on every active row with r_i > 0 (R12); then, if every active row has
  * r_i <= 0, record the incumbent and set the cutoff rhs to c.x - delta; log. */
 int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int64_t n_iters,

@@ -1105,6 +1105,8 @@ extern "C" chap_status chap_params_default(chap_params* out) {
   out->graph_iters = 16;
   out->binary_kernel = 0;
   out->pdl = 0;
+  out->l2_persist = 1;
+  out->aspiration = 0;
   return CHAP_OK;
 }
 
@@ -1116,6 +1118,8 @@ static chap_status check_params(const chap_params& q) {
   if (q.graph_iters < 0) return fail(CHAP_ERR_INVALID_ARG, "graph_iters < 0");
   if (q.binary_kernel < 0 || q.binary_kernel > 2) return fail(CHAP_ERR_INVALID_ARG, "binary_kernel not in {0, 1, 2}");
   if (q.pdl < 0 || q.pdl > 1) return fail(CHAP_ERR_INVALID_ARG, "pdl not in {0, 1}");
+  if (q.l2_persist < 0 || q.l2_persist > 1) return fail(CHAP_ERR_INVALID_ARG, "l2_persist not in {0, 1}");
+  if (q.aspiration < 0 || q.aspiration > 1) return fail(CHAP_ERR_INVALID_ARG, "aspiration not in {0, 1}");
   return CHAP_OK;
 }
 
@@ -1187,6 +1191,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.lss = p->lscr_per_walker;
   TRY(B.alloc(&Wk.lscr, Wk.lss * W));
   TRY(B.alloc(&S->d_bad, 1));
+  Wk.asp = nullptr;
+  if (prm.aspiration && prm.tenure > 0) TRY(B.alloc(&Wk.asp, (size_t)prm.tenure * W));   // R18 slots
   Wk.xs = n;
   Wk.rss = mn + 1;
   Wk.ts = n;
@@ -1196,6 +1202,30 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.wcap = prm.weight_cap;
   Wk.delta = prm.cutoff_delta;
   CUDA_TRY(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+  if (prm.l2_persist) {   // the gathered row state persists in L2 (window on the stream,
+                          // copied onto every kernel node of the captured graphs)
+    const size_t rs_bytes = sizeof(RowState) * (mn + 1) * (size_t)rg * Wk.n_groups;
+    int max_persist = 0, max_win = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, p->device);
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, p->device);
+    if (max_persist > 0 && max_win > 0) {
+      const size_t win = std::min(rs_bytes, (size_t)max_win);
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (cur < std::min(win, (size_t)max_persist))
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(win, (size_t)max_persist));
+      cudaAccessPolicyWindow& a = S->l2win;
+      a.base_ptr = Wk.rs;
+      a.num_bytes = win;
+      a.hitRatio = (float)std::min(1.0, (double)max_persist / (double)win);
+      a.hitProp = cudaAccessPropertyPersisting;
+      a.missProp = cudaAccessPropertyStreaming;
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow = a;
+      if (cudaStreamSetAttribute(S->stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess) S->l2win_on = true;
+      cudaGetLastError();
+    }
+  }
   CUDA_TRY(cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&S->ev_out, cudaEventDisableTiming));
   cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -1205,6 +1235,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.rs, 0, sizeof(RowState) * (mn + 1) * (size_t)rg * Wk.n_groups, s));
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
+  if (Wk.asp) CUDA_TRY(cudaMemsetAsync(Wk.asp, 0xff, sizeof(Cand) * (size_t)prm.tenure * W, s));   // p = -1
   if (D.n > 0)
     k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
   k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1);
@@ -1246,6 +1277,20 @@ static chap_status capture_iterations(chap_walkers* S, cudaStream_t s, int iters
   cudaError_t ce = cudaStreamEndCapture(s, &graph);
   if (st != CHAP_OK) return st;
   if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+  if (S->l2win_on) {   // the row state's L2 window on every kernel node
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+    cudaKernelNodeAttrValue v{};
+    v.accessPolicyWindow = S->l2win;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel)
+        cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v);
+    }
+    cudaGetLastError();
+  }
   ce = cudaGraphInstantiate(out, graph, 0);
   cudaGraphDestroy(graph);
   if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));

@@ -308,6 +308,9 @@ struct DevWalkers {
   float wcap;
   double delta;                        // NaN = auto
   unsigned long long* kt;              // [kKtWords] kernel timing, NULL = off
+  Cand* asp;                           // [W][tenure] aspiration slots (chap_params.aspiration), NULL = off:
+                                       // the eval kernels note every tabu column with s > 0 in slot
+                                       // tabu_until % tenure; the select takes the feasible ones (R18)
 };
 
 // The row state of one walker: base pointer and stride (in records) between consecutive rows.

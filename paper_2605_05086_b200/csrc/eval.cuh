@@ -104,14 +104,40 @@ __device__ __forceinline__ void write_part(Cand* dst, const Best& b) {
   *dst = c;
 }
 
-// The result of one column: outputs (eval API) and the admissible-best update (R6, R13).
+// Aspiration slots of one walker (R18): a tabu column with s > 0 is noted in slot tabu_until % T
+// (the <= T tabu variables have distinct expiries k'+1+T, k' in [k-T, k-1]); a = NULL: off.
+struct AspRef {
+  Cand* a = nullptr;
+  int T = 1;
+};
+__device__ __forceinline__ AspRef asp_ref(const DevWalkers& Wk, int w) {
+  AspRef r;
+  r.a = Wk.asp ? Wk.asp + (size_t)w * Wk.tenure : nullptr;
+  r.T = Wk.tenure > 0 ? Wk.tenure : 1;
+  return r;
+}
+__device__ __forceinline__ void asp_note(const AspRef& A, int p, int j, long long tabu_p, double v, double s) {
+  if (!A.a || !(s > 0.0)) return;
+  Cand c;
+  c.s = s;
+  c.v = v;
+  c.j = j;
+  c.p = p;
+  A.a[tabu_p % A.T] = c;
+}
+
+// The result of one column: outputs (eval API) and the admissible-best update (R6, R13); a tabu
+// column is noted for aspiration (R18).
 __device__ __forceinline__ void finish_column_j(int p, int j, int32_t tabu_p, double xb, double v,
                                                 double s, Best& b, double* oxhat, double* oscore,
-                                                long long k, int use_tabu) {
+                                                long long k, int use_tabu, AspRef A = AspRef()) {
   if (s == -INFINITY) v = xb;
   if (oxhat) oxhat[j] = v;
   if (oscore) oscore[j] = s;
-  if (use_tabu && (long long)tabu_p > k) return;
+  if (use_tabu && (long long)tabu_p > k) {
+    asp_note(A, p, j, tabu_p, v, s);
+    return;
+  }
   if (better_move(s, j, b.s, b.j)) {
     b.s = s;
     b.v = v;
@@ -121,8 +147,8 @@ __device__ __forceinline__ void finish_column_j(int p, int j, int32_t tabu_p, do
 }
 __device__ __forceinline__ void finish_column(const DevProblem& P, int p, double xb, double v,
                                               double s, Best& b, double* oxhat, double* oscore,
-                                              const int32_t* tabu, long long k, int use_tabu) {
-  finish_column_j(p, P.perm[p], use_tabu ? tabu[p] : 0, xb, v, s, b, oxhat, oscore, k, use_tabu);
+                                              const int32_t* tabu, long long k, int use_tabu, AspRef A) {
+  finish_column_j(p, P.perm[p], use_tabu ? tabu[p] : 0, xb, v, s, b, oxhat, oscore, k, use_tabu, A);
 }
 
 // One 16-byte row-state gather (r f64, w f32). The inactive cutoff row holds r = -inf, w = 0,
@@ -205,6 +231,7 @@ struct TileCtx {
   int use_tabu;
   double* oxhat;
   double* oscore;
+  AspRef asp;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -251,7 +278,7 @@ __device__ __forceinline__ void wtile_empty(const DevProblem& P, const TileCtx& 
     if (isfinite(l) && l != xb) { bs = 0.0; bv = l; }
     if (isfinite(u) && u != xb && better_shift(0.0, u, bs, bv, xb)) { bs = 0.0; bv = u; }
   }
-  finish_column_j(p, j, tb, xb, bv, bs, b, C.oxhat, C.oscore, C.k, C.use_tabu);
+  finish_column_j(p, j, tb, xb, bv, bs, b, C.oxhat, C.oscore, C.k, C.use_tabu, C.asp);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -381,7 +408,7 @@ __device__ __forceinline__ void tile_genm(const DevProblem& P, const TileCtx& C,
     if (better_shift(sig, t, bs, bv, xb)) { bs = sig; bv = t; }
   }
   block_best_shift(bs, bv, xb, sm_b);
-  if (tid == 0) finish_column(P, p, xb, bv, bs, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu);
+  if (tid == 0) finish_column(P, p, xb, bv, bs, b, C.oxhat, C.oscore, C.tabu, C.k, C.use_tabu, C.asp);
   __syncthreads();
 }
 
@@ -556,7 +583,7 @@ __device__ __forceinline__ void sortcol_finish(const DevProblem& P, const DevWal
     if (s > -INFINITY && better_shift(s, v, bs, bv, xb)) { bs = s; bv = v; }
   }
   finish_column_j(C.p, P.perm[C.p], use_tabu ? Wk.tabu[(size_t)walker * Wk.ts + C.p] : 0, xb, bv, bs, b, oxhat, oscore,
-                  kk, use_tabu);
+                  kk, use_tabu, asp_ref(Wk, walker));
 }
 
 // last-block handshake (the global select): returns true in every thread of the last block
@@ -575,8 +602,8 @@ __device__ __forceinline__ bool last_chunk(unsigned* cnt, int nchunks, int* s_fl
 // The global select (R6), run by the last block of a walker's final eval kernel: the
 // best admissible move over the walker's nparts block parts, written as the walker's decision (and
 // to best_out for the eval API).
-__device__ __forceinline__ void select_walker(const DevWalkers& Wk, int walker, int nparts, Best* sm_b,
-                                              chap_move* best_out, const double* x) {
+__device__ __forceinline__ void select_walker(const DevProblem& P, const DevWalkers& Wk, int walker, int nparts,
+                                              Best* sm_b, chap_move* best_out, const double* x) {
   const Cand* part = Wk.part + (size_t)walker * Wk.ps;
   Best g;
   g.init();
@@ -589,6 +616,52 @@ __device__ __forceinline__ void select_walker(const DevWalkers& Wk, int walker, 
     g.take(o);
   }
   g = block_reduce_best(g, sm_b);
+  if (Wk.asp) {   // incumbent aspiration (R18): a noted tabu move that beats the best admissible one
+                  // is taken if no active row stays violated after it (violated + Δ == 0)
+    __shared__ Best s_g;
+    __shared__ Cand s_c;
+    __shared__ int s_ok;
+    __shared__ double s_red[32];
+    if (threadIdx.x == 0) s_g = g;
+    const int T = Wk.tenure > 0 ? Wk.tenure : 1;
+    Cand* slots = Wk.asp + (size_t)walker * Wk.tenure;
+    const long long k = Wk.sc[walker].k;
+    const RowView rv = row_view(Wk, walker);
+    for (int q = 0; q < T; ++q) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const Cand c = slots[q];
+        bool ok = c.p >= 0 && c.s > 0.0 && better_move(c.s, c.j, s_g.s, s_g.j);
+        if (ok) {
+          const long long tp = Wk.tabu[(size_t)walker * Wk.ts + c.p];
+          ok = tp > k && tp % T == q;
+        }
+        s_c = c;
+        s_ok = ok;
+        slots[q].p = -1;   // consumed: the next pass notes afresh
+      }
+      __syncthreads();
+      if (!s_ok) continue;
+      const Cand c = s_c;
+      const double d = c.v - x[c.p];
+      double dv = 0.0;
+      for (int e = P.col_ptr[c.p] + threadIdx.x; e < P.col_ptr[c.p + 1]; e += blockDim.x) {
+        const double r0 = rv[P.row_idx[e]].r;   // the inert rows (inactive cutoff, padding): -inf
+        if (r0 == -INFINITY) continue;
+        const double r1 = r0 + P.val[e] * d;
+        dv += (double)(r1 > 0.0) - (double)(r0 > 0.0);
+      }
+      dv = block_sum(dv, s_red);
+      if (threadIdx.x == 0 && (double)Wk.sc[walker].violated + dv == 0.0) {
+        s_g.s = c.s;
+        s_g.v = c.v;
+        s_g.j = c.j;
+        s_g.p = c.p;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) g = s_g;
+  }
   if (threadIdx.x == 0) {
     WalkerScalars* scw = Wk.sc + walker;
     const bool found = g.p >= 0;
@@ -677,7 +750,7 @@ __device__ __forceinline__ void lbin_finalize(const DevProblem& P, const DevWalk
   *acc = 0.0;
   const double xb = __ldg(Wk.x + (size_t)walker * Wk.xs + p);
   finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(Wk.tabu + (size_t)walker * Wk.ts + p) : 0, xb,
-                  1.0 - xb, s, b, oxhat, oscore, kk, use_tabu);
+                  1.0 - xb, s, b, oxhat, oscore, kk, use_tabu, asp_ref(Wk, walker));
 }
 
 // A warp chunk (<= kWChunk nonzeros) of a long binary column: warp-reduced flip sum added to the
@@ -714,7 +787,7 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
   if (L.nchunks == 1) {
     if (lane == 0)
       finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, 1.0 - xb, own, b, oxhat,
-                      oscore, kk, use_tabu);
+                      oscore, kk, use_tabu, asp_ref(Wk, walker));
     return;
   }
   if (lane == 0) atomicAdd(Wk.lscr + (size_t)walker * Wk.lss + L.scr, own);
@@ -826,7 +899,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
       if (k < len && (end || k == len - 1)) cs[cq[q]] = tot;
     }
     __syncwarp();
-    if (lane < nc) finish_column_j(p, j, tb, xb, 1.0 - xb, cs[lane], b, oxhat, oscore, kk, use_tabu);
+    if (lane < nc) finish_column_j(p, j, tb, xb, 1.0 - xb, cs[lane], b, oxhat, oscore, kk, use_tabu, asp_ref(Wk, walker));
     __syncwarp();
   }
   b = block_reduce_best(b, sm_b);
@@ -835,7 +908,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   if (select_parts <= 0) return;
   __shared__ int s_flag;
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
-  select_walker(Wk, walker, select_parts, sm_b, best_out, X);
+  select_walker(P, Wk, walker, select_parts, sm_b, best_out, X);
   KT_END(Wk, 0);
 }
 
@@ -877,14 +950,24 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
   KT_BEGIN(Wk, 0);
   Best b;
   b.init();
-  // admissibility (R13) is read only for a column that would become the lane's best
+  // admissibility (R13) is read only for a column that would become the lane's best (or, with
+  // aspiration, for every column with s > 0: a tabu one is noted, R18)
+  const AspRef A = asp_ref(Wk, wr);
   auto offer = [&](double sc, int j, int p, double v) {
-    if (better_move(sc, j, b.s, b.j) && (!use_tabu || (long long)__ldg(TB + p) <= kk)) {
-      b.s = sc;
-      b.v = v;
-      b.j = j;
-      b.p = p;
+    const bool bm = better_move(sc, j, b.s, b.j);
+    if (!bm && !(A.a && sc > 0.0)) return;
+    if (use_tabu) {
+      const int32_t tp = __ldg(TB + p);
+      if ((long long)tp > kk) {
+        if (live) asp_note(A, p, j, tp, v, sc);
+        return;
+      }
     }
+    if (!bm) return;
+    b.s = sc;
+    b.v = v;
+    b.j = j;
+    b.p = p;
   };
   const int nwarps = gridDim.x * (kBinWmThreads / 32);
   int t = blockIdx.x * (kBinWmThreads / 32) + wid;
@@ -1043,6 +1126,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
   const int32_t* __restrict__ TB = Wk.tabu;
   const long long kk = Wk.sc[0].k;
   const int use_tabu = Wk.use_tabu;
+  const AspRef A = asp_ref(Wk, 0);
   if (tid == 0) {
     for (int q = 0; q < kRowStages; ++q) {
       mbar_init(&R.full[q], 1);
@@ -1138,9 +1222,17 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
         const int v = vq + i * kRowThreads;
         if (v >= v1) break;
         const double s = 0.5 * (double)tot[i];
-        if (!better_move(s, jq[i], b.s, b.j)) continue;
+        const bool bm = better_move(s, jq[i], b.s, b.j);
+        if (!bm && !(A.a && s > 0.0)) continue;
         const int p = p0 + v * nb;
-        if (use_tabu && (long long)__ldg(TB + p) > kk) continue;
+        if (use_tabu) {
+          const int32_t tp = __ldg(TB + p);
+          if ((long long)tp > kk) {
+            asp_note(A, p, jq[i], tp, 1.0 - (double)((bits[v >> 5] >> (v & 31)) & 1u), s);
+            continue;
+          }
+        }
+        if (!bm) continue;
         b.s = s;
         b.v = 1.0 - (double)((bits[v >> 5] >> (v & 31)) & 1u);
         b.j = jq[i];
@@ -1248,12 +1340,20 @@ __device__ __forceinline__ bool better_off(S s1, int v1, S s0, int v0) {
 // that would become the lane's best.
 __device__ __forceinline__ void offer_column(int p, int j, const int32_t* __restrict__ TB, double xb, double v,
                                              double s, Best& b, double* oxhat, double* oscore, long long k,
-                                             int use_tabu) {
+                                             int use_tabu, AspRef A) {
   if (s == -INFINITY) v = xb;
   if (oxhat) oxhat[j] = v;
   if (oscore) oscore[j] = s;
-  if (!better_move(s, j, b.s, b.j)) return;
-  if (use_tabu && (long long)__ldg(TB + p) > k) return;
+  const bool bm = better_move(s, j, b.s, b.j);
+  if (!bm && !(A.a && s > 0.0)) return;
+  if (use_tabu) {
+    const int32_t tp = __ldg(TB + p);
+    if ((long long)tp > k) {
+      asp_note(A, p, j, tp, v, s);
+      return;
+    }
+  }
+  if (!bm) return;
   b.s = s;
   b.v = v;
   b.j = j;
@@ -1395,7 +1495,7 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
                                            const int32_t* __restrict__ TB, const WTile& T, const WTile& Tn,
                                            bool has_next, GenRound& R, int lane, GenWarp& S, bool rint,
                                            const int4* __restrict__ tab, Best& b, double* oxhat, double* oscore,
-                                           long long kk, int use_tabu) {
+                                           long long kk, int use_tabu, AspRef A) {
   const int nc = T.ncols, len = T.e1 - T.e0;
   // column data of lane c (loads in flight during phase 1)
   const int p = T.p0 + lane;
@@ -1434,7 +1534,7 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
   if (ovf) {   // an offset beyond the int path: every column of the tile in double
     double v, sv;
     gen_column_serial(P, X, RS, st, p, v, sv);
-    offer_column(p, j, TB, xb, v, sv, b, oxhat, oscore, kk, use_tabu);
+    offer_column(p, j, TB, xb, v, sv, b, oxhat, oscore, kk, use_tabu, A);
     return;
   }
   // phase 2, pass 0: β, α, the nearest candidate on each side (bounds included) and the positive
@@ -1541,7 +1641,7 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
     // a bound beyond the clamp is the farthest candidate of its side: report its exact value
     v = (bv == hi && ufin && hid > (double)kKeyLim) ? u : ((bv == lo && lfin && lod < -(double)kKeyLim) ? l : xb + (double)bv);
   }
-  offer_column(p, j, TB, xb, v, sres, b, oxhat, oscore, kk, use_tabu);
+  offer_column(p, j, TB, xb, v, sres, b, oxhat, oscore, kk, use_tabu, A);
 }
 
 // A warp chunk (<= kBktChunk nonzeros) of a long general integer column with domain [l, u],
@@ -1726,7 +1826,7 @@ __device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalk
   }
   if (lane == 0)
     finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, bv, bs, b, oxhat,
-                    oscore, kk, use_tabu);
+                    oscore, kk, use_tabu, asp_ref(Wk, walker));
 }
 
 // wm_mode 1 (walker groups): the integer general tiles and the empty columns are k_eval_gen_wm's;
@@ -1764,6 +1864,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   C.use_tabu = use_tabu;
   C.oxhat = oxhat;
   C.oscore = oscore;
+  C.asp = asp_ref(Wk, walker);
   Best b;
   b.init();
   const bool wint = sc->wint != 0;   // integral weights <= 2^20: the int paths
@@ -1784,8 +1885,8 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     if (has_next) Tn = P.gitems[t + nwarps];
     if (T.kind == CC_GEN) {
       if (!r_ok) R = gen_round(P, T, 4 * lane);
-      if (wint) gen32_tile<true>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu);
-      else gen32_tile<false>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu);
+      if (wint) gen32_tile<true>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
+      else gen32_tile<false>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
       r_ok = has_next && Tn.kind == CC_GEN;
     } else if (T.kind == CC_LBKT) {
       const LongCol L = P.lcols[T.e1];
@@ -1799,7 +1900,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
         const int p = T.p0 + lane;
         double v, sv;
         gen_column_serial(P, X, RS, st, p, v, sv);
-        offer_column(p, __ldg(P.perm + p), TB, __ldg(X + p), v, sv, b, oxhat, oscore, kk, use_tabu);
+        offer_column(p, __ldg(P.perm + p), TB, __ldg(X + p), v, sv, b, oxhat, oscore, kk, use_tabu, C.asp);
       }
     } else {
       wtile_empty(P, C, T, lane, b);
@@ -1813,7 +1914,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   if (select_parts <= 0) return;   // as in k_eval_bin: the last eval kernel selects
   __shared__ int s_flag;
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
-  select_walker(Wk, walker, select_parts, sm_b, best_out, X);
+  select_walker(P, Wk, walker, select_parts, sm_b, best_out, X);
   KT_END(Wk, 1);
 }
 
@@ -1852,13 +1953,22 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
   KT_BEGIN(Wk, 1);
   Best b;
   b.init();
+  const AspRef A = asp_ref(Wk, wr);
   auto offer = [&](double sc, double v, int j, int p) {
-    if (better_move(sc, j, b.s, b.j) && (!use_tabu || (long long)__ldg(TB + p) <= kk)) {
-      b.s = sc;
-      b.v = v;
-      b.j = j;
-      b.p = p;
+    const bool bm = better_move(sc, j, b.s, b.j);
+    if (!bm && !(A.a && sc > 0.0)) return;
+    if (use_tabu) {
+      const int32_t tp = __ldg(TB + p);
+      if ((long long)tp > kk) {
+        if (live) asp_note(A, p, j, tp, v, sc);
+        return;
+      }
     }
+    if (!bm) return;
+    b.s = sc;
+    b.v = v;
+    b.j = j;
+    b.p = p;
   };
   const int nwarps = gridDim.x * (kGenWmThreads / 32);
   for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < P.n_wtiles; t += nwarps) {
@@ -1973,6 +2083,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   C.use_tabu = Wk.use_tabu;
   C.oxhat = oxhat;
   C.oscore = oscore;
+  C.asp = asp_ref(Wk, walker);
   Best b;
   b.init();
   // long binary columns of walker groups (k_eval_bin_wm takes no chunk tickets), finished after all
@@ -1997,7 +2108,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
   KT_END(Wk, 2);
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
-  select_walker(Wk, walker, part_base + (int)gridDim.x, sm_b, best_out, C.x);
+  select_walker(P, Wk, walker, part_base + (int)gridDim.x, sm_b, best_out, C.x);
   KT_END(Wk, 2);
 }
 

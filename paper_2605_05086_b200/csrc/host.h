@@ -161,6 +161,8 @@ struct chap_walkers {
   int genwm_grid = 0;          // k_eval_gen_wm blocks per walker group (walker groups), 0 = off
   bool pdl = false;            // tabu iterations launched with programmatic dependent launch (CHAP_PDL=1)
   size_t genwm_smem = 0;
+  cudaAccessPolicyWindow l2win{};      // chap_params.l2_persist: the row state's L2 window
+  bool l2win_on = false;
   ~chap_walkers() {
     if (xs) chap_exchange_state_free(xs);
     if (gexec) cudaGraphExecDestroy(gexec);

@@ -189,12 +189,13 @@ def test_host_buffer_variant_equals_device():
     assert mh.tobytes() == chap.move_from_bytes(md).tobytes()
 
 
-def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10, binary_kernel=0):
+def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10, binary_kernel=0,
+                  aspiration=0):
     P = chap.Problem.from_instance(inst)
     O = oracle.Problem.from_instance(inst)
     prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure,
-                              binary_kernel=binary_kernel)
-    oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap)
+                              binary_kernel=binary_kernel, aspiration=aspiration)
+    oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap, aspiration=aspiration)
     X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
     Wk = chap.Walkers(P, X0, prm)
     log = chap.records(Wk.step(n_iters, log=True)).reshape(n_iters, len(x0s))
@@ -544,3 +545,21 @@ def test_gridsort_1e5_column():
     v, sc = exact.alg1(sub, r, x, w[col], jl, lb[jl], ub[jl], True)
     assert sc is not None
     assert gs[jl] == float(sc) and gx[jl] == float(v), (gx[jl], gs[jl], float(v), float(sc))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_trajectory_aspiration_config_T(seed, binrow):
+    """NEXT f1 (R18, incumbent aspiration): 300-iteration trajectories bit-exact against the oracle's
+    rule (itself replayed in exact arithmetic by tests/test_oracle_tabu.py), which takes aspiration
+    moves on every one of these walks."""
+    inst = synth.tiny(seed)
+    _traj_compare(inst, [synth.x_lower(inst)], 300, aspiration=1, binary_kernel=binrow)
+
+
+def test_trajectory_aspiration_mixed_and_groups():
+    """Aspiration through every column class (general tiles, long chunks, sorted columns) and with
+    walker groups (6 walkers: the walker-minor kernels note tabu columns per lane)."""
+    inst = _sorted_mix(seed=21)
+    _traj_compare(inst, [synth.x_lower(inst)], 60, aspiration=1, tenure=6)
+    inst = synth.mixed(seed=4, n=3000, m=600, n_long=4, long_lo=300, long_hi=5000)
+    _traj_compare(inst, [synth.x_random(inst, s) for s in range(6)], 60, aspiration=1, tenure=5)

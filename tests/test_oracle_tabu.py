@@ -63,6 +63,7 @@ def _replay(inst, P, x0, log, params, check_alg1=True):
             rr.append(({j: c[j] for j in range(n) if c[j] != 0}, cut, -1, 0))
         return rr
 
+    n_asp = [0]          # moves admitted by aspiration
     # k = 0 incumbent check (R15)
     r = resid()
     if all(v <= 0 for v in r):
@@ -74,13 +75,22 @@ def _replay(inst, P, x0, log, params, check_alg1=True):
         r = resid()
         xf = [float(v) for v in x]
         # admissible argmax by Algorithm 1 in exact arithmetic
+        def feasible_after(j, v):   # aspiration (R18): no active row violated after x_j <- v
+            keep = x[j]
+            x[j] = F(v)
+            ok = all(q <= 0 for q in resid())
+            x[j] = keep
+            return ok
+
         if check_alg1:
             best = None
             for j in range(n):
-                if lb[j] == ub[j] or tabu[j] > k:
+                if lb[j] == ub[j]:
                     continue
                 v, s = exact.alg1(rr, r, xf, [float(q) for q in w], j, lb[j], ub[j], True)
                 s = s if s is not None else -math.inf
+                if tabu[j] > k and not (getattr(params, "aspiration", 0) and s > 0 and feasible_after(j, v)):
+                    continue
                 if best is None or s > best[0]:
                     best = (s, j, v)
             exp_s = best[0] if best else -math.inf
@@ -91,7 +101,9 @@ def _replay(inst, P, x0, log, params, check_alg1=True):
                 assert rec["j"] == -1, k
         if rec["j"] >= 0:
             j, v = int(rec["j"]), F(rec["v"])
-            assert tabu[j] <= k                     # admissible
+            if tabu[j] > k:                         # admissible only by aspiration (R18)
+                assert getattr(params, "aspiration", 0) and feasible_after(j, v), k
+                n_asp[0] += 1
             assert lb[j] <= v <= ub[j] and v != x[j] and v.denominator == 1
             # chosen score == recomputed sum of penalties (north star invariant)
             s = exact.score(rr, r, xf, [float(q) for q in w], j, v)
@@ -112,6 +124,7 @@ def _replay(inst, P, x0, log, params, check_alg1=True):
         assert rec["obj"] == float(sum(ci * xi for ci, xi in zip(c, x)))
         assert all(1 <= q <= params.weight_cap for q in w)
         objs.append(best_obj)
+    _replay.n_asp = n_asp[0]
     return best_obj
 
 
@@ -231,3 +244,20 @@ def test_summary_and_restart_golden():
         assert W.has_incumbent == bool(exp["has_incumbent"])
         if exp["has_incumbent"]:
             assert W.best_obj == exp["best_obj"] and W.cutoff_rhs == exp["cutoff_rhs"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tabu_replay_aspiration(seed):
+    """NEXT f1, R18 (incumbent aspiration): every logged step of an oracle walk with aspiration on is
+    recomputed in exact arithmetic — Algorithm 1 for every variable, tabu variables admitted only
+    when the exact residuals after their move leave no active row violated — and the walk takes
+    aspiration moves (config T, tenure 10)."""
+    inst = synth.tiny(seed)
+    P = oracle.Problem.from_instance(inst)
+    prm = oracle.TabuParams(tenure=10, aspiration=1)
+    x0 = synth.x_lower(inst)
+    W = oracle.TabuWalker(P, x0, prm)
+    log = W.run(120)
+    best = _replay(inst, P, x0, log, prm)
+    assert (best is None and not W.has_incumbent) or float(best) == W.best_obj
+    assert _replay.n_asp > 0, "no aspiration move in this walk"
