@@ -300,6 +300,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=200)
     ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--no-cutoff", action="store_true",
+                    help="A/B runs: leave the cutoff row inactive (no planted objective)")
     ap.add_argument("--param", action="append", default=[],
                     help="chap_params field override NAME=VALUE (A/B runs, e.g. l2_persist=0)")
     args = ap.parse_args()
@@ -333,7 +335,7 @@ def main():
         k, v = kv.split("=", 1)
         setattr(prm, k, type(getattr(prm, k))(float(v)) if isinstance(getattr(prm, k), float) else int(v))
     ws = chap.Walkers(P, x0, prm)
-    z_star = planted_objective(inst)
+    z_star = None if args.no_cutoff else planted_objective(inst)
     if z_star is not None:
         ws.set_cutoff(z_star)   # the cutoff row is active from the start
     ws.timing(1)   # per-kernel %globaltimer spans inside the graphs (no events), on before the warm-up

@@ -194,6 +194,12 @@ typedef struct {
   int32_t aspiration;    /* 1 = incumbent aspiration (NEXT f1, DESIGN R18): a tabu variable is
                             admissible when its best shift makes the point feasible (a new
                             incumbent, the cutoff row included); 0 (default) = off           */
+  int32_t lazy;          /* 1 = selective re-evaluation (NEXT f2, an A/B against the paper's
+                            from-scratch pass): only the columns whose x̄ or row
+                            state changed are re-evaluated, the others keep their cached best
+                            shift (identical results); one walker only; 0 (default) = every
+                            variable every iteration                                          */
+  int32_t pad_params;
 } chap_params;
 
 /* Fill *out with the defaults above (n_restart = -1 meaning W_total/8). */

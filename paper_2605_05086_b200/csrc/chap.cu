@@ -919,10 +919,13 @@ static chap_status launch_binrow(const chap_problem* P, const DevWalkers& Wk, in
 // Part slots of one walker: [k_eval_bin | k_eval_gen | k_eval_binrow | k_eval]; k_eval reduces them.
 chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                               int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best,
-                              cudaStream_t s, bool pdl) {
+                              cudaStream_t s, bool pdl, int sel_grid) {
   // k_eval only selects when there are no long columns and no sort tiles: then the last eval kernel
   // (k_eval_gen, else k_eval_bin) selects in its last block and k_eval is not launched
-  const bool sel_only = Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && P->dp.n_scols == 0 && wgrid == 0;
+  // sel_grid > 0 (chap_params.lazy): the eval kernels only refresh the per-column cache, k_eval runs
+  // only for the sort tiles, and k_select_cache selects
+  const bool lazy = sel_grid > 0;
+  const bool sel_only = !lazy && Wk.W == 1 && Wk.rg == 1 && P->dp.n_tiles == 0 && P->dp.n_scols == 0 && wgrid == 0;
   const int gen_sel = (sel_only && ggrid > 0) ? bgrid + ggrid + rgrid : 0;
   const int bin_sel = (sel_only && ggrid == 0 && rgrid == 0 && bgrid > 0) ? bgrid : 0;
   if (bgrid > 0) {
@@ -943,9 +946,10 @@ chap_status chap::launch_eval(const chap_problem* P, const DevWalkers& Wk, int g
     TRY(lk(k_sort_chunks, dim3(P->dp.n_schunks, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk));
     TRY(lk(k_sort_rank, dim3(P->dp.n_schunks, Wk.W), kTileThreads, 0, s, pdl, 1, P->dp, Wk));
   }
-  if (!gen_sel && !bin_sel)
+  if (!gen_sel && !bin_sel && (!lazy || P->dp.n_tiles > 0 || P->dp.n_scols > 0))
     TRY(lk(k_eval, dim3(grid, Wk.W), kTileThreads, kTileSmem, s, pdl, 1, P->dp, Wk, oxhat, oscore, best,
            bgrid + ggrid + rgrid + wgrid, Wk.rg > 1 ? 1 : 0));
+  if (lazy) TRY(lk(k_select_cache, dim3(sel_grid), kTileThreads, 0, s, pdl, 1, P->dp, Wk));
   return CHAP_OK;
 }
 
@@ -1010,7 +1014,7 @@ static chap_status eval_launch(const chap_problem* p, const double* x, const flo
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
     k_fixed_out<<<grid_for(D.n_fixed, 256, 4 * p->sm_count), 256, 0, s>>>(D, p->e_x, xhat, score);
-  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s, false));
+  TRY(launch_eval(p, Wk, p->eval_grid, p->bin_grid, p->gen_grid, 0, 0, xhat, score, best, s, false, 0));
   CUDA_TRY(cudaMemcpyAsync(p->h_bad, p->e_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -1107,6 +1111,8 @@ extern "C" chap_status chap_params_default(chap_params* out) {
   out->pdl = 0;
   out->l2_persist = 1;
   out->aspiration = 0;
+  out->lazy = 0;
+  out->pad_params = 0;
   return CHAP_OK;
 }
 
@@ -1120,6 +1126,7 @@ static chap_status check_params(const chap_params& q) {
   if (q.pdl < 0 || q.pdl > 1) return fail(CHAP_ERR_INVALID_ARG, "pdl not in {0, 1}");
   if (q.l2_persist < 0 || q.l2_persist > 1) return fail(CHAP_ERR_INVALID_ARG, "l2_persist not in {0, 1}");
   if (q.aspiration < 0 || q.aspiration > 1) return fail(CHAP_ERR_INVALID_ARG, "aspiration not in {0, 1}");
+  if (q.lazy < 0 || q.lazy > 1) return fail(CHAP_ERR_INVALID_ARG, "lazy not in {0, 1}");
   return CHAP_OK;
 }
 
@@ -1132,6 +1139,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   chap_params prm;
   if (params) prm = *params; else chap_params_default(&prm);
   TRY(check_params(prm));
+  if (prm.lazy && W != 1) return fail(CHAP_ERR_INVALID_ARG, "lazy (selective re-evaluation) takes one walker");
   DeviceGuard g(p->device);
   auto S = new chap_walkers();
   std::unique_ptr<chap_walkers> holder(S);
@@ -1165,7 +1173,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   // one walker with integral weights whose column sums fit int32: packed binary columns row-wise
   S->binrow_grid = 0;
   const bool want_row = prm.binary_kernel == 2 || (prm.binary_kernel == 0 && p->binrow_auto);
-  if (W == 1 && want_row && p->binrow_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) &&
+  if (W == 1 && !prm.lazy && want_row && p->binrow_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) &&
       2.0 * (double)prm.weight_cap * (double)std::max(1, p->binrow_maxdeg) < 2147483647.0) {
     S->binrow_grid = p->binrow_grid;
     // the long binary chunks ride in k_eval_gen when it runs (with_lbin), else in k_eval_bin
@@ -1186,6 +1194,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
     }
   }
   Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid + S->genwm_grid;
+  if (prm.lazy) Wk.ps = std::max(Wk.ps, 4 * p->sm_count);   // k_select_cache's parts
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
   TRY(B.alloc(&Wk.sel_count, W));
   Wk.lss = p->lscr_per_walker;
@@ -1193,6 +1202,15 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   TRY(B.alloc(&S->d_bad, 1));
   Wk.asp = nullptr;
   if (prm.aspiration && prm.tenure > 0) TRY(B.alloc(&Wk.asp, (size_t)prm.tenure * W));   // R18 slots
+  Wk.cs = Wk.cv = nullptr;
+  Wk.dirty = nullptr;
+  Wk.dwords = (int32_t)((n + 31) / 32);
+  if (prm.lazy) {   // f2: per-column cache and the two dirty sets (every column dirty at first)
+    TRY(B.alloc(&Wk.cs, n));
+    TRY(B.alloc(&Wk.cv, n));
+    TRY(B.alloc(&Wk.dirty, 2 * ((size_t)Wk.dwords + 1)));
+    S->sel_grid = std::max(1, std::min((int)((n + kTileThreads - 1) / kTileThreads), 4 * p->sm_count));
+  }
   Wk.xs = n;
   Wk.rss = mn + 1;
   Wk.ts = n;
@@ -1236,6 +1254,10 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   CUDA_TRY(cudaMemsetAsync(Wk.rs, 0, sizeof(RowState) * (mn + 1) * (size_t)rg * Wk.n_groups, s));
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));
   if (Wk.asp) CUDA_TRY(cudaMemsetAsync(Wk.asp, 0xff, sizeof(Cand) * (size_t)prm.tenure * W, s));   // p = -1
+  if (Wk.dirty) {
+    CUDA_TRY(cudaMemsetAsync(Wk.dirty, 0, sizeof(uint32_t) * 2 * ((size_t)Wk.dwords + 1), s));
+    k_dirty_all<<<1, 32, 0, s>>>(Wk);
+  }
   if (D.n > 0)
     k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
   k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1);
@@ -1262,7 +1284,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
 static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
   const chap_problem* P = S->P;
   TRY(launch_eval(P, S->wk, S->eval_grid, S->bin_grid, S->gen_grid, S->binrow_grid, S->genwm_grid, nullptr, nullptr,
-                  nullptr, s, S->pdl));
+                  nullptr, s, S->pdl, S->wk.cs ? S->sel_grid : 0));
   TRY(lk(k_apply, dim3(S->apply_grid, S->W), kApplyThreads, 0, s, S->pdl, 1, P->dp, S->wk));
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
@@ -1367,6 +1389,7 @@ extern "C" chap_status chap_walkers_set_cutoff(chap_walkers* S, double z_best, v
   if (!S || !std::isfinite(z_best)) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or non-finite z_best");
   DeviceGuard g(S->P->device);
   k_set_cutoff<<<(S->W + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>(S->P->dp, S->wk, z_best);
+  if (S->wk.dirty) k_dirty_all<<<1, 32, 0, (cudaStream_t)cuda_stream>>>(S->wk);   // f2: the cutoff row moved
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -1393,6 +1416,7 @@ extern "C" chap_status chap_walkers_restart(chap_walkers* S, int32_t walker, con
   TRY(chap::walker_recompute(S->P, Wk, walker, s));
   k_tabu_clear<<<dim3(gx, 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, walker);
   k_walker_finalize_init<<<1, 1, 0, s>>>(D, Wk, 1, walker);
+  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk);   // f2: a new point
   k_flush_incumbent<<<dim3(gx, S->W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());
@@ -1493,6 +1517,9 @@ extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int
   const bool fused = sel_only && (S->gen_grid > 0 || (S->binrow_grid == 0 && S->bin_grid > 0));
   *out = (S->bin_grid > 0) + (S->gen_grid > 0) + (S->binrow_grid > 0) + (S->genwm_grid > 0) + (fused ? 0 : 1) + 1 +
          (D.n_schunks > 0 ? 2 : 0);
+  if (S->wk.cs)   // lazy: k_eval only for the sort tiles, then k_select_cache
+    *out = (S->bin_grid > 0) + (S->gen_grid > 0) + ((D.n_tiles > 0 || D.n_scols > 0) ? 1 : 0) + 1 + 1 +
+           (D.n_schunks > 0 ? 2 : 0);
   return CHAP_OK;
 }
 

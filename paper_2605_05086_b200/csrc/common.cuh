@@ -308,6 +308,13 @@ struct DevWalkers {
   float wcap;
   double delta;                        // NaN = auto
   unsigned long long* kt;              // [kKtWords] kernel timing, NULL = off
+  // selective re-evaluation (chap_params.lazy, NEXT f2; one walker): cached per-column results and
+  // two dirty bitsets over the internal columns (iteration k evaluates set k & 1, its apply marks set
+  // (k + 1) & 1 and clears set k & 1); word dwords of a set = "every column dirty"
+  double* cs;                          // [n] cached s_j (internal order), NULL = from scratch
+  double* cv;                          // [n] cached x̂_j
+  uint32_t* dirty;                     // [2][dwords + 1]
+  int32_t dwords;
   Cand* asp;                           // [W][tenure] aspiration slots (chap_params.aspiration), NULL = off:
                                        // the eval kernels note every tabu column with s > 0 in slot
                                        // tabu_until % tenure; the select takes the feasible ones (R18)

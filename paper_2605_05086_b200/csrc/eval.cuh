@@ -106,15 +106,40 @@ __device__ __forceinline__ void write_part(Cand* dst, const Best& b) {
 
 // Aspiration slots of one walker (R18): a tabu column with s > 0 is noted in slot tabu_until % T
 // (the <= T tabu variables have distinct expiries k'+1+T, k' in [k-T, k-1]); a = NULL: off.
+// The same reference carries the per-column result cache of selective re-evaluation (f2).
 struct AspRef {
   Cand* a = nullptr;
   int T = 1;
+  double* cs = nullptr;   // chap_params.lazy: cached (s_j, x̂_j) by internal column
+  double* cv = nullptr;
 };
 __device__ __forceinline__ AspRef asp_ref(const DevWalkers& Wk, int w) {
   AspRef r;
   r.a = Wk.asp ? Wk.asp + (size_t)w * Wk.tenure : nullptr;
   r.T = Wk.tenure > 0 ? Wk.tenure : 1;
+  r.cs = Wk.cs;
+  r.cv = Wk.cv;
   return r;
+}
+__device__ __forceinline__ void cache_col(const AspRef& A, int p, double v, double s) {
+  if (A.cs) {
+    A.cs[p] = s;
+    A.cv[p] = v;
+  }
+}
+// f2: does any of the internal columns [p0, p0 + nc) (nc <= 33) need re-evaluation at iteration k?
+__device__ __forceinline__ bool cols_dirty(const DevWalkers& Wk, long long k, int p0, int nc) {
+  if (!Wk.dirty || nc <= 0) return true;
+  const uint32_t* d = Wk.dirty + (size_t)(k & 1) * (Wk.dwords + 1);
+  if (__ldcg(d + Wk.dwords)) return true;
+  const int p1 = p0 + nc - 1;
+  for (int w = p0 >> 5; w <= (p1 >> 5); ++w) {
+    uint32_t m = __ldcg(d + w);
+    if (w == (p0 >> 5)) m &= ~0u << (p0 & 31);
+    if (w == (p1 >> 5)) m &= ~0u >> (31 - (p1 & 31));
+    if (m) return true;
+  }
+  return false;
 }
 __device__ __forceinline__ void asp_note(const AspRef& A, int p, int j, long long tabu_p, double v, double s) {
   if (!A.a || !(s > 0.0)) return;
@@ -134,6 +159,7 @@ __device__ __forceinline__ void finish_column_j(int p, int j, int32_t tabu_p, do
   if (s == -INFINITY) v = xb;
   if (oxhat) oxhat[j] = v;
   if (oscore) oscore[j] = s;
+  cache_col(A, p, v, s);
   if (use_tabu && (long long)tabu_p > k) {
     asp_note(A, p, j, tabu_p, v, s);
     return;
@@ -427,6 +453,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_chunks(DevProblem P, DevW
   const int walker = blockIdx.y, tid = threadIdx.x;
   const Tile T = P.schunks[blockIdx.x];
   const int p = T.p0, ch = T.ncols, d = T.e1 - T.e0;
+  if (!cols_dirty(Wk, Wk.sc[walker].k, p, 1)) return;   // f2: a clean column keeps its cached result
   const double* X = Wk.x + (size_t)walker * Wk.xs;
   const RowView rs = row_view(Wk, walker);
   const double xb = X[p], l = P.lb[p], u = P.ub[p];
@@ -520,6 +547,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_rank(DevProblem P, DevWal
   const int walker = blockIdx.y, tid = threadIdx.x;
   const Tile T = P.schunks[blockIdx.x];
   const int p = T.p0, ch = T.ncols;
+  if (!cols_dirty(Wk, Wk.sc[walker].k, p, 1)) return;
   const SortCol C = P.scols[T.pad];
   const double* X = Wk.x + (size_t)walker * Wk.xs;
   const double xb = X[p];
@@ -819,7 +847,8 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   int t = blockIdx.x * (kBinThreads / 32) + wid;
   // chunks of long columns first (their latency overlaps the packed tiles of other warps)
   for (; t < P.n_bchunks; t += nwarps)
-    lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
+    if (cols_dirty(Wk, kk, P.bchunks[t].p0, 1))
+      lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
   t -= P.n_bchunks;
   const int hwi = lane >> 3, sh = 4 * (lane & 7);   // head word and bit offset of my 4 slots
   WTile Tn;
@@ -827,6 +856,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   for (; t < P.n_btiles; t += nwarps) {
     const WTile T = Tn;
     if (t + nwarps < P.n_btiles) Tn = P.btiles[t + nwarps];
+    if (!cols_dirty(Wk, kk, T.p0, T.ncols)) continue;   // f2
     const int nc = T.ncols, len = T.e1 - T.e0;
     // slots 4 lane .. 4 lane + 3: one 16-byte index load, two 16-byte value loads
     const bool act = 4 * lane < len;
@@ -1344,6 +1374,7 @@ __device__ __forceinline__ void offer_column(int p, int j, const int32_t* __rest
   if (s == -INFINITY) v = xb;
   if (oxhat) oxhat[j] = v;
   if (oscore) oscore[j] = s;
+  cache_col(A, p, v, s);
   const bool bm = better_move(s, j, b.s, b.j);
   if (!bm && !(A.a && s > 0.0)) return;
   if (use_tabu) {
@@ -1883,7 +1914,10 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     const bool has_next = t + nwarps < iend;
     WTile Tn;
     if (has_next) Tn = P.gitems[t + nwarps];
-    if (T.kind == CC_GEN) {
+    const bool chunk = T.kind == CC_LBKT || T.kind == CC_LBIN;
+    if (!cols_dirty(Wk, kk, T.p0, chunk ? 1 : (int)T.ncols)) {   // f2: a clean item keeps its cached results
+      r_ok = false;
+    } else if (T.kind == CC_GEN) {
       if (!r_ok) R = gen_round(P, T, 4 * lane);
       if (wint) gen32_tile<true>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
       else gen32_tile<false>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
@@ -2097,19 +2131,62 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_eval(DevProblem P, DevWalke
   }
   // long general columns sorted grid-wide (k_sort_chunks, k_sort_rank ran before this kernel)
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < P.n_scols; q += gridDim.x * blockDim.x)
-    sortcol_finish(P, Wk, walker, P.scols[q], b, oxhat, oscore, C.k, C.use_tabu);
+    if (cols_dirty(Wk, C.k, P.scols[q].p, 1)) sortcol_finish(P, Wk, walker, P.scols[q], b, oxhat, oscore, C.k, C.use_tabu);
   // block tiles: single-column sorts
   for (int t = blockIdx.x; t < P.n_tiles; t += gridDim.x)
-    tile_genm(P, C, P.tiles[t], *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b);
+    if (cols_dirty(Wk, C.k, P.tiles[t].p0, 1))
+      tile_genm(P, C, P.tiles[t], *reinterpret_cast<SmemGenM*>(smem), sm_red, sm_b, b);
   __syncthreads();
   // publish the block's best; the last block of this walker selects (R6)
   b = block_reduce_best(b, sm_b);
   Cand* part = Wk.part + (size_t)walker * Wk.ps;
   if (threadIdx.x == 0) write_part(part + part_base + blockIdx.x, b);
   KT_END(Wk, 2);
+  if (Wk.cs) return;   // f2: k_select_cache selects from the cached results
   if (!last_chunk(Wk.sel_count + walker, gridDim.x, &s_flag)) return;
   select_walker(P, Wk, walker, part_base + (int)gridDim.x, sm_b, best_out, C.x);
   KT_END(Wk, 2);
+}
+
+// f2 (chap_params.lazy, one walker): the best admissible move (R6, R13; aspiration notes, R18) over
+// the cached per-column results: the columns evaluated this iteration (dirty) and the clean ones,
+// whose cached (s_j, x̂_j) is unchanged because neither x̄_j nor any row state of the column changed.
+__global__ void __launch_bounds__(kTileThreads) k_select_cache(DevProblem P, DevWalkers Wk) {
+  pdl_wait_trigger();
+  __shared__ Best sm_b[32];
+  __shared__ int s_flag;
+  const long long kk = Wk.sc[0].k;
+  const AspRef A = asp_ref(Wk, 0);
+  Best b;
+  b.init();
+  for (int p = P.n_fixed + blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) {
+    const double s = __ldcg(Wk.cs + p);
+    if (s == -INFINITY) continue;
+    const int j = __ldg(P.perm + p);
+    const bool bm = better_move(s, j, b.s, b.j);
+    if (!bm && !(A.a && s > 0.0)) continue;
+    if (Wk.use_tabu) {
+      const int32_t tp = Wk.tabu[p];
+      if ((long long)tp > kk) {
+        asp_note(A, p, j, tp, __ldcg(Wk.cv + p), s);
+        continue;
+      }
+    }
+    if (!bm) continue;
+    b.s = s;
+    b.v = __ldcg(Wk.cv + p);
+    b.j = j;
+    b.p = p;
+  }
+  b = block_reduce_best(b, sm_b);
+  if (threadIdx.x == 0) write_part(Wk.part + blockIdx.x, b);
+  if (!last_chunk(Wk.sel_count, gridDim.x, &s_flag)) return;
+  select_walker(P, Wk, 0, (int)gridDim.x, sm_b, nullptr, Wk.x);
+}
+
+// f2: every column of both dirty sets (walker create, restart, an external cutoff).
+__global__ void k_dirty_all(DevWalkers Wk) {
+  if (Wk.dirty && threadIdx.x < 2) Wk.dirty[(size_t)threadIdx.x * (Wk.dwords + 1) + Wk.dwords] = 1u;
 }
 
 // Outputs of fixed variables (internal [0, n_fixed)): (x̄, -inf) (R2 leaves no candidate).

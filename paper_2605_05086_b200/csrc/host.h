@@ -159,6 +159,7 @@ struct chap_walkers {
   int gen_grid = 0;            // k_eval_gen blocks per walker
   int binrow_grid = 0;         // k_eval_binrow CTAs (one walker, row-wise binary columns), 0 = off
   int genwm_grid = 0;          // k_eval_gen_wm blocks per walker group (walker groups), 0 = off
+  int sel_grid = 0;            // k_select_cache blocks (chap_params.lazy)
   bool pdl = false;            // tabu iterations launched with programmatic dependent launch (CHAP_PDL=1)
   size_t genwm_smem = 0;
   cudaAccessPolicyWindow l2win{};      // chap_params.l2_persist: the row state's L2 window
@@ -178,7 +179,7 @@ namespace chap {
 // shared launch helpers (chap.cu)
 chap_status launch_eval(const chap_problem* P, const DevWalkers& Wk, int grid, int bgrid, int ggrid,
                         int rgrid, int wgrid, double* oxhat, double* oscore, chap_move* best, cudaStream_t s,
-                        bool pdl);
+                        bool pdl, int sel_grid);
 int grid_for(long long work, int threads, int cap);
 chap_status walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s);
 

@@ -186,6 +186,7 @@ static chap_status restart_internal(chap_walkers* S, int w, const double* x_int,
   TRY(chap::walker_recompute(P, Wk, w, s));
   k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, w);
   k_walker_finalize_init<<<1, 1, 0, s>>>(D, Wk, 1, w);
+  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk);   // f2: a new point
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), S->W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());

@@ -258,6 +258,30 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
       if (rw[i].r > 0.0) rw[i].w = fminf(rw[i].w + 1.0f, Wk.wcap);
     }
   }
+  if (Wk.dirty) {   // f2: mark the columns whose result changes for iteration k + 1; clear set k & 1
+    const long long kd = sc->k;
+    uint32_t* cur = Wk.dirty + (size_t)(kd & 1) * (Wk.dwords + 1);
+    uint32_t* nxt = Wk.dirty + (size_t)((kd + 1) & 1) * (Wk.dwords + 1);
+    for (int q = gtid; q <= Wk.dwords; q += gstride) cur[q] = 0u;
+    if (d.move) {   // x̄_j* and the row state of the rows of column j*: every column of those rows
+      if (gtid == 0) atomicOr(nxt + (d.p >> 5), 1u << (d.p & 31));
+      const int e0 = P.col_ptr[d.p], e1 = P.col_ptr[d.p + 1];
+      for (int e = e0 + gtid; e < e1; e += gstride) {
+        const int i = P.row_idx[e];
+        if ((i == P.cut_row && !cut_active) || i == P.dummy_row) continue;
+        if (i == P.cut_row) {   // the dense cutoff row: every column
+          nxt[Wk.dwords] = 1u;
+          continue;
+        }
+        for (int e2 = P.rp[i]; e2 < P.rp[i + 1]; ++e2) {
+          const int q = P.ci[e2];
+          atomicOr(nxt + (q >> 5), 1u << (q & 31));
+        }
+      }
+    } else if (gtid == 0) {   // a weight bump (every violated row): every column
+      nxt[Wk.dwords] = 1u;
+    }
+  }
   for (int off = 16; off > 0; off >>= 1) dv += __shfl_xor_sync(kFull, dv, off);
   if ((tid & 31) == 0) smv[tid >> 5] = dv;
   __syncthreads();
@@ -293,7 +317,10 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   } else {
     sc->n_stuck = vsc->n_stuck + 1;
   }
-  if (vsc->violated == 0) take_incumbent(P, Wk, sc, rw);   // PAPER.md:373, R15
+  if (vsc->violated == 0) {   // PAPER.md:373, R15
+    take_incumbent(P, Wk, sc, rw);
+    if (Wk.dirty) Wk.dirty[(size_t)((k + 1) & 1) * (Wk.dwords + 1) + Wk.dwords] = 1u;   // the cutoff row moved
+  }
   chap_step_record* log = vsc->log;
   if (log) {
     chap_step_record rec;

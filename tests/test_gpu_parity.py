@@ -190,11 +190,11 @@ def test_host_buffer_variant_equals_device():
 
 
 def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10, binary_kernel=0,
-                  aspiration=0):
+                  aspiration=0, lazy=0):
     P = chap.Problem.from_instance(inst)
     O = oracle.Problem.from_instance(inst)
     prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure,
-                              binary_kernel=binary_kernel, aspiration=aspiration)
+                              binary_kernel=binary_kernel, aspiration=aspiration, lazy=lazy)
     oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap, aspiration=aspiration)
     X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
     Wk = chap.Walkers(P, X0, prm)
@@ -563,3 +563,31 @@ def test_trajectory_aspiration_mixed_and_groups():
     _traj_compare(inst, [synth.x_lower(inst)], 60, aspiration=1, tenure=6)
     inst = synth.mixed(seed=4, n=3000, m=600, n_long=4, long_lo=300, long_hi=5000)
     _traj_compare(inst, [synth.x_random(inst, s) for s in range(6)], 60, aspiration=1, tenure=5)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_trajectory_lazy_config_T(seed):
+    """NEXT f2 (selective re-evaluation, chap_params.lazy): only the columns whose x̄ or row state
+    changed are re-evaluated; the trajectory (moves, stuck bumps, incumbents that move the dense
+    cutoff row) is bit-exact against the oracle's from-scratch walk, with and without aspiration."""
+    inst = synth.tiny(seed)
+    _traj_compare(inst, [synth.x_lower(inst)], 400, lazy=1, graph_iters=16 if seed % 2 else 0)
+    _traj_compare(inst, [synth.x_lower(inst)], 200, lazy=1, aspiration=1)
+
+
+def test_trajectory_lazy_all_classes():
+    """Selective re-evaluation through every column class: packed binary and general tiles, long
+    binary and bounded-integer chunks (tickets), block-sorted and grid-sorted general columns."""
+    _traj_compare(_sorted_mix(seed=22), [synth.x_lower(_sorted_mix(seed=22))], 80, lazy=1)
+    inst = _gridsort_mix(seed=23)
+    _traj_compare(inst, [synth.x_random(inst, 2, spread=30)], 20, lazy=1)
+    inst = synth.setcover(seed=3, m=1500, n=6000)
+    _traj_compare(inst, [synth.x_lower(inst)], 300, lazy=1)
+
+
+def test_lazy_rejects_walker_sets():
+    inst = synth.tiny(1)
+    P = chap.Problem.from_instance(inst)
+    X0 = torch.from_numpy(np.stack([synth.x_lower(inst)] * 2)).cuda()
+    with pytest.raises(chap.ChapError):
+        chap.Walkers(P, X0, chap.default_params(lazy=1))
