@@ -1905,19 +1905,10 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   const int ifirst = with_lbin ? 0 : P.n_bchunks;
   const int iend = wm_mode ? P.n_bchunks + P.n_gchunks + P.n_ctiles : P.n_gitems;
   const int nwarps = gridDim.x * (kGenThreads / 32);
-  int t = ifirst + blockIdx.x * (kGenThreads / 32) + wid;
-  WTile T;
-  if (t < iend) T = P.gitems[t];
   GenRound R;
   bool r_ok = false;   // R holds T's first round
-  for (; t < iend; t += nwarps) {
-    const bool has_next = t + nwarps < iend;
-    WTile Tn;
-    if (has_next) Tn = P.gitems[t + nwarps];
-    const bool chunk = T.kind == CC_LBKT || T.kind == CC_LBIN;
-    if (!cols_dirty(Wk, kk, T.p0, chunk ? 1 : (int)T.ncols)) {   // f2: a clean item keeps its cached results
-      r_ok = false;
-    } else if (T.kind == CC_GEN) {
+  auto run_item = [&](const WTile& T, const WTile& Tn, bool has_next) {
+    if (T.kind == CC_GEN) {
       if (!r_ok) R = gen_round(P, T, 4 * lane);
       if (wint) gen32_tile<true>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
       else gen32_tile<false>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
@@ -1940,7 +1931,42 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
       wtile_empty(P, C, T, lane, b);
     }
     __syncwarp();
-    T = Tn;
+  };
+  const int t0 = ifirst + blockIdx.x * (kGenThreads / 32) + wid;
+  if (Wk.dirty) {
+    // f2: the warp's items 32 at a time, lane l testing item l (one round of loads for 32 items);
+    // only the items with a dirty column are evaluated, the others keep their cached results
+    for (int base = t0; base < iend; base += 32 * nwarps) {
+      const int tl = base + lane * nwarps;
+      WTile Tl;
+      bool dl = false;
+      if (tl < iend) {
+        Tl = P.gitems[tl];
+        dl = cols_dirty(Wk, kk, Tl.p0, (Tl.kind == CC_LBKT || Tl.kind == CC_LBIN) ? 1 : (int)Tl.ncols);
+      }
+      for (unsigned m = __ballot_sync(kFull, dl); m; m &= m - 1) {
+        const int q = __ffs(m) - 1;
+        WTile T;
+        T.p0 = __shfl_sync(kFull, Tl.p0, q);
+        T.e0 = __shfl_sync(kFull, Tl.e0, q);
+        T.e1 = __shfl_sync(kFull, Tl.e1, q);
+        T.ncols = (int16_t)__shfl_sync(kFull, (int)Tl.ncols, q);
+        T.kind = (int8_t)__shfl_sync(kFull, (int)Tl.kind, q);
+        r_ok = false;
+        run_item(T, T, false);
+      }
+    }
+  } else {
+    int t = t0;
+    WTile T;
+    if (t < iend) T = P.gitems[t];
+    for (; t < iend; t += nwarps) {
+      const bool has_next = t + nwarps < iend;
+      WTile Tn;
+      if (has_next) Tn = P.gitems[t + nwarps];
+      run_item(T, Tn, has_next);
+      T = Tn;
+    }
   }
   b = block_reduce_best(b, sm_b);
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);

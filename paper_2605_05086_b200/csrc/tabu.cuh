@@ -266,14 +266,15 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     if (d.move) {   // x̄_j* and the row state of the rows of column j*: every column of those rows
       if (gtid == 0) atomicOr(nxt + (d.p >> 5), 1u << (d.p & 31));
       const int e0 = P.col_ptr[d.p], e1 = P.col_ptr[d.p + 1];
-      for (int e = e0 + gtid; e < e1; e += gstride) {
+      const int lane = tid & 31, gw = gtid >> 5, nw = gstride >> 5;
+      for (int e = e0 + gw; e < e1; e += nw) {   // a warp per row of the column
         const int i = P.row_idx[e];
         if ((i == P.cut_row && !cut_active) || i == P.dummy_row) continue;
         if (i == P.cut_row) {   // the dense cutoff row: every column
-          nxt[Wk.dwords] = 1u;
+          if (lane == 0) nxt[Wk.dwords] = 1u;
           continue;
         }
-        for (int e2 = P.rp[i]; e2 < P.rp[i + 1]; ++e2) {
+        for (int e2 = P.rp[i] + lane; e2 < P.rp[i + 1]; e2 += 32) {
           const int q = P.ci[e2];
           atomicOr(nxt + (q >> 5), 1u << (q & 31));
         }
