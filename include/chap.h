@@ -99,6 +99,9 @@ typedef struct {
                                  than 2043 nonzeros): chunk sorts plus co-ranking across blocks
                                  ("grid-wide primitives")           */
   int32_t pad_info;
+  int64_t exchange_point_bytes; /* bytes of one packed elite point of the portfolio exchange:
+                                 binaries as bits, integers as int32 (int64 if a bound is
+                                 infinite or beyond 2^31), continuous as f64   */
 } chap_problem_info;
 
 /* Build a problem from HOST CSR data (copied; the caller may free its arrays on return).

@@ -38,7 +38,7 @@ class chap_problem_info(ctypes.Structure):
                 ("auto_cutoff_delta", c_f64), ("device_bytes", c_i64), ("model_bytes_A", c_i64),
                 ("model_bytes_pass", c_i64), ("model_bytes_kernel", c_i64 * 3), ("nnz_kernel", c_i64 * 3),
                 ("eval_launches", c_i32), ("n_sorted_columns", c_i32), ("model_bytes_walker_kernel", c_i64 * 3),
-                ("n_gridsort_columns", c_i32), ("pad_info", c_i32)]
+                ("n_gridsort_columns", c_i32), ("pad_info", c_i32), ("exchange_point_bytes", c_i64)]
 
 
 class chap_move(ctypes.Structure):

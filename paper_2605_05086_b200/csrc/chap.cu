@@ -740,6 +740,35 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.n_fixed = I.n_fixed;
   D.auto_delta = I.auto_cutoff_delta;
   D.rint_base = rint_base ? 1 : 0;
+  {  // packed exchange points: the internal columns of each class
+    std::vector<int32_t> kb, ki, kc;
+    bool i64 = false;
+    for (int32_t q = 0; q < n; ++q) {
+      const int32_t j = perm[q];
+      if (vclass[j] == 1) kb.push_back(q);
+      else if (vclass[j] == 2) {
+        ki.push_back(q);
+        if (!(std::isfinite(l[j]) && std::isfinite(u[j]) && std::fabs(l[j]) < 2147483647.0 && std::fabs(u[j]) < 2147483647.0))
+          i64 = true;
+      } else if (vclass[j] == 3) kc.push_back(q);
+    }
+    int32_t *d_kb, *d_ki, *d_kc;
+    TRY(B.upload(&d_kb, kb));
+    TRY(B.upload(&d_ki, ki));
+    TRY(B.upload(&d_kc, kc));
+    D.pk_bin = d_kb;
+    D.pk_int = d_ki;
+    D.pk_cont = d_kc;
+    D.pk_nbin = (int32_t)kb.size();
+    D.pk_nint = (int32_t)ki.size();
+    D.pk_ncont = (int32_t)kc.size();
+    D.pk_int64 = i64 ? 1 : 0;
+    auto al8 = [](int64_t b) { return (b + 7) & ~(int64_t)7; };
+    D.pk_off_int = al8(4LL * ((D.pk_nbin + 31) / 32));
+    D.pk_off_cont = al8(D.pk_off_int + (int64_t)D.pk_nint * (i64 ? 8 : 4));
+    D.pk_bytes = std::max<int64_t>(8, al8(D.pk_off_cont + 8LL * D.pk_ncont));
+    I.exchange_point_bytes = D.pk_bytes;
+  }
 
   // launch geometry: a persistent grid of (resident blocks) per walker set
   CUDA_TRY(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));

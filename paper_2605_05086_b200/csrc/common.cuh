@@ -275,6 +275,11 @@ struct DevProblem {
   const int32_t* rb_row;     // [entries] row of each entry (sorted within a slice)
   const uint32_t* rb_cv;     // [entries] column within the block (low 16 bits) | int16 a_ij (high 16)
   const RowStage* rb_stage;  // stages of the slices (RowBlock::st)
+  // packed points of the portfolio exchange: binaries as bits (PAPER.md:349's bitset),
+  // integers as int32 (int64 when a bound is infinite or beyond 2^31), continuous as f64
+  const int32_t* pk_bin; const int32_t* pk_int; const int32_t* pk_cont;   // internal columns of each class
+  int32_t pk_nbin, pk_nint, pk_ncont, pk_int64;
+  int64_t pk_off_int, pk_off_cont, pk_bytes;   // byte offsets of the sections, bytes per point
   int32_t n_fixed;           // internal columns [0, n_fixed) are fixed
   int32_t rint_base;         // integer data with |coefficients| <= 2^22 and no continuous variable: every
                              // residual is an integer while the cutoff rhs is (WalkerScalars::rint)

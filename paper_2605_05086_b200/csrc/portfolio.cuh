@@ -198,7 +198,8 @@ struct chap_exchange_state {
   int nranks = 0;
   DeviceBuffers buf;
   chap_walker_summary *d_sum_local = nullptr, *d_sum_all = nullptr;
-  double *d_send = nullptr, *d_recv = nullptr;
+  unsigned char *d_send = nullptr, *d_recv = nullptr;   // packed elite points (DevProblem::pk_bytes each)
+  double* d_x = nullptr;                                // one unpacked point (internal order)
   std::vector<chap_walker_summary> h_all;
   std::vector<int32_t> e_gid, e_slot, r_gid, r_src;
   std::vector<int8_t> e_kind;
@@ -227,8 +228,10 @@ static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want
     X.nranks = nranks;
     TRY(X.buf.alloc(&X.d_sum_local, W_local));
     TRY(X.buf.alloc(&X.d_sum_all, W_total));
-    TRY(X.buf.alloc(&X.d_send, (size_t)2 * std::max(E, 1) * std::max(n, 1)));
-    TRY(X.buf.alloc(&X.d_recv, (size_t)nranks * 2 * std::max(E, 1) * std::max(n, 1)));
+    const size_t pb = (size_t)p->dp.pk_bytes;
+    TRY(X.buf.alloc(&X.d_send, (size_t)2 * std::max(E, 1) * pb));
+    TRY(X.buf.alloc(&X.d_recv, (size_t)nranks * 2 * std::max(E, 1) * pb));
+    TRY(X.buf.alloc(&X.d_x, (size_t)std::max(n, 1)));
     X.h_all.resize(W_total);
     X.e_gid.resize(2 * E + 1);
     X.e_slot.resize(2 * E + 1);
@@ -269,14 +272,16 @@ static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want
       for (int q = 0; q < (int)loc.size() && q < E; ++q) {
         const int w = loc[q].second;
         const double* src = (kind == 0 ? Wk.best_x : Wk.x) + (size_t)w * Wk.xs;
-        CUDA_TRY(cudaMemcpyAsync(X.d_send + (size_t)(kind * E + q) * n, src, sizeof(double) * n,
-                                 cudaMemcpyDeviceToDevice, s));
+        k_pack_point<<<grid_for(n, 256, 2 * p->sm_count), 256, 0, s>>>(p->dp, src,
+                                                                        X.d_send + (size_t)(kind * E + q) * p->dp.pk_bytes);
       }
     }
+    CUDA_TRY(cudaGetLastError());
+    const size_t bytes = (size_t)2 * E * p->dp.pk_bytes;
     if (comm) {
-      NCCL_TRY(nccl().AllGather(X.d_send, X.d_recv, (size_t)2 * E * n, ncclFloat64, comm->comm, s));
+      NCCL_TRY(nccl().AllGather(X.d_send, X.d_recv, bytes, ncclUint8, comm->comm, s));
     } else {
-      CUDA_TRY(cudaMemcpyAsync(X.d_recv, X.d_send, sizeof(double) * 2 * E * n, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(X.d_recv, X.d_send, bytes, cudaMemcpyDeviceToDevice, s));
     }
   }
   if (st) return CHAP_OK;
@@ -285,7 +290,9 @@ static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want
   for (int q = 0; q < nr; ++q) {
     const int gid = X.r_gid[q];
     if (gid / W_local != rank) continue;
-    TRY(restart_internal(S, gid % W_local, X.d_recv + (size_t)X.e_slot[X.r_src[q]] * n, s));
+    k_unpack_point<<<grid_for(n, 256, 2 * p->sm_count), 256, 0, s>>>(
+        p->dp, X.d_recv + (size_t)X.e_slot[X.r_src[q]] * p->dp.pk_bytes, X.d_x);
+    TRY(restart_internal(S, gid % W_local, X.d_x, s));
   }
   return CHAP_OK;
 }
@@ -340,8 +347,9 @@ extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, 
   out->epochs = epochs;
   if (best_x && X.zg >= 0 && E > 0) {
     // E[0] is the global best incumbent; export it in user order
-    const double* src = X.d_recv + (size_t)X.e_slot[0] * n;
-    k_export_point<<<grid_for(n, 256, 4 * p->sm_count), 256, 0, s>>>(p->dp, src, best_x);
+    k_unpack_point<<<grid_for(n, 256, 2 * p->sm_count), 256, 0, s>>>(p->dp, X.d_recv + (size_t)X.e_slot[0] * p->dp.pk_bytes,
+                                                                       X.d_x);
+    k_export_point<<<grid_for(n, 256, 4 * p->sm_count), 256, 0, s>>>(p->dp, X.d_x, best_x);
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaStreamSynchronize(s));

@@ -476,6 +476,50 @@ __global__ void __launch_bounds__(256) k_summaries(DevProblem P, DevWalkers Wk, 
 }  // namespace chap
 
 namespace chap {
+// A point (internal order) to its packed form (DevProblem::pk_*): binaries as bits, integers as
+// int32 / int64, continuous values as f64.
+__global__ void k_pack_point(DevProblem P, const double* __restrict__ x, unsigned char* out) {
+  const int nw = (P.pk_nbin + 31) >> 5;
+  uint32_t* words = reinterpret_cast<uint32_t*>(out);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nw + P.pk_nint + P.pk_ncont; q += gridDim.x * blockDim.x) {
+    if (q < nw) {
+      uint32_t wd = 0u;
+      for (int b = 0; b < 32 && 32 * q + b < P.pk_nbin; ++b)
+        if (x[P.pk_bin[32 * q + b]] != 0.0) wd |= 1u << b;
+      words[q] = wd;
+    } else if (q < nw + P.pk_nint) {
+      const int sl = q - nw;
+      const double v = x[P.pk_int[sl]];
+      if (P.pk_int64) reinterpret_cast<long long*>(out + P.pk_off_int)[sl] = (long long)v;
+      else reinterpret_cast<int32_t*>(out + P.pk_off_int)[sl] = (int32_t)v;
+    } else {
+      const int sl = q - nw - P.pk_nint;
+      reinterpret_cast<double*>(out + P.pk_off_cont)[sl] = x[P.pk_cont[sl]];
+    }
+  }
+}
+
+// The inverse: a packed point to internal order (fixed variables at their bound).
+__global__ void k_unpack_point(DevProblem P, const unsigned char* __restrict__ in, double* x) {
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(in);
+  const int tot = P.n_fixed + P.pk_nbin + P.pk_nint + P.pk_ncont;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += gridDim.x * blockDim.x) {
+    if (q < P.n_fixed) {
+      x[q] = P.lb[q];
+    } else if (q < P.n_fixed + P.pk_nbin) {
+      const int sl = q - P.n_fixed;
+      x[P.pk_bin[sl]] = (double)((words[sl >> 5] >> (sl & 31)) & 1u);
+    } else if (q < P.n_fixed + P.pk_nbin + P.pk_nint) {
+      const int sl = q - P.n_fixed - P.pk_nbin;
+      x[P.pk_int[sl]] = P.pk_int64 ? (double)reinterpret_cast<const long long*>(in + P.pk_off_int)[sl]
+                                   : (double)reinterpret_cast<const int32_t*>(in + P.pk_off_int)[sl];
+    } else {
+      const int sl = q - P.n_fixed - P.pk_nbin - P.pk_nint;
+      x[P.pk_cont[sl]] = reinterpret_cast<const double*>(in + P.pk_off_cont)[sl];
+    }
+  }
+}
+
 // One internal-order point to user order.
 __global__ void k_export_point(DevProblem P, const double* xi, double* xu) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) xu[P.perm[p]] = xi[p];

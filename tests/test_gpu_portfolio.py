@@ -85,3 +85,57 @@ def test_walkers_exchange_epochs_match_oracle(seed, comm_kind):
         assert st["stats"][w]["has_incumbent"] == int(ow.has_incumbent), w
         if ow.has_incumbent:
             assert st["stats"][w]["best_obj"] == ow.best_obj, w
+
+
+def test_packed_exchange_points():
+    """elite points travel packed — binaries as bits, bounded integers
+    as int32 — config P's 10^5 binaries in 12.5 KB instead of 800 KB of f64."""
+    al8 = lambda b: (b + 7) // 8 * 8   # noqa: E731
+    P = chap.Problem.from_instance(synth.packing())
+    assert P.info.exchange_point_bytes == al8(4 * ((P.info.n_binary + 31) // 32)) <= 12_504
+    Q = chap.Problem.from_instance(synth.tiny(0))
+    assert Q.info.exchange_point_bytes == al8(4 * ((Q.info.n_binary + 31) // 32)) + al8(4 * Q.info.n_integer)
+
+
+def _rank_run(rank, world, uid, inst_seed, W, K, E, ne, nr, q):
+    import torch as th
+    import paper_2605_05086_b200 as ch
+    th.cuda.set_device(rank)
+    inst = synth.tiny(inst_seed)
+    Wl = W // world
+    x0s = np.stack([np.clip(synth.x_random(inst, 100 + w), inst.lb, inst.ub) for w in range(W)])
+    P = ch.Problem.from_instance(inst, device=rank)
+    comm = ch.Comm(uid, world, rank, rank)
+    prm = ch.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8)
+    res, bx = ch.run_walkers(P, th.from_numpy(x0s[rank * Wl:(rank + 1) * Wl]).cuda(rank), prm, comm, max_iters=K * E)
+    th.cuda.synchronize()
+    comm.close()
+    q.put((rank, res.best_obj, res.best_walker, bx.cpu().numpy() if bx is not None else None))
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (one NCCL rank per GPU)")
+def test_two_ranks_equal_one_rank():
+    """SURVEY §8(e) invariant on the CUDA path: 2 ranks x W/2 walkers reach the same best objective,
+    best walker (global id) and best point as 1 rank x W walkers (the exchange plan is the same
+    deterministic function of the gathered summaries)."""
+    import torch.multiprocessing as mp
+    inst = synth.tiny(3)
+    W, K, E, ne, nr = 8, 30, 4, 2, 2
+    x0s = np.stack([np.clip(synth.x_random(inst, 100 + w), inst.lb, inst.ub) for w in range(W)])
+    P = chap.Problem.from_instance(inst)
+    prm = chap.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8)
+    res1, bx1 = chap.run_walkers(P, torch.from_numpy(x0s).cuda(), prm, None, max_iters=K * E)
+    torch.cuda.synchronize()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    uid = chap.comm_unique_id()
+    ps = [ctx.Process(target=_rank_run, args=(r, 2, uid, 3, W, K, E, ne, nr, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    for rank, obj, bw, bx in out:
+        assert obj == res1.best_obj and bw == res1.best_walker
+        if res1.has_incumbent:
+            assert np.array_equal(bx, bx1.cpu().numpy())
