@@ -579,14 +579,14 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
               int32_t glo = lo, ghi = hi;
               for (int64_t k = e1; k < e1 + 4; ++k)
                 if (rb_cv[k] != 0u) { glo = std::min(glo, rb_row[k]); ghi = std::max(ghi, rb_row[k]); }
-              if (e1 > e && ghi >= 0 && ghi - glo + 1 > kRowSpan) break;
+              if (!CHAP_ROW_GATHER && e1 > e && ghi >= 0 && ghi - glo + 1 > kRowSpan) break;
               lo = glo;
               hi = ghi;
             }
             RowStage G{};
             G.e0 = (int32_t)e;
             G.ne = (int32_t)(e1 - e);
-            const bool fits = hi >= 0 && hi - lo + 1 <= kRowSpan;
+            const bool fits = !CHAP_ROW_GATHER && hi >= 0 && hi - lo + 1 <= kRowSpan;
             G.r0 = fits ? lo : 0;
             G.nr = fits ? hi - lo + 1 : 0;
             rb_stage.push_back(G);
@@ -680,11 +680,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.upload(&d_schunks, schunks));
   TRY(B.upload(&d_scols, scols));
   RowBlock* d_rblocks;
-  int32_t* d_rb_row;
-  uint32_t* d_rb_cv;
+  int2* d_rb_rc;
   TRY(B.upload(&d_rblocks, rblocks));
-  TRY(B.upload(&d_rb_row, rb_row));
-  TRY(B.upload(&d_rb_cv, rb_cv));
+  {
+    std::vector<int2> rc(rb_row.size());
+    for (size_t q = 0; q < rb_row.size(); ++q) rc[q] = make_int2(rb_row[q], (int)rb_cv[q]);
+    TRY(B.upload(&d_rb_rc, rc));
+  }
   RowStage* d_rb_stage;
   TRY(B.upload(&d_rb_stage, rb_stage));
   int32_t* d_rb_perm;
@@ -699,8 +701,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   D.rb_pb0 = P->binrow_pb0;
   D.rb_perm = d_rb_perm;
   D.rb_nbin = P->binrow_nbin;
-  D.rb_row = d_rb_row;
-  D.rb_cv = d_rb_cv;
+  D.rb_rc = d_rb_rc;
   D.n = n;
   D.m_norm = m_norm;
   D.cut_row = cut_row;

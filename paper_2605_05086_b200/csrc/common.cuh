@@ -99,13 +99,16 @@ constexpr int kRowVmax = 32768;                   // variables per block: int32 
 constexpr int kRowWpb = kRowVmax / 32;            // bitset words per block
 constexpr int kRowConsumers = kRowThreads - 32;   // consumer threads (the last warp produces)
 #ifndef CHAP_ROW_PER
-#define CHAP_ROW_PER 2
+#define CHAP_ROW_PER 5
 #endif
 #ifndef CHAP_ROW_STAGES
 #define CHAP_ROW_STAGES 2
 #endif
+#ifndef CHAP_ROW_GATHER
+#define CHAP_ROW_GATHER 1
+#endif
 #ifndef CHAP_ROW_SPAN
-#define CHAP_ROW_SPAN 2000
+#define CHAP_ROW_SPAN (CHAP_ROW_GATHER ? 2 : 2000)
 #endif
 constexpr int kRowPer = CHAP_ROW_PER;             // entries per consumer thread per stage
 constexpr int kRowChunk = kRowPer * kRowConsumers;   // max entries per stage (a multiple of 4)
@@ -272,8 +275,8 @@ struct DevProblem {
   int32_t rb_cluster;        // CTAs per cluster of k_eval_binrow (= slices per block)
   int32_t rb_pb0, rb_nbin;   // packed binary columns [rb_pb0, rb_pb0 + rb_nbin), round-robin over blocks
   const int32_t* rb_perm;    // [n_rblocks][kRowVmax] user index of column k of block b (block order)
-  const int32_t* rb_row;     // [entries] row of each entry (sorted within a slice)
-  const uint32_t* rb_cv;     // [entries] column within the block (low 16 bits) | int16 a_ij (high 16)
+  const int2* rb_rc;         // [entries] row of each entry (sorted within a slice), column within the
+                             // block (low 16 bits) | int16 a_ij (high 16)
   const RowStage* rb_stage;  // stages of the slices (RowBlock::st)
   // packed points of the portfolio exchange: binaries as bits (PAPER.md:349's bitset),
   // integers as int32 (int64 when a bound is infinite or beyond 2^31), continuous as f64

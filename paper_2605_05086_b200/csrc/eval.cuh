@@ -1123,8 +1123,7 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
 // finished with the stage; full barrier: the copies' bytes landed). A stage whose rows span more
 // than kRowSpan rows (very sparse slices) gathers its row state instead (nr = 0).
 struct RowRing {
-  int32_t row[kRowStages][kRowChunk];
-  uint32_t cv[kRowStages][kRowChunk];
+  int2 rc[kRowStages][kRowChunk];   // entries: row, column-in-block | int16 coefficient (one 8-byte word)
   double2 rs[kRowStages][kRowSpan];
   uint64_t full[kRowStages];
   uint64_t empty[kRowStages];
@@ -1133,6 +1132,16 @@ constexpr size_t kRowSmem = sizeof(RowRing) + sizeof(int) * kRowVmax + sizeof(ui
 
 // Cluster barrier with release/acquire at cluster scope (shared-memory counters become visible to
 // the other CTAs of the cluster).
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ int ld_dsmem_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cluster_sync_acqrel() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -1157,6 +1166,9 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
   const long long kk = Wk.sc[0].k;
   const int use_tabu = Wk.use_tabu;
   const AspRef A = asp_ref(Wk, 0);
+  uint32_t rsc[kRowCluster];   // the counters of every CTA of the cluster (shared::cluster addresses)
+#pragma unroll
+  for (int q = 0; q < kRowCluster; ++q) rsc[q] = mapa_u32(smem_u32(sc), q < C ? q : 0);
   if (tid == 0) {
     for (int q = 0; q < kRowStages; ++q) {
       mbar_init(&R.full[q], 1);
@@ -1182,8 +1194,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
           const RowStage G = P.rb_stage[st0 + c];
           if (q >= kRowStages) mbar_wait(&R.empty[st], (unsigned)((q / kRowStages) - 1) & 1u);
           mbar_expect_tx(&R.full[st], (unsigned)(8 * G.ne + 16 * G.nr));
-          tma_load_1d(R.row[st], P.rb_row + G.e0, 4u * G.ne, &R.full[st]);
-          tma_load_1d(R.cv[st], P.rb_cv + G.e0, 4u * G.ne, &R.full[st]);
+          tma_load_1d(R.rc[st], P.rb_rc + G.e0, 8u * G.ne, &R.full[st]);
           if (G.nr > 0) tma_load_1d(R.rs[st], RS + G.r0, 16u * G.nr, &R.full[st]);
         }
       __syncwarp();
@@ -1192,26 +1203,30 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
         const int q = g + c, st = q % kRowStages;
         const RowStage G = P.rb_stage[st0 + c];
         mbar_wait(&R.full[st], (unsigned)(q / kRowStages) & 1u);
-        int id[kRowPer];
-        uint32_t u[kRowPer];
-        double2 rv[kRowPer];
+        int2 e[kRowPer];
 #pragma unroll
         for (int k = 0; k < kRowPer; ++k) {
           const int i = tid + k * kRowConsumers;
-          id[k] = i < G.ne ? R.row[st][i] : 0;
-          u[k] = i < G.ne ? R.cv[st][i] : 0u;   // 0: no entry, or inert padding (a coefficient is never 0)
+          e[k] = i < G.ne ? R.rc[st][i] : make_int2(0, 0);   // cv 0: no entry, or inert padding
         }
+        double2 rv[kRowPer];
+        if (G.nr > 0) {   // the stage's row state came with it (shared memory)
+          const double2* rss = R.rs[st] - G.r0;
 #pragma unroll
-        for (int k = 0; k < kRowPer; ++k)
-          rv[k] = u[k] == 0u ? make_double2(-INFINITY, 0.0) : (G.nr > 0 ? R.rs[st][id[k] - G.r0] : __ldg(RS + id[k]));
+          for (int k = 0; k < kRowPer; ++k) rv[k] = e[k].y ? rss[e[k].x] : make_double2(-INFINITY, 0.0);
+        } else {          // a stage spanning too many rows gathers it
+#pragma unroll
+          for (int k = 0; k < kRowPer; ++k) rv[k] = e[k].y ? __ldg(RS + e[k].x) : make_double2(-INFINITY, 0.0);
+        }
 #pragma unroll
         for (int k = 0; k < kRowPer; ++k) {
           // 2·p(w, r, r + d) with d = a (1 - 2x̄), in integers: satisfied
           // before is r <= 0, after is r <= -d (exact: r + d is exact when it is near 0,
           // Sterbenz), a violated row gets less violated iff d < 0; w is integral (R11). Inert
           // rows give 0.
-          const int c2 = (int)(u[k] & 0xffffu);
-          const int ai = (int)(int16_t)(u[k] >> 16);
+          const uint32_t uk = (uint32_t)e[k].y;
+          const int c2 = (int)(uk & 0xffffu);
+          const int ai = (int)(int16_t)(uk >> 16);
           const bool xb = (bits[c2 >> 5] >> (c2 & 31)) & 1u;
           const int nd = xb ? ai : -ai;   // -d
           const double r = rv[k].x;
@@ -1243,7 +1258,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
         if (v < v1) {
 #pragma unroll
           for (int q = 0; q < kRowCluster; ++q)
-            if (q < C) tot[i] += cl.map_shared_rank(sc, q)[v];
+            if (q < C) tot[i] += ld_dsmem_s32(rsc[q] + 4u * (uint32_t)v);
           jq[i] = __ldg(bperm + v);
         }
       }
