@@ -268,6 +268,27 @@ chap_status chap_walkers_restart(chap_walkers* ws, int32_t walker, const double*
                                  void* cuda_stream);
 chap_status chap_walkers_destroy(chap_walkers* ws);
 
+/* ---------------------------------------------------------------------------------------- */
+/* Streamed LP iterates for LP-seeded start points (NEXT f4, DESIGN R19)    */
+/* ---------------------------------------------------------------------------------------- */
+
+/* The LP relaxation min c.x s.t. the normalised rows (the cutoff row is not part of
+ * it), l <= x <= u, by restarted PDHG: x+ = proj_[l,u](x - eta (c + A^T y)),
+ * y+ = max(0, y + tau (A (2x+ - x) - b)), eta = tau = step, running averages of x+ and y+ and a
+ * restart to them every restart_period iterations; x0 = proj_[l,u](0), y0 = 0. At each of the
+ * n_cp strictly increasing checkpoints (HOST int64, e.g. 100, 1000, 10000: "after 10^2, 10^3,
+ * 10^4 ... PDHG iterations, warm-starting each phase from the previous iterate")
+ * the current primal average goes to x_out (DEVICE [n_cp][n], user order) and info_out (HOST
+ * [n_cp][4]) receives {iteration, c.x, max_i (A x - b)_i^+, step}. step <= 0: 0.9/||A||_2 from 100
+ * power iterations on the device. Synchronises the stream; CHAP_ERR_INVALID_ARG on bad arguments. */
+chap_status chap_lp_pdhg(const chap_problem* p, const int64_t* checkpoints, int32_t n_cp, double step,
+                         int32_t restart_period, double* x_out, double* info_out, void* cuda_stream);
+
+/* An LP point (DEVICE [n], user order) to a tabu start point (DEVICE [n], user order): integer
+ * variables rounded to the nearest integer (half away from zero), every value clamped to its
+ * bounds ("LP snapshot rounded to nearest integer"); stream-ordered. */
+chap_status chap_lp_round(const chap_problem* p, const double* x_lp, double* x_out, void* cuda_stream);
+
 /* Diagnostic timing: n_iters tabu iterations (identical semantics to chap_tabu_step, no log),
  * captured as one CUDA graph with a CUDA-event pair around every kernel node (so no launch latency
  * is inside an interval) and run once on the walkers' stream; ms_per_iter HOST [5] receives the

@@ -102,6 +102,8 @@ _SIGS = {
     "chap_walkers_get": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "chap_walkers_set_cutoff": (ctypes.c_int, [_P, c_f64, _P]),
     "chap_walkers_restart": (ctypes.c_int, [_P, c_i32, _P, _P]),
+    "chap_lp_pdhg": (ctypes.c_int, [_P, _P, c_i32, ctypes.c_double, c_i32, _P, _P, _P]),
+    "chap_lp_round": (ctypes.c_int, [_P, _P, _P, _P]),
     "chap_walkers_destroy": (ctypes.c_int, [_P]),
     "chap_walkers_profile": (ctypes.c_int, [_P, c_i32, _P, _P]),
     "chap_walkers_timing": (ctypes.c_int, [_P, c_i32, _P, _P]),
@@ -373,3 +375,24 @@ def exchange_plan(summaries: np.ndarray, W_local: int, n_elite: int, n_restart: 
     return {"z_best": z.value, "best_gid": bg.value, "elite_gid": eg[:ne.value].copy(),
             "elite_kind": ek[:ne.value].copy(), "elite_slot": es[:ne.value].copy(),
             "restart_gid": rg[:nr.value].copy(), "restart_src": rs[:nr.value].copy()}
+
+
+def lp_pdhg(problem: Problem, checkpoints=(100, 1000, 10000), step: float = 0.0, restart_period: int = 400,
+            stream=None):
+    """chap_lp_pdhg: the streamed PDHG snapshots of the LP relaxation.
+    Returns (x [n_cp][n] device tensor, info numpy [n_cp][4] = iteration, c.x, max violation, step)."""
+    import torch
+    cps = np.ascontiguousarray(checkpoints, np.int64)
+    x = torch.empty((len(cps), problem.n), dtype=torch.float64, device=f"cuda:{problem.device}")
+    info = np.zeros((len(cps), 4))
+    _check(chap_lp_pdhg(problem.h, cps.ctypes.data, int(len(cps)), float(step), int(restart_period), _ptr(x),
+                        info.ctypes.data, _stream(stream)))
+    return x, info
+
+
+def lp_round(problem: Problem, x_lp, stream=None):
+    """chap_lp_round: an LP point to a tabu start point (integers rounded, bounds clamped)."""
+    import torch
+    out = torch.empty_like(x_lp)
+    _check(chap_lp_round(problem.h, _ptr(x_lp.contiguous()), _ptr(out), _stream(stream)))
+    return out

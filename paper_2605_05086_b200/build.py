@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libchap.so")
 SOURCES = ["chap.cu"]
-HEADERS = ["common.cuh", "eval.cuh", "tabu.cuh", "host.h", "portfolio.cuh"]
+HEADERS = ["common.cuh", "eval.cuh", "tabu.cuh", "host.h", "portfolio.cuh", "lp.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared", "--expt-relaxed-constexpr"]
 

@@ -1539,6 +1539,7 @@ extern "C" chap_status chap_walkers_destroy(chap_walkers* S) {
 }
 
 #include "portfolio.cuh"
+#include "lp.cuh"
 
 extern "C" chap_status chap_walkers_launches_per_iter(const chap_walkers* S, int32_t* out) {
   if (!S || !out) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or out");
