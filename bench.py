@@ -43,8 +43,11 @@ CONFIGS = {
               walkers=64),
     # BASELINE.json configs[4], the scaling sweep: generator X at a requested nonzero count
     "X1e5": dict(desc="X: scaling sweep, generator G scaled to ~1e5 nnz (BASELINE.json configs[4])", walkers=1),
+    "X3e5": dict(desc="X: scaling sweep, generator G scaled to ~3e5 nnz (BASELINE.json configs[4])", walkers=1),
     "X1e6": dict(desc="X: scaling sweep, generator G scaled to ~1e6 nnz (BASELINE.json configs[4])", walkers=1),
+    "X3e6": dict(desc="X: scaling sweep, generator G scaled to ~3e6 nnz (BASELINE.json configs[4])", walkers=1),
     "X1e7": dict(desc="X: scaling sweep, generator G scaled to ~1e7 nnz (BASELINE.json configs[4])", walkers=1),
+    "X2e7": dict(desc="X: scaling sweep, generator G scaled to ~2e7 nnz (BASELINE.json configs[4])", walkers=1),
     "X5e7": dict(desc="X: scaling sweep, generator G scaled to ~5e7 nnz (BASELINE.json configs[4])", walkers=1),
     # diagnostic variants of G (not BASELINE configs): same structure, one variable class only
     "Gbin": dict(desc="diagnostic: config G structure with every short variable binary", walkers=1),

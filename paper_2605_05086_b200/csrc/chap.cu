@@ -484,7 +484,13 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
       if (cudaFuncSetAttribute(k_eval_binrow, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         cudaGetLastError();
       if (e1 == cudaSuccess) {
-        for (int c = kRowCluster; c >= 4; --c) {
+#ifndef CHAP_ROW_CMAX
+#define CHAP_ROW_CMAX kRowCluster
+#endif
+#ifndef CHAP_ROW_CMIN
+#define CHAP_ROW_CMIN 4
+#endif
+        for (int c = CHAP_ROW_CMAX; c >= CHAP_ROW_CMIN; --c) {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3(c * std::max(1, P->sm_count / c));
           cfg.blockDim = dim3(kRowThreads);
