@@ -677,6 +677,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   gitems.insert(gitems.end(), wtiles.begin() + n_gtiles + n_ctiles, wtiles.end());
   WTile* d_gitems;
   TRY(B.upload(&d_gitems, gitems));
+  P->h_lcols = lcols;   // (host copy: walker creation checks the long bounded-integer domains)
   if (lcols.empty()) lcols.push_back(LongCol{});
   int32_t* d_lfin;
   TRY(B.upload(&d_lfin, lfin));
@@ -1228,6 +1229,19 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
       S->genwm_grid = std::max(1, std::min((p->dp.n_wtiles + warps - 1) / warps,
                                            (occ * p->sm_count + Wk.n_groups - 1) / Wk.n_groups));
     }
+  }
+  // a10: with walker groups the long bounded-integer chunks go to k_eval_gen_wm (A read once per group)
+  // when every such column's lane-private histogram fits the kernel's per-warp shared memory
+  Wk.lbkt_wm = 0;
+  if (S->genwm_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) && prm.weight_cap <= 1048576.0f &&
+      p->dp.n_gchunks > 0) {
+    const int kmax = std::max(1, p->gen_kmax);
+    bool fits = true;
+    for (int q = 0; q < p->dp.n_long; ++q) {
+      const LongCol& L = p->h_lcols[q];
+      if (L.kind == CC_LBKT && (L.dom + 1 + (L.dom + 31) / 32) > 2 * kmax) fits = false;
+    }
+    Wk.lbkt_wm = fits ? 1 : 0;
   }
   Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid + S->genwm_grid;
   if (prm.lazy) Wk.ps = std::max(Wk.ps, 4 * p->sm_count);   // k_select_cache's parts

@@ -1818,12 +1818,12 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
 // The end of a long bounded-integer column (after every chunk has added its part): line 14 as a scan
 // of D in coalesced rounds of 32 buckets, line 16 with R4; the accumulators are zeroed for the next
 // pass.
-__device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
-                                              const LongCol& L, int lane, Best& b, double* oxhat,
-                                              double* oscore, long long kk, int use_tabu) {
+// The column's (s, x̂) in every lane (warp-cooperative); lbkt_finalize offers it.
+__device__ __forceinline__ void lbkt_finalize_core(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                                   const LongCol& L, int lane, double& bs_out, double& bv_out,
+                                                   double& xb_out) {
   const int p = L.p, dom = L.dom;
   const double* X = Wk.x + (size_t)walker * Wk.xs;
-  const int32_t* TB = Wk.tabu + (size_t)walker * Wk.ts;
   const double xb = __ldg(X + p), l = __ldg(P.lb + p);
   double* Dg = Wk.lscr + (size_t)walker * Wk.lss + L.scr;
   double* BA = Dg + dom + 1;
@@ -1870,9 +1870,19 @@ __device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalk
     const double so = __shfl_xor_sync(kFull, bs, off), vo = __shfl_xor_sync(kFull, bv, off);
     if (better_shift(so, vo, bs, bv, xb)) { bs = so; bv = vo; }
   }
+  bs_out = bs;
+  bv_out = bv;
+  xb_out = xb;
+}
+__device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalkers& Wk, int walker,
+                                              const LongCol& L, int lane, Best& b, double* oxhat,
+                                              double* oscore, long long kk, int use_tabu) {
+  double bs, bv, xb;
+  lbkt_finalize_core(P, Wk, walker, L, lane, bs, bv, xb);
+  const int p = L.p;
   if (lane == 0)
-    finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(TB + p) : 0, xb, bv, bs, b, oxhat,
-                    oscore, kk, use_tabu, asp_ref(Wk, walker));
+    finish_column_j(p, __ldg(P.perm + p), use_tabu ? __ldg(Wk.tabu + (size_t)walker * Wk.ts + p) : 0, xb, bv, bs, b,
+                    oxhat, oscore, kk, use_tabu, asp_ref(Wk, walker));
 }
 
 // wm_mode 1 (walker groups): the integer general tiles and the empty columns are k_eval_gen_wm's;
@@ -1929,6 +1939,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
       else gen32_tile<false>(P, X, RS, st, TB, T, Tn, has_next, R, lane, S, rint, s_tab, b, oxhat, oscore, kk, use_tabu, C.asp);
       r_ok = has_next && Tn.kind == CC_GEN;
     } else if (T.kind == CC_LBKT) {
+      if (wm_mode && Wk.lbkt_wm) return;   // walker groups: k_eval_gen_wm takes the chunk for the group
       const LongCol L = P.lcols[T.e1];
       if (wint) lbkt_chunk<true>(P, Wk, walker, X, RS, st, T, L, lane, reinterpret_cast<unsigned char*>(&S), rint, s_tab);
       else lbkt_chunk<false>(P, Wk, walker, X, RS, st, T, L, lane, reinterpret_cast<unsigned char*>(&S), rint, s_tab);
@@ -2046,6 +2057,76 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
     b.p = p;
   };
   const int nwarps = gridDim.x * (kGenWmThreads / 32);
+  // a10: the long bounded-integer chunks for the whole group. The chunk's CSC entries are read once
+  // for the group, lane (slot, walker) takes entries slot, slot + NS, ... of its walker (one coalesced
+  // RG x 16-byte row-state read per entry), counts F into a lane-private int32 histogram in this
+  // warp's shared memory ([bucket][lane], conflict-free) and adds it to its walker's accumulators;
+  // the walkers whose ticket completes are finished by the warp, one after the other.
+  const int ng = Wk.lbkt_wm ? P.n_gchunks : 0;
+  if (ng > 0) {
+    __shared__ int4 s_tab[6];
+    off_table_init(s_tab);
+    __syncthreads();
+    int* hist = reinterpret_cast<int*>(skey);   // this warp's [kmax][32] doubles: [dom + 1][32] ints, then words
+    for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < ng; t += nwarps) {
+      const WTile T = P.gchunks[t];
+      const LongCol L = P.lcols[T.e1];
+      const int p = T.p0, dom = L.dom, len = T.ncols, nwords = (dom + 31) >> 5;
+      unsigned* hcw = reinterpret_cast<unsigned*>(hist + (dom + 1) * 32);   // [nwords][32]
+      for (int q = 0; q <= dom; ++q) hist[q * 32 + lane] = 0;
+      for (int q = 0; q < nwords; ++q) hcw[q * 32 + lane] = 0u;
+      const int xl = (int)(__ldg(X + p) - __ldg(P.lb + p));
+      const bool rint = Wk.sc[wr].rint != 0;
+      int b2 = 0, a2 = 0;
+      bool ovf = false;
+      for (int k = slot; k < len; k += NS) {
+        const int i = __ldg(P.row_idx + T.e0 + k);
+        const double a = __ldg(P.val + T.e0 + k);
+        const double2 rv = __ldg(RS + (size_t)i * RG);
+        const int4 E = off_entry<true>(rv.x, __int_as_float((int)__double2loint(rv.y)), a, rint, s_tab, ovf);
+        b2 += E.z;
+        a2 += E.w;
+        const int code = E.x & 7, key = E.x >> 3;
+        if (code == 2) continue;
+        const int bk = key + xl, cv = key - (code & 1) + xl;
+        if (bk < 0) b2 += E.y;                          // below l: in every prefix
+        else if (bk < dom) hist[bk * 32 + lane] += E.y;
+        if (cv >= 0 && cv < dom) hcw[(cv >> 5) * 32 + lane] |= 1u << (cv & 31);
+      }
+      double* Dg = Wk.lscr + (size_t)wr * Wk.lss + L.scr;
+      double* BA = Dg + dom + 1;
+      unsigned* Cw = reinterpret_cast<unsigned*>(BA + 2);
+      if (live) {
+        for (int q = 0; q <= dom; ++q) {
+          const int h = hist[q * 32 + lane];
+          if (h != 0) atomicAdd(Dg + q, 0.5 * (double)h);
+        }
+        for (int q = 0; q < nwords; ++q) {
+          const unsigned c = hcw[q * 32 + lane];
+          if (c != 0u && (__ldcg(Cw + q) & c) != c) atomicOr(Cw + q, c);
+        }
+        if (b2 != 0) atomicAdd(BA, 0.5 * (double)b2);
+        if (a2 != 0) atomicAdd(BA + 1, 0.5 * (double)a2);
+      }
+      __syncwarp();
+      // per-walker ticket (slot 0 lanes), acquire-release at gpu scope (see long_last)
+      unsigned last = 0u;
+      if (slot == 0 && live) {
+        unsigned* tk = reinterpret_cast<unsigned*>(Wk.lscr + (size_t)w * Wk.lss + L.tix);
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(tk) : "memory");
+        last = old == (unsigned)(L.nchunks - 1);
+        if (last) *tk = 0u;
+      }
+      for (unsigned m = __ballot_sync(kFull, last != 0u); m; m &= m - 1) {
+        const int wq = __ffs(m) - 1;   // slot 0: lane == walker-in-group
+        double fs, fv, fx;
+        lbkt_finalize_core(P, Wk, g * RG + wq, L, lane, fs, fv, fx);
+        if (lane == wq) offer(fs, fs == -INFINITY ? fx : fv, __ldg(P.perm + p), p);
+      }
+      __syncwarp();
+    }
+  }
   for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < P.n_wtiles; t += nwarps) {
     const WTile T = P.wtiles[t];
     if (T.kind == CC_GENC) continue;   // continuous columns: k_eval_gen (wm_mode 1)

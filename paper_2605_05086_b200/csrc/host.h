@@ -105,6 +105,7 @@ struct chap_problem {
   int64_t binrow_entries = 0;  // stored entries (incl. slice padding)
   int rows_grid = 1;
   size_t lscr_per_walker = 1;   // doubles
+  std::vector<LongCol> h_lcols;  // the long columns (host copy)
   // eval workspace (one virtual walker)
   double* e_x = nullptr;
   RowState* e_rs = nullptr;
