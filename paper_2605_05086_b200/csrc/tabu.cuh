@@ -233,7 +233,12 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   const Decision d = sc->dec;
   KT_BEGIN(Wk, 3);
   const int cut_active = sc->cut_active;
-  const int gtid = blockIdx.x * blockDim.x + tid, gstride = gridDim.x * blockDim.x;
+  // a move of a short column with nothing else to do is applied and finalised by block 0 alone (no
+  // grid-wide last-block handshake); bumps, long columns, incumbent copies and dirty marking use the grid
+  const bool solo = d.move && !sc->pending_copy && !Wk.dirty && Wk.W == 1 &&
+                    P.col_ptr[d.p + 1] - P.col_ptr[d.p] <= 4 * kApplyThreads;
+  if (solo && blockIdx.x != 0) return;
+  const int gtid = solo ? tid : blockIdx.x * blockDim.x + tid, gstride = solo ? (int)blockDim.x : gridDim.x * blockDim.x;
   // phase 0: an incumbent found by the previous iteration: best_x <- x (x unchanged since)
   if (sc->pending_copy) {
     double* bx = Wk.best_x + (size_t)w * Wk.xs;
@@ -291,12 +296,17 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += smv[q];
     if (t) atomicAdd((unsigned long long*)&sc->violated, (unsigned long long)t);
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&sc->apply_counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last || tid != 0) return;
-  __threadfence();
+  if (solo) {
+    __syncthreads();
+    if (tid != 0) return;
+  } else {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(&sc->apply_counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+  }
   volatile WalkerScalars* vsc = sc;
   const long long k = vsc->k;
   sc->pending_copy = 0;
