@@ -902,7 +902,7 @@ static chap_status launch_gen_wm(const chap_problem* P, const DevWalkers& Wk, in
                                  bool pdl) {
   const dim3 grid(wgrid, Wk.n_groups);
   const int kmax = std::max(1, P->gen_kmax);
-  const size_t sm = gen_wm_smem(kmax);
+  const size_t sm = gen_wm_smem_all(kmax, Wk.lbkt_wm_words);
   switch (Wk.rg) {
     case 1: TRY(lk(k_eval_gen_wm<1>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
     case 2: TRY(lk(k_eval_gen_wm<2>, grid, kGenWmThreads, sm, s, pdl, 1, P->dp, Wk, part_base, kmax)); break;
@@ -1221,28 +1221,34 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   // slower on config G (0.1344 vs 0.1273 ms; early-scheduled k_eval_gen blocks disturb its
   // persistent grid), so off by default
   S->pdl = prm.pdl != 0;
+  // a10: with walker groups the long bounded-integer chunks go to k_eval_gen_wm (A read once per group);
+  // each of its warps then needs a lane-private histogram of every such column's domain
+  Wk.lbkt_wm = 0;
+  Wk.lbkt_wm_words = 0;
+  if (rg > 1 && p->dp.n_wtiles > 0 && prm.weight_cap == std::floor(prm.weight_cap) && prm.weight_cap <= 1048576.0f &&
+      p->dp.n_gchunks > 0) {
+    int words = 0;
+    for (int q = 0; q < p->dp.n_long; ++q) {
+      const LongCol& L = p->h_lcols[q];
+      if (L.kind == CC_LBKT) words = std::max(words, 32 * (L.dom + 1 + (L.dom + 31) / 32));
+    }
+    if ((size_t)words * 4 * (kGenWmThreads / 32) <= 160 * 1024) Wk.lbkt_wm_words = words;
+  }
   S->genwm_grid = 0;   // walker groups: integer general tiles and empty columns per group (k_eval_gen_wm)
   if (rg > 1 && p->dp.n_wtiles > 0) {
-    const int occ = gen_wm_occupancy(rg, gen_wm_smem(std::max(1, p->gen_kmax)));
+    int occ = gen_wm_occupancy(rg, gen_wm_smem_all(std::max(1, p->gen_kmax), Wk.lbkt_wm_words));
+    if (occ == 0 && Wk.lbkt_wm_words > 0) {   // the histograms do not fit: the chunks stay per walker
+      Wk.lbkt_wm_words = 0;
+      occ = gen_wm_occupancy(rg, gen_wm_smem_all(std::max(1, p->gen_kmax), 0));
+    }
     if (occ > 0) {
       const int warps = kGenWmThreads / 32;
       S->genwm_grid = std::max(1, std::min((p->dp.n_wtiles + warps - 1) / warps,
                                            (occ * p->sm_count + Wk.n_groups - 1) / Wk.n_groups));
     }
   }
-  // a10: with walker groups the long bounded-integer chunks go to k_eval_gen_wm (A read once per group)
-  // when every such column's lane-private histogram fits the kernel's per-warp shared memory
-  Wk.lbkt_wm = 0;
-  if (S->genwm_grid > 0 && prm.weight_cap == std::floor(prm.weight_cap) && prm.weight_cap <= 1048576.0f &&
-      p->dp.n_gchunks > 0) {
-    const int kmax = std::max(1, p->gen_kmax);
-    bool fits = true;
-    for (int q = 0; q < p->dp.n_long; ++q) {
-      const LongCol& L = p->h_lcols[q];
-      if (L.kind == CC_LBKT && (L.dom + 1 + (L.dom + 31) / 32) > 2 * kmax) fits = false;
-    }
-    Wk.lbkt_wm = fits ? 1 : 0;
-  }
+  if (S->genwm_grid > 0 && Wk.lbkt_wm_words > 0) Wk.lbkt_wm = 1;
+  else Wk.lbkt_wm_words = 0;
   Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid + S->genwm_grid;
   if (prm.lazy) Wk.ps = std::max(Wk.ps, 4 * p->sm_count);   // k_select_cache's parts
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));

@@ -327,6 +327,7 @@ struct DevWalkers {
   uint32_t* dirty;                     // [2][dwords + 1]
   int32_t dwords;
   int32_t lbkt_wm;                     // walker groups: k_eval_gen_wm takes the long bounded-integer chunks (a10)
+  int32_t lbkt_wm_words;               // ... with this many ints of shared memory per warp for the histograms
   Cand* asp;                           // [W][tenure] aspiration slots (chap_params.aspiration), NULL = off:
                                        // the eval kernels note every tabu column with s > 0 in slot
                                        // tabu_until % tenure; the select takes the feasible ones (R18)

@@ -2017,6 +2017,15 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
 // different walkers. Sums of ±w, ±w/2 in double are exact (R11), so the scores equal the per-walker
 // kernels' bit for bit.
 constexpr int kGenWmThreads = 128;
+// per warp: kmax x 32 (key f64, δ f32) for the tiles, or lbkt_words ints for a long chunk's
+// histograms (DevWalkers::lbkt_wm), whichever is larger (16-byte multiple)
+__host__ __device__ constexpr size_t gen_wm_region(int kmax, int lbkt_words) {
+  return (((size_t)kmax * 32 * (sizeof(double) + sizeof(float)) > (size_t)lbkt_words * 4
+               ? (size_t)kmax * 32 * (sizeof(double) + sizeof(float)) : (size_t)lbkt_words * 4) + 15) / 16 * 16;
+}
+__host__ __device__ constexpr size_t gen_wm_smem_all(int kmax, int lbkt_words) {
+  return (size_t)(kGenWmThreads / 32) * gen_wm_region(kmax, lbkt_words);
+}
 template <int RG>
 __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, DevWalkers Wk, int part_base, int kmax) {
   pdl_wait_trigger();
@@ -2028,9 +2037,10 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
   const int w = g * RG + wl;
   const bool live = w < Wk.W;
   const int wr = live ? w : g * RG;
-  double* skey = reinterpret_cast<double*>(smem) + (size_t)wid * kmax * 32;                 // [kmax][32]
-  float* sD = reinterpret_cast<float*>(reinterpret_cast<double*>(smem) + (size_t)(kGenWmThreads / 32) * kmax * 32) +
-              (size_t)wid * kmax * 32;                                                       // [kmax][32]
+  // this warp's region of shared memory: the tiles' (key, δ) columns, or a long chunk's histograms
+  unsigned char* wreg = smem + (size_t)wid * gen_wm_region(kmax, Wk.lbkt_wm_words);
+  double* skey = reinterpret_cast<double*>(wreg);                                  // [kmax][32]
+  float* sD = reinterpret_cast<float*>(wreg + (size_t)kmax * 32 * sizeof(double));  // [kmax][32]
   const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)g * Wk.rss * RG) + wl;
   const double* __restrict__ X = Wk.x + (size_t)wr * Wk.xs;
   const int32_t* __restrict__ TB = Wk.tabu + (size_t)wr * Wk.ts;
@@ -2067,7 +2077,7 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
     __shared__ int4 s_tab[6];
     off_table_init(s_tab);
     __syncthreads();
-    int* hist = reinterpret_cast<int*>(skey);   // this warp's [kmax][32] doubles: [dom + 1][32] ints, then words
+    int* hist = reinterpret_cast<int*>(wreg);   // [dom + 1][32] ints, then the candidate words
     for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < ng; t += nwarps) {
       const WTile T = P.gchunks[t];
       const LongCol L = P.lcols[T.e1];
@@ -2210,9 +2220,6 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
     if (ww < Wk.W) write_part(Wk.part + (size_t)ww * Wk.ps + part_base + blockIdx.x, o);
   }
   KT_END(Wk, 1);
-}
-__host__ __device__ constexpr size_t gen_wm_smem(int kmax) {
-  return (size_t)(kGenWmThreads / 32) * kmax * 32 * (sizeof(double) + sizeof(float));
 }
 
 // ------------------------------------------------------------------------------------------
