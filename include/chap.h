@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CHAP_ABI_VERSION 3
+#define CHAP_ABI_VERSION 4
 
 typedef enum {
   CHAP_OK = 0,
@@ -202,7 +202,19 @@ typedef struct {
                             state changed are re-evaluated, the others keep their cached best
                             shift (identical results); one walker only; 0 (default) = every
                             variable every iteration                                          */
+  int32_t perturb;        /* 1 = perturbation after a stuck iteration (NEXT f1, DESIGN R21): the
+                            stuck iteration k draws a row (uniform over the violated active rows,
+                            else over all active rows: the least (h >> 32, i) of
+                            h = H(seed, walker, k, i)), an entry of it (H(.., 2^62) mod its
+                            length) and a new value (H(.., 2^62 + 1)): binary 1 - x̄, integer
+                            uniform over the domain minus x̄, continuous uniform on [lo, hi], an
+                            infinite side replaced by x̄ -/+ perturb_radius; iteration k + 1
+                            applies that move in place of its selection (logged with pad = 1,
+                            s = NaN). H(s, a, b, c) = g(g(g(g(s) ^ a) ^ b) ^ c), g = SplitMix64's
+                            output function. 0 (default) = off                               */
+  int32_t perturb_radius; /* window half-width on an infinite side (default 16, >= 1)         */
   int32_t pad_params;
+  uint64_t perturb_seed;  /* the seed of H (default 0); give each rank its own               */
 } chap_params;
 
 /* Fill *out with the defaults above (n_restart = -1 meaning W_total/8). */
@@ -211,9 +223,10 @@ chap_status chap_params_default(chap_params* out);
 typedef struct {
   int64_t k;        /* iteration index                                                       */
   int32_t j;        /* moved variable (user index), -1 = stuck: weights bumped, no move      */
-  int32_t pad;
+  int32_t flags;    /* 1 = the move is a perturbation (chap_params.perturb, R21), else 0      */
   double v;         /* new value of x_j (NaN if stuck)                                        */
-  double s;         /* its score; if stuck, the best admissible s_j (<= 0) or -INF if none    */
+  double s;         /* its score; if stuck, the best admissible s_j (<= 0) or -INF if none;
+                       NaN for a perturbation                                                 */
   int64_t violated; /* active rows with r > 0 after the step (cutoff row included)           */
   double obj;       /* c.x̄ after the step                                                     */
 } chap_step_record; /* 48 bytes; bit-identical to the oracle's log in the exact domain        */

@@ -35,18 +35,19 @@ _lib = None
 
 
 class Record(ctypes.Structure):
-    _fields_ = [("k", ctypes.c_int64), ("j", ctypes.c_int32), ("pad", ctypes.c_int32),
+    _fields_ = [("k", ctypes.c_int64), ("j", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("v", ctypes.c_double), ("s", ctypes.c_double), ("violated", ctypes.c_int64),
                 ("obj", ctypes.c_double)]
 
 
-RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("pad", "<i4"), ("v", "<f8"), ("s", "<f8"),
+RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("flags", "<i4"), ("v", "<f8"), ("s", "<f8"),
                          ("violated", "<i8"), ("obj", "<f8")])
 
 
 class Params(ctypes.Structure):
     _fields_ = [("tenure", ctypes.c_int32), ("weight_cap", ctypes.c_float),
-                ("cutoff_delta", ctypes.c_double), ("aspiration", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("cutoff_delta", ctypes.c_double), ("aspiration", ctypes.c_int32), ("perturb", ctypes.c_int32),
+                ("perturb_radius", ctypes.c_int32), ("pad", ctypes.c_int32), ("perturb_seed", ctypes.c_uint64)]
 
 
 class Walker(ctypes.Structure):
@@ -54,7 +55,8 @@ class Walker(ctypes.Structure):
                 ("tabu_until", ctypes.POINTER(ctypes.c_int64)),
                 ("best_x", ctypes.POINTER(ctypes.c_double)), ("k", ctypes.c_int64),
                 ("cutoff_rhs", ctypes.c_double), ("best_obj", ctypes.c_double),
-                ("has_incumbent", ctypes.c_int32), ("initialised", ctypes.c_int32)]
+                ("has_incumbent", ctypes.c_int32), ("initialised", ctypes.c_int32), ("id", ctypes.c_int64),
+                ("force_j", ctypes.c_int32), ("pad", ctypes.c_int32), ("force_v", ctypes.c_double)]
 
 
 def _p(a, t):
@@ -98,6 +100,10 @@ def lib():
         L.orc_run_walkers.argtypes = [P, ctypes.POINTER(Params), P, ctypes.c_int32, ctypes.c_int64,
                                       ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int]
         L.orc_run_walkers.restype = ctypes.c_int
+        L.orc_splitmix64.argtypes = [ctypes.c_uint64]
+        L.orc_splitmix64.restype = ctypes.c_uint64
+        L.orc_draw.argtypes = [ctypes.c_uint64] * 4
+        L.orc_draw.restype = ctypes.c_uint64
         _lib = L
     return _lib
 
@@ -110,6 +116,17 @@ class OracleError(RuntimeError):
 
 def penalty(w, r_old, r_new) -> float:
     return lib().orc_penalty(float(w), float(r_old), float(r_new))
+
+
+def splitmix64(state: int) -> int:
+    """g(state): the first output of SplitMix64 seeded with state (R21)."""
+    return lib().orc_splitmix64(state & (2**64 - 1))
+
+
+def draw(seed: int, a: int, b: int, c: int) -> int:
+    """The counter-based draw H(seed, a, b, c) = g(g(g(g(seed) ^ a) ^ b) ^ c) of R21."""
+    M = 2**64 - 1
+    return lib().orc_draw(seed & M, a & M, b & M, c & M)
 
 
 def breakpoint(x_j, r_i, a_ij, is_integer) -> float:
@@ -205,15 +222,19 @@ class TabuParams:
     weight_cap: float = 1e6
     cutoff_delta: float = math.nan
     aspiration: int = 0
+    perturb: int = 0
+    perturb_radius: int = 16
+    perturb_seed: int = 0
 
     def c(self):
-        return Params(self.tenure, self.weight_cap, self.cutoff_delta, self.aspiration, 0)
+        return Params(self.tenure, self.weight_cap, self.cutoff_delta, self.aspiration, self.perturb,
+                      self.perturb_radius, 0, self.perturb_seed)
 
 
 class TabuWalker:
     """One oracle walker (own solution, tabu list and weights)."""
 
-    def __init__(self, prob: Problem, x0, params: TabuParams = TabuParams()):
+    def __init__(self, prob: Problem, x0, params: TabuParams = TabuParams(), walker_id: int = 0):
         self.prob = prob
         self.params = params
         self._prm = params.c()
@@ -222,7 +243,7 @@ class TabuWalker:
         self.tabu_until = np.zeros(max(n, 1), np.int64); self.best_x = np.zeros(max(n, 1))
         self.S = Walker(_p(self.x, ctypes.c_double), _p(self.w, ctypes.c_float),
                         _p(self.tabu_until, ctypes.c_int64), _p(self.best_x, ctypes.c_double),
-                        0, math.inf, math.inf, 0, 0)
+                        0, math.inf, math.inf, 0, 0, int(walker_id), -1, 0, 0.0)
         x0 = np.ascontiguousarray(x0, np.float64)
         st = lib().orc_walker_init(prob.h, ctypes.byref(self._prm), x0.ctypes.data, ctypes.byref(self.S))
         if st != ORC_OK:

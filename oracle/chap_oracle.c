@@ -358,6 +358,7 @@ int orc_walker_init(const orc_problem* P, const orc_params* prm, const double* x
   }
   for (int32_t i = 0; i < P->m_norm; i++) S->w[i] = 1.0f;
   S->k = 0; S->cutoff_rhs = INFINITY; S->best_obj = INFINITY; S->has_incumbent = 0;
+  S->force_j = -1;
   double* r = (double*)malloc(sizeof(double) * P->m_norm);
   incumbent_check(P, prm, S, r);
   free(r);
@@ -372,6 +373,85 @@ static int feasible_after(const orc_problem* P, const orc_walker* S, int32_t j, 
   xt[j] = v;
   orc_residuals(P, xt, S->cutoff_rhs, r);
   return count_violated(P, r, S->cutoff_rhs < INFINITY) == 0;
+}
+
+/* SplitMix64 (Steele, Lea & Flood, OOPSLA 2014): the state advances by the golden gamma
+ * 0x9e3779b97f4a7c15 and the output is the new state through the mix below; g(state) is the first
+ * output of a generator seeded with state. */
+uint64_t orc_splitmix64(uint64_t state) {
+  uint64_t z = state + 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t orc_draw(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return orc_splitmix64(orc_splitmix64(orc_splitmix64(orc_splitmix64(seed) ^ a) ^ b) ^ c);
+}
+
+/* The perturbation of R21 ("perturb"), drawn at stuck iteration k from the
+ * residuals r of the current point, step by step:
+ *  1. a row: uniform over the active rows with r_i > 0, else over all active rows — the row with
+ *     the least pair (H(seed, id, k, i) >> 32, i); independent uniform draws make every eligible
+ *     row equally likely to hold the least one;
+ *  2. an entry of that normalised row (input order; the cutoff row: increasing j over c_j != 0):
+ *     number H(seed, id, k, 2^62) mod (its length);
+ *  3. a value for its variable from h = H(seed, id, k, 2^62 + 1): binary 1 - x_j; integer: with
+ *     lo = l_j (x_j - R if infinite), hi = u_j (x_j + R if infinite), cnt = min(hi - lo, 2^52)
+ *     values other than x_j, v = lo + (h mod cnt), then v + 1 if v >= x_j; continuous:
+ *     v = lo + (hi - lo) * ((h >> 11) * 2^-53), at most hi; fixed or cnt < 1: no move.
+ * Returns 1 with (*jo, *vo) when a move was drawn. */
+static int perturb_draw(const orc_problem* P, const orc_params* prm, const orc_walker* S, int64_t k,
+                        const double* r, int32_t* jo, double* vo) {
+  int32_t mn = P->m_norm;
+  int cut_active = S->cutoff_rhs < INFINITY;
+  uint64_t hv = 0, ha = 0;
+  int32_t iv = -1, ia = -1;
+  for (int32_t i = 0; i < mn; i++) {
+    if (i == mn - 1 && !cut_active) continue;
+    uint64_t h = orc_draw(prm->perturb_seed, (uint64_t)S->id, (uint64_t)k, (uint64_t)i) >> 32;
+    if (ia < 0 || h < ha) { ia = i; ha = h; }              /* i increases: ties keep the lower i */
+    if (r[i] > 0.0 && (iv < 0 || h < hv)) { iv = i; hv = h; }
+  }
+  int32_t row = iv >= 0 ? iv : ia;
+  if (row < 0) return 0;
+  int64_t len = 0;
+  if (row < mn - 1) len = P->rp[row + 1] - P->rp[row];
+  else
+    for (int32_t j = 0; j < P->n; j++) len += (P->c[j] != 0.0);
+  if (len == 0) return 0;
+  int64_t q = (int64_t)(orc_draw(prm->perturb_seed, (uint64_t)S->id, (uint64_t)k, 1ULL << 62) % (uint64_t)len);
+  int32_t j = -1;
+  if (row < mn - 1) j = P->ci[P->rp[row] + q];
+  else
+    for (int32_t jj = 0; jj < P->n; jj++)
+      if (P->c[jj] != 0.0 && q-- == 0) { j = jj; break; }
+  uint64_t h = orc_draw(prm->perturb_seed, (uint64_t)S->id, (uint64_t)k, (1ULL << 62) + 1);
+  double xj = S->x[j], R = (double)prm->perturb_radius;
+  double lo = isfinite(P->lb[j]) ? P->lb[j] : xj - R;
+  double hi = isfinite(P->ub[j]) ? P->ub[j] : xj + R;
+  double v;
+  switch (P->vclass[j]) {
+    case 1: v = 1.0 - xj; break;
+    case 2: {
+      double cnt = hi - lo;
+      if (!(cnt >= 1.0)) return 0;
+      if (cnt > 4503599627370496.0) cnt = 4503599627370496.0;   /* 2^52 */
+      v = lo + (double)(h % (uint64_t)cnt);
+      if (v >= xj) v = v + 1.0;
+      break;
+    }
+    case 3: {
+      double u = (double)(h >> 11) * 0x1.0p-53;
+      v = lo + (hi - lo) * u;
+      if (v > hi) v = hi;
+      break;
+    }
+    default: return 0;   /* fixed */
+  }
+  *jo = j;
+  *vo = v;
+  return 1;
 }
 
 int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int64_t n_iters,
@@ -394,6 +474,19 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
   for (int64_t it = 0; it < n_iters; it++) {
     int64_t k = S->k;
     int cut_active = S->cutoff_rhs < INFINITY;
+    if (S->force_j >= 0) {   /* R21: the perturbation drawn by the stuck iteration k - 1 */
+      orc_record rec;
+      memset(&rec, 0, sizeof(rec));
+      rec.k = k; rec.j = S->force_j; rec.flags = 1; rec.v = S->force_v; rec.s = NAN;
+      S->x[S->force_j] = S->force_v;
+      S->tabu_until[S->force_j] = k + 1 + prm->tenure;
+      S->force_j = -1;
+      rec.violated = incumbent_check(P, prm, S, r);
+      rec.obj = objective(P, S->x);
+      if (log) log[it] = rec;
+      S->k = k + 1;
+      continue;
+    }
     activities(P, S->x, y);
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 256)
@@ -426,6 +519,10 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
           S->w[i] = nw < prm->weight_cap ? nw : prm->weight_cap;
         }
       }
+      if (prm->perturb) {   /* R21: drawn from this point's residuals, applied next iteration */
+        int32_t jp; double vp;
+        if (perturb_draw(P, prm, S, k, r, &jp, &vp)) { S->force_j = jp; S->force_v = vp; }
+      }
     }
     rec.s = (js >= 0) ? ss : -INFINITY;
     rec.violated = incumbent_check(P, prm, S, r);
@@ -447,6 +544,7 @@ int orc_walker_restart(const orc_problem* P, const orc_params* prm, orc_walker* 
     S->x[j] = x[j];
     S->tabu_until[j] = 0;
   }
+  S->force_j = -1;
   double* r = (double*)malloc(sizeof(double) * P->m_norm);
   incumbent_check(P, prm, S, r);
   free(r);

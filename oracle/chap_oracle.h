@@ -79,18 +79,32 @@ typedef struct {
   double cutoff_delta;   /* NaN = auto (R14)                                                  */
   int32_t aspiration;    /* 1: a tabu variable is admissible when moving it to its best shift
                             makes the point feasible, i.e. gives a new incumbent (R18, NEXT f1) */
+  int32_t perturb;       /* 1: perturbation after a stuck iteration (R21, NEXT f1)             */
+  int32_t perturb_radius;/* half-width of the value window on an infinite side (R21)          */
   int32_t pad;
+  uint64_t perturb_seed; /* seed of the counter-based draws (R21)                              */
 } orc_params;
 
 typedef struct {
-  int64_t k; int32_t j; int32_t pad; double v; double s; int64_t violated; double obj;
-} orc_record;            /* identical field order to chap_step_record (48 bytes)               */
+  int64_t k; int32_t j; int32_t flags; double v; double s; int64_t violated; double obj;
+} orc_record;            /* identical field order to chap_step_record (48 bytes); flags = 1 for
+                            a perturbation move (R21)                                          */
 
 /* One walker's state. x [n], w [m_norm], tabu_until [n], best_x [n] are caller-owned. */
 typedef struct {
   double* x; float* w; int64_t* tabu_until; double* best_x;
   int64_t k; double cutoff_rhs; double best_obj; int32_t has_incumbent; int32_t initialised;
+  int64_t id;            /* walker index: the a of the draws H(seed, a, k, c) (R21)            */
+  int32_t force_j;       /* a perturbation drawn at a stuck iteration, applied by the next one
+                            (-1: none); cleared by init and restart                            */
+  int32_t pad;
+  double force_v;
 } orc_walker;
+
+/* SplitMix64's output function g (the first output of SplitMix64 seeded with state) and the
+ * counter-based draw H(seed, a, b, c) = g(g(g(g(seed) ^ a) ^ b) ^ c) of R21. */
+uint64_t orc_splitmix64(uint64_t state);
+uint64_t orc_draw(uint64_t seed, uint64_t a, uint64_t b, uint64_t c);
 
 /* Initialise a walker at x0 (copied): w = 1, tabu_until = 0, k = 0, cutoff inactive; then the
  * k = 0 incumbent check (R15). */

@@ -49,11 +49,12 @@ class chap_params(ctypes.Structure):
     _fields_ = [("tenure", c_i32), ("weight_cap", c_f32), ("cutoff_delta", c_f64), ("exchange_K", c_i32),
                 ("n_elite", c_i32), ("n_restart", c_i32), ("graph_iters", c_i32),
                 ("binary_kernel", c_i32), ("pdl", c_i32), ("l2_persist", c_i32), ("aspiration", c_i32),
-                ("lazy", c_i32), ("pad_params", c_i32)]
+                ("lazy", c_i32), ("perturb", c_i32), ("perturb_radius", c_i32), ("pad_params", c_i32),
+                ("perturb_seed", ctypes.c_uint64)]
 
 
 class chap_step_record(ctypes.Structure):
-    _fields_ = [("k", c_i64), ("j", c_i32), ("pad", c_i32), ("v", c_f64), ("s", c_f64), ("violated", c_i64),
+    _fields_ = [("k", c_i64), ("j", c_i32), ("flags", c_i32), ("v", c_f64), ("s", c_f64), ("violated", c_i64),
                 ("obj", c_f64)]
 
 
@@ -74,7 +75,7 @@ class chap_walker_summary(ctypes.Structure):
 SUMMARY_DTYPE = np.dtype([("best_obj", "<f8"), ("violated", "<i8"), ("sumviol", "<f8"), ("gid", "<i4"),
                           ("flags", "<i4")])
 MOVE_DTYPE = np.dtype([("j", "<i4"), ("pad", "<i4"), ("v", "<f8"), ("s", "<f8")])
-RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("pad", "<i4"), ("v", "<f8"), ("s", "<f8"),
+RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("flags", "<i4"), ("v", "<f8"), ("s", "<f8"),
                          ("violated", "<i8"), ("obj", "<f8")])
 STATS_DTYPE = np.dtype([("k", "<i8"), ("violated", "<i8"), ("obj", "<f8"), ("best_obj", "<f8"),
                         ("cutoff_rhs", "<f8"), ("has_incumbent", "<i4"), ("pad", "<i4"), ("n_moves", "<i8"),

@@ -1149,7 +1149,10 @@ extern "C" chap_status chap_params_default(chap_params* out) {
   out->l2_persist = 1;
   out->aspiration = 0;
   out->lazy = 0;
+  out->perturb = 0;
+  out->perturb_radius = 16;
   out->pad_params = 0;
+  out->perturb_seed = 0;
   return CHAP_OK;
 }
 
@@ -1164,6 +1167,8 @@ static chap_status check_params(const chap_params& q) {
   if (q.l2_persist < 0 || q.l2_persist > 1) return fail(CHAP_ERR_INVALID_ARG, "l2_persist not in {0, 1}");
   if (q.aspiration < 0 || q.aspiration > 1) return fail(CHAP_ERR_INVALID_ARG, "aspiration not in {0, 1}");
   if (q.lazy < 0 || q.lazy > 1) return fail(CHAP_ERR_INVALID_ARG, "lazy not in {0, 1}");
+  if (q.perturb < 0 || q.perturb > 1) return fail(CHAP_ERR_INVALID_ARG, "perturb not in {0, 1}");
+  if (q.perturb_radius < 1) return fail(CHAP_ERR_INVALID_ARG, "perturb_radius < 1");
   return CHAP_OK;
 }
 
@@ -1274,6 +1279,9 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.W = W;
   Wk.tenure = prm.tenure;
   Wk.wcap = prm.weight_cap;
+  Wk.perturb = prm.perturb;
+  Wk.perturb_radius = prm.perturb_radius;
+  Wk.perturb_seed = prm.perturb_seed;
   Wk.delta = prm.cutoff_delta;
   CUDA_TRY(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
   if (prm.l2_persist) {   // the gathered row state persists in L2 (window on the stream,

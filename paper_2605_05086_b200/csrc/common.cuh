@@ -185,7 +185,30 @@ struct WalkerScalars {
   long long vcount;           // violated active rows (k_viol_count)
   int wint;                   // every weight is an integer <= 2^20 (the int path of gen32_tile)
   int rint;                   // every residual is an integer (DevProblem::rint_base and an integral cutoff rhs)
+  // perturbation (chap_params.perturb, NEXT f1, DESIGN R21): a stuck iteration's row draw (minimum of
+  // (h32 << 32 | i) over the violated / over all active rows, ~0 = none yet) and the move it yields,
+  // which iteration k + 1 applies in place of its selection (force_p = -1: none pending)
+  unsigned long long pert_kv;
+  unsigned long long pert_ka;
+  int force_p;
+  int pad2;
+  double force_v;
 };
+
+// SplitMix64's output function (Steele, Lea, Flood 2014; the first output of a generator seeded
+// with z) and the counter-based draw of R21: H(seed, a, b, c) = g(g(g(g(seed) ^ a) ^ b) ^ c).
+__host__ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ unsigned long long rng_draw(unsigned long long seed, unsigned long long a,
+                                                              unsigned long long b, unsigned long long c) {
+  return splitmix64(splitmix64(splitmix64(splitmix64(seed) ^ a) ^ b) ^ c);
+}
+constexpr unsigned long long kDrawEntry = 1ull << 62;         // c of the entry draw (rows use c = i)
+constexpr unsigned long long kDrawValue = (1ull << 62) + 1;   // c of the value draw
 
 // Per-kernel device time (chap_walkers_timing): %globaltimer at every block's start (atomic min)
 // and end (atomic max) into DevWalkers::kt when it is non-NULL; k_apply accumulates the spans.
@@ -328,6 +351,9 @@ struct DevWalkers {
   int32_t dwords;
   int32_t lbkt_wm;                     // walker groups: k_eval_gen_wm takes the long bounded-integer chunks (a10)
   int32_t lbkt_wm_words;               // ... with this many ints of shared memory per warp for the histograms
+  int32_t perturb;                     // chap_params.perturb (R21)
+  int32_t perturb_radius;              // the window half-width on an infinite side
+  unsigned long long perturb_seed;
   Cand* asp;                           // [W][tenure] aspiration slots (chap_params.aspiration), NULL = off:
                                        // the eval kernels note every tabu column with s > 0 in slot
                                        // tabu_until % tenure; the select takes the feasible ones (R18)

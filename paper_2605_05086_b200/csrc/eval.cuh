@@ -701,6 +701,16 @@ __device__ __forceinline__ void select_walker(const DevProblem& P, const DevWalk
     d.v = g.v;
     d.s = found ? g.s : -INFINITY;
     d.delta = d.move ? (g.v - x[g.p]) : 0.0;
+    if (scw->force_p >= 0) {   // the perturbation drawn by the previous (stuck) iteration (R21)
+      d.move = 1;
+      d.p = scw->force_p;
+      d.j = P.perm[d.p];
+      d.pad = 1;
+      d.v = scw->force_v;
+      d.s = NAN;
+      d.delta = d.v - x[d.p];
+      scw->force_p = -1;
+    }
     scw->dec = d;
     if (best_out) {
       chap_move mv;

@@ -124,6 +124,9 @@ __global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, in
     const double zt = sc->cdot;        // k_cut_dot
     sc->violated = vt;
     sc->obj = zt;
+    sc->force_p = -1;   // a restart drops a pending perturbation (R21)
+    sc->pert_kv = ~0ull;
+    sc->pert_ka = ~0ull;
     if (mode == 0) {
       // weights start at 1 and grow by +1 up to the cap (R12): integers <= 2^20 when the cap is one
       sc->wint = Wk.wcap == floorf(Wk.wcap) && Wk.wcap <= 1048576.0f;
@@ -222,6 +225,35 @@ __global__ void k_tabu_clear(int32_t* tabu, size_t ts, int n, int only_walker) {
 }
 
 // Apply the selected move or bump weights, then (last block) finalise the iteration.
+// The perturbation's new value of internal column p at x̄ = xb (R21): binary: 1 - x̄; integer: a
+// uniform draw over the domain minus x̄ (an infinite side replaced by x̄ ∓ R, at most 2^52 values);
+// continuous: lo + (hi - lo) u, u = (h >> 11) 2^-53, rounded once per operation (no contraction);
+// fixed or a one-value domain: none.
+__device__ __forceinline__ bool perturb_value(const DevProblem& P, int p, double xb, int R, unsigned long long h,
+                                              double* out) {
+  const int cls = P.vclass[p];
+  if (cls == 0) return false;
+  if (cls == 1) {
+    *out = 1.0 - xb;
+    return true;
+  }
+  const double l = P.lb[p], u = P.ub[p];
+  const double lo = isfinite(l) ? l : xb - (double)R, hi = isfinite(u) ? u : xb + (double)R;
+  if (cls == 2) {
+    double cnt = hi - lo;   // the values other than x̄
+    if (!(cnt >= 1.0)) return false;
+    if (cnt > 4503599627370496.0) cnt = 4503599627370496.0;
+    double v = lo + (double)(h % (unsigned long long)cnt);
+    if (v >= xb) v += 1.0;
+    *out = v;
+    return true;
+  }
+  double v = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), (double)(h >> 11) * 0x1.0p-53));
+  if (v > hi) v = hi;
+  *out = v;
+  return true;
+}
+
 __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalkers Wk) {
   pdl_wait_trigger();
   __shared__ long long smv[32];
@@ -257,10 +289,32 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
       dv += (long long)(r1 > 0.0) - (long long)(r0 > 0.0);
     }
   } else {
-    // stuck: w_i <- min(w_i + 1, cap) on every active violated row (R12)
+    // stuck: w_i <- min(w_i + 1, cap) on every active violated row (R12); with the perturbation
+    // (R21) also the row draw: the least (h32 << 32 | i) over the violated and over all active rows
+    unsigned long long kv = ~0ull, ka = ~0ull;
+    const bool pert = Wk.perturb != 0;
+    const unsigned long long h0 =
+        pert ? splitmix64(splitmix64(splitmix64(Wk.perturb_seed) ^ (unsigned long long)w) ^ (unsigned long long)sc->k) : 0ull;
     for (int i = gtid; i < P.m_norm; i += gstride) {
       if (i == P.cut_row && !cut_active) continue;
-      if (rw[i].r > 0.0) rw[i].w = fminf(rw[i].w + 1.0f, Wk.wcap);
+      const bool viol = rw[i].r > 0.0;
+      if (viol) rw[i].w = fminf(rw[i].w + 1.0f, Wk.wcap);
+      if (pert) {
+        const unsigned long long key = (splitmix64(h0 ^ (unsigned long long)i) & 0xFFFFFFFF00000000ull) | (unsigned)i;
+        ka = key < ka ? key : ka;
+        if (viol) kv = key < kv ? key : kv;
+      }
+    }
+    if (pert) {
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long ov = __shfl_xor_sync(kFull, kv, off), oa = __shfl_xor_sync(kFull, ka, off);
+        kv = ov < kv ? ov : kv;
+        ka = oa < ka ? oa : ka;
+      }
+      if ((tid & 31) == 0) {
+        if (kv != ~0ull) atomicMin(&sc->pert_kv, kv);
+        if (ka != ~0ull) atomicMin(&sc->pert_ka, ka);
+      }
     }
   }
   if (Wk.dirty) {   // f2: mark the columns whose result changes for iteration k + 1; clear set k & 1
@@ -327,6 +381,26 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     sc->n_moves = vsc->n_moves + 1;
   } else {
     sc->n_stuck = vsc->n_stuck + 1;
+    if (Wk.perturb) {   // R21: the perturbation move, applied by iteration k + 1
+      const unsigned long long kv = vsc->pert_kv, ka = vsc->pert_ka;
+      sc->pert_kv = ~0ull;
+      sc->pert_ka = ~0ull;
+      const unsigned long long key = kv != ~0ull ? kv : ka;
+      if (key != ~0ull) {
+        const int i = (int)(key & 0xFFFFFFFFull);
+        const int e0 = P.rp[i], len = P.rp[i + 1] - e0;
+        if (len > 0) {
+          const unsigned long long h0 =
+              splitmix64(splitmix64(splitmix64(Wk.perturb_seed) ^ (unsigned long long)w) ^ (unsigned long long)k);
+          const int p = P.ci[e0 + (int)(splitmix64(h0 ^ kDrawEntry) % (unsigned long long)len)];
+          double v;
+          if (perturb_value(P, p, x[p], Wk.perturb_radius, splitmix64(h0 ^ kDrawValue), &v)) {
+            sc->force_p = p;
+            sc->force_v = v;
+          }
+        }
+      }
+    }
   }
   if (vsc->violated == 0) {   // PAPER.md:373, R15
     take_incumbent(P, Wk, sc, rw);
@@ -337,7 +411,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     chap_step_record rec;
     rec.k = k;
     rec.j = d.move ? d.j : -1;
-    rec.pad = 0;
+    rec.flags = d.pad;   // 1: a perturbation (R21)
     rec.v = d.move ? d.v : NAN;
     rec.s = d.s;
     rec.violated = vsc->violated;
@@ -451,6 +525,7 @@ __global__ void k_eval_scalars(WalkerScalars* sc, double cutoff_rhs, int rint_ba
   sc->cut_active = cutoff_rhs < INFINITY;
   sc->cutoff_rhs = cutoff_rhs;
   sc->cdot = 0.0;
+  sc->force_p = -1;
 }
 
 }  // namespace chap

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     import paper_2605_05086_b200 as chap
     assert set(declared) <= set(chap.EXPORTED)
-    assert chap.chap_abi_version() == 3
+    assert chap.chap_abi_version() == 4
     assert chap.chap_status_string(7) == b"CHAP_ERR_UNSUPPORTED"
 
 

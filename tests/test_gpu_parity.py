@@ -190,22 +190,30 @@ def test_host_buffer_variant_equals_device():
 
 
 def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10, binary_kernel=0,
-                  aspiration=0, lazy=0):
+                  aspiration=0, lazy=0, perturb=0, perturb_seed=0, perturb_radius=16, split=None):
     P = chap.Problem.from_instance(inst)
     O = oracle.Problem.from_instance(inst)
     prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure,
-                              binary_kernel=binary_kernel, aspiration=aspiration, lazy=lazy)
-    oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap, aspiration=aspiration)
+                              binary_kernel=binary_kernel, aspiration=aspiration, lazy=lazy, perturb=perturb,
+                              perturb_seed=perturb_seed, perturb_radius=perturb_radius)
+    oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap, aspiration=aspiration, perturb=perturb,
+                             perturb_seed=perturb_seed, perturb_radius=perturb_radius)
     X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
     Wk = chap.Walkers(P, X0, prm)
-    log = chap.records(Wk.step(n_iters, log=True)).reshape(n_iters, len(x0s))
+    if split is None:   # one chap_tabu_step call
+        log = chap.records(Wk.step(n_iters, log=True)).reshape(n_iters, len(x0s))
+    else:               # several calls (state such as a pending perturbation crosses them)
+        parts = [chap.records(Wk.step(q, log=True)).reshape(q, len(x0s)) for q in split]
+        log = np.concatenate(parts)
+        assert sum(split) == n_iters
     st = Wk.get()
     for wi, x0 in enumerate(x0s):
-        ow = oracle.TabuWalker(O, x0, oprm)
+        ow = oracle.TabuWalker(O, x0, oprm, walker_id=wi)
         olog = ow.run(n_iters)
         glog = log[:, wi]
-        for f in ("k", "j", "violated", "obj", "s"):
-            bad = np.nonzero(glog[f] != olog[f])[0]
+        for f in ("k", "j", "flags", "violated", "obj", "s"):
+            ne = ~((glog[f] == olog[f]) | (np.isnan(glog[f]) & np.isnan(olog[f]))) if f == "s" else glog[f] != olog[f]
+            bad = np.nonzero(ne)[0]
             assert bad.size == 0, (inst.name, wi, f, bad[:3], glog[bad[:3]], olog[bad[:3]])
         mv = glog["j"] >= 0
         assert np.array_equal(glog["v"][mv], olog["v"][mv])
@@ -591,3 +599,35 @@ def test_lazy_rejects_walker_sets():
     X0 = torch.from_numpy(np.stack([synth.x_lower(inst)] * 2)).cuda()
     with pytest.raises(chap.ChapError):
         chap.Walkers(P, X0, chap.default_params(lazy=1))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_trajectory_perturb_config_T(seed, binrow):
+    """NEXT f1 (R21, perturbation after a stuck iteration, counter-based draws): trajectories
+    bit-exact against the oracle's step-by-step rule (pinned in tests/test_oracle_perturb.py),
+    including the drawn row, entry and value of every perturbation."""
+    inst = synth.tiny(seed)
+    log = _traj_compare(inst, [synth.x_lower(inst)], 500, graph_iters=16 if seed % 2 else 0, binary_kernel=binrow,
+                        perturb=1, perturb_seed=1000 + seed, tenure=4)
+    assert (log["flags"] == 1).any()
+
+
+def test_trajectory_perturb_classes_groups_lazy():
+    """Perturbations through every column class, with walker groups (distinct draws per walker id),
+    selective re-evaluation, aspiration, and across chap_tabu_step calls (a pending perturbation
+    drawn by the last iteration of one call is applied by the first of the next)."""
+    inst = synth.mixed(seed=5, n=600, m=400, n_long=6, long_lo=100, long_hi=600,
+                       long_kinds=("unb", "big", "bkt", "bin"))
+    assert chap.Problem.from_instance(inst).info.n_sorted_columns >= 1
+    log = _traj_compare(inst, [inst.x_star, synth.x_lower(inst)], 300, perturb=1, perturb_seed=8, tenure=3)
+    assert (log["flags"] == 1).sum() >= 10
+    inst = synth.mixed(seed=5, n=3000, m=600, n_long=6, long_lo=100, long_hi=600)
+    x0s = [synth.x_lower(inst), inst.x_star] + [synth.x_random(inst, s) for s in range(4)]
+    log = _traj_compare(inst, x0s, 300, perturb=1, perturb_seed=8, tenure=3)
+    assert (log["flags"] == 1).any()
+    inst = synth.tiny(2)
+    log = _traj_compare(inst, [synth.x_lower(inst)], 300, lazy=1, perturb=1, perturb_seed=9, tenure=4)
+    assert (log["flags"] == 1).any()
+    log = _traj_compare(inst, [synth.x_lower(inst)], 300, aspiration=1, perturb=1, perturb_seed=10, tenure=4,
+                        split=[7, 1, 13, 29, 250])
+    assert (log["flags"] == 1).any()
