@@ -213,8 +213,11 @@ typedef struct {
                             s = NaN). H(s, a, b, c) = g(g(g(g(s) ^ a) ^ b) ^ c), g = SplitMix64's
                             output function. 0 (default) = off                               */
   int32_t perturb_radius; /* window half-width on an infinite side (default 16, >= 1)         */
-  int32_t pad_params;
-  uint64_t perturb_seed;  /* the seed of H (default 0); give each rank its own               */
+  float smooth_prob;      /* weight smoothing (NEXT f1, DESIGN R22): a stuck iteration k with
+                            u = (H(seed, walker, k, 2^62 + 2) >> 11) 2^-53 < smooth_prob
+                            lowers w_i <- w_i - 1 on every active satisfied row with w_i > 1
+                            instead of the bump; 0 (default) = always bump, in [0, 1]          */
+  uint64_t rng_seed;      /* the seed of H (default 0); give each rank its own                */
 } chap_params;
 
 /* Fill *out with the defaults above (n_restart = -1 meaning W_total/8). */

@@ -47,7 +47,7 @@ RECORD_DTYPE = np.dtype([("k", "<i8"), ("j", "<i4"), ("flags", "<i4"), ("v", "<f
 class Params(ctypes.Structure):
     _fields_ = [("tenure", ctypes.c_int32), ("weight_cap", ctypes.c_float),
                 ("cutoff_delta", ctypes.c_double), ("aspiration", ctypes.c_int32), ("perturb", ctypes.c_int32),
-                ("perturb_radius", ctypes.c_int32), ("pad", ctypes.c_int32), ("perturb_seed", ctypes.c_uint64)]
+                ("perturb_radius", ctypes.c_int32), ("smooth_prob", ctypes.c_float), ("rng_seed", ctypes.c_uint64)]
 
 
 class Walker(ctypes.Structure):
@@ -224,11 +224,12 @@ class TabuParams:
     aspiration: int = 0
     perturb: int = 0
     perturb_radius: int = 16
-    perturb_seed: int = 0
+    smooth_prob: float = 0.0
+    rng_seed: int = 0
 
     def c(self):
         return Params(self.tenure, self.weight_cap, self.cutoff_delta, self.aspiration, self.perturb,
-                      self.perturb_radius, 0, self.perturb_seed)
+                      self.perturb_radius, self.smooth_prob, self.rng_seed)
 
 
 class TabuWalker:

@@ -409,7 +409,7 @@ static int perturb_draw(const orc_problem* P, const orc_params* prm, const orc_w
   int32_t iv = -1, ia = -1;
   for (int32_t i = 0; i < mn; i++) {
     if (i == mn - 1 && !cut_active) continue;
-    uint64_t h = orc_draw(prm->perturb_seed, (uint64_t)S->id, (uint64_t)k, (uint64_t)i) >> 32;
+    uint64_t h = orc_draw(prm->rng_seed, (uint64_t)S->id, (uint64_t)k, (uint64_t)i) >> 32;
     if (ia < 0 || h < ha) { ia = i; ha = h; }              /* i increases: ties keep the lower i */
     if (r[i] > 0.0 && (iv < 0 || h < hv)) { iv = i; hv = h; }
   }
@@ -420,13 +420,13 @@ static int perturb_draw(const orc_problem* P, const orc_params* prm, const orc_w
   else
     for (int32_t j = 0; j < P->n; j++) len += (P->c[j] != 0.0);
   if (len == 0) return 0;
-  int64_t q = (int64_t)(orc_draw(prm->perturb_seed, (uint64_t)S->id, (uint64_t)k, 1ULL << 62) % (uint64_t)len);
+  int64_t q = (int64_t)(orc_draw(prm->rng_seed, (uint64_t)S->id, (uint64_t)k, 1ULL << 62) % (uint64_t)len);
   int32_t j = -1;
   if (row < mn - 1) j = P->ci[P->rp[row] + q];
   else
     for (int32_t jj = 0; jj < P->n; jj++)
       if (P->c[jj] != 0.0 && q-- == 0) { j = jj; break; }
-  uint64_t h = orc_draw(prm->perturb_seed, (uint64_t)S->id, (uint64_t)k, (1ULL << 62) + 1);
+  uint64_t h = orc_draw(prm->rng_seed, (uint64_t)S->id, (uint64_t)k, (1ULL << 62) + 1);
   double xj = S->x[j], R = (double)prm->perturb_radius;
   double lo = isfinite(P->lb[j]) ? P->lb[j] : xj - R;
   double hi = isfinite(P->ub[j]) ? P->ub[j] : xj + R;
@@ -510,11 +510,19 @@ int orc_tabu_run(const orc_problem* P, const orc_params* prm, orc_walker* S, int
       S->x[js] = xhat[js];
       S->tabu_until[js] = k + 1 + prm->tenure;
     } else {
-      /* stuck: bump every active violated row (R12) */
+      /* stuck: bump every active violated row (R12) — or, when the smoothing draw of R22 falls
+       * below smooth_prob, lower every active satisfied row's weight above 1 by one instead */
       rec.j = -1; rec.v = NAN;
+      int smooth = 0;
+      if (prm->smooth_prob > 0.0f) {
+        double u = (double)(orc_draw(prm->rng_seed, (uint64_t)S->id, (uint64_t)k, (1ULL << 62) + 2) >> 11) * 0x1.0p-53;
+        smooth = u < (double)prm->smooth_prob;
+      }
       for (int32_t i = 0; i < mn; i++) {
         if (i == mn - 1 && !cut_active) continue;
-        if (r[i] > 0.0) {
+        if (smooth) {
+          if (!(r[i] > 0.0) && S->w[i] > 1.0f) S->w[i] = S->w[i] - 1.0f;
+        } else if (r[i] > 0.0) {
           float nw = S->w[i] + 1.0f;
           S->w[i] = nw < prm->weight_cap ? nw : prm->weight_cap;
         }

@@ -81,8 +81,8 @@ typedef struct {
                             makes the point feasible, i.e. gives a new incumbent (R18, NEXT f1) */
   int32_t perturb;       /* 1: perturbation after a stuck iteration (R21, NEXT f1)             */
   int32_t perturb_radius;/* half-width of the value window on an infinite side (R21)          */
-  int32_t pad;
-  uint64_t perturb_seed; /* seed of the counter-based draws (R21)                              */
+  float smooth_prob;     /* weight smoothing probability per stuck iteration (R22)            */
+  uint64_t rng_seed;     /* seed of the counter-based draws (R21, R22)                        */
 } orc_params;
 
 typedef struct {

@@ -49,8 +49,8 @@ class chap_params(ctypes.Structure):
     _fields_ = [("tenure", c_i32), ("weight_cap", c_f32), ("cutoff_delta", c_f64), ("exchange_K", c_i32),
                 ("n_elite", c_i32), ("n_restart", c_i32), ("graph_iters", c_i32),
                 ("binary_kernel", c_i32), ("pdl", c_i32), ("l2_persist", c_i32), ("aspiration", c_i32),
-                ("lazy", c_i32), ("perturb", c_i32), ("perturb_radius", c_i32), ("pad_params", c_i32),
-                ("perturb_seed", ctypes.c_uint64)]
+                ("lazy", c_i32), ("perturb", c_i32), ("perturb_radius", c_i32), ("smooth_prob", c_f32),
+                ("rng_seed", ctypes.c_uint64)]
 
 
 class chap_step_record(ctypes.Structure):

@@ -1151,8 +1151,8 @@ extern "C" chap_status chap_params_default(chap_params* out) {
   out->lazy = 0;
   out->perturb = 0;
   out->perturb_radius = 16;
-  out->pad_params = 0;
-  out->perturb_seed = 0;
+  out->smooth_prob = 0.0f;
+  out->rng_seed = 0;
   return CHAP_OK;
 }
 
@@ -1169,6 +1169,7 @@ static chap_status check_params(const chap_params& q) {
   if (q.lazy < 0 || q.lazy > 1) return fail(CHAP_ERR_INVALID_ARG, "lazy not in {0, 1}");
   if (q.perturb < 0 || q.perturb > 1) return fail(CHAP_ERR_INVALID_ARG, "perturb not in {0, 1}");
   if (q.perturb_radius < 1) return fail(CHAP_ERR_INVALID_ARG, "perturb_radius < 1");
+  if (!(q.smooth_prob >= 0.0f && q.smooth_prob <= 1.0f)) return fail(CHAP_ERR_INVALID_ARG, "smooth_prob not in [0, 1]");
   return CHAP_OK;
 }
 
@@ -1281,7 +1282,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.wcap = prm.weight_cap;
   Wk.perturb = prm.perturb;
   Wk.perturb_radius = prm.perturb_radius;
-  Wk.perturb_seed = prm.perturb_seed;
+  Wk.rng_seed = prm.rng_seed;
+  Wk.smooth_prob = prm.smooth_prob;
   Wk.delta = prm.cutoff_delta;
   CUDA_TRY(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
   if (prm.l2_persist) {   // the gathered row state persists in L2 (window on the stream,

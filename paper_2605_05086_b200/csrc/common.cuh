@@ -209,6 +209,7 @@ __host__ __device__ __forceinline__ unsigned long long rng_draw(unsigned long lo
 }
 constexpr unsigned long long kDrawEntry = 1ull << 62;         // c of the entry draw (rows use c = i)
 constexpr unsigned long long kDrawValue = (1ull << 62) + 1;   // c of the value draw
+constexpr unsigned long long kDrawSmooth = (1ull << 62) + 2;  // c of the weight-smoothing draw (R22)
 
 // Per-kernel device time (chap_walkers_timing): %globaltimer at every block's start (atomic min)
 // and end (atomic max) into DevWalkers::kt when it is non-NULL; k_apply accumulates the spans.
@@ -353,7 +354,8 @@ struct DevWalkers {
   int32_t lbkt_wm_words;               // ... with this many ints of shared memory per warp for the histograms
   int32_t perturb;                     // chap_params.perturb (R21)
   int32_t perturb_radius;              // the window half-width on an infinite side
-  unsigned long long perturb_seed;
+  unsigned long long rng_seed;         // the seed of the draws (R21, R22)
+  float smooth_prob;                   // chap_params.smooth_prob (R22)
   Cand* asp;                           // [W][tenure] aspiration slots (chap_params.aspiration), NULL = off:
                                        // the eval kernels note every tabu column with s > 0 in slot
                                        // tabu_until % tenure; the select takes the feasible ones (R18)

@@ -289,16 +289,25 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
       dv += (long long)(r1 > 0.0) - (long long)(r0 > 0.0);
     }
   } else {
-    // stuck: w_i <- min(w_i + 1, cap) on every active violated row (R12); with the perturbation
+    // stuck: w_i <- min(w_i + 1, cap) on every active violated row (R12), or with weight smoothing
+    // (R22) drawn, w_i <- w_i - 1 on every active satisfied row with w_i > 1; with the perturbation
     // (R21) also the row draw: the least (h32 << 32 | i) over the violated and over all active rows
     unsigned long long kv = ~0ull, ka = ~0ull;
     const bool pert = Wk.perturb != 0;
     const unsigned long long h0 =
-        pert ? splitmix64(splitmix64(splitmix64(Wk.perturb_seed) ^ (unsigned long long)w) ^ (unsigned long long)sc->k) : 0ull;
+        (pert || Wk.smooth_prob > 0.0f)
+            ? splitmix64(splitmix64(splitmix64(Wk.rng_seed) ^ (unsigned long long)w) ^ (unsigned long long)sc->k)
+            : 0ull;
+    const bool smooth =
+        Wk.smooth_prob > 0.0f && (double)(splitmix64(h0 ^ kDrawSmooth) >> 11) * 0x1.0p-53 < (double)Wk.smooth_prob;
     for (int i = gtid; i < P.m_norm; i += gstride) {
       if (i == P.cut_row && !cut_active) continue;
       const bool viol = rw[i].r > 0.0;
-      if (viol) rw[i].w = fminf(rw[i].w + 1.0f, Wk.wcap);
+      if (smooth) {
+        if (!viol && rw[i].w > 1.0f) rw[i].w = rw[i].w - 1.0f;
+      } else if (viol) {
+        rw[i].w = fminf(rw[i].w + 1.0f, Wk.wcap);
+      }
       if (pert) {
         const unsigned long long key = (splitmix64(h0 ^ (unsigned long long)i) & 0xFFFFFFFF00000000ull) | (unsigned)i;
         ka = key < ka ? key : ka;
@@ -391,7 +400,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
         const int e0 = P.rp[i], len = P.rp[i + 1] - e0;
         if (len > 0) {
           const unsigned long long h0 =
-              splitmix64(splitmix64(splitmix64(Wk.perturb_seed) ^ (unsigned long long)w) ^ (unsigned long long)k);
+              splitmix64(splitmix64(splitmix64(Wk.rng_seed) ^ (unsigned long long)w) ^ (unsigned long long)k);
           const int p = P.ci[e0 + (int)(splitmix64(h0 ^ kDrawEntry) % (unsigned long long)len)];
           double v;
           if (perturb_value(P, p, x[p], Wk.perturb_radius, splitmix64(h0 ^ kDrawValue), &v)) {

@@ -190,14 +190,14 @@ def test_host_buffer_variant_equals_device():
 
 
 def _traj_compare(inst, x0s, n_iters, params=None, graph_iters=16, weight_cap=1e6, tenure=10, binary_kernel=0,
-                  aspiration=0, lazy=0, perturb=0, perturb_seed=0, perturb_radius=16, split=None):
+                  aspiration=0, lazy=0, perturb=0, rng_seed=0, perturb_radius=16, smooth_prob=0.0, split=None):
     P = chap.Problem.from_instance(inst)
     O = oracle.Problem.from_instance(inst)
     prm = chap.default_params(graph_iters=graph_iters, weight_cap=weight_cap, tenure=tenure,
                               binary_kernel=binary_kernel, aspiration=aspiration, lazy=lazy, perturb=perturb,
-                              perturb_seed=perturb_seed, perturb_radius=perturb_radius)
+                              rng_seed=rng_seed, perturb_radius=perturb_radius, smooth_prob=smooth_prob)
     oprm = oracle.TabuParams(tenure=tenure, weight_cap=weight_cap, aspiration=aspiration, perturb=perturb,
-                             perturb_seed=perturb_seed, perturb_radius=perturb_radius)
+                             rng_seed=rng_seed, perturb_radius=perturb_radius, smooth_prob=smooth_prob)
     X0 = torch.from_numpy(np.ascontiguousarray(np.stack(x0s), np.float64)).cuda()
     Wk = chap.Walkers(P, X0, prm)
     if split is None:   # one chap_tabu_step call
@@ -608,7 +608,7 @@ def test_trajectory_perturb_config_T(seed, binrow):
     including the drawn row, entry and value of every perturbation."""
     inst = synth.tiny(seed)
     log = _traj_compare(inst, [synth.x_lower(inst)], 500, graph_iters=16 if seed % 2 else 0, binary_kernel=binrow,
-                        perturb=1, perturb_seed=1000 + seed, tenure=4)
+                        perturb=1, rng_seed=1000 + seed, tenure=4)
     assert (log["flags"] == 1).any()
 
 
@@ -619,15 +619,30 @@ def test_trajectory_perturb_classes_groups_lazy():
     inst = synth.mixed(seed=5, n=600, m=400, n_long=6, long_lo=100, long_hi=600,
                        long_kinds=("unb", "big", "bkt", "bin"))
     assert chap.Problem.from_instance(inst).info.n_sorted_columns >= 1
-    log = _traj_compare(inst, [inst.x_star, synth.x_lower(inst)], 300, perturb=1, perturb_seed=8, tenure=3)
+    log = _traj_compare(inst, [inst.x_star, synth.x_lower(inst)], 300, perturb=1, rng_seed=8, tenure=3)
     assert (log["flags"] == 1).sum() >= 10
     inst = synth.mixed(seed=5, n=3000, m=600, n_long=6, long_lo=100, long_hi=600)
     x0s = [synth.x_lower(inst), inst.x_star] + [synth.x_random(inst, s) for s in range(4)]
-    log = _traj_compare(inst, x0s, 300, perturb=1, perturb_seed=8, tenure=3)
+    log = _traj_compare(inst, x0s, 300, perturb=1, rng_seed=8, tenure=3)
     assert (log["flags"] == 1).any()
     inst = synth.tiny(2)
-    log = _traj_compare(inst, [synth.x_lower(inst)], 300, lazy=1, perturb=1, perturb_seed=9, tenure=4)
+    log = _traj_compare(inst, [synth.x_lower(inst)], 300, lazy=1, perturb=1, rng_seed=9, tenure=4)
     assert (log["flags"] == 1).any()
-    log = _traj_compare(inst, [synth.x_lower(inst)], 300, aspiration=1, perturb=1, perturb_seed=10, tenure=4,
+    log = _traj_compare(inst, [synth.x_lower(inst)], 300, aspiration=1, perturb=1, rng_seed=10, tenure=4,
                         split=[7, 1, 13, 29, 250])
     assert (log["flags"] == 1).any()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_trajectory_weight_smoothing(seed, binrow):
+    """NEXT f1 (R22, weight smoothing): stuck iterations that draw u < smooth_prob lower the weights
+    of the satisfied rows instead of bumping the violated ones; trajectories and final weights
+    bit-exact against the oracle, alone and with the perturbation, with walker groups."""
+    inst = synth.tiny(seed)
+    _traj_compare(inst, [synth.x_lower(inst)], 500, binary_kernel=binrow, smooth_prob=0.4, rng_seed=seed, tenure=4)
+    _traj_compare(inst, [synth.x_lower(inst)], 400, binary_kernel=binrow, smooth_prob=0.3, perturb=1,
+                  rng_seed=50 + seed, tenure=4, graph_iters=0)
+    if seed == 0:
+        inst = synth.mixed(seed=5, n=3000, m=600, n_long=6, long_lo=100, long_hi=600)
+        x0s = [synth.x_lower(inst), inst.x_star] + [synth.x_random(inst, s) for s in range(4)]
+        _traj_compare(inst, x0s, 300, perturb=1, smooth_prob=0.5, rng_seed=8, tenure=3)

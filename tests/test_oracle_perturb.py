@@ -77,7 +77,7 @@ def test_binary_perturbation_flips_exactly_one_bit_uniform_rows():
     n = 10
     inst = _always_violated(n)
     O = oracle.Problem.from_instance(inst)
-    prm = oracle.TabuParams(tenure=10**8, perturb=1, perturb_seed=12345)
+    prm = oracle.TabuParams(tenure=10**8, perturb=1, rng_seed=12345)
     x0 = np.zeros(n)
     ow = oracle.TabuWalker(O, x0, prm)
     log = ow.run(6000)
@@ -107,7 +107,7 @@ def test_row_draw_is_uniform_over_the_violated_rows_only():
     rows = [([i], [1.0], 2.0, math.inf) for i in range(6)] + [([i], [1.0], -math.inf, 1.0) for i in range(6, 12)]
     inst = _inst("half_violated", rows, n, [0] * n, [1] * n, [1] * n)
     O = oracle.Problem.from_instance(inst)
-    ow = oracle.TabuWalker(O, np.zeros(n), oracle.TabuParams(tenure=10**8, perturb=1, perturb_seed=99))
+    ow = oracle.TabuWalker(O, np.zeros(n), oracle.TabuParams(tenure=10**8, perturb=1, rng_seed=99))
     log = ow.run(5000)
     pj = log["j"][log["flags"] == 1]
     assert pj.size > 2000 and pj.max() < 6
@@ -123,7 +123,7 @@ def test_cutoff_row_is_eligible():
     # (stuck); the perturbation draws the cutoff row, i.e. a variable with c_j != 0
     inst = _inst("cutoff_only", [([0, 1], [1.0, 1.0], -math.inf, 2.0)], 2, [0, 0], [1, 1], [1, 1], c=[1.0, 1.0])
     O = oracle.Problem.from_instance(inst)
-    ow = oracle.TabuWalker(O, np.zeros(2), oracle.TabuParams(tenure=3, perturb=1, perturb_seed=5))
+    ow = oracle.TabuWalker(O, np.zeros(2), oracle.TabuParams(tenure=3, perturb=1, rng_seed=5))
     assert ow.has_incumbent and ow.best_obj == 0.0
     log = ow.run(40)
     assert log["j"][0] == -1 and log["flags"][1] == 1
@@ -135,7 +135,7 @@ def test_integer_values_uniform_excluding_current():
     # perturbation draws uniformly from {0..4} minus the current value
     inst = _inst("int_dom", [([0], [1.0], 10.0, math.inf)], 1, [0], [4], [1])
     O = oracle.Problem.from_instance(inst)
-    ow = oracle.TabuWalker(O, np.zeros(1), oracle.TabuParams(tenure=10**8, perturb=1, perturb_seed=3))
+    ow = oracle.TabuWalker(O, np.zeros(1), oracle.TabuParams(tenure=10**8, perturb=1, rng_seed=3))
     log = ow.run(8001)
     pts = _replay(inst, log, np.zeros(1))
     pairs = np.zeros((5, 5), int)
@@ -158,7 +158,7 @@ def test_unbounded_and_continuous_windows():
                  2, [0, -math.inf], [math.inf, math.inf], [1, 0])
     O = oracle.Problem.from_instance(inst)
     ow = oracle.TabuWalker(O, np.zeros(2), oracle.TabuParams(tenure=10**8, perturb=1, perturb_radius=R,
-                                                             perturb_seed=17))
+                                                             rng_seed=17))
     log = ow.run(3000)
     pts = _replay(inst, log, np.zeros(2))
     ks = np.nonzero(log["flags"] == 1)[0]
@@ -181,16 +181,16 @@ def test_seeded_replay_and_restart_clears_pending():
     O = oracle.Problem.from_instance(inst)
     logs = []
     for seed in (1, 1, 2):
-        ow = oracle.TabuWalker(O, np.zeros(6), oracle.TabuParams(tenure=10**8, perturb=1, perturb_seed=seed))
+        ow = oracle.TabuWalker(O, np.zeros(6), oracle.TabuParams(tenure=10**8, perturb=1, rng_seed=seed))
         logs.append(ow.run(400))
     assert logs[0].tobytes() == logs[1].tobytes()
     assert not np.array_equal(logs[0]["j"], logs[2]["j"])
     # walker ids are draw arguments: two walkers of one set walk differently
-    ow2 = oracle.TabuWalker(O, np.zeros(6), oracle.TabuParams(tenure=10**8, perturb=1, perturb_seed=1),
+    ow2 = oracle.TabuWalker(O, np.zeros(6), oracle.TabuParams(tenure=10**8, perturb=1, rng_seed=1),
                             walker_id=1)
     assert not np.array_equal(ow2.run(400)["j"], logs[0]["j"])
     # a stuck last iteration leaves a pending perturbation; a restart drops it
-    ow = oracle.TabuWalker(O, np.zeros(6), oracle.TabuParams(tenure=10**8, perturb=1, perturb_seed=1))
+    ow = oracle.TabuWalker(O, np.zeros(6), oracle.TabuParams(tenure=10**8, perturb=1, rng_seed=1))
     lg = ow.run(7)    # 6 flips, then stuck
     assert lg["j"][6] == -1 and ow.S.force_j >= 0
     ow.restart(np.ones(6))
@@ -203,3 +203,39 @@ def test_perturb_off_is_the_plain_walk():
     O = oracle.Problem.from_instance(inst)
     a = oracle.TabuWalker(O, np.zeros(5), oracle.TabuParams(tenure=10**8)).run(50)
     assert (a["flags"] == 0).all() and (a["j"][5:] == -1).all()
+
+
+def test_weight_smoothing_rule():
+    """R22: every stuck iteration either bumps the violated rows (+1, capped) or, when its draw falls
+    below smooth_prob, lowers the satisfied rows with w > 1 by one; never both, nothing else changes;
+    the smoothing share is binomial(p); p = 1 never bumps, p = 0 never smooths."""
+    # rows: x_0 >= 2 (always violated), x_1 <= 1 (always satisfied), x_0 + x_1 <= 1 (flips)
+    n = 2
+    rows = [([0], [1.0], 2.0, math.inf), ([1], [1.0], -math.inf, 1.0), ([0, 1], [1.0, 1.0], -math.inf, 1.0)]
+    inst = _inst("smooth", rows, n, [0, 0], [1, 1], [1, 1])
+    O = oracle.Problem.from_instance(inst)
+    for p, lo, hi in ((0.5, 0.4, 0.6), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0)):
+        ow = oracle.TabuWalker(O, np.zeros(n), oracle.TabuParams(tenure=2, smooth_prob=p, rng_seed=77, weight_cap=1e6))
+        n_smooth = n_bump = 0
+        for _ in range(3000):
+            w0 = ow.w.copy()
+            x0 = ow.x[:n].copy()
+            r0 = O.residuals(x0, ow.cutoff_rhs)
+            rec = ow.run(1)[0]
+            dw = ow.w - w0
+            if rec["j"] >= 0:
+                assert not dw.any()
+                continue
+            viol = r0 > 0
+            act = np.isfinite(r0)
+            bump = np.where(viol & act, 1.0, 0)   # row 0 is always violated: a bump is never empty
+            smooth = np.where(~viol & act & (w0 > 1), -1.0, 0)
+            if np.array_equal(dw, bump) and bump.any():
+                n_bump += 1
+            elif np.array_equal(dw, smooth):
+                n_smooth += 1
+            else:
+                raise AssertionError((rec, w0, ow.w, r0))
+        assert (ow.w >= 1).all()
+        frac = n_smooth / max(1, n_smooth + n_bump)
+        assert n_smooth + n_bump > 1000 and lo - 0.05 <= frac <= hi + 0.05, (p, n_smooth, n_bump)
