@@ -1541,6 +1541,107 @@ __device__ __forceinline__ GenRound gen_round(const DevProblem& P, const WTile& 
   return R;
 }
 
+// Pass 0 of lines 13-16 on integer offsets, one off_entry word x3 at a time: the nearest candidate
+// on each side (vup, vdn; bounds preset by the caller) and the first six positive steps c2..c7.
+__device__ __forceinline__ void off_pass0(int x3, int hi, int lo, int& vup, int& vdn, int& c2, int& c3, int& c4,
+                                          int& c5, int& c6, int& c7, int& nstep) {
+  const int code = x3 & 7;
+  const int v = (x3 >> 3) - (code & 1);
+  // up side (codes 6, 3 and the tight code 2, whose v exceeds hi): in bounds iff v <= hi;
+  // down side (codes 0, 5): iff v >= lo
+  const bool up = code & 2;
+  const bool inb = up ? v <= hi : v >= lo;
+  if (inb) {
+    if (up) vup = min(vup, v); else vdn = max(vdn, v);
+    if (code & 4) {   // a positive step (codes 6, 5)
+      c7 = nstep == 5 ? v : c7;
+      c6 = nstep == 4 ? v : c6;
+      c5 = nstep == 3 ? v : c5;
+      c4 = nstep == 2 ? v : c4;
+      c3 = nstep == 1 ? v : c3;
+      c2 = nstep == 0 ? v : c2;
+      ++nstep;
+    }
+  }
+}
+
+// Lines 13-16 on integer offsets for one column whose off_entry words are at(e),
+// e in [e0, e1): σ2 (twice the score) at the reduced candidate set {vup, vdn, positive steps c2..c7
+// and beyond} with R4, given β2, α2 and the pass-0 candidates. Returns whether a candidate exists.
+template <bool INTW, class At>
+__device__ __forceinline__ bool offsets_best(At at, int e0, int e1,
+                                             typename std::conditional<INTW, int, double>::type b2,
+                                             typename std::conditional<INTW, int, double>::type a2, int hi, int lo,
+                                             int vup, int vdn, int c2, int c3, int c4, int c5, int c6, int c7,
+                                             int nstep, typename std::conditional<INTW, int, double>::type& bs2,
+                                             int& bv) {
+  using Acc = typename std::conditional<INTW, int, double>::type;
+  auto fv = [](int bits) -> Acc { if (INTW) return (Acc)bits; else return (Acc)__int_as_float(bits); };
+  // the best (σ2, v) of the column under R4: with integer scores one packed key, higher is better
+  // (σ2, then smaller |v|, then smaller v)
+  long long bkey = LLONG_MIN;
+  bs2 = 0;
+  bv = 0;
+  bool have = false;
+  auto offer2 = [&](Acc sg, int v) {
+    if (INTW) {
+      const unsigned tie = 0x7fffffffu - (((unsigned)abs(v) << 1) | (v > 0 ? 1u : 0u));
+      bkey = max(bkey, (long long)sg * 4294967296ll + (long long)tie);
+    } else if (!have || better_off(sg, v, bs2, bv)) {
+      bs2 = sg;
+      bv = v;
+      have = true;
+    }
+  };
+  // σ2 at up to four candidate offsets (INT_MAX / INT_MIN: none) in one pass
+  auto score4 = [&](int q0, int q1, int q2, int q3) {
+    auto lim = [](int q) { return (q == INT_MAX || q == INT_MIN) ? INT_MIN : ((q << 3) | 7); };   // key <= v  <=>  x <= v << 3 | 7
+    const int l0 = lim(q0), l1 = lim(q1), l2 = lim(q2), l3 = lim(q3);
+    Acc s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int e = e0; e < e1; ++e) {
+      const int2 E = at(e);
+      const Acc F = fv(E.y);
+      s0 += E.x <= l0 ? F : (Acc)0;
+      s1 += E.x <= l1 ? F : (Acc)0;
+      s2 += E.x <= l2 ? F : (Acc)0;
+      s3 += E.x <= l3 ? F : (Acc)0;
+    }
+    if (l0 != INT_MIN) offer2(b2 + s0 + (q0 > 0 ? a2 : (Acc)0), q0);
+    if (l1 != INT_MIN) offer2(b2 + s1 + (q1 > 0 ? a2 : (Acc)0), q1);
+    if (l2 != INT_MIN) offer2(b2 + s2 + (q2 > 0 ? a2 : (Acc)0), q2);
+    if (l3 != INT_MIN) offer2(b2 + s3 + (q3 > 0 ? a2 : (Acc)0), q3);
+  };
+  score4(vup, vdn, c2, c3);
+  if (nstep > 2) score4(c4, c5, c6, c7);
+  if (nstep > 6) {   // steps 7, 8, ... (rare): rescan for them, four per pass
+    int q0 = INT_MIN, q1 = INT_MIN, q2 = INT_MIN, q3 = INT_MIN;
+    int seen = 0, nq = 0;
+    for (int e = e0; e < e1; ++e) {
+      const int x3 = at(e).x, code = x3 & 7, v = (x3 >> 3) - (code & 1);
+      const bool up = code & 2;
+      if (!((code & 4) && (up ? v <= hi : v >= lo))) continue;
+      if (seen++ < 6) continue;
+      q0 = nq == 0 ? v : q0;
+      q1 = nq == 1 ? v : q1;
+      q2 = nq == 2 ? v : q2;
+      q3 = nq == 3 ? v : q3;
+      if (++nq == 4) {
+        score4(q0, q1, q2, q3);
+        nq = 0;
+        q0 = q1 = q2 = q3 = INT_MIN;
+      }
+    }
+    if (nq > 0) score4(q0, q1, q2, q3);
+  }
+  if (INTW && bkey != LLONG_MIN) {
+    have = true;
+    bs2 = (Acc)(bkey >> 32);
+    const unsigned t = 0x7fffffffu - (unsigned)(bkey & 0xffffffffll);
+    bv = (t & 1u) ? (int)(t >> 1) : -(int)(t >> 1);
+  }
+  return have;
+}
+
 // One tile of packed general integer columns (see above). INTW: integral weights <= 2^20. R holds
 // the tile's first round (loaded by the caller); the rounds are software-pipelined (the next round's
 // loads are in flight while this round's gathers return), and when the warp's next item Tn is a
@@ -1610,87 +1711,12 @@ __device__ __forceinline__ void gen32_tile(const DevProblem& P, const double* __
     const int4 E = ent[e];
     b2 += fv(E.z);
     a2 += fv(E.w);
-    const int code = E.x & 7;
-    const int v = (E.x >> 3) - (code & 1);
-    // up side (codes 6, 3 and the tight code 2, whose v exceeds hi): in bounds iff v <= hi;
-    // down side (codes 0, 5): iff v >= lo
-    const bool up = code & 2;
-    const bool inb = up ? v <= hi : v >= lo;
-    if (inb) {
-      if (up) vup = min(vup, v); else vdn = max(vdn, v);
-      if (code & 4) {   // a positive step (codes 6, 5)
-        c7 = nstep == 5 ? v : c7;
-        c6 = nstep == 4 ? v : c6;
-        c5 = nstep == 3 ? v : c5;
-        c4 = nstep == 2 ? v : c4;
-        c3 = nstep == 1 ? v : c3;
-        c2 = nstep == 0 ? v : c2;
-        ++nstep;
-      }
-    }
+    off_pass0(E.x, hi, lo, vup, vdn, c2, c3, c4, c5, c6, c7, nstep);
   }
-  // the best (σ2, v) of the column under R4: with integer scores one packed key, higher is better
-  // (σ2, then smaller |v|, then smaller v)
-  long long bkey = LLONG_MIN;
-  Acc bs2 = 0;
-  int bv = 0;
-  bool have = false;
-  auto offer2 = [&](Acc sg, int v) {
-    if (INTW) {
-      const unsigned tie = 0x7fffffffu - (((unsigned)abs(v) << 1) | (v > 0 ? 1u : 0u));
-      bkey = max(bkey, (long long)sg * 4294967296ll + (long long)tie);
-    } else if (!have || better_off(sg, v, bs2, bv)) {
-      bs2 = sg;
-      bv = v;
-      have = true;
-    }
-  };
-  // σ2 at up to four candidate offsets (INT_MAX / INT_MIN: none) in one pass
-  auto score4 = [&](int q0, int q1, int q2, int q3) {
-    auto lim = [](int q) { return (q == INT_MAX || q == INT_MIN) ? INT_MIN : ((q << 3) | 7); };   // key <= v  <=>  x <= v << 3 | 7
-    const int l0 = lim(q0), l1 = lim(q1), l2 = lim(q2), l3 = lim(q3);
-    Acc s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    for (int e = cb; e < ce; ++e) {
-      const int2 E = *reinterpret_cast<const int2*>(&ent[e]);
-      const Acc F = fv(E.y);
-      s0 += E.x <= l0 ? F : (Acc)0;
-      s1 += E.x <= l1 ? F : (Acc)0;
-      s2 += E.x <= l2 ? F : (Acc)0;
-      s3 += E.x <= l3 ? F : (Acc)0;
-    }
-    if (l0 != INT_MIN) offer2(b2 + s0 + (q0 > 0 ? a2 : (Acc)0), q0);
-    if (l1 != INT_MIN) offer2(b2 + s1 + (q1 > 0 ? a2 : (Acc)0), q1);
-    if (l2 != INT_MIN) offer2(b2 + s2 + (q2 > 0 ? a2 : (Acc)0), q2);
-    if (l3 != INT_MIN) offer2(b2 + s3 + (q3 > 0 ? a2 : (Acc)0), q3);
-  };
-  score4(vup, vdn, c2, c3);
-  if (nstep > 2) score4(c4, c5, c6, c7);
-  if (nstep > 6) {   // steps 7, 8, ... (rare): rescan for them, four per pass
-    int q0 = INT_MIN, q1 = INT_MIN, q2 = INT_MIN, q3 = INT_MIN;
-    int seen = 0, nq = 0;
-    for (int e = cb; e < ce; ++e) {
-      const int x3 = ent[e].x, code = x3 & 7, v = (x3 >> 3) - (code & 1);
-      const bool up = code & 2;
-      if (!((code & 4) && (up ? v <= hi : v >= lo))) continue;
-      if (seen++ < 6) continue;
-      q0 = nq == 0 ? v : q0;
-      q1 = nq == 1 ? v : q1;
-      q2 = nq == 2 ? v : q2;
-      q3 = nq == 3 ? v : q3;
-      if (++nq == 4) {
-        score4(q0, q1, q2, q3);
-        nq = 0;
-        q0 = q1 = q2 = q3 = INT_MIN;
-      }
-    }
-    if (nq > 0) score4(q0, q1, q2, q3);
-  }
-  if (INTW && bkey != LLONG_MIN) {
-    have = true;
-    bs2 = (Acc)(bkey >> 32);
-    const unsigned t = 0x7fffffffu - (unsigned)(bkey & 0xffffffffll);
-    bv = (t & 1u) ? (int)(t >> 1) : -(int)(t >> 1);
-  }
+  Acc bs2;
+  int bv;
+  const bool have = offsets_best<INTW>([&](int e) { return *reinterpret_cast<const int2*>(&ent[e]); }, cb, ce, b2, a2,
+                                       hi, lo, vup, vdn, c2, c3, c4, c5, c6, c7, nstep, bs2, bv);
   double v = xb, sres = -INFINITY;
   if (have) {
     sres = 0.5 * (double)bs2;
@@ -2027,6 +2053,64 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
 // different walkers. Sums of ±w, ±w/2 in double are exact (R11), so the scores equal the per-walker
 // kernels' bit for bit.
 constexpr int kGenWmThreads = 128;
+// The integer path of k_eval_gen_wm for one packed general column of lane (slot, walker): lines
+// 3-11 by off_entry (gen32_tile's table and float-quotient offsets) into the lane's shared-memory
+// column (lane-interleaved int2 [k][32]) with pass 0 fused into the emission, then offsets_best
+// over the reduced candidate set. Returns false when an offset is beyond the int path
+// (the caller re-evaluates the column in double).
+template <bool INTW, int RG>
+__device__ __forceinline__ bool wm_off_column(const DevProblem& P, const double2* __restrict__ RS, int cb, int k,
+                                              double xb, double l, double u, bool rint,
+                                              const int4* __restrict__ tab, int2* __restrict__ sent, int lane,
+                                              double& bs, double& bv) {
+  using Acc = typename std::conditional<INTW, int, double>::type;
+  auto fv = [](int bits) -> Acc { if (INTW) return (Acc)bits; else return (Acc)__int_as_float(bits); };
+  const bool ufin = isfinite(u), lfin = isfinite(l);
+  const double hid = u - xb, lod = l - xb;
+  const int hi = ufin ? (int)fmin(hid, (double)kKeyLim) : kKeyLim;
+  const int lo = lfin ? (int)fmax(lod, -(double)kKeyLim) : -kKeyLim;
+  int vup = (ufin && hi > 0) ? hi : INT_MAX;
+  int vdn = (lfin && lo < 0) ? lo : INT_MIN;
+  int c2 = INT_MIN, c3 = INT_MIN, c4 = INT_MIN, c5 = INT_MIN, c6 = INT_MIN, c7 = INT_MIN, nstep = 0;
+  Acc b2 = 0, a2 = 0;
+  bool ovf = false;
+  for (int e0 = 0; e0 < k; e0 += 4) {
+    int id[4];
+    double av[4];
+    double2 rv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      id[q] = e0 + q < k ? __ldg(P.row_idx + cb + e0 + q) : -1;
+      av[q] = e0 + q < k ? __ldg(P.val + cb + e0 + q) : 1.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q;
+      if (e >= k) break;
+      const int4 E = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), av[q], rint, tab, ovf);
+      b2 += fv(E.z);
+      a2 += fv(E.w);
+      off_pass0(E.x, hi, lo, vup, vdn, c2, c3, c4, c5, c6, c7, nstep);
+      sent[e * 32 + lane] = make_int2(E.x, E.y);
+    }
+  }
+  if (ovf) return false;
+  Acc bs2;
+  int bo;
+  const bool have = offsets_best<INTW>([&](int e) { return sent[e * 32 + lane]; }, 0, k, b2, a2, hi, lo, vup, vdn, c2,
+                                       c3, c4, c5, c6, c7, nstep, bs2, bo);
+  bs = -INFINITY;
+  bv = xb;
+  if (have) {
+    bs = 0.5 * (double)bs2;
+    // a bound beyond the clamp is the farthest candidate of its side: its exact value
+    bv = (bo == hi && ufin && hid > (double)kKeyLim) ? u : ((bo == lo && lfin && lod < -(double)kKeyLim) ? l : xb + (double)bo);
+  }
+  return true;
+}
+
 // per warp: kmax x 32 (key f64, δ f32) for the tiles, or lbkt_words ints for a long chunk's
 // histograms (DevWalkers::lbkt_wm), whichever is larger (16-byte multiple)
 __host__ __device__ constexpr size_t gen_wm_region(int kmax, int lbkt_words) {
@@ -2083,10 +2167,13 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
   // warp's shared memory ([bucket][lane], conflict-free) and adds it to its walker's accumulators;
   // the walkers whose ticket completes are finished by the warp, one after the other.
   const int ng = Wk.lbkt_wm ? P.n_gchunks : 0;
+  __shared__ int4 s_tab[6];
+  off_table_init(s_tab);
+  __syncthreads();
+  // the integer path of the tiles: every walker of the warp with integral weights <= 2^20 (INTW)
+  const bool wint_all = __all_sync(kFull, Wk.sc[wr].wint != 0);
+  const bool rint_l = Wk.sc[wr].rint != 0;
   if (ng > 0) {
-    __shared__ int4 s_tab[6];
-    off_table_init(s_tab);
-    __syncthreads();
     int* hist = reinterpret_cast<int*>(wreg);   // [dom + 1][32] ints, then the candidate words
     for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < ng; t += nwarps) {
       const WTile T = P.gchunks[t];
@@ -2167,7 +2254,17 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
         continue;
       }
       const int cb = __ldg(P.col_ptr + p), k = __ldg(P.col_ptr + p + 1) - cb;
-      // lines 3-11 per entry into the lane's (key, δ) column
+      {
+        double s1, v1;
+        int2* sent = reinterpret_cast<int2*>(skey);   // the lane's int2 slots alias its own key slots
+        const bool ok = wint_all ? wm_off_column<true, RG>(P, RS, cb, k, xb, l, u, rint_l, s_tab, sent, lane, s1, v1)
+                                 : wm_off_column<false, RG>(P, RS, cb, k, xb, l, u, rint_l, s_tab, sent, lane, s1, v1);
+        if (ok) {
+          if (live) offer(s1, v1, j, p);
+          continue;
+        }
+      }
+      // an offset beyond the int path: lines 3-11 per entry into the lane's (key, δ) column in double
       double beta = 0.0, alpha = 0.0, pl = 0.0, pu = 0.0;
       unsigned long long cm = 0ull;   // candidate entries
       for (int e0 = 0; e0 < k; e0 += 4) {
