@@ -2053,6 +2053,9 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
 // different walkers. Sums of ±w, ±w/2 in double are exact (R11), so the scores equal the per-walker
 // kernels' bit for bit.
 constexpr int kGenWmThreads = 128;
+#ifndef CHAP_WM_ROUND
+#define CHAP_WM_ROUND 4   // entries per round of loads in wm_off_column
+#endif
 // The integer path of k_eval_gen_wm for one packed general column of lane (slot, walker): lines
 // 3-11 by off_entry (gen32_tile's table and float-quotient offsets) into the lane's shared-memory
 // column (lane-interleaved int2 [k][32]) with pass 0 fused into the emission, then offsets_best
@@ -2074,19 +2077,19 @@ __device__ __forceinline__ bool wm_off_column(const DevProblem& P, const double2
   int c2 = INT_MIN, c3 = INT_MIN, c4 = INT_MIN, c5 = INT_MIN, c6 = INT_MIN, c7 = INT_MIN, nstep = 0;
   Acc b2 = 0, a2 = 0;
   bool ovf = false;
-  for (int e0 = 0; e0 < k; e0 += 4) {
-    int id[4];
-    double av[4];
-    double2 rv[4];
+  for (int e0 = 0; e0 < k; e0 += CHAP_WM_ROUND) {
+    int id[CHAP_WM_ROUND];
+    double av[CHAP_WM_ROUND];
+    double2 rv[CHAP_WM_ROUND];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < CHAP_WM_ROUND; ++q) {
       id[q] = e0 + q < k ? __ldg(P.row_idx + cb + e0 + q) : -1;
       av[q] = e0 + q < k ? __ldg(P.val + cb + e0 + q) : 1.0;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+    for (int q = 0; q < CHAP_WM_ROUND; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < CHAP_WM_ROUND; ++q) {
       const int e = e0 + q;
       if (e >= k) break;
       const int4 E = off_entry<INTW>(rv[q].x, __int_as_float((int)__double2loint(rv[q].y)), av[q], rint, tab, ovf);
@@ -2111,17 +2114,20 @@ __device__ __forceinline__ bool wm_off_column(const DevProblem& P, const double2
   return true;
 }
 
-// per warp: kmax x 32 (key f64, δ f32) for the tiles, or lbkt_words ints for a long chunk's
-// histograms (DevWalkers::lbkt_wm), whichever is larger (16-byte multiple)
+// per warp: kmax x 32 int2 (off_entry key and δ words) for the tiles, or lbkt_words ints for a long
+// chunk's histograms (DevWalkers::lbkt_wm), whichever is larger (16-byte multiple)
 __host__ __device__ constexpr size_t gen_wm_region(int kmax, int lbkt_words) {
-  return (((size_t)kmax * 32 * (sizeof(double) + sizeof(float)) > (size_t)lbkt_words * 4
-               ? (size_t)kmax * 32 * (sizeof(double) + sizeof(float)) : (size_t)lbkt_words * 4) + 15) / 16 * 16;
+  return (((size_t)kmax * 32 * sizeof(int2) > (size_t)lbkt_words * 4 ? (size_t)kmax * 32 * sizeof(int2)
+                                                                       : (size_t)lbkt_words * 4) + 15) / 16 * 16;
 }
 __host__ __device__ constexpr size_t gen_wm_smem_all(int kmax, int lbkt_words) {
   return (size_t)(kGenWmThreads / 32) * gen_wm_region(kmax, lbkt_words);
 }
 template <int RG>
-__global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, DevWalkers Wk, int part_base, int kmax) {
+#ifndef CHAP_GENWM_MINB
+#define CHAP_GENWM_MINB 5   // 5 blocks per SM (96 registers): 1.26 vs 1.85 ms at 1 (128 registers) on G-32
+#endif
+__global__ void __launch_bounds__(kGenWmThreads, CHAP_GENWM_MINB) k_eval_gen_wm(DevProblem P, DevWalkers Wk, int part_base, int kmax) {
   pdl_wait_trigger();
   constexpr int NS = 32 / RG;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -2131,10 +2137,9 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
   const int w = g * RG + wl;
   const bool live = w < Wk.W;
   const int wr = live ? w : g * RG;
-  // this warp's region of shared memory: the tiles' (key, δ) columns, or a long chunk's histograms
+  // this warp's region of shared memory: the tiles' off_entry columns, or a long chunk's histograms
   unsigned char* wreg = smem + (size_t)wid * gen_wm_region(kmax, Wk.lbkt_wm_words);
-  double* skey = reinterpret_cast<double*>(wreg);                                  // [kmax][32]
-  float* sD = reinterpret_cast<float*>(wreg + (size_t)kmax * 32 * sizeof(double));  // [kmax][32]
+  int2* sent = reinterpret_cast<int2*>(wreg);   // [kmax][32]
   const double2* __restrict__ RS = reinterpret_cast<const double2*>(Wk.rs + (size_t)g * Wk.rss * RG) + wl;
   const double* __restrict__ X = Wk.x + (size_t)wr * Wk.xs;
   const int32_t* __restrict__ TB = Wk.tabu + (size_t)wr * Wk.ts;
@@ -2256,7 +2261,6 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
       const int cb = __ldg(P.col_ptr + p), k = __ldg(P.col_ptr + p + 1) - cb;
       {
         double s1, v1;
-        int2* sent = reinterpret_cast<int2*>(skey);   // the lane's int2 slots alias its own key slots
         const bool ok = wint_all ? wm_off_column<true, RG>(P, RS, cb, k, xb, l, u, rint_l, s_tab, sent, lane, s1, v1)
                                  : wm_off_column<false, RG>(P, RS, cb, k, xb, l, u, rint_l, s_tab, sent, lane, s1, v1);
         if (ok) {
@@ -2264,55 +2268,12 @@ __global__ void __launch_bounds__(kGenWmThreads) k_eval_gen_wm(DevProblem P, Dev
           continue;
         }
       }
-      // an offset beyond the int path: lines 3-11 per entry into the lane's (key, δ) column in double
-      double beta = 0.0, alpha = 0.0, pl = 0.0, pu = 0.0;
-      unsigned long long cm = 0ull;   // candidate entries
-      for (int e0 = 0; e0 < k; e0 += 4) {
-        int id[4];
-        double av[4];
-        double2 rv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          id[q] = e0 + q < k ? __ldg(P.row_idx + cb + e0 + q) : -1;
-          av[q] = e0 + q < k ? __ldg(P.val + cb + e0 + q) : 1.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = e0 + q;
-          if (e >= k) break;
-          const double wv = (double)__int_as_float((int)__double2loint(rv[q].y));
-          const Elem el = emit(xb, rv[q].x, av[q], wv, 1);   // inert rows emit nothing
-          beta += el.beta;
-          alpha += el.alpha;
-          double key = INFINITY;
-          float D = 0.f;
-          if (el.valid && isfinite(el.t)) {
-            D = (float)el.delta;
-            key = el.delta > 0.0 ? el.t : el.t + 1.0;   // integer column: nothing lies in (t, t+1)
-            if (el.t >= l && el.t <= u && el.t != xb) cm |= 1ull << e;
-          }
-          skey[e * 32 + lane] = key;
-          sD[e * 32 + lane] = D;
-          if (key <= l) pl += (double)D;   // the bounds' prefix sums (lines 13-14 at l and u)
-          if (key <= u) pu += (double)D;
-        }
+      // an offset beyond the int path: the column in double (Algorithm 1 serially, no shared memory)
+      {
+        double v2, s2;
+        gen_column_serial(P, X, RS, RG, p, v2, s2);
+        if (live) offer(s2, s2 == -INFINITY ? xb : v2, j, p);
       }
-      // lines 13-16 without the sort: each candidate's prefix sum over the column
-      for (unsigned long long m = cm; m; m &= m - 1) {
-        const int c2 = __ffsll((long long)m) - 1;
-        const double kc = skey[c2 * 32 + lane];
-        const double v = sD[c2 * 32 + lane] > 0.f ? kc : kc - 1.0;
-        double acc = 0.0;
-        for (int e = 0; e < k; ++e)
-          if (skey[e * 32 + lane] <= v) acc += (double)sD[e * 32 + lane];
-        const double sig = beta + acc + (v > xb ? alpha : 0.0);
-        if (better_shift(sig, v, bs, bv, xb)) { bs = sig; bv = v; }
-      }
-      if (isfinite(l) && l != xb && better_shift(beta + pl, l, bs, bv, xb)) { bs = beta + pl; bv = l; }   // l < x̄
-      if (isfinite(u) && u != xb && better_shift(beta + alpha + pu, u, bs, bv, xb)) { bs = beta + alpha + pu; bv = u; }
-      if (live) offer(bs, bs == -INFINITY ? xb : bv, j, p);
     }
   }
   // per-walker block best: slots, then warps, in fixed order

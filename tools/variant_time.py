@@ -11,11 +11,13 @@ import torch  # noqa: E402
 import paper_2605_05086_b200 as chap  # noqa: E402
 import synth  # noqa: E402
 
-cfg = sys.argv[1]
+cfg, _, nw = sys.argv[1].partition(":")   # CFG[:walkers]
+W = int(nw) if nw else 1
 inst = {"G": synth.mixed, "S": synth.setcover, "P": synth.packing,
         "Gbin": lambda: synth.mixed(p_binary=1.0, p_bounded=0.0),
         "Gint": lambda: synth.mixed(p_binary=0.0, p_bounded=1.0),
         "Gnl": lambda: synth.mixed(n_long=0)}[cfg]()
+X0 = np.stack([synth.x_lower(inst)] + [synth.x_random(inst, s) for s in range(1, W)])
 orig = chap._lib
 for path in sys.argv[2:]:
     lib = ctypes.CDLL(os.path.abspath(path))
@@ -25,7 +27,7 @@ for path in sys.argv[2:]:
         setattr(chap, name, f)
     chap._lib = lib
     P = chap.Problem.from_instance(inst)
-    ws = chap.Walkers(P, torch.from_numpy(synth.x_lower(inst)[None, :]).cuda(), chap.default_params(graph_iters=0))
+    ws = chap.Walkers(P, torch.from_numpy(X0).cuda(), chap.default_params(graph_iters=0))
     ws.step(20)
     torch.cuda.synchronize()
     k = ws.profile(200)
