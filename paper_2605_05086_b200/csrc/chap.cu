@@ -811,11 +811,11 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
   TRY(B.alloc(&P->e_bx, n));
   TRY(B.alloc(&P->e_sc, 1));
   TRY(B.alloc(&P->e_part, P->eval_grid + P->bin_grid + P->gen_grid));
-  TRY(B.alloc(&P->e_selcnt, 1));
+  TRY(B.alloc(&P->e_selcnt, 3));   // the select counter, then k_eval_gen's item counters
   TRY(B.alloc(&P->e_bad, 1));
   CUDA_TRY(cudaMallocHost(&P->h_bad, sizeof(int)));
   *P->h_bad = 0;
-  CUDA_TRY(cudaMemset(P->e_selcnt, 0, sizeof(unsigned)));
+  CUDA_TRY(cudaMemset(P->e_selcnt, 0, 3 * sizeof(unsigned)));
   TRY(B.alloc(&P->e_lscr, P->lscr_per_walker));
   CUDA_TRY(cudaMemset(P->e_sc, 0, sizeof(WalkerScalars)));
   CUDA_TRY(cudaMemset(P->e_lscr, 0, sizeof(double) * P->lscr_per_walker));
@@ -1006,6 +1006,7 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.part = P->e_part;
   Wk.ps = P->eval_grid + P->bin_grid + P->gen_grid;
   Wk.sel_count = P->e_selcnt;
+  Wk.gen_ctr = P->e_selcnt + 1;
   Wk.lscr = P->e_lscr;
   Wk.lss = P->lscr_per_walker;
   Wk.use_tabu = 0;
@@ -1258,7 +1259,8 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.ps = S->eval_grid + S->bin_grid + S->gen_grid + S->binrow_grid + S->genwm_grid;
   if (prm.lazy) Wk.ps = std::max(Wk.ps, 4 * p->sm_count);   // k_select_cache's parts
   TRY(B.alloc(&Wk.part, (size_t)Wk.ps * W));
-  TRY(B.alloc(&Wk.sel_count, W));
+  TRY(B.alloc(&Wk.sel_count, 3 * (size_t)W));   // [W] select counters, then [W][2] k_eval_gen item counters
+  Wk.gen_ctr = Wk.sel_count + W;
   Wk.lss = p->lscr_per_walker;
   TRY(B.alloc(&Wk.lscr, Wk.lss * W));
   TRY(B.alloc(&S->d_bad, 1));
@@ -1315,7 +1317,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   cudaStream_t s = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaMemsetAsync(Wk.sc, 0, sizeof(WalkerScalars) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.lscr, 0, sizeof(double) * Wk.lss * W, s));
-  CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * W, s));
+  CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * 3 * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.rs, 0, sizeof(RowState) * (mn + 1) * (size_t)rg * Wk.n_groups, s));
   CUDA_TRY(cudaMemsetAsync(S->d_bad, 0, sizeof(int), s));

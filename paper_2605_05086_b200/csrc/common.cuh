@@ -336,6 +336,7 @@ struct DevWalkers {
   WalkerScalars* sc;                   // [W]
   Cand* part;           int32_t ps;    // [W][ps] one per eval block
   unsigned* sel_count;                 // [W] last-block-done counter of the eval kernel
+  unsigned* gen_ctr;                   // [W][2] k_eval_gen: next item, blocks done (re-armed by the last block)
   double* lscr;         size_t lss;    // [W][lss]
   int32_t use_tabu;
   int32_t W;

@@ -1346,14 +1346,13 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
 // the column's entries. The number of positive steps is the number of violated rows of the
 // column (cutoff row included), a few in a tabu walk.
 //
-// The kernel is a software pipeline per warp over a static round-robin list of warp items (a
-// general tile of <= 32 whole columns and <= kGI entries, or a <= kGI-nonzero chunk of a long
-// column): the CSC range of item i+2 arrives by two bulk copies (TMA, cp.async.bulk, one mbarrier
-// per stage), the row state of every entry of item i+1 and its columns' data by per-lane cp.async
-// gathers into shared memory, while item i is computed from shared memory. No register is held by
-// a load in flight, so a few warps per SM keep ~2 items of gathers outstanding each.
+// Each warp works through a list of warp items (a general tile of <= 32 whole columns and
+// <= kG32Max entries, or a chunk of a long column): its first item is static, the later ones come
+// from a per-walker counter in list order, taken while the current item is evaluated. Within a
+// tile the CSC indices and coefficients of the next round of 128 entries are in flight (registers)
+// while this round's row state is gathered (one 16-byte __ldg per entry, L2-resident).
 // A general tile: phase 1 (slot-parallel) turns every entry's row state into {key << 3 | code, F,
-// β2, α2} in place; phase 2 (lane c = column c) makes one pass for β, α, the nearest candidates and
+// β2, α2} in the warp's shared-memory tile; phase 2 (lane c = column c) makes one pass for β, α, the nearest candidates and
 // the positive steps, then one pass per four candidates. The int path needs weights that are
 // integers <= 2^20 (WalkerScalars::wint; |Σ F| < 2^27) and offsets |d| < 2^28; with other weights
 // the F, β2, α2 words are floats summed in double (same candidates, scores up to summation order,
@@ -2019,18 +2018,39 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
       }
     }
   } else {
+    // one walker: items handed out in list order by a counter (long-column chunks first, then the
+    // tiles), the first item of every warp static; a warp takes its next item while it evaluates the
+    // current one. Several walkers (fewer blocks each): the static round-robin, t += nwarps.
+    const bool dyn = gridDim.y == 1;
+    unsigned* gctr = Wk.gen_ctr + 2 * walker;
+    auto next_item = [&](int t) {
+      if (!dyn) return t + nwarps;
+      unsigned v = 0u;
+      if (lane == 0) v = atomicAdd(gctr, 1u);
+      return ifirst + nwarps + (int)__shfl_sync(kFull, v, 0);
+    };
     int t = t0;
     WTile T;
     if (t < iend) T = P.gitems[t];
-    for (; t < iend; t += nwarps) {
-      const bool has_next = t + nwarps < iend;
+    while (t < iend) {
+      const int tn = next_item(t);
+      const bool has_next = tn < iend;
       WTile Tn;
-      if (has_next) Tn = P.gitems[t + nwarps];
+      if (has_next) Tn = P.gitems[tn];
       run_item(T, Tn, has_next);
       T = Tn;
+      t = tn;
     }
   }
   b = block_reduce_best(b, sm_b);
+  if (!Wk.dirty && gridDim.y == 1 && threadIdx.x == 0) {   // every warp of the block is past its last
+    __threadfence();   // grab: the last block re-arms the walker's item counter for the next launch
+    unsigned* gctr = Wk.gen_ctr + 2 * walker;
+    if (atomicAdd(gctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(gctr, 0u);
+      atomicExch(gctr + 1, 0u);
+    }
+  }
   if (threadIdx.x == 0) write_part(Wk.part + (size_t)walker * Wk.ps + part_base + blockIdx.x, b);
   KT_END(Wk, 1);
   if (select_parts <= 0) return;   // as in k_eval_bin: the last eval kernel selects
