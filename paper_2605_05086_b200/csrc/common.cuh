@@ -77,7 +77,10 @@ struct LongCol {
   int32_t p;         // the column (internal order)
   int32_t kind;      // CC_LBIN or CC_LBKT
 };
-constexpr int kWChunk = 256;                      // nonzeros per warp chunk of a long binary column
+#ifndef CHAP_WCHUNK
+#define CHAP_WCHUNK 256
+#endif
+constexpr int kWChunk = CHAP_WCHUNK;                      // nonzeros per warp chunk of a long binary column
 #ifndef CHAP_BKT_CHUNK
 #define CHAP_BKT_CHUNK 512
 #endif

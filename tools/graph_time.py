@@ -13,16 +13,18 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2605_05086_b200 as chap  # noqa: E402
 
-cfg, _, nw = sys.argv[1].partition(":")
+argv = [a for a in sys.argv[1:] if not a.startswith("--param=")]
+params = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--param=")]   # --param=NAME=VALUE
+cfg, _, nw = argv[0].partition(":")
 W = int(nw) if nw else 1
-iters = int(sys.argv[2])
-rounds = int(sys.argv[3])
+iters = int(argv[1])
+rounds = int(argv[2])
 inst = bench.make_instance(cfg)
 x0 = bench.start_points(inst, cfg, W, 0)
 z = bench.planted_objective(inst)
 orig = chap._lib
 libs = []
-for path in sys.argv[4:]:
+for path in argv[3:]:
     lib = ctypes.CDLL(os.path.abspath(path))
     for name in chap.EXPORTED:
         f = getattr(lib, name)
@@ -40,7 +42,11 @@ for r in range(rounds):
     for path, lib in libs:
         use(lib)
         P = chap.Problem.from_instance(inst)
-        ws = chap.Walkers(P, torch.from_numpy(x0).cuda(), chap.default_params(graph_iters=32))
+        prm = chap.default_params(graph_iters=32)
+        for kv in params:
+            k, v = kv.split("=", 1)
+            setattr(prm, k, type(getattr(prm, k))(float(v)) if isinstance(getattr(prm, k), float) else int(v))
+        ws = chap.Walkers(P, torch.from_numpy(x0).cuda(), prm)
         if z is not None:
             ws.set_cutoff(z)
         ws.timing(1)
