@@ -344,6 +344,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     W.ncols = (int16_t)(r.second - r.first);
     W.kind = (int8_t)CC_GEN;
     for (int32_t q = r.first; q < r.second; ++q) P->gen_kmax = std::max(P->gen_kmax, col_ptr[q + 1] - col_ptr[q]);
+    P->gen_tile_nnz += W.e1 - W.e0;
     wtiles.push_back(W);
   }
   const int32_t n_gtiles = (int32_t)wtiles.size();
@@ -417,6 +418,7 @@ extern "C" chap_status chap_problem_create(int32_t n, int32_t m, int64_t nnz, co
     const int csz = (k == CC_LBKT) ? kBktChunk : kWChunk;
     const int nch = std::max(1, (d + csz - 1) / csz);
     const int dom = (k == CC_LBKT) ? (int)(u[j] - l[j] + 1.0) : 0;
+    if (k == CC_LBKT) P->lbkt_nnz += d;
     for (int q = 0; q < nch; ++q) {
       WTile W{};
       W.p0 = p;
@@ -1244,10 +1246,17 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   S->genwm_grid = 0;   // walker groups: integer general tiles and empty columns per group (k_eval_gen_wm)
   if (rg > 1 && p->dp.n_wtiles > 0) {
     int occ = gen_wm_occupancy(rg, gen_wm_smem_all(std::max(1, p->gen_kmax), Wk.lbkt_wm_words));
-    if (occ == 0 && Wk.lbkt_wm_words > 0) {   // the histograms do not fit: the chunks stay per walker
+    const int occ0 = gen_wm_occupancy(rg, gen_wm_smem_all(std::max(1, p->gen_kmax), 0));
+    // the histograms do not fit, or the long bounded-integer columns hold less than an eighth as
+    // many entries as the general tiles: the chunks stay per walker (k_eval_gen). Measured per
+    // iteration, groups vs per walker: G with 32 walkers (long bounded-integer entries 0.49 of the
+    // tiles') 1.70 vs 2.27 ms; X1e6 with 64 (0.02) 0.63 vs 0.35 ms.
+    if (Wk.lbkt_wm_words > 0 && (occ == 0 || 8 * p->lbkt_nnz < p->gen_tile_nnz)) {
       Wk.lbkt_wm_words = 0;
-      occ = gen_wm_occupancy(rg, gen_wm_smem_all(std::max(1, p->gen_kmax), 0));
+      occ = occ0;
     }
+    // (the kernel's shared-memory attribute is left at the size the launches use)
+    gen_wm_occupancy(rg, gen_wm_smem_all(std::max(1, p->gen_kmax), Wk.lbkt_wm_words));
     if (occ > 0) {
       const int warps = kGenWmThreads / 32;
       S->genwm_grid = std::max(1, std::min((p->dp.n_wtiles + warps - 1) / warps,

@@ -98,6 +98,8 @@ struct chap_problem {
   int binrow_grid = 0;         // k_eval_binrow CTAs (clusters x kRowCluster; 0: no row-wise blocks)
   bool binrow_auto = false;    // the size rule chooses the row-wise binary kernel (chap_params.binary_kernel 0)
   int gen_kmax = 0;            // longest packed general column (entries incl. padding)
+  int64_t gen_tile_nnz = 0;     // entries of the packed general tiles
+  int64_t lbkt_nnz = 0;         // entries of the long bounded-integer columns
   int binrow_maxdeg = 0;       // longest packed binary column (incl. its cutoff entry)
   int binrow_cluster = 0;      // CTAs per cluster of k_eval_binrow
   int binrow_pb0 = 0, binrow_nbin = 0;   // the packed binary columns [pb0, pb0 + nbin)
