@@ -32,6 +32,9 @@ import synth  # noqa: E402
 
 METRIC = "best-shift move evaluations/sec and tabu iterations/sec; % of HBM roofline"
 UNIT = "move_evals/s"
+# kernels of one epoch's tail (chap_walkers_epoch): the incumbent flush (2) and the device exchange
+# (summaries, plan, packing, cutoff, restart batch: 14 with elite points and the bitset kept)
+EXCHANGE_KERNELS = 16
 
 CONFIGS = {
     "G": dict(desc="G: synthetic mixed general-integer MIP 200k rows x 1M vars, ~10.4M nnz, 100 long columns "
@@ -354,6 +357,8 @@ def main():
             dist.barrier()
 
     ws.step(args.warmup)
+    if args.steps > K_x:   # the epoch graph (exchange_K iterations + the exchange) is captured here,
+        ws.epoch(K_x, comm)   # untimed, like the iteration graphs
     torch.cuda.synchronize()
     ws.timing(1)   # zero the sums: they cover exactly the timed region
     barrier()
@@ -364,13 +369,14 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         done = n_exchanges = 0
-        while done < args.steps:   # epochs of exchange_K tabu iterations with the exchange between
-            k = min(K_x, args.steps - done)
-            ws.step(k)
-            done += k
-            if done < args.steps:
-                ws.exchange(comm)
+        while done < args.steps:   # epochs of exchange_K tabu iterations with the exchange between:
+            k = min(K_x, args.steps - done)   # each one CUDA graph (iterations + device exchange)
+            if done + k < args.steps:
+                ws.epoch(k, comm)
                 n_exchanges += 1
+            else:
+                ws.step(k)
+            done += k
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -496,7 +502,7 @@ def main():
                 # nonzeros visited per second (every nonzero incl. cutoff-row entries, per walker)
                 "nnz_visits_per_s": float(info.nnz_norm + info.nnz_cut) * W * args.steps * world / sec,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_iter * args.steps + 4 + 2 * n_exchanges,
+                "gpu_launches": launches_per_iter * args.steps + 4 + EXCHANGE_KERNELS * n_exchanges,
                 "clocks": clk.summary(),
                 "walker": {"moves": int(st["n_moves"].sum()), "stuck": int(st["n_stuck"].sum()),
                            "has_incumbent": int(st["has_incumbent"].sum()),

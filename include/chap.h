@@ -381,14 +381,25 @@ chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, const chap_walk
                                int32_t* restart_gid, int32_t* restart_src);
 
 /* One portfolio exchange on existing walkers, the step chap_run_walkers runs every
- * exchange_K iterations: per-walker summaries are all-gathered (NCCL when comm is non-NULL),
- * chap_exchange_plan picks the elite, their points are all-gathered, every walker's cutoff is
- * tightened to the best incumbent and the planned local walkers restart from elite
- * points (weights kept, tabu cleared). The best incumbent seen by any exchange of these walkers
- * persists across calls: z_best HOST [1] and z_walker HOST [1] (global walker id, -1 if none) may
- * be NULL. Every rank must call it the same number of times. Synchronises the stream. */
+ * exchange_K iterations: per-walker summaries are all-gathered (NCCL when comm is non-NULL), the
+ * plan of chap_exchange_plan is computed on the device, the elite points are all-gathered, every
+ * walker's cutoff is tightened to the best incumbent and the planned local walkers
+ * restart from elite points (weights kept, tabu cleared), all stream-ordered on cuda_stream. The best
+ * incumbent of the gathered walkers: z_best HOST [1] and z_walker HOST [1] (global walker id, -1 if
+ * none); when either is non-NULL the call synchronises the stream to return them, when both are
+ * NULL it does not. Every rank must call it the same number of times. */
 chap_status chap_walkers_exchange(chap_walkers* ws, chap_comm* comm, double* z_best, int32_t* z_walker,
                                   void* cuda_stream);
+
+/* One epoch of the portfolio: n_iters tabu iterations of
+ * every walker (chap_tabu_step) followed by one chap_walkers_exchange, launched as ONE CUDA graph:
+ * captured on the first call for a given (n_iters, comm) and replayed by later calls, so an epoch
+ * costs one graph launch and no host round trip. Same results as chap_tabu_step(n_iters) followed
+ * by chap_walkers_exchange. z_best / z_walker as for chap_walkers_exchange (NULL: no
+ * synchronisation). Errors: CHAP_ERR_INVALID_ARG (NULL walkers, n_iters < 1, n_elite < 0, comm on
+ * another device), CHAP_ERR_CUDA / CHAP_ERR_NCCL from the capture or the launch. */
+chap_status chap_walkers_epoch(chap_walkers* ws, chap_comm* comm, int32_t n_iters, double* z_best,
+                               int32_t* z_walker, void* cuda_stream);
 
 /* The portfolio loop: W_local walkers from x0 DEVICE [W_local][n] (global
  * walker id = rank*W_local + w), epochs of params.exchange_K iterations; after each epoch an

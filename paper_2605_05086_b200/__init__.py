@@ -110,6 +110,7 @@ _SIGS = {
     "chap_walkers_timing": (ctypes.c_int, [_P, c_i32, _P, _P]),
     "chap_walkers_launches_per_iter": (ctypes.c_int, [_P, _P]),
     "chap_walkers_exchange": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "chap_walkers_epoch": (ctypes.c_int, [_P, _P, c_i32, _P, _P, _P]),
     "chap_comm_unique_id": (ctypes.c_int, [_P]),
     "chap_comm_create": (ctypes.c_int, [_P, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "chap_comm_destroy": (ctypes.c_int, [_P]),
@@ -307,13 +308,25 @@ class Walkers:
         _check(chap_walkers_timing(self.h, int(mode), out.ctypes.data, _stream(stream)))
         return out
 
-    def exchange(self, comm: Optional["Comm"] = None, stream=None):
-        """chap_walkers_exchange: one portfolio exchange; returns (best objective, its global walker id)."""
+    def exchange(self, comm: Optional["Comm"] = None, result: bool = True, stream=None):
+        """chap_walkers_exchange: one portfolio exchange (on the device); with result=True returns (best
+        objective, its global walker id) (synchronising), else None (stream-ordered, no sync)."""
         z = ctypes.c_double()
         g = ctypes.c_int32()
-        _check(chap_walkers_exchange(self.h, comm.h if comm is not None else None, ctypes.addressof(z),
-                                     ctypes.addressof(g), _stream(stream)))
-        return z.value, g.value
+        _check(chap_walkers_exchange(self.h, comm.h if comm is not None else None,
+                                     ctypes.addressof(z) if result else None, ctypes.addressof(g) if result else None,
+                                     _stream(stream)))
+        return (z.value, g.value) if result else None
+
+    def epoch(self, n_iters: int, comm: Optional["Comm"] = None, result: bool = False, stream=None):
+        """chap_walkers_epoch: n_iters tabu iterations + one exchange as one CUDA graph; with result=True
+        returns (best objective, its global walker id) (synchronising), else None."""
+        z = ctypes.c_double()
+        g = ctypes.c_int32()
+        _check(chap_walkers_epoch(self.h, comm.h if comm is not None else None, int(n_iters),
+                                  ctypes.addressof(z) if result else None, ctypes.addressof(g) if result else None,
+                                  _stream(stream)))
+        return (z.value, g.value) if result else None
 
     def set_cutoff(self, z_best: float, stream=None):
         _check(chap_walkers_set_cutoff(self.h, float(z_best), _stream(stream)))

@@ -1009,6 +1009,7 @@ static DevWalkers eval_walkers(const chap_problem* P) {
   Wk.ps = P->eval_grid + P->bin_grid + P->gen_grid;
   Wk.sel_count = P->e_selcnt;
   Wk.gen_ctr = P->e_selcnt + 1;
+  Wk.rmask = nullptr;
   Wk.lscr = P->e_lscr;
   Wk.lss = P->lscr_per_walker;
   Wk.use_tabu = 0;
@@ -1028,9 +1029,9 @@ int chap::grid_for(long long work, int threads, int cap) {
 // kept, and the violated count: the state k_walker_finalize_init completes.
 chap_status chap::walker_recompute(const chap_problem* P, DevWalkers& Wk, int w, cudaStream_t s) {
   const DevProblem& D = P->dp;
-  k_acc_zero<<<1, 1, 0, s>>>(Wk.sc, w);
+  k_acc_zero<<<1, 1, 0, s>>>(Wk.sc, w, nullptr);
   if (D.n > 0)
-    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, w);
+    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, w, nullptr);
   k_rows_init<<<dim3(P->rows_grid, 1), 256, 0, s>>>(D, Wk, 0, nullptr, w, nullptr);
   k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * P->sm_count), 1), 256, 0, s>>>(D, Wk, w);
   if (Wk.xbits && D.n > 0) k_xbits_build<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(D, Wk, w);
@@ -1049,7 +1050,7 @@ static chap_status eval_launch(const chap_problem* p, const double* x, const flo
   k_eval_scalars<<<1, 1, 0, s>>>(p->e_sc, cutoff_rhs, p->dp.rint_base);
   if (D.n > 0) k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), 1), 256, 0, s>>>(D, x, D.n, p->e_x, D.n, p->e_bad);
   if (cutoff_rhs < INFINITY && D.n > 0)
-    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1);
+    k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), 1), 256, 0, s>>>(D, p->e_x, D.n, p->e_sc, -1, nullptr);
   k_rows_init<<<dim3(p->rows_grid, 1), 256, 0, s>>>(D, Wk, 2, w, 0, p->e_bad);
   CUDA_TRY(cudaGetLastError());
   if (D.n_fixed > 0 && (xhat || score))
@@ -1273,6 +1274,11 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   Wk.lss = p->lscr_per_walker;
   TRY(B.alloc(&Wk.lscr, Wk.lss * W));
   TRY(B.alloc(&S->d_bad, 1));
+  {
+    int32_t* rm = nullptr;   // the device exchange's restart slots (portfolio.cuh)
+    TRY(B.alloc(&rm, W));
+    Wk.rmask = rm;
+  }
   Wk.asp = nullptr;
   if (prm.aspiration && prm.tenure > 0) TRY(B.alloc(&Wk.asp, (size_t)prm.tenure * W));   // R18 slots
   Wk.cs = Wk.cv = nullptr;
@@ -1325,6 +1331,7 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   CUDA_TRY(cudaEventCreateWithFlags(&S->ev_out, cudaEventDisableTiming));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaMemsetAsync(Wk.sc, 0, sizeof(WalkerScalars) * W, s));
+  CUDA_TRY(cudaMemsetAsync(const_cast<int32_t*>(Wk.rmask), 0xff, sizeof(int32_t) * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.lscr, 0, sizeof(double) * Wk.lss * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.sel_count, 0, sizeof(unsigned) * 3 * W, s));
   CUDA_TRY(cudaMemsetAsync(Wk.best_x, 0, sizeof(double) * n * W, s));
@@ -1333,17 +1340,17 @@ extern "C" chap_status chap_walkers_create(const chap_problem* p, int32_t W, con
   if (Wk.asp) CUDA_TRY(cudaMemsetAsync(Wk.asp, 0xff, sizeof(Cand) * (size_t)prm.tenure * W, s));   // p = -1
   if (Wk.dirty) {
     CUDA_TRY(cudaMemsetAsync(Wk.dirty, 0, sizeof(uint32_t) * 2 * ((size_t)Wk.dwords + 1), s));
-    k_dirty_all<<<1, 32, 0, s>>>(Wk);
+    k_dirty_all<<<1, 32, 0, s>>>(Wk, -1);
   }
   if (D.n > 0)
     k_permute_in<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, x0, D.n, Wk.x, Wk.xs, S->d_bad);
-  k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1);
-  if (D.n > 0) k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, -1);
+  k_acc_zero<<<W, 1, 0, s>>>(Wk.sc, -1, nullptr);
+  if (D.n > 0) k_cut_dot<<<dim3(grid_for(D.n, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, -1, nullptr);
   k_rows_init<<<dim3(p->rows_grid, W), 256, 0, s>>>(D, Wk, 1, nullptr, -1, nullptr);
   k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * p->sm_count), W), 256, 0, s>>>(D, Wk, -1);
   if (Wk.xbits && D.n > 0)
     k_xbits_build<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), Wk.n_groups), 256, 0, s>>>(D, Wk, -1);
-  k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, -1);
+  k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, -1, nullptr);
   k_walker_finalize_init<<<W, 1, 0, s>>>(D, Wk, 0, -1);
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * p->sm_count), W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(W + 255) / 256, 256, 0, s>>>(Wk);
@@ -1368,11 +1375,15 @@ static chap_status launch_iteration(chap_walkers* S, cudaStream_t s) {
 }
 
 // Capture `iters` tabu iterations of the walkers as one instantiated CUDA graph.
-static chap_status capture_iterations(chap_walkers* S, cudaStream_t s, int iters, cudaGraphExec_t* out) {
+// A graph of `iters` tabu iterations followed by whatever `tail` launches (chap_walkers_epoch: the
+// device exchange), instantiated into *out.
+template <class Tail>
+static chap_status capture_graph(chap_walkers* S, cudaStream_t s, int iters, Tail tail, cudaGraphExec_t* out) {
   cudaGraph_t graph;
   CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   chap_status st = CHAP_OK;
   for (int it = 0; it < iters && st == CHAP_OK; ++it) st = launch_iteration(S, s);
+  if (st == CHAP_OK) st = tail(s);
   cudaError_t ce = cudaStreamEndCapture(s, &graph);
   if (st != CHAP_OK) return st;
   if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
@@ -1394,6 +1405,9 @@ static chap_status capture_iterations(chap_walkers* S, cudaStream_t s, int iters
   cudaGraphDestroy(graph);
   if (ce != cudaSuccess) return fail(CHAP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
   return CHAP_OK;
+}
+static chap_status capture_iterations(chap_walkers* S, cudaStream_t s, int iters, cudaGraphExec_t* out) {
+  return capture_graph(S, s, iters, [](cudaStream_t) { return CHAP_OK; }, out);
 }
 
 extern "C" chap_status chap_tabu_step(chap_walkers* S, int32_t n_iters, chap_step_record* log,
@@ -1466,7 +1480,7 @@ extern "C" chap_status chap_walkers_set_cutoff(chap_walkers* S, double z_best, v
   if (!S || !std::isfinite(z_best)) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or non-finite z_best");
   DeviceGuard g(S->P->device);
   k_set_cutoff<<<(S->W + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>(S->P->dp, S->wk, z_best);
-  if (S->wk.dirty) k_dirty_all<<<1, 32, 0, (cudaStream_t)cuda_stream>>>(S->wk);   // f2: the cutoff row moved
+  if (S->wk.dirty) k_dirty_all<<<1, 32, 0, (cudaStream_t)cuda_stream>>>(S->wk, -1);   // f2: the cutoff row moved
   CUDA_TRY(cudaGetLastError());
   return CHAP_OK;
 }
@@ -1491,9 +1505,9 @@ extern "C" chap_status chap_walkers_restart(chap_walkers* S, int32_t walker, con
   if (bad) return fail(CHAP_ERR_INVALID_ARG, "restart point out of bounds or fractional on an integer variable");
   if (D.n > 0) k_permute_in<<<dim3(gx, 1), 256, 0, s>>>(D, x, D.n, Wk.x + (size_t)walker * Wk.xs, Wk.xs, nullptr);
   TRY(chap::walker_recompute(S->P, Wk, walker, s));
-  k_tabu_clear<<<dim3(gx, 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, walker);
+  k_tabu_clear<<<dim3(gx, 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, walker, nullptr);
   k_walker_finalize_init<<<1, 1, 0, s>>>(D, Wk, 1, walker);
-  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk);   // f2: a new point
+  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk, -1);   // f2: a new point
   k_flush_incumbent<<<dim3(gx, S->W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());

@@ -270,6 +270,10 @@ __device__ __forceinline__ void pdl_wait_trigger() {
 
 #define KT_BEGIN(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMin((WK).kt + 2 * (q), chap::kt_now()); } while (0)
 #define KT_END(WK, q) do { if ((WK).kt && threadIdx.x == 0) atomicMax((WK).kt + 2 * (q) + 1, chap::kt_now()); } while (0)
+constexpr int kRestartSet = -2;   // only_walker: every walker w with DevWalkers::rmask[w] >= 0 (blockIdx)
+__device__ __forceinline__ bool skip_walker(const int32_t* rmask, int only_walker, int w) {
+  return only_walker == kRestartSet && rmask[w] < 0;
+}
 constexpr int kKtWords = 16;   // [2q, 2q+1] start/end of kernel q (0 bin, 1 gen, 2 eval, 3 apply); [8..13] sums
 
 // Everything the kernels need about the immutable problem (internal variable order).
@@ -340,6 +344,9 @@ struct DevWalkers {
   Cand* part;           int32_t ps;    // [W][ps] one per eval block
   unsigned* sel_count;                 // [W] last-block-done counter of the eval kernel
   unsigned* gen_ctr;                   // [W][2] k_eval_gen: next item, blocks done (re-armed by the last block)
+  const int32_t* rmask;                // [W] device exchange: the restart source slot of each walker (-1: none);
+                                       // the restart kernels launched with only_walker = kRestartSet skip
+                                       // the walkers without one
   double* lscr;         size_t lss;    // [W][lss]
   int32_t use_tabu;
   int32_t W;

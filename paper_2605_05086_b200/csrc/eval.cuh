@@ -2402,7 +2402,8 @@ __global__ void __launch_bounds__(kTileThreads) k_select_cache(DevProblem P, Dev
 }
 
 // f2: every column of both dirty sets (walker create, restart, an external cutoff).
-__global__ void k_dirty_all(DevWalkers Wk) {
+__global__ void k_dirty_all(DevWalkers Wk, int only_walker) {
+  if (skip_walker(Wk.rmask, only_walker, 0)) return;   // (selective re-evaluation runs one walker)
   if (Wk.dirty && threadIdx.x < 2) Wk.dirty[(size_t)threadIdx.x * (Wk.dwords + 1) + Wk.dwords] = 1u;
 }
 

@@ -156,6 +156,9 @@ struct chap_walkers {
   int g_iters = 0;
   cudaGraphExec_t gexec_rem = nullptr;  // graph of g_rem iterations (the remainder of a call)
   int g_rem = 0;
+  cudaGraphExec_t gexec_ep = nullptr;   // graph of one epoch: ep_iters iterations + the device exchange
+  int ep_iters = 0;
+  const void* ep_comm = nullptr;        // (the communicator the epoch graph was captured with)
   int apply_grid = 1;
   int eval_grid = 1;           // k_eval blocks per walker
   int bin_grid = 0;            // k_eval_bin blocks per walker
@@ -171,6 +174,7 @@ struct chap_walkers {
     if (xs) chap_exchange_state_free(xs);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (gexec_rem) cudaGraphExecDestroy(gexec_rem);
+    if (gexec_ep) cudaGraphExecDestroy(gexec_ep);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (stream) cudaStreamDestroy(stream);

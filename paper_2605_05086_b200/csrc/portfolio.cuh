@@ -173,6 +173,86 @@ extern "C" chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, cons
 }
 
 // ------------------------------------------------------------------------------------------
+// the exchange on the device (no host round trip: capturable into the epoch graph)
+// ------------------------------------------------------------------------------------------
+namespace chap {
+// The plan of chap_exchange_plan computed by one block from the gathered summaries, by rank
+// counting (O(W_total^2) comparisons, W_total <= a few thousand): the rank of walker g among the
+// feasible walkers by (best_obj, gid), among all by (violated, sumviol, gid), the same within its
+// rank's own walkers, and its restart rank by (violated, gid) descending. Outputs (device):
+//   z[0]: the best incumbent objective (+INF: none); ip[0]: its gid (-1), ip[1]: |E|, ip[2]: restarts;
+//   elite_gid / elite_slot [2 E] (feasible elite first); local_rank [2][W_local]: this rank's walkers'
+//   positions among its own top-E of each kind (-1: not sent); restart_gid / restart_src [W_total];
+//   rmask [W_local]: the gathered-buffer slot each local walker restarts from (-1: none).
+__global__ void __launch_bounds__(1024) k_exchange_plan(const chap_walker_summary* __restrict__ s, int W, int W_local,
+                                                        int rank, int E, int n_restart, double* z, int32_t* ip,
+                                                        int32_t* elite_gid, int32_t* elite_slot, int32_t* local_rank,
+                                                        int32_t* restart_gid, int32_t* restart_src, int32_t* rmask) {
+  __shared__ int s_nfeas;
+  if (threadIdx.x == 0) s_nfeas = 0;
+  __syncthreads();
+  for (int g = threadIdx.x; g < W; g += blockDim.x)
+    if (s[g].flags & 1) atomicAdd(&s_nfeas, 1);
+  if (threadIdx.x == 0) { *z = INFINITY; ip[0] = -1; }
+  __syncthreads();
+  const int nf = min(s_nfeas, E), ni = min(W, E), ne = nf + ni;
+  const int nr = ne > 0 ? min(n_restart, W) : 0;
+  auto feas_less = [&](int h, int g) {   // (best_obj, gid)
+    return s[h].best_obj < s[g].best_obj || (s[h].best_obj == s[g].best_obj && h < g);
+  };
+  auto inf_less = [&](int h, int g) {    // (violated, sumviol, gid)
+    if (s[h].violated != s[g].violated) return s[h].violated < s[g].violated;
+    if (s[h].sumviol != s[g].sumviol) return s[h].sumviol < s[g].sumviol;
+    return h < g;
+  };
+  for (int g = threadIdx.x; g < W; g += blockDim.x) {
+    const bool fe = s[g].flags & 1;
+    const int r = g / W_local, lo = r * W_local, hi = lo + W_local;
+    int fr = 0, lfr = 0, ir = 0, lir = 0, rr = 0;
+    for (int h = 0; h < W; ++h) {
+      const bool loc = h >= lo && h < hi;
+      if (fe && (s[h].flags & 1) && feas_less(h, g)) { ++fr; lfr += loc; }
+      if (inf_less(h, g)) { ++ir; lir += loc; }
+      if (s[h].violated > s[g].violated || (s[h].violated == s[g].violated && h > g)) ++rr;
+    }
+    if (fe && fr == 0) { *z = s[g].best_obj; ip[0] = g; }
+    if (fe && fr < nf) { elite_gid[fr] = g; elite_slot[fr] = r * 2 * E + lfr; }
+    if (ir < ni) { elite_gid[nf + ir] = g; elite_slot[nf + ir] = r * 2 * E + E + lir; }
+    if (r == rank) {
+      local_rank[g - lo] = (fe && lfr < E) ? lfr : -1;
+      local_rank[W_local + g - lo] = lir < E ? lir : -1;
+      rmask[g - lo] = -1;
+    }
+    if (rr < nr) { restart_gid[rr] = g; restart_src[rr] = rr % ne; }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nr; q += blockDim.x) {
+    const int g = restart_gid[q];
+    if (g / W_local == rank) rmask[g % W_local] = elite_slot[restart_src[q]];
+  }
+  if (threadIdx.x == 0) { ip[1] = ne; ip[2] = nr; }
+}
+
+// Pack the points this rank sends: walker w's best point (kind 0) or current point (kind 1) into
+// slot kind E + local_rank[kind][w] of the send buffer; blockIdx = (part, w, kind).
+__global__ void k_pack_tops(DevProblem P, DevWalkers Wk, const int32_t* __restrict__ local_rank, int W_local, int E,
+                            unsigned char* send) {
+  const int w = blockIdx.y, kind = blockIdx.z;
+  const int q = local_rank[kind * W_local + w];
+  if (q < 0) return;
+  pack_point(P, (kind == 0 ? Wk.best_x : Wk.x) + (size_t)w * Wk.xs, send + (size_t)(kind * E + q) * P.pk_bytes);
+}
+
+// The restarting walkers' new points from the gathered buffer (rmask: slot); blockIdx = (part, w).
+__global__ void k_unpack_restarts(DevProblem P, DevWalkers Wk, const unsigned char* __restrict__ recv) {
+  const int w = blockIdx.y;
+  const int slot = Wk.rmask[w];
+  if (slot < 0) return;
+  unpack_point(P, recv + (size_t)slot * P.pk_bytes, Wk.x + (size_t)w * Wk.xs);
+}
+}  // namespace chap
+
+// ------------------------------------------------------------------------------------------
 // chap_run_walkers
 // ------------------------------------------------------------------------------------------
 
@@ -184,9 +264,9 @@ static chap_status restart_internal(chap_walkers* S, int w, const double* x_int,
   DevWalkers& Wk = S->wk;
   CUDA_TRY(cudaMemcpyAsync(Wk.x + (size_t)w * Wk.xs, x_int, sizeof(double) * D.n, cudaMemcpyDeviceToDevice, s));
   TRY(chap::walker_recompute(P, Wk, w, s));
-  k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, w);
+  k_tabu_clear<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), 1), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, w, nullptr);
   k_walker_finalize_init<<<1, 1, 0, s>>>(D, Wk, 1, w);
-  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk);   // f2: a new point
+  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk, -1);   // f2: a new point
   k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * P->sm_count), S->W), 256, 0, s>>>(D, Wk);
   k_flush_done<<<(S->W + 255) / 256, 256, 0, s>>>(Wk);
   CUDA_TRY(cudaGetLastError());
@@ -205,25 +285,26 @@ struct chap_exchange_state {
   std::vector<int8_t> e_kind;
   double z = INFINITY;   // best incumbent objective seen by any exchange (persists)
   int32_t zg = -1;       // its global walker id
+  // the device exchange's plan (k_exchange_plan)
+  double* d_z = nullptr;                                // [1]
+  int32_t *d_ip = nullptr, *d_egid = nullptr, *d_eslot = nullptr, *d_lrank = nullptr, *d_rgid = nullptr,
+          *d_rsrc = nullptr;
 };
 
 void chap_exchange_state_free(chap_exchange_state* x) { delete x; }
 
-// One portfolio exchange (DESIGN §7): summaries -> allgather -> plan -> elite points -> allgather ->
-// cutoff -> restarts. want_stop marks this rank's summaries; *stop = any rank marked. With
-// need_points = false and *stop set, the point exchange is skipped.
-static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want_stop, bool need_points,
-                                     bool* stop, cudaStream_t s) {
+// The exchange buffers of a walkers object for a communicator size ((re)allocated when it changes;
+// z and zg persist). Called before any capture of the device exchange.
+static chap_status exchange_prepare(chap_walkers* S, chap_comm* comm) {
   const chap_problem* p = S->P;
-  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  const int nranks = comm ? comm->nranks : 1;
   const int W_local = S->W, W_total = nranks * W_local;
-  const chap_params& prm = S->prm;
-  const int n_restart = prm.n_restart < 0 ? W_total / 8 : prm.n_restart;
-  const int E = prm.n_elite;
+  const int E = S->prm.n_elite;
   const int n = p->dp.n;
   if (!S->xs) S->xs = new chap_exchange_state();
   chap_exchange_state& X = *S->xs;
-  if (X.nranks != nranks) {   // (re)allocate for this communicator size; z and zg persist
+  if (X.nranks == nranks) return CHAP_OK;
+  {
     X.buf = DeviceBuffers();
     X.nranks = nranks;
     TRY(X.buf.alloc(&X.d_sum_local, W_local));
@@ -238,7 +319,31 @@ static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want
     X.e_kind.resize(2 * E + 1);
     X.r_gid.resize(W_total + 1);
     X.r_src.resize(W_total + 1);
+    TRY(X.buf.alloc(&X.d_z, 1));
+    TRY(X.buf.alloc(&X.d_ip, 4));
+    TRY(X.buf.alloc(&X.d_egid, 2 * (size_t)std::max(E, 1)));
+    TRY(X.buf.alloc(&X.d_eslot, 2 * (size_t)std::max(E, 1)));
+    TRY(X.buf.alloc(&X.d_lrank, 2 * (size_t)W_local));
+    TRY(X.buf.alloc(&X.d_rgid, (size_t)W_total));
+    TRY(X.buf.alloc(&X.d_rsrc, (size_t)W_total));
   }
+  return CHAP_OK;
+}
+
+// One portfolio exchange (DESIGN §7): summaries -> allgather -> plan -> elite points -> allgather ->
+// cutoff -> restarts. want_stop marks this rank's summaries; *stop = any rank marked. With
+// need_points = false and *stop set, the point exchange is skipped.
+static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want_stop, bool need_points,
+                                     bool* stop, cudaStream_t s) {
+  const chap_problem* p = S->P;
+  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  const int W_local = S->W, W_total = nranks * W_local;
+  const chap_params& prm = S->prm;
+  const int n_restart = prm.n_restart < 0 ? W_total / 8 : prm.n_restart;
+  const int E = prm.n_elite;
+  const int n = p->dp.n;
+  TRY(exchange_prepare(S, comm));
+  chap_exchange_state& X = *S->xs;
   const DevWalkers& Wk = S->wk;
   // 1. summaries -> allgather
   k_summaries<<<W_local, 256, 0, s>>>(p->dp, Wk, X.d_sum_local, rank * W_local, want_stop ? 1 : 0);
@@ -297,17 +402,119 @@ static chap_status exchange_internal(chap_walkers* S, chap_comm* comm, bool want
   return CHAP_OK;
 }
 
+// The same exchange (without the stop vote) entirely on the device: summaries, their allgather,
+// k_exchange_plan, the local elite packed and all-gathered, the cutoff from the plan's z, and the
+// planned restarts as one batch (the restart kernels over the walkers rmask marks). Identical in
+// effect to exchange_internal; no host synchronisation, so it can be captured into a graph.
+static chap_status exchange_device(chap_walkers* S, chap_comm* comm, cudaStream_t s) {
+  const chap_problem* p = S->P;
+  const DevProblem& D = p->dp;
+  const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+  const int W_local = S->W, W_total = nranks * W_local;
+  const chap_params& prm = S->prm;
+  const int n_restart = prm.n_restart < 0 ? W_total / 8 : prm.n_restart;
+  const int E = prm.n_elite;
+  chap_exchange_state& X = *S->xs;
+  const DevWalkers& Wk = S->wk;
+  k_summaries<<<W_local, 256, 0, s>>>(D, Wk, X.d_sum_local, rank * W_local, 0);
+  CUDA_TRY(cudaGetLastError());
+  if (comm) {
+    NCCL_TRY(nccl().AllGather(X.d_sum_local, X.d_sum_all, sizeof(chap_walker_summary) * W_local, ncclUint8, comm->comm, s));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(X.d_sum_all, X.d_sum_local, sizeof(chap_walker_summary) * W_local, cudaMemcpyDeviceToDevice, s));
+  }
+  k_exchange_plan<<<1, 1024, 0, s>>>(X.d_sum_all, W_total, W_local, rank, E, n_restart, X.d_z, X.d_ip, X.d_egid,
+                                     X.d_eslot, X.d_lrank, X.d_rgid, X.d_rsrc, const_cast<int32_t*>(Wk.rmask));
+  CUDA_TRY(cudaGetLastError());
+  const int gx = grid_for(D.n, 256, 2 * p->sm_count);
+  if (E > 0) {
+    k_pack_tops<<<dim3(gx, W_local, 2), 256, 0, s>>>(D, Wk, X.d_lrank, W_local, E, X.d_send);
+    CUDA_TRY(cudaGetLastError());
+    const size_t bytes = (size_t)2 * E * D.pk_bytes;
+    if (comm) {
+      NCCL_TRY(nccl().AllGather(X.d_send, X.d_recv, bytes, ncclUint8, comm->comm, s));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(X.d_recv, X.d_send, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  k_set_cutoff_from<<<(W_local + 255) / 256, 256, 0, s>>>(D, Wk, X.d_z);
+  if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk, -1);   // f2: the cutoff row moved
+  if (E > 0) {   // the restarts (none without an elite): rmask marks the walkers and their slots
+    const int gx4 = grid_for(D.n, 256, 4 * p->sm_count);
+    k_unpack_restarts<<<dim3(gx, W_local), 256, 0, s>>>(D, Wk, X.d_recv);
+    k_acc_zero<<<W_local, 1, 0, s>>>(Wk.sc, kRestartSet, Wk.rmask);
+    if (D.n > 0) k_cut_dot<<<dim3(gx, W_local), 256, 0, s>>>(D, Wk.x, Wk.xs, Wk.sc, kRestartSet, Wk.rmask);
+    k_rows_init<<<dim3(p->rows_grid, W_local), 256, 0, s>>>(D, Wk, 0, nullptr, kRestartSet, nullptr);
+    k_viol_count<<<dim3(grid_for(D.m_norm, 256, 2 * p->sm_count), W_local), 256, 0, s>>>(D, Wk, kRestartSet);
+    if (Wk.xbits && D.n > 0) k_xbits_build<<<dim3(gx4, Wk.n_groups), 256, 0, s>>>(D, Wk, kRestartSet);
+    k_tabu_clear<<<dim3(gx4, W_local), 256, 0, s>>>(Wk.tabu, Wk.ts, D.n, kRestartSet, Wk.rmask);
+    k_walker_finalize_init<<<W_local, 1, 0, s>>>(D, Wk, 1, kRestartSet);
+    if (Wk.dirty) k_dirty_all<<<1, 32, 0, s>>>(Wk, kRestartSet);   // f2: a new point
+    k_flush_incumbent<<<dim3(gx4, W_local), 256, 0, s>>>(D, Wk);
+    k_flush_done<<<(W_local + 255) / 256, 256, 0, s>>>(Wk);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
+// The persistent best incumbent of the device exchanges to the host (synchronises s; nothing to do
+// when both outputs are NULL).
+static chap_status exchange_result(chap_walkers* S, double* z_best, int32_t* z_walker, cudaStream_t s) {
+  if (!z_best && !z_walker) return CHAP_OK;
+  chap_exchange_state& X = *S->xs;
+  double z = INFINITY;
+  int32_t zg = -1;
+  CUDA_TRY(cudaMemcpyAsync(&z, X.d_z, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(&zg, X.d_ip, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  X.z = z;
+  X.zg = zg;
+  if (z_best) *z_best = z;
+  if (z_walker) *z_walker = zg;
+  return CHAP_OK;
+}
+
 extern "C" chap_status chap_walkers_exchange(chap_walkers* S, chap_comm* comm, double* z_best,
                                              int32_t* z_walker, void* cuda_stream) {
   if (!S) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers");
   if (S->prm.exchange_K < 1 || S->prm.n_elite < 0) return fail(CHAP_ERR_INVALID_ARG, "n_elite < 0");
   if (comm && comm->device != S->P->device) return fail(CHAP_ERR_INVALID_ARG, "comm and walkers on different devices");
   DeviceGuard g(S->P->device);
-  bool stop = false;
-  TRY(exchange_internal(S, comm, false, false, &stop, (cudaStream_t)cuda_stream));
-  if (z_best) *z_best = S->xs->z;
-  if (z_walker) *z_walker = S->xs->zg;
-  return CHAP_OK;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  TRY(exchange_prepare(S, comm));
+  TRY(exchange_device(S, comm, s));
+  return exchange_result(S, z_best, z_walker, s);
+}
+
+extern "C" chap_status chap_walkers_epoch(chap_walkers* S, chap_comm* comm, int32_t n_iters, double* z_best,
+                                          int32_t* z_walker, void* cuda_stream) {
+  if (!S || n_iters < 1) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or n_iters < 1");
+  if (S->prm.exchange_K < 1 || S->prm.n_elite < 0) return fail(CHAP_ERR_INVALID_ARG, "n_elite < 0");
+  if (comm && comm->device != S->P->device) return fail(CHAP_ERR_INVALID_ARG, "comm and walkers on different devices");
+  DeviceGuard g(S->P->device);
+  cudaStream_t us = (cudaStream_t)cuda_stream;
+  cudaStream_t s = S->stream;
+  TRY(exchange_prepare(S, comm));
+  if (S->gexec_ep && (S->ep_iters != n_iters || S->ep_comm != (const void*)comm)) {
+    cudaGraphExecDestroy(S->gexec_ep);
+    S->gexec_ep = nullptr;
+  }
+  CUDA_TRY(cudaEventRecord(S->ev_in, us));
+  CUDA_TRY(cudaStreamWaitEvent(s, S->ev_in, 0));
+  if (!S->gexec_ep) {
+    TRY(capture_graph(S, s, n_iters, [&](cudaStream_t cs) -> chap_status {
+      const DevProblem& D = S->P->dp;
+      k_flush_incumbent<<<dim3(grid_for(D.n, 256, 4 * S->P->sm_count), S->W), 256, 0, cs>>>(D, S->wk);
+      k_flush_done<<<(S->W + 255) / 256, 256, 0, cs>>>(S->wk);
+      return exchange_device(S, comm, cs);
+    }, &S->gexec_ep));
+    S->ep_iters = n_iters;
+    S->ep_comm = comm;
+  }
+  CUDA_TRY(cudaGraphLaunch(S->gexec_ep, s));
+  CUDA_TRY(cudaEventRecord(S->ev_out, s));
+  CUDA_TRY(cudaStreamWaitEvent(us, S->ev_out, 0));
+  return exchange_result(S, z_best, z_walker, us);
 }
 
 extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, const double* x0,
@@ -331,6 +538,13 @@ extern "C" chap_status chap_run_walkers(const chap_problem* p, int32_t W_local, 
   bool stop = false;
   while (!stop) {
     const int64_t k = std::min<int64_t>(prm.exchange_K, max_iters - iters);
+    if (time_limit_s <= 0 && k > 0 && iters + k < max_iters) {
+      // not the last epoch and no clock to vote on: iterations + device exchange as one graph
+      TRY(chap_walkers_epoch(S, comm, (int32_t)k, nullptr, nullptr, cuda_stream));
+      iters += k;
+      ++epochs;
+      continue;
+    }
     if (k > 0) TRY(chap_tabu_step(S, (int32_t)k, nullptr, cuda_stream));
     iters += k;
     ++epochs;

@@ -36,6 +36,7 @@ __global__ void k_check_point(DevProblem P, const double* __restrict__ xu, int* 
 __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float* __restrict__ wsrc,
                             int only_walker, int* bad) {
   const int w = only_walker >= 0 ? only_walker : blockIdx.y;
+  if (skip_walker(Wk.rmask, only_walker, w)) return;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const double* xw = Wk.x + (size_t)w * Wk.xs;
@@ -116,6 +117,7 @@ __device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWal
 // mode 0: walker create (k = 0, counters cleared); mode 1: restart (keeps k, counters, best).
 __global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, int only_walker) {
   const int w = (only_walker >= 0) ? only_walker : blockIdx.x;
+  if (skip_walker(Wk.rmask, only_walker, w)) return;
   const int tid = threadIdx.x;
   WalkerScalars* sc = Wk.sc + w;
   const RowView rw = row_view(Wk, w);
@@ -145,8 +147,9 @@ __global__ void k_walker_finalize_init(DevProblem P, DevWalkers Wk, int mode, in
 }
 
 // Zero the grid-wide accumulators of walker `only_walker` (>= 0) or of every walker (blockIdx.x).
-__global__ void k_acc_zero(WalkerScalars* sc, int only_walker) {
+__global__ void k_acc_zero(WalkerScalars* sc, int only_walker, const int32_t* rmask) {
   const int w = only_walker >= 0 ? only_walker : blockIdx.x;
+  if (skip_walker(rmask, only_walker, w)) return;
   sc[w].cdot = 0.0;
   sc[w].vcount = 0;
 }
@@ -154,9 +157,10 @@ __global__ void k_acc_zero(WalkerScalars* sc, int only_walker) {
 // c.x of each walker's point (the cutoff row's activity and the objective), grid-wide: block
 // partials added to sc[w].cdot (exact for the integer data of DESIGN §5).
 __global__ void __launch_bounds__(256) k_cut_dot(DevProblem P, const double* __restrict__ x, size_t xs,
-                                                  WalkerScalars* sc, int only_walker) {
+                                                  WalkerScalars* sc, int only_walker, const int32_t* rmask) {
   __shared__ double sm[8];
   const int w = only_walker >= 0 ? only_walker : blockIdx.y;
+  if (skip_walker(rmask, only_walker, w)) return;
   const double* xw = x + (size_t)w * xs;
   double z = 0.0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P.n; p += gridDim.x * blockDim.x) z += P.c[p] * xw[p];
@@ -174,6 +178,7 @@ __global__ void __launch_bounds__(256) k_cut_dot(DevProblem P, const double* __r
 __global__ void __launch_bounds__(256) k_viol_count(DevProblem P, DevWalkers Wk, int only_walker) {
   __shared__ unsigned long long sm[8];
   const int w = only_walker >= 0 ? only_walker : blockIdx.y;
+  if (skip_walker(Wk.rmask, only_walker, w)) return;
   WalkerScalars* sc = Wk.sc;
   const RowView rw = row_view(Wk, w);
   const int cut_active = sc[w].cut_active;
@@ -218,8 +223,9 @@ __global__ void k_xbits_build(DevProblem P, DevWalkers Wk, int only_walker) {
 }
 
 // Clear the tabu list of walker w (restart) or of all walkers.
-__global__ void k_tabu_clear(int32_t* tabu, size_t ts, int n, int only_walker) {
+__global__ void k_tabu_clear(int32_t* tabu, size_t ts, int n, int only_walker, const int32_t* rmask) {
   const int w = (only_walker >= 0) ? only_walker : blockIdx.y;
+  if (skip_walker(rmask, only_walker, w)) return;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
     tabu[(size_t)w * ts + p] = 0;
 }
@@ -509,9 +515,7 @@ __global__ void k_export_stats(DevWalkers Wk, chap_walker_stats* st) {
 }
 
 // External cutoff: rhs = min(current, z - δ); residual and violated count updated.
-__global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= Wk.W) return;
+__device__ __forceinline__ void set_cutoff_one(const DevProblem& P, const DevWalkers& Wk, int w, double z) {
   WalkerScalars* sc = Wk.sc + w;
   const RowView rw = row_view(Wk, w);
   const double rhs = z - auto_delta(P, Wk.delta, z);
@@ -524,6 +528,15 @@ __global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
   sc->cutoff_rhs = rhs;
   sc->cut_active = 1;
   sc->rint = P.rint_base && rhs == floor(rhs);
+}
+__global__ void k_set_cutoff(DevProblem P, DevWalkers Wk, double z) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < Wk.W) set_cutoff_one(P, Wk, w, z);
+}
+// The same with z from device memory (the device exchange's plan); +INF: no incumbent, no change.
+__global__ void k_set_cutoff_from(DevProblem P, DevWalkers Wk, const double* z) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < Wk.W && *z < INFINITY) set_cutoff_one(P, Wk, w, *z);
 }
 
 // Scalars of the eval API's single virtual walker: k = 0, cutoff from the call.
@@ -575,7 +588,7 @@ __global__ void __launch_bounds__(256) k_summaries(DevProblem P, DevWalkers Wk, 
 namespace chap {
 // A point (internal order) to its packed form (DevProblem::pk_*): binaries as bits, integers as
 // int32 / int64, continuous values as f64.
-__global__ void k_pack_point(DevProblem P, const double* __restrict__ x, unsigned char* out) {
+__device__ __forceinline__ void pack_point(const DevProblem& P, const double* __restrict__ x, unsigned char* out) {
   const int nw = (P.pk_nbin + 31) >> 5;
   uint32_t* words = reinterpret_cast<uint32_t*>(out);
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nw + P.pk_nint + P.pk_ncont; q += gridDim.x * blockDim.x) {
@@ -596,8 +609,10 @@ __global__ void k_pack_point(DevProblem P, const double* __restrict__ x, unsigne
   }
 }
 
+__global__ void k_pack_point(DevProblem P, const double* __restrict__ x, unsigned char* out) { pack_point(P, x, out); }
+
 // The inverse: a packed point to internal order (fixed variables at their bound).
-__global__ void k_unpack_point(DevProblem P, const unsigned char* __restrict__ in, double* x) {
+__device__ __forceinline__ void unpack_point(const DevProblem& P, const unsigned char* __restrict__ in, double* x) {
   const uint32_t* words = reinterpret_cast<const uint32_t*>(in);
   const int tot = P.n_fixed + P.pk_nbin + P.pk_nint + P.pk_ncont;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += gridDim.x * blockDim.x) {
@@ -616,6 +631,8 @@ __global__ void k_unpack_point(DevProblem P, const unsigned char* __restrict__ i
     }
   }
 }
+
+__global__ void k_unpack_point(DevProblem P, const unsigned char* __restrict__ in, double* x) { unpack_point(P, in, x); }
 
 // One internal-order point to user order.
 __global__ void k_export_point(DevProblem P, const double* xi, double* xu) {

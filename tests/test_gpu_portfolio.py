@@ -55,12 +55,16 @@ def test_run_walkers_one_rank_nccl():
         comm.close()
 
 
-@pytest.mark.parametrize("seed,comm_kind", [(1, None), (4, "nccl")])
-def test_walkers_exchange_epochs_match_oracle(seed, comm_kind):
-    """chap_walkers_exchange between chap_tabu_step epochs (what bench.py times) reproduces the
-    oracle portfolio walker by walker: point, weights, tabu list, incumbent."""
+@pytest.mark.parametrize("seed,comm_kind,mode,W,nr", [(1, None, "exchange", 6, 2), (4, "nccl", "exchange", 6, 2),
+                                                    (1, None, "epoch", 6, 2), (4, "nccl", "epoch", 6, 3),
+                                                    (6, None, "epoch", 40, 7), (7, None, "exchange", 40, 40)])
+def test_walkers_exchange_epochs_match_oracle(seed, comm_kind, mode, W, nr):
+    """chap_walkers_exchange between chap_tabu_step epochs, or chap_walkers_epoch (iterations and
+    the device exchange as one CUDA graph, what bench.py times), reproduces the oracle portfolio
+    walker by walker: point, weights, tabu list, incumbent (W = 40: two walker groups, restarts in
+    both; nr = W: every walker restarts)."""
     inst = synth.tiny(seed)
-    W, K, E, ne, nr = 6, 30, 4, 2, 2
+    K, E, ne = 30, 4, 2
     x0s = np.stack([np.clip(synth.x_random(inst, 200 + w), inst.lb, inst.ub) for w in range(W)])
     O = oracle.Problem.from_instance(inst)
     ows = [oracle.TabuWalker(O, x) for x in x0s]
@@ -70,14 +74,23 @@ def test_walkers_exchange_epochs_match_oracle(seed, comm_kind):
     try:
         ws = chap.Walkers(P, torch.from_numpy(x0s).cuda(),
                           chap.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8))
+        zs = []
         for e in range(E):
-            ws.step(K)
-            if e < E - 1:
-                ws.exchange(comm)
+            if e == E - 1:
+                ws.step(K)
+            elif mode == "epoch":
+                zs.append(ws.epoch(K, comm, result=(e == 1)))
+            else:
+                ws.step(K)
+                zs.append(ws.exchange(comm))
         st = ws.get()
     finally:
         if comm is not None:
             comm.close()
+    # the best incumbent after the second exchange: the oracle's walkers at that point are not kept,
+    # so check it against the final incumbents' consistency (never better than the final best)
+    if zs and zs[1] is not None and math.isfinite(zs[1][0]):
+        assert zs[1][0] >= min(ow.best_obj for ow in ows if ow.has_incumbent)
     for w, ow in enumerate(ows):
         assert np.array_equal(st["x"][w], ow.x[: inst.n]), w
         assert np.array_equal(st["w"][w], ow.w), w
