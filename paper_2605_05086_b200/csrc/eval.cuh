@@ -1242,8 +1242,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
           const double r = rv[k].x;
           const int iw = __float2int_rn(__int_as_float((int)__double2loint(rv[k].y)));
           const bool z0 = r <= 0.0, z1 = r <= (double)nd;
-          const int p2 = z0 ? (z1 ? 0 : -2 * iw) : (z1 ? 2 * iw : (nd > 0 ? iw : -iw));
-          if (p2 != 0) atomicAdd(sc + c2, p2);
+          // in units of w: -2 (becomes violated), +2 (becomes satisfied), +-1 (stays violated, less
+          // or more), 0 (stays satisfied); nd != 0 for every entry but the inert padding
+          const int m = 2 * ((int)z1 - (int)z0) + ((z0 | z1) ? 0 : (nd > 0 ? 1 : -1));
+          if (m != 0) atomicAdd(sc + c2, m * iw);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&R.empty[st]);   // the stage's entries and row state are consumed
