@@ -1922,8 +1922,8 @@ __device__ __forceinline__ void lbkt_finalize(const DevProblem& P, const DevWalk
                     oxhat, oscore, kk, use_tabu, asp_ref(Wk, walker));
 }
 
-// wm_mode 1 (walker groups): the integer general tiles and the empty columns are k_eval_gen_wm's;
-// this kernel takes the long bounded-integer chunks and the tiles holding a continuous column.
+// wm_mode 1 (walker groups): the general tiles (integer and continuous) and the empty columns are
+// k_eval_gen_wm's; this kernel takes the long bounded-integer chunks the groups do not take.
 // with_lbin (one walker, row-wise binary mode): this kernel also takes the long binary chunks.
 // Warp w of the grid takes items w, w + nwarps, ... of its range of P.gitems (long-column chunks
 // first: their gathers overlap the packed tiles of other warps).
@@ -1965,7 +1965,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   // items: P.gitems = [long binary chunks | long bounded-integer chunks | continuous tiles | general
   // tiles | empty tiles]
   const int ifirst = with_lbin ? 0 : P.n_bchunks;
-  const int iend = wm_mode ? P.n_bchunks + P.n_gchunks + P.n_ctiles : P.n_gitems;
+  const int iend = wm_mode ? P.n_bchunks + P.n_gchunks : P.n_gitems;
   const int nwarps = gridDim.x * (kGenThreads / 32);
   GenRound R;
   bool r_ok = false;   // R holds T's first round
@@ -2263,11 +2263,16 @@ __global__ void __launch_bounds__(kGenWmThreads, CHAP_GENWM_MINB) k_eval_gen_wm(
   }
   for (int t = blockIdx.x * (kGenWmThreads / 32) + wid; t < P.n_wtiles; t += nwarps) {
     const WTile T = P.wtiles[t];
-    if (T.kind == CC_GENC) continue;   // continuous columns: k_eval_gen (wm_mode 1)
     for (int c = slot; c < T.ncols; c += NS) {
       const int p = T.p0 + c;
       const double xb = __ldg(X + p), l = __ldg(P.lb + p), u = __ldg(P.ub + p);
       const int j = __ldg(P.perm + p);
+      if (T.kind == CC_GENC) {   // a continuous column: Algorithm 1 serially in double, per walker of
+        double v2, s2;           // the group (its entries read once per group through L1)
+        gen_column_serial(P, X, RS, RG, p, v2, s2);
+        if (live) offer(s2, s2 == -INFINITY ? xb : v2, j, p);
+        continue;
+      }
       double bs = -INFINITY, bv = xb;
       if (T.kind != CC_GEN) {   // a column without nonzeros (R2, R4, R5)
         if (__ldg(P.vclass + p) == 1) {

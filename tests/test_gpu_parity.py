@@ -646,3 +646,42 @@ def test_trajectory_weight_smoothing(seed, binrow):
         inst = synth.mixed(seed=5, n=3000, m=600, n_long=6, long_lo=100, long_hi=600)
         x0s = [synth.x_lower(inst), inst.x_star] + [synth.x_random(inst, s) for s in range(4)]
         _traj_compare(inst, x0s, 300, perturb=1, smooth_prob=0.5, rng_seed=8, tenure=3)
+
+
+def test_walker_groups_continuous_columns_match_single_walkers():
+    """a10 for continuous columns: in walker groups k_eval_gen_wm evaluates the packed continuous
+    columns for the whole group (gen_column_serial per lane, the group's row-state layout). The
+    continuous path is checked against exact-rational Algorithm 1 in tolerance mode above
+    (test_continuous_columns_tolerance_mode); here every walker of a 12-walker group follows,
+    bit for bit, the trajectory the same walker follows alone (one walker: k_eval_gen's per-walker
+    path with the same arithmetic)."""
+    import dataclasses
+    inst = synth.mixed(seed=9, n=4000, m=800, n_long=0)
+    rng = np.random.default_rng(31)
+    gen = np.nonzero((inst.is_int == 1) & (inst.ub > 1.0) & np.isfinite(inst.ub))[0]
+    cont = rng.choice(gen, size=len(gen) // 2, replace=False)
+    is_int = inst.is_int.copy()
+    is_int[cont] = 0
+    inst = dataclasses.replace(inst, is_int=is_int, name=inst.name + "-cont")
+    P = chap.Problem.from_instance(inst)
+    assert P.info.n_continuous >= 100
+    x0s = np.stack([synth.x_lower(inst)] + [synth.x_random(inst, s) for s in range(11)])
+    prm = chap.default_params(graph_iters=0)
+    G = chap.Walkers(P, torch.from_numpy(x0s).cuda(), prm)
+    glog = chap.records(G.step(40, log=True)).reshape(40, len(x0s))
+    gst = G.get()
+    for wi in range(len(x0s)):
+        S1 = chap.Walkers(P, torch.from_numpy(x0s[wi:wi + 1]).cuda(), prm)
+        slog = chap.records(S1.step(40, log=True)).reshape(40, 1)[:, 0]
+        sst = S1.get()
+        for f in ("k", "j", "flags", "violated"):
+            assert np.array_equal(glog[f][:, wi], slog[f]), (wi, f)
+        mv = slog["j"] >= 0
+        assert np.array_equal(glog["v"][mv, wi], slog["v"][mv]), wi
+        # c.x of fractional points is a grid-wide sum (k_cut_dot) whose order follows the launch
+        # shape: the objective and the cutoff row's residual agree to rounding (DESIGN §5)
+        assert np.allclose(glog["obj"][:, wi], slog["obj"], rtol=1e-12, atol=0), wi
+        assert np.array_equal(gst["x"][wi], sst["x"][0]), wi
+        assert np.array_equal(gst["r"][wi][:-1], sst["r"][0][:-1]), wi
+        assert np.allclose(gst["r"][wi][-1:], sst["r"][0][-1:], rtol=1e-12, atol=1e-9), wi
+        S1.close()
