@@ -1,6 +1,7 @@
 """Small workloads for compute-sanitizer (memcheck / racecheck / synccheck): the eval API on the
 tiny, mixed and sorted-class instances, tabu steps with the row-wise binary kernel forced (one
-walker) and with walker groups (W = 6: row-state groups of 8), the column-wise kernel forced.
+walker) and with walker groups (W = 6: row-state groups of 8) including the device exchange and
+an epoch graph, the column-wise kernel forced.
 Usage: compute-sanitizer --tool TOOL python tools/sanitize_run.py [T|S|M]"""
 import os
 import sys
@@ -32,7 +33,10 @@ for bk in (2, 1):   # row-wise forced, column-wise forced
     torch.cuda.synchronize()
     Wk.close()
 X0 = np.stack([synth.x_random(inst, s) for s in range(6)])
-Wk = chap.Walkers(P, torch.from_numpy(X0).cuda(), chap.default_params(graph_iters=4))
+Wk = chap.Walkers(P, torch.from_numpy(X0).cuda(), chap.default_params(graph_iters=4, n_elite=2, n_restart=3))
 Wk.step(10)
+Wk.exchange()          # the device exchange: plan, packing, cutoff, restarts
+Wk.epoch(5)            # iterations + exchange as one captured graph, then replayed
+Wk.epoch(5, result=True)
 torch.cuda.synchronize()
 print("sanitize workload done", which, inst.n, inst.m)
