@@ -1765,8 +1765,6 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
   using Acc = typename std::conditional<INTW, int, double>::type;
   Acc b2 = 0, a2 = 0;
   bool ovf = false;   // irrelevant here: a clamped offset lies outside [l, u]
-  int hb = -1, hs = 0, hwq = -1;   // the lane's pending bucket and sum, candidate word and bits
-  unsigned hbits = 0u;
   for (int r0 = 0; r0 < len; r0 += 32 * kWSlotsGen) {
     int id[kWSlotsGen];
     double av[kWSlotsGen];
@@ -1794,20 +1792,9 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
         }
         if (cv >= 0 && cv < dom) cq = cv;
       }
-      if (local) {   // run-length per lane: breakpoints of a long column crowd onto a few buckets
-        if (bq != hb) {
-          if (hb >= 0 && hs != 0) atomicAdd(hist + hb, hs);
-          hb = bq;
-          hs = 0;
-        }
-        hs += bq >= 0 ? E.y : 0;
-        const int cw = cq >= 0 ? (cq >> 5) : -1;
-        if (cw != hwq) {
-          if (hwq >= 0) atomicOr(hcw + hwq, hbits);
-          hwq = cw;
-          hbits = 0u;
-        }
-        hbits |= cq >= 0 ? (1u << (cq & 31)) : 0u;
+      if (local) {   // the warp's shared histogram and candidate words (shared-memory atomics)
+        if (bq >= 0 && E.y != 0) atomicAdd(hist + bq, E.y);
+        if (cq >= 0) atomicOr(hcw + (cq >> 5), 1u << (cq & 31));
         continue;
       }
       // bucket deltas: one atomic per distinct bucket of the 32 entries
@@ -1829,8 +1816,6 @@ __device__ __forceinline__ void lbkt_chunk(const DevProblem& P, const DevWalkers
     }
   }
   if (local) {   // one addition per nonzero bucket and candidate word
-    if (hb >= 0 && hs != 0) atomicAdd(hist + hb, hs);
-    if (hwq >= 0) atomicOr(hcw + hwq, hbits);
     __syncwarp();
     for (int q = lane; q <= dom; q += 32) {
       const int h = hist[q];
