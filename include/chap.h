@@ -380,6 +380,22 @@ chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, const chap_walk
                                int8_t* elite_kind, int32_t* elite_slot, int32_t* n_restart_out,
                                int32_t* restart_gid, int32_t* restart_src);
 
+/* chap_exchange_plan on the device, as the exchange of chap_walkers_exchange / chap_walkers_epoch
+ * computes it (k_exchange_plan: one block, rank counting), for the walkers of rank `rank`. All
+ * pointers are DEVICE memory, stream-ordered on cuda_stream; s[W_total] indexed by gid as for
+ * chap_exchange_plan. Outputs: z_best [1] (+INF: no incumbent); counts [4]: best gid (-1), |E|,
+ * the number of restarts, unused; elite_gid / elite_slot [2 n_elite] (the first |E| valid, feasible
+ * elite first, slots as for chap_exchange_plan); local_rank [2][W_local]: for this rank's walkers
+ * their position among the rank's own top n_elite best points (row 0) and current points (row 1),
+ * -1 if not sent; restart_gid / restart_src [W_total] (the first counts[2] valid); restart_slot
+ * [W_local]: the gathered-buffer slot each local walker restarts from, -1 if none. Errors:
+ * CHAP_ERR_INVALID_ARG (sizes, rank out of range, NULL pointers), CHAP_ERR_CUDA. */
+chap_status chap_exchange_plan_device(int32_t W_total, int32_t W_local, int32_t rank,
+                                      const chap_walker_summary* s, int32_t n_elite, int32_t n_restart,
+                                      double* z_best, int32_t* counts, int32_t* elite_gid, int32_t* elite_slot,
+                                      int32_t* local_rank, int32_t* restart_gid, int32_t* restart_src,
+                                      int32_t* restart_slot, void* cuda_stream);
+
 /* One portfolio exchange on existing walkers, the step chap_run_walkers runs every
  * exchange_K iterations: per-walker summaries are all-gathered (NCCL when comm is non-NULL), the
  * plan of chap_exchange_plan is computed on the device, the elite points are all-gathered, every

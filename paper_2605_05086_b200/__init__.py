@@ -111,6 +111,8 @@ _SIGS = {
     "chap_walkers_launches_per_iter": (ctypes.c_int, [_P, _P]),
     "chap_walkers_exchange": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "chap_walkers_epoch": (ctypes.c_int, [_P, _P, c_i32, _P, _P, _P]),
+    "chap_exchange_plan_device": (ctypes.c_int, [c_i32, c_i32, c_i32, _P, c_i32, c_i32, _P, _P, _P, _P, _P, _P,
+                                                  _P, _P, _P]),
     "chap_comm_unique_id": (ctypes.c_int, [_P]),
     "chap_comm_create": (ctypes.c_int, [_P, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "chap_comm_destroy": (ctypes.c_int, [_P]),
@@ -372,6 +374,39 @@ def run_walkers(problem: Problem, x0, params: Optional[chap_params] = None, comm
                             comm.h if comm is not None else None, int(max_iters), float(time_limit_s), _ptr(bx),
                             ctypes.byref(res), _stream(stream)))
     return res, bx
+
+
+def exchange_plan_device(summaries: np.ndarray, W_local: int, rank: int, n_elite: int, n_restart: int,
+                         device: int = 0) -> dict:
+    """chap_exchange_plan_device: the exchange decisions as the device exchange computes them (for
+    rank `rank`), returned as host arrays (the same keys as exchange_plan, plus local_rank and
+    restart_slot)."""
+    import torch
+    s = np.ascontiguousarray(summaries, SUMMARY_DTYPE)
+    W = int(s.shape[0])
+    dev = torch.device("cuda", device)
+    ds = torch.from_numpy(s.view(np.uint8).copy()).to(dev)
+    E = max(2 * n_elite, 1)
+    z = torch.empty(1, dtype=torch.float64, device=dev)
+    cnt = torch.zeros(4, dtype=torch.int32, device=dev)
+    eg = torch.full((E,), -1, dtype=torch.int32, device=dev)
+    es = torch.full((E,), -1, dtype=torch.int32, device=dev)
+    lr = torch.full((2 * W_local,), -2, dtype=torch.int32, device=dev)
+    rg = torch.full((W,), -1, dtype=torch.int32, device=dev)
+    rs = torch.full((W,), -1, dtype=torch.int32, device=dev)
+    sl = torch.full((W_local,), -2, dtype=torch.int32, device=dev)
+    _check(chap_exchange_plan_device(W, int(W_local), int(rank), _ptr(ds), int(n_elite), int(n_restart), _ptr(z),
+                                     _ptr(cnt), _ptr(eg), _ptr(es), _ptr(lr), _ptr(rg), _ptr(rs), _ptr(sl),
+                                     _stream(None)))
+    torch.cuda.synchronize(dev)
+    c = cnt.cpu().numpy()
+    ne, nr = int(c[1]), int(c[2])
+    nf = int(np.count_nonzero(s["flags"] & 1))
+    nf = min(nf, n_elite)
+    return {"z_best": float(z.item()), "best_gid": int(c[0]), "elite_gid": eg.cpu().numpy()[:ne],
+            "elite_kind": (np.arange(ne) >= nf).astype(np.int8), "elite_slot": es.cpu().numpy()[:ne],
+            "restart_gid": rg.cpu().numpy()[:nr], "restart_src": rs.cpu().numpy()[:nr],
+            "local_rank": lr.cpu().numpy().reshape(2, W_local), "restart_slot": sl.cpu().numpy()}
 
 
 def exchange_plan(summaries: np.ndarray, W_local: int, n_elite: int, n_restart: int) -> dict:

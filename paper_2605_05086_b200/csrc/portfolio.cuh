@@ -486,6 +486,22 @@ extern "C" chap_status chap_walkers_exchange(chap_walkers* S, chap_comm* comm, d
   return exchange_result(S, z_best, z_walker, s);
 }
 
+extern "C" chap_status chap_exchange_plan_device(int32_t W_total, int32_t W_local, int32_t rank,
+                                                 const chap_walker_summary* s, int32_t n_elite, int32_t n_restart,
+                                                 double* z_best, int32_t* counts, int32_t* elite_gid,
+                                                 int32_t* elite_slot, int32_t* local_rank, int32_t* restart_gid,
+                                                 int32_t* restart_src, int32_t* restart_slot, void* cuda_stream) {
+  if (W_total < 1 || W_local < 1 || W_total % W_local || rank < 0 || rank >= W_total / W_local || !s ||
+      n_elite < 0 || n_restart < 0 || !z_best || !counts || !elite_gid || !elite_slot || !local_rank ||
+      !restart_gid || !restart_src || !restart_slot)
+    return fail(CHAP_ERR_INVALID_ARG, "bad device exchange-plan arguments");
+  k_exchange_plan<<<1, 1024, 0, (cudaStream_t)cuda_stream>>>(s, W_total, W_local, rank, n_elite, n_restart, z_best,
+                                                             counts, elite_gid, elite_slot, local_rank, restart_gid,
+                                                             restart_src, restart_slot);
+  CUDA_TRY(cudaGetLastError());
+  return CHAP_OK;
+}
+
 extern "C" chap_status chap_walkers_epoch(chap_walkers* S, chap_comm* comm, int32_t n_iters, double* z_best,
                                           int32_t* z_walker, void* cuda_stream) {
   if (!S || n_iters < 1) return fail(CHAP_ERR_INVALID_ARG, "NULL walkers or n_iters < 1");

@@ -152,3 +152,51 @@ def test_two_ranks_equal_one_rank():
         assert obj == res1.best_obj and bw == res1.best_walker
         if res1.has_incumbent:
             assert np.array_equal(bx, bx1.cpu().numpy())
+
+
+def _random_summaries(rng, W):
+    """Gathered summaries with many ties: objectives and violation counts from small ranges."""
+    S = np.zeros(W, chap.SUMMARY_DTYPE)
+    feas = rng.random(W) < 0.5
+    S["best_obj"] = np.where(feas, rng.integers(-5, 5, W).astype(np.float64), math.inf)
+    S["violated"] = rng.integers(0, 4, W)
+    S["sumviol"] = rng.integers(0, 3, W) * 0.5
+    S["gid"] = np.arange(W)
+    S["flags"] = feas.astype(np.int32)
+    return S
+
+
+@pytest.mark.parametrize("nranks,W_local", [(1, 1), (1, 7), (2, 3), (4, 8), (8, 5), (8, 64)])
+def test_device_exchange_plan_matches_host_plan(nranks, W_local):
+    """k_exchange_plan (the device exchange of chap_walkers_exchange / chap_walkers_epoch) makes
+    chap_exchange_plan's decisions for every rank of a multi-rank portfolio — reachable here on one
+    GPU by asking for each rank's view of random gathered summaries with ties: the same best, elite
+    (gid, kind, slot) and restarts; each rank's local ranks place its elite members in their slots
+    and its restart slots point at their sources' slots."""
+    rng = np.random.default_rng([nranks, W_local])
+    W = nranks * W_local
+    for trial in range(6):
+        S = _random_summaries(rng, W)
+        ne, nr = [(0, 0), (1, 1), (2, W // 8), (4, W), (3, 2), (2, W + 3)][trial]
+        host = chap.exchange_plan(S, W_local, ne, nr)
+        E = len(host["elite_gid"])
+        for rank in range(nranks):
+            dev = chap.exchange_plan_device(S, W_local, rank, ne, nr)
+            if math.isinf(host["z_best"]):
+                assert math.isinf(dev["z_best"])
+            else:
+                assert dev["z_best"] == host["z_best"]
+            assert dev["best_gid"] == host["best_gid"]
+            for k in ("elite_gid", "elite_kind", "elite_slot", "restart_gid", "restart_src"):
+                assert np.array_equal(dev[k], host[k]), (trial, rank, k, dev[k], host[k])
+            lo = rank * W_local
+            for q in range(E):
+                g, kind = int(host["elite_gid"][q]), int(host["elite_kind"][q])
+                if lo <= g < lo + W_local:
+                    assert host["elite_slot"][q] == rank * 2 * ne + kind * ne + dev["local_rank"][kind][g - lo]
+            slots = np.full(W_local, -1)
+            for q in range(len(host["restart_gid"])):
+                g = int(host["restart_gid"][q])
+                if lo <= g < lo + W_local:
+                    slots[g - lo] = host["elite_slot"][host["restart_src"][q]]
+            assert np.array_equal(dev["restart_slot"], slots), (trial, rank)
