@@ -42,8 +42,16 @@ constexpr int kApplyThreads = 256;
 struct __align__(16) RowState {
   double r;
   float w;
-  uint32_t pad;
+  int32_t rc;   // ceil(r) clamped to int32 (r <= v <=> rc <= v for integers v): kept with r by every
+                // writer (set_r) so that k_eval_binrow tests feasibility in integers
 };
+__host__ __device__ __forceinline__ int32_t r_ceil(double r) {
+  return r >= 2147483647.0 ? 2147483647 : (r <= -2147483648.0 ? (-2147483647 - 1) : (int32_t)ceil(r));
+}
+__host__ __device__ __forceinline__ void set_r(RowState& s, double r) {
+  s.r = r;
+  s.rc = r_ceil(r);
+}
 
 // Column classes (the paper's length-specialised dispatch, re-designed).
 enum ColClass : int {

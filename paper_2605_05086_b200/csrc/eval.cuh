@@ -1239,9 +1239,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_eval_binrow(DevProblem P, De
           const int ai = (int)(int16_t)(uk >> 16);
           const bool xb = (bits[c2 >> 5] >> (c2 & 31)) & 1u;
           const int nd = xb ? ai : -ai;   // -d
-          const double r = rv[k].x;
+          // r <= v <=> ceil(r) <= v for the integers 0 and nd: the row state's RowState::rc
+          const int rc = __double2hiint(rv[k].y);
           const int iw = __float2int_rn(__int_as_float((int)__double2loint(rv[k].y)));
-          const bool z0 = r <= 0.0, z1 = r <= (double)nd;
+          const bool z0 = rc <= 0, z1 = rc <= nd;
           // in units of w: -2 (becomes violated), +2 (becomes satisfied), +-1 (stays violated, less
           // or more), 0 (stays satisfied); nd != 0 for every entry but the inert padding
           const int m = 2 * ((int)z1 - (int)z0) + ((z0 | z1) ? 0 : (nd > 0 ? 1 : -1));

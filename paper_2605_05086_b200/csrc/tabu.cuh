@@ -44,22 +44,20 @@ __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float
   const WalkerScalars* sc = Wk.sc;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     RowState d;
-    d.r = -INFINITY;
+    set_r(d, -INFINITY);
     d.w = 0.0f;
-    d.pad = 0;
     rw[P.dummy_row] = d;   // inert padding row
   }
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < P.m_norm; i += nwarps) {
     if (i == P.cut_row) {   // c.x comes from k_cut_dot (a grid-wide sum): no warp walks this row
       if (lane == 0) {
         RowState s = rw[i];
-        s.r = sc[w].cut_active ? sc[w].cdot - sc[w].cutoff_rhs : -INFINITY;
+        set_r(s, sc[w].cut_active ? sc[w].cdot - sc[w].cutoff_rhs : -INFINITY);
         if (init_w == 1) s.w = 1.0f;
         else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
         if (init_w == 2 && bad && !(s.w >= 0.0f)) atomicOr(bad, 1);   // weights must be >= 0 (R11)
         if (init_w == 2 && !(s.w == truncf(s.w) && s.w <= 1048576.0f)) atomicAnd(&Wk.sc[w].wint, 0);
         if (!sc[w].cut_active) s.w = 0.0f;
-        s.pad = 0;
         rw[i] = s;
       }
       continue;
@@ -77,13 +75,12 @@ __global__ void k_rows_init(DevProblem P, DevWalkers Wk, int init_w, const float
         r = sc[w].cut_active ? y - sc[w].cutoff_rhs : -INFINITY;
       }
       RowState s = rw[i];
-      s.r = r;
+      set_r(s, r);
       if (init_w == 1) s.w = 1.0f;
       else if (init_w == 2) s.w = wsrc ? wsrc[i] : 1.0f;
       if (init_w == 2 && bad && !(s.w >= 0.0f)) atomicOr(bad, 1);
       if (init_w == 2 && !(s.w == truncf(s.w) && s.w <= 1048576.0f)) atomicAnd(&Wk.sc[w].wint, 0);
       if (i == P.cut_row && !sc[w].cut_active) s.w = 0.0f;
-      s.pad = 0;
       rw[i] = s;
     }
   }
@@ -109,7 +106,7 @@ __device__ __forceinline__ void take_incumbent(const DevProblem& P, const DevWal
   sc->cut_active = 1;
   sc->rint = P.rint_base && rhs == floor(rhs);
   const double r = z - rhs;
-  rw[P.cut_row].r = r;
+  set_r(rw[P.cut_row], r);
   sc->violated = (r > 0.0) ? 1 : 0;
 }
 
@@ -291,7 +288,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
       if ((i == P.cut_row && !cut_active) || i == P.dummy_row) continue;
       const double r0 = rw[i].r;
       const double r1 = r0 + P.val[e] * d.delta;
-      rw[i].r = r1;
+      set_r(rw[i], r1);
       dv += (long long)(r1 > 0.0) - (long long)(r0 > 0.0);
     }
   } else {
@@ -524,7 +521,7 @@ __device__ __forceinline__ void set_cutoff_one(const DevProblem& P, const DevWal
   const double r_new = sc->obj - rhs;
   sc->violated += (long long)(r_new > 0.0) - (long long)(r_old > 0.0);
   if (!sc->cut_active) rw[P.cut_row].w = 1.0f;
-  rw[P.cut_row].r = r_new;
+  set_r(rw[P.cut_row], r_new);
   sc->cutoff_rhs = rhs;
   sc->cut_active = 1;
   sc->rint = P.rint_base && rhs == floor(rhs);
