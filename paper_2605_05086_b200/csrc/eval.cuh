@@ -36,6 +36,20 @@ __device__ __forceinline__ double penalty(double w, double r0, double r1) {
   return s0 ? from_sat : from_vio;
 }
 
+// penalty(w, r, r + d) / (w / 2) as an integer in {-2, -1, 0, 1, 2} from a row-state record
+// (r, w | rc): feasibility before from RowState::rc (r <= 0 <=> ceil(r) <= 0), after from r + d,
+// and a row violated on both sides gets less violated iff d < 0. For integer data (DESIGN §5:
+// r and d integers, r + d exact; DevProblem::rint_base) w m / 2 equals penalty() exactly; inert
+// rows (r = -inf) give 0. With integral weights a column's flip score is (Σ m w) / 2, summed in
+// integers.
+__device__ __forceinline__ int penalty_m(const double2& rv, double d) {
+  const bool z0 = __double2hiint(rv.y) <= 0, z1 = rv.x + d <= 0.0;
+  return 2 * ((int)z1 - (int)z0) + ((z0 | z1) ? 0 : (d < 0.0 ? 1 : -1));
+}
+__device__ __forceinline__ int weight_int(const double2& rv) {
+  return __float2int_rn(__int_as_float((int)__double2loint(rv.y)));
+}
+
 // Within one variable: higher score, then closer to x̄, then smaller value (R4).
 __device__ __forceinline__ bool better_shift(double s1, double v1, double s0, double v0, double xb) {
   if (s1 != s0) return s1 > s0;
@@ -798,7 +812,7 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
                                            const double* __restrict__ X, const double2* __restrict__ RS,
                                            const int32_t* __restrict__ TB, const WTile& T, int lane,
                                            Best& b, double* oxhat, double* oscore, long long kk,
-                                           int use_tabu) {
+                                           int use_tabu, bool wint) {
   const int p = T.p0, len = T.ncols;
   const int* __restrict__ ridx = P.row_idx + T.e0;
   const double* __restrict__ rval = P.val + T.e0;
@@ -813,14 +827,26 @@ __device__ __forceinline__ void lbin_chunk(const DevProblem& P, const DevWalkers
     av[q] = k < len ? __ldcs(rval + k) : 0.0;
   }
   double own = 0.0;
+  if (wint) {   // integer data, integral weights: (Σ m w) / 2 in integers (penalty_m)
+    int own2 = 0;
 #pragma unroll
-  for (int q = 0; q < kWChunk / 32; ++q) {
-    const double2 rv = __ldg(RS + id[q]);
-    const double r = rv.x, w = (double)__int_as_float((int)__double2loint(rv.y));
-    own += penalty(w, r, r + av[q] * dir);   // the inert dummy row adds 0
+    for (int q = 0; q < kWChunk / 32; ++q) {
+      const double2 rv = __ldg(RS + id[q]);
+      own2 += penalty_m(rv, av[q] * dir) * weight_int(rv);   // the inert dummy row adds 0
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) own2 += __shfl_xor_sync(kFull, own2, off);
+    own = 0.5 * (double)own2;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kWChunk / 32; ++q) {
+      const double2 rv = __ldg(RS + id[q]);
+      const double r = rv.x, w = (double)__int_as_float((int)__double2loint(rv.y));
+      own += penalty(w, r, r + av[q] * dir);   // the inert dummy row adds 0
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) own += __shfl_xor_sync(kFull, own, off);
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) own += __shfl_xor_sync(kFull, own, off);
   const LongCol L = P.lcols[T.e1];
   if (L.nchunks == 1) {
     if (lane == 0)
@@ -858,7 +884,8 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
   // chunks of long columns first (their latency overlaps the packed tiles of other warps)
   for (; t < P.n_bchunks; t += nwarps)
     if (cols_dirty(Wk, kk, P.bchunks[t].p0, 1))
-      lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu);
+      lbin_chunk(P, Wk, walker, X, RS, TB, P.bchunks[t], lane, b, oxhat, oscore, kk, use_tabu,
+                 P.rint_base && sc->wint != 0);
   t -= P.n_bchunks;
   const int hwi = lane >> 3, sh = 4 * (lane & 7);   // head word and bit offset of my 4 slots
   WTile Tn;
@@ -1010,6 +1037,8 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
     b.p = p;
   };
   const int nwarps = gridDim.x * (kBinWmThreads / 32);
+  // integer data and integral weights <= 2^20 for every walker of the warp: flip sums in integers
+  const bool wint_all = P.rint_base && __all_sync(kFull, Wk.sc[wr].wint != 0);
   int t = blockIdx.x * (kBinWmThreads / 32) + wid;
   for (; t < P.n_bchunks; t += nwarps) {
     const WTile T = P.bchunks[t];
@@ -1031,10 +1060,17 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+      if (wint_all) {   // (Σ m w) / 2 of the 4 entries: exact in double (half-integers)
+        int a2 = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double r = rv[q].x, wv = (double)__int_as_float((int)__double2loint(rv[q].y));
-        acc += penalty(wv, r, r + av[q] * dir);
+        for (int q = 0; q < 4; ++q) a2 += penalty_m(rv[q], av[q] * dir) * weight_int(rv[q]);
+        acc += 0.5 * (double)a2;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double r = rv[q].x, wv = (double)__int_as_float((int)__double2loint(rv[q].y));
+          acc += penalty(wv, r, r + av[q] * dir);
+        }
       }
     }
 #pragma unroll
@@ -1072,6 +1108,28 @@ __global__ void __launch_bounds__(kBinWmThreads) k_eval_bin_wm(DevProblem P, Dev
       const double xb = (double)((__shfl_sync(kFull, xw, c) >> wl) & 1u);
       const double dir = 1.0 - 2.0 * xb;
       double acc = 0.0;
+      if (wint_all) {   // integral weights: the flip score in half weights, in integers (penalty_m)
+        int acc2 = 0;
+        for (int k0 = e0 + slot; k0 < e1; k0 += 4 * NS) {
+          int id[4];
+          double av[4];
+          double2 rv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int k = k0 + q * NS;
+            id[q] = k < e1 ? S.id[k] : -1;
+            av[q] = k < e1 ? S.a[k] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rv[q] = id[q] >= 0 ? __ldg(RS + (size_t)id[q] * RG) : make_double2(-INFINITY, 0.0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc2 += penalty_m(rv[q], av[q] * dir) * weight_int(rv[q]);
+        }
+#pragma unroll
+        for (int off = RG; off < 32; off <<= 1) acc2 += __shfl_xor_sync(kFull, acc2, off);
+        if (slot == 0 && live) offer(0.5 * (double)acc2, jc, T.p0 + c, 1.0 - xb);
+        continue;
+      }
       for (int k0 = e0 + slot; k0 < e1; k0 += 4 * NS) {
         int id[4];
         double av[4];
@@ -1968,7 +2026,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
       else lbkt_chunk<false>(P, Wk, walker, X, RS, st, T, L, lane, reinterpret_cast<unsigned char*>(&S), rint, s_tab);
       if (long_last(Wk, walker, L, lane)) lbkt_finalize(P, Wk, walker, L, lane, b, oxhat, oscore, kk, use_tabu);
     } else if (T.kind == CC_LBIN) {
-      lbin_chunk(P, Wk, walker, X, RS, TB, T, lane, b, oxhat, oscore, kk, use_tabu);
+      lbin_chunk(P, Wk, walker, X, RS, TB, T, lane, b, oxhat, oscore, kk, use_tabu, P.rint_base && wint);
     } else if (T.kind == CC_GENC) {
       if (lane < T.ncols) {
         const int p = T.p0 + lane;
