@@ -55,14 +55,16 @@ def test_run_walkers_one_rank_nccl():
         comm.close()
 
 
-@pytest.mark.parametrize("seed,comm_kind,mode,W,nr", [(1, None, "exchange", 6, 2), (4, "nccl", "exchange", 6, 2),
-                                                    (1, None, "epoch", 6, 2), (4, "nccl", "epoch", 6, 3),
-                                                    (6, None, "epoch", 40, 7), (7, None, "exchange", 40, 40)])
-def test_walkers_exchange_epochs_match_oracle(seed, comm_kind, mode, W, nr):
+@pytest.mark.parametrize("seed,comm_kind,mode,W,nr,lazy", [(1, None, "exchange", 6, 2, 0), (4, "nccl", "exchange", 6, 2, 0),
+                                                         (1, None, "epoch", 6, 2, 0), (4, "nccl", "epoch", 6, 3, 0),
+                                                         (6, None, "epoch", 40, 7, 0), (7, None, "exchange", 40, 40, 0),
+                                                         (2, None, "epoch", 1, 1, 1), (3, None, "epoch", 1, 1, 0)])
+def test_walkers_exchange_epochs_match_oracle(seed, comm_kind, mode, W, nr, lazy):
     """chap_walkers_exchange between chap_tabu_step epochs, or chap_walkers_epoch (iterations and
     the device exchange as one CUDA graph, what bench.py times), reproduces the oracle portfolio
     walker by walker: point, weights, tabu list, incumbent (W = 40: two walker groups, restarts in
-    both; nr = W: every walker restarts)."""
+    both; nr = W: every walker restarts; W = 1: the single-walker kernels restart the walker from its
+    own elite point, from scratch and with selective re-evaluation)."""
     inst = synth.tiny(seed)
     K, E, ne = 30, 4, 2
     x0s = np.stack([np.clip(synth.x_random(inst, 200 + w), inst.lb, inst.ub) for w in range(W)])
@@ -73,7 +75,7 @@ def test_walkers_exchange_epochs_match_oracle(seed, comm_kind, mode, W, nr):
     comm = chap.Comm(chap.comm_unique_id(), 1, 0, 0) if comm_kind else None
     try:
         ws = chap.Walkers(P, torch.from_numpy(x0s).cuda(),
-                          chap.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8))
+                          chap.default_params(exchange_K=K, n_elite=ne, n_restart=nr, graph_iters=8, lazy=lazy))
         zs = []
         for e in range(E):
             if e == E - 1:
