@@ -685,3 +685,45 @@ def test_walker_groups_continuous_columns_match_single_walkers():
         assert np.array_equal(gst["r"][wi][:-1], sst["r"][0][:-1]), wi
         assert np.allclose(gst["r"][wi][-1:], sst["r"][0][-1:], rtol=1e-12, atol=1e-9), wi
         S1.close()
+
+
+@pytest.mark.parametrize("kind", ["big_int_weights", "float_weights", "huge_residuals", "huge_and_float"])
+def test_eval_edge_domains(kind):
+    """The kernels' alternative paths against the oracle, bit for bit, on an instance with packed
+    general tiles, long bounded-integer and long binary columns:
+      - integral weights above 2^20 (the general kernels' float-word path instead of the int path,
+        and the double binary penalties instead of the integer flip sums);
+      - non-integral float weights (the same paths; every term and sum still exact in double);
+      - unbounded integer variables at ~1e9 and rows far from tight, so residuals reach ~1e11:
+        the double division of lines 3-4 instead of the float quotient (|r| >= 2^23), and offsets
+        beyond the int path (|d| >= 2^28: the tile re-evaluated in double by gen_column_serial)."""
+    inst = synth.mixed(seed=5, n=4000, m=800, n_long=6, long_lo=300, long_hi=3000)
+    P = chap.Problem.from_instance(inst)
+    O = oracle.Problem.from_instance(inst)
+    rng = np.random.default_rng([0xED, len(kind)])
+    x = synth.x_random(inst, 7)
+    if kind in ("huge_residuals", "huge_and_float"):
+        unb = np.nonzero(np.isinf(inst.ub) & (inst.is_int == 1))[0]
+        assert unb.size > 10
+        x[unb] = rng.integers(10**8, 10**9, unb.size).astype(np.float64)
+    if kind == "big_int_weights":
+        w = rng.integers(2**20 + 1, 2**22, P.m_norm).astype(np.float32)
+    elif kind in ("float_weights", "huge_and_float"):
+        w = rng.uniform(0.1, 10.0, P.m_norm).astype(np.float32)
+    else:
+        w = rng.integers(1, 6, P.m_norm).astype(np.float32)
+    for cut in (math.inf, float(inst.c @ x) - 1.0):
+        g, o = _eval_both(inst, x, w, cut, P, O)
+        _assert_same(g, o, f"{kind} cut={cut}")
+
+
+def test_trajectory_huge_residuals():
+    """A walk started with the unbounded integer variables at ~1e9 (residuals ~1e11: the double
+    division and the double re-evaluation of offsets beyond the int path, inside the tabu step with
+    its dynamic item hand-out) stays bit-exact with the oracle's walk."""
+    inst = synth.mixed(seed=5, n=4000, m=800, n_long=6, long_lo=300, long_hi=3000)
+    rng = np.random.default_rng(0xED)
+    x = synth.x_random(inst, 7)
+    unb = np.nonzero(np.isinf(inst.ub) & (inst.is_int == 1))[0]
+    x[unb] = rng.integers(10**8, 10**9, unb.size).astype(np.float64)
+    _traj_compare(inst, [x], 40)
