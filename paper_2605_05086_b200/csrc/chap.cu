@@ -1648,6 +1648,10 @@ extern "C" chap_status chap_walkers_timing(chap_walkers* S, int32_t mode, uint64
       cudaGraphExecDestroy(S->gexec_rem);
       S->gexec_rem = nullptr;
     }
+    if (S->gexec_ep) {   // (the epoch graph: chap_walkers_epoch)
+      cudaGraphExecDestroy(S->gexec_ep);
+      S->gexec_ep = nullptr;
+    }
   }
   return CHAP_OK;
 }
