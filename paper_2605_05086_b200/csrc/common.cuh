@@ -25,11 +25,11 @@ constexpr int kBinThreads = 256;                  // k_eval_bin block
 #endif
 constexpr int kBinMinBlocks = CHAP_BIN_MINB;      // k_eval_bin resident blocks per SM (register budget)
 #ifndef CHAP_GEN_THREADS
-#define CHAP_GEN_THREADS 160
+#define CHAP_GEN_THREADS 320
 #endif
 constexpr int kGenThreads = CHAP_GEN_THREADS;     // k_eval_gen block
 #ifndef CHAP_GEN_MINB
-#define CHAP_GEN_MINB 4
+#define CHAP_GEN_MINB 2
 #endif
 constexpr int kGenMinBlocks = CHAP_GEN_MINB;      // k_eval_gen resident blocks per SM (register budget)
 constexpr int kShortDeg = 64;                     // binary deg <= 64 / general deg+2 <= 64: packed tiles
