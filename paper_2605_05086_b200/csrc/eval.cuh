@@ -888,6 +888,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
                  P.rint_base && sc->wint != 0);
   t -= P.n_bchunks;
   const int hwi = lane >> 3, sh = 4 * (lane & 7);   // head word and bit offset of my 4 slots
+  const bool intp = P.rint_base && sc->wint != 0;    // integer data, integral weights <= 2^20
   WTile Tn;
   if (t < P.n_btiles) Tn = P.btiles[t];
   for (; t < P.n_btiles; t += nwarps) {
@@ -930,41 +931,53 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
     const int base = (hwi > 0 ? __popc(h0) : 0) + (hwi > 1 ? __popc(h1) : 0) + (hwi > 2 ? __popc(h2) : 0) - 1;
     const unsigned hb = (hw >> sh) & 0xFu;                      // heads among my slots
     const unsigned hn = (lane & 7) == 7 ? (hnext & 1u) : ((hw >> (sh + 4)) & 1u);   // head after them
-    // flip penalties and the within-lane segmented prefix
-    double sq[4];
+    // flip penalties and the within-lane segmented prefix; with integer data and
+    // integral weights in integers, in half weights (penalty_m), else in double
     int cq[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      cq[q] = base + __popc(hw & ((2u << (sh + q)) - 1u));
-      const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
-      const double x = (double)((xm >> (cq[q] & 31)) & 1u);
-      const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
-      const double pk = penalty(w, r, r + a * (1.0 - 2.0 * x));   // inert rows: 0
-      sq[q] = (q == 0 || ((hb >> q) & 1u)) ? pk : sq[q - 1] + pk;
-    }
-    // columns crossing lanes: segmented scan of the lanes' last runs
-    double v = sq[3];
-    bool f = hb != 0u;
+    for (int q = 0; q < 4; ++q) cq[q] = base + __popc(hw & ((2u << (sh + q)) - 1u));
+    auto column_sums = [&](auto zero) {
+      using Acc = decltype(zero);
+      Acc sq[4];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double y = __shfl_up_sync(kFull, v, off);
-      const bool g = __shfl_up_sync(kFull, f, off);
-      if (lane >= off) {
-        if (!f) v += y;
-        f = f || g;
+      for (int q = 0; q < 4; ++q) {
+        const double a = q == 0 ? a01.x : (q == 1 ? a01.y : (q == 2 ? a23.x : a23.y));
+        const double d = a * (1.0 - 2.0 * (double)((xm >> (cq[q] & 31)) & 1u));
+        Acc pk;
+        if constexpr (std::is_same<Acc, int>::value) {
+          pk = penalty_m(rv[q], d) * weight_int(rv[q]);   // inert rows: 0
+        } else {
+          const double r = rv[q].x, w = (double)__int_as_float((int)__double2loint(rv[q].y));
+          pk = penalty(w, r, r + d);   // inert rows: 0
+        }
+        sq[q] = (q == 0 || ((hb >> q) & 1u)) ? pk : sq[q - 1] + pk;
       }
-    }
-    double carry = __shfl_up_sync(kFull, v, 1);
-    if (lane == 0 || (hb & 1u)) carry = 0.0;
-    // a slot that ends its column publishes the column's sum
+      // columns crossing lanes: segmented scan of the lanes' last runs
+      Acc v = sq[3];
+      bool f = hb != 0u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool cont = (hb & ((2u << q) - 1u)) == 0u;          // no head in slots 0..q: continues
-      const double tot = sq[q] + (cont ? carry : 0.0);
-      const bool end = (q < 3) ? (((hb >> (q + 1)) & 1u) != 0u) : (hn != 0u);
-      const int k = 4 * lane + q;
-      if (k < len && (end || k == len - 1)) cs[cq[q]] = tot;
-    }
+      for (int off = 1; off < 32; off <<= 1) {
+        const Acc y = __shfl_up_sync(kFull, v, off);
+        const bool g = __shfl_up_sync(kFull, f, off);
+        if (lane >= off) {
+          if (!f) v += y;
+          f = f || g;
+        }
+      }
+      Acc carry = __shfl_up_sync(kFull, v, 1);
+      if (lane == 0 || (hb & 1u)) carry = 0;
+      // a slot that ends its column publishes the column's sum
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool cont = (hb & ((2u << q) - 1u)) == 0u;          // no head in slots 0..q: continues
+        const Acc tot = sq[q] + (cont ? carry : (Acc)0);
+        const bool end = (q < 3) ? (((hb >> (q + 1)) & 1u) != 0u) : (hn != 0u);
+        const int k = 4 * lane + q;
+        if (k < len && (end || k == len - 1))
+          cs[cq[q]] = std::is_same<Acc, int>::value ? 0.5 * (double)tot : (double)tot;
+      }
+    };
+    if (intp) column_sums(0); else column_sums(0.0);
     __syncwarp();
     if (lane < nc) finish_column_j(p, j, tb, xb, 1.0 - xb, cs[lane], b, oxhat, oscore, kk, use_tabu, asp_ref(Wk, walker));
     __syncwarp();
