@@ -19,7 +19,10 @@ constexpr int kWTileGen = 32 * kWSlotsGen;        // Alg. 1 elements per general
 constexpr int kWTileCols = 32;                    // columns per warp tile (one lane each)
 constexpr int kBinSlots = 4;                      // slots per lane of a binary warp tile
 constexpr int kBinTile = 32 * kBinSlots;          // nonzeros per binary warp tile
-constexpr int kBinThreads = 256;                  // k_eval_bin block
+#ifndef CHAP_BIN_THREADS
+#define CHAP_BIN_THREADS 256
+#endif
+constexpr int kBinThreads = CHAP_BIN_THREADS;     // k_eval_bin block
 #ifndef CHAP_BIN_MINB
 #define CHAP_BIN_MINB 4
 #endif
