@@ -1005,7 +1005,10 @@ __global__ void __launch_bounds__(kBinThreads, kBinMinBlocks) k_eval_bin(DevProb
 // half-integer partials (R11), so the scores are bit-identical to the walker-major kernel's.
 // A chunk of a long binary column adds each walker's partial to that walker's accumulator;
 // k_eval finishes the column.
-constexpr int kBinWmThreads = 256;
+#ifndef CHAP_BINWM_THREADS
+#define CHAP_BINWM_THREADS 256
+#endif
+constexpr int kBinWmThreads = CHAP_BINWM_THREADS;
 struct BinWmWarp {
   int id[kBinTile];
   double a[kBinTile];
