@@ -2134,7 +2134,10 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
 // argmax with R4. No cross-lane coordination: the lanes of a slot do identical control flow on
 // different walkers. Sums of ±w, ±w/2 in double are exact (R11), so the scores equal the per-walker
 // kernels' bit for bit.
-constexpr int kGenWmThreads = 128;
+#ifndef CHAP_GENWM_THREADS
+#define CHAP_GENWM_THREADS 128
+#endif
+constexpr int kGenWmThreads = CHAP_GENWM_THREADS;
 #ifndef CHAP_WM_ROUND
 #define CHAP_WM_ROUND 4   // entries per round of loads in wm_off_column
 #endif
