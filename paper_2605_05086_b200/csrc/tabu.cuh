@@ -273,6 +273,16 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   const bool solo = d.move && !sc->pending_copy && !Wk.dirty && Wk.W == 1 &&
                     P.col_ptr[d.p + 1] - P.col_ptr[d.p] <= 4 * kApplyThreads;
   if (solo && blockIdx.x != 0) return;
+  // solo: no other block writes the walker's scalars, so thread 0 reads them now (independent loads,
+  // their latency hidden behind the column's update) instead of one after another at the end
+  long long s_k = 0, s_viol = 0, s_nm = 0;
+  double s_obj = 0.0;
+  if (solo && tid == 0) {
+    s_k = sc->k;
+    s_viol = sc->violated;
+    s_nm = sc->n_moves;
+    s_obj = sc->obj;
+  }
   const int gtid = solo ? tid : blockIdx.x * blockDim.x + tid, gstride = solo ? (int)blockDim.x : gridDim.x * blockDim.x;
   // phase 0: an incumbent found by the previous iteration: best_x <- x (x unchanged since)
   if (sc->pending_copy) {
@@ -360,10 +370,14 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   if (tid == 0) {
     long long t = 0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += smv[q];
-    if (t) atomicAdd((unsigned long long*)&sc->violated, (unsigned long long)t);
+    if (solo) {
+      s_viol += t;
+      sc->violated = s_viol;
+    } else if (t) {
+      atomicAdd((unsigned long long*)&sc->violated, (unsigned long long)t);
+    }
   }
   if (solo) {
-    __syncthreads();
     if (tid != 0) return;
   } else {
     __threadfence();
@@ -374,7 +388,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
     __threadfence();
   }
   volatile WalkerScalars* vsc = sc;
-  const long long k = vsc->k;
+  const long long k = solo ? s_k : vsc->k;
   sc->pending_copy = 0;
   if (d.move) {
     x[d.p] = d.v;
@@ -389,8 +403,8 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
       if (d.v != 0.0) atomicOr(word, bit); else atomicAnd(word, ~bit);
     }
     Wk.tabu[(size_t)w * Wk.ts + d.p] = (int32_t)(k + 1 + Wk.tenure);
-    sc->obj = vsc->obj + P.c[d.p] * d.delta;
-    sc->n_moves = vsc->n_moves + 1;
+    sc->obj = (solo ? s_obj : vsc->obj) + P.c[d.p] * d.delta;
+    sc->n_moves = (solo ? s_nm : vsc->n_moves) + 1;
   } else {
     sc->n_stuck = vsc->n_stuck + 1;
     if (Wk.perturb) {   // R21: the perturbation move, applied by iteration k + 1
@@ -414,7 +428,7 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
       }
     }
   }
-  if (vsc->violated == 0) {   // PAPER.md:373, R15
+  if ((solo ? s_viol : vsc->violated) == 0) {   // PAPER.md:373, R15
     take_incumbent(P, Wk, sc, rw);
     if (Wk.dirty) Wk.dirty[(size_t)((k + 1) & 1) * (Wk.dwords + 1) + Wk.dwords] = 1u;   // the cutoff row moved
   }
