@@ -448,9 +448,9 @@ __global__ void __launch_bounds__(kApplyThreads) k_apply(DevProblem P, DevWalker
   sc->apply_counter = 0;
   // kernel timing: the last walker to finish its apply accumulates this iteration's spans and
   // re-arms (kt[14] counts the walkers done; every walker's blocks stamp the same start/end words)
-  if (Wk.kt && atomicAdd(Wk.kt + 14, 1ull) == (unsigned long long)(Wk.W - 1)) {
+  if (Wk.kt && (Wk.W == 1 || atomicAdd(Wk.kt + 14, 1ull) == (unsigned long long)(Wk.W - 1))) {
     unsigned long long* kt = Wk.kt;
-    kt[14] = 0ull;
+    if (Wk.W > 1) kt[14] = 0ull;
     const unsigned long long now = kt_now();
     for (int q = 0; q < 3; ++q)
       if (kt[2 * q + 1] > kt[2 * q]) kt[8 + q] += kt[2 * q + 1] - kt[2 * q];   // a kernel not launched: 0

@@ -13,7 +13,8 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2605_05086_b200 as chap  # noqa: E402
 
-argv = [a for a in sys.argv[1:] if not a.startswith("--param=")]
+notiming = "--notiming" in sys.argv   # step time by events only, kernel timestamps off
+argv = [a for a in sys.argv[1:] if not a.startswith("--param=") and a != "--notiming"]
 params = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--param=")]   # --param=NAME=VALUE
 cfg, _, nw = argv[0].partition(":")
 W = int(nw) if nw else 1
@@ -49,17 +50,19 @@ for r in range(rounds):
         ws = chap.Walkers(P, torch.from_numpy(x0).cuda(), prm)
         if z is not None:
             ws.set_cutoff(z)
-        ws.timing(1)
+        if not notiming:
+            ws.timing(1)
         ws.step(64)
         torch.cuda.synchronize()
-        ws.timing(1)
+        if not notiming:
+            ws.timing(1)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         ws.step(iters)
         e1.record()
         torch.cuda.synchronize()
-        kt = ws.timing(0).astype(np.float64)
+        kt = ws.timing(-1).astype(np.float64) if notiming else ws.timing(0).astype(np.float64)
         n = max(1.0, kt[5])
         print("%-14s step %.4f ms  bin %.4f gen %.4f eval %.4f apply %.4f  eval-span %.4f" % (
             os.path.basename(path), e0.elapsed_time(e1) / iters, kt[0] / n / 1e6, kt[1] / n / 1e6, kt[2] / n / 1e6,
