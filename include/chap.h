@@ -380,8 +380,10 @@ chap_status chap_exchange_plan(int32_t W_total, int32_t W_local, const chap_walk
                                int8_t* elite_kind, int32_t* elite_slot, int32_t* n_restart_out,
                                int32_t* restart_gid, int32_t* restart_src);
 
-/* chap_exchange_plan on the device, as the exchange of chap_walkers_exchange / chap_walkers_epoch
- * computes it (k_exchange_plan: one block, rank counting), for the walkers of rank `rank`. All
+/* chap_exchange_plan on the device (the portfolio exchange of PAPER.md:359-363 across GPUs, SURVEY
+ * §8(e)), as the exchange of chap_walkers_exchange / chap_walkers_epoch computes it
+ * (k_exchange_plan: one block, rank counting, O(W_total^2) comparisons), for the walkers of rank
+ * `rank`. Caller-owned buffers, nothing retained after the call. All
  * pointers are DEVICE memory, stream-ordered on cuda_stream; s[W_total] indexed by gid as for
  * chap_exchange_plan. Outputs: z_best [1] (+INF: no incumbent); counts [4]: best gid (-1), |E|,
  * the number of restarts, unused; elite_gid / elite_slot [2 n_elite] (the first |E| valid, feasible
