@@ -312,8 +312,10 @@ struct DevProblem {
   const WTile* btiles; int32_t n_btiles;                // pipelined binary warp tiles
   const WTile* bchunks; int32_t n_bchunks;              // warp chunks of long binary columns
   const WTile* gchunks; int32_t n_gchunks;              // warp chunks of long bounded-integer columns
-  const WTile* gitems; int32_t n_gitems;                // k_eval_gen's items: bchunks, gchunks, continuous tiles,
-                                                        // general tiles, empty tiles
+  const WTile* gitems; int32_t n_gitems;                // k_eval_gen's items: bchunks and gchunks interleaved,
+                                                        // continuous tiles, general tiles, empty tiles
+  const WTile* gitems2; int32_t n_gitems2;              // the same without the long binary chunks (the modes
+                                                        // where k_eval_bin / k_eval_bin_wm take them)
   const LongCol* lcols;                                 // [n_long]
   const int32_t* lfin; int32_t n_lfin;                  // long columns k_eval finishes
   const RowBlock* rblocks; int32_t n_rblocks;           // row-wise binary blocks (0: not built)

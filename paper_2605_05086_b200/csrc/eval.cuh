@@ -2022,10 +2022,12 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
   b.init();
   const bool wint = sc->wint != 0;   // integral weights <= 2^20: the int paths
   const bool rint = sc->rint != 0;   // integral residuals: the exact float-quotient path
-  // items: P.gitems = [long binary chunks | long bounded-integer chunks | continuous tiles | general
-  // tiles | empty tiles]
-  const int ifirst = with_lbin ? 0 : P.n_bchunks;
-  const int iend = wm_mode ? P.n_bchunks + P.n_gchunks : P.n_gitems;
+  // items: P.gitems = [long binary and long bounded-integer chunks, interleaved | continuous tiles |
+  // general tiles | empty tiles]; without the long binary chunks (with_lbin = 0, walker groups
+  // included) P.gitems2 = [long bounded-integer chunks | the same tiles]
+  const WTile* __restrict__ items = with_lbin ? P.gitems : P.gitems2;
+  const int ifirst = 0;
+  const int iend = wm_mode ? P.n_gchunks : (with_lbin ? P.n_gitems : P.n_gitems2);
   const int nwarps = gridDim.x * (kGenThreads / 32);
   GenRound R;
   bool r_ok = false;   // R holds T's first round
@@ -2064,7 +2066,7 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
       WTile Tl;
       bool dl = false;
       if (tl < iend) {
-        Tl = P.gitems[tl];
+        Tl = items[tl];
         dl = cols_dirty(Wk, kk, Tl.p0, (Tl.kind == CC_LBKT || Tl.kind == CC_LBIN) ? 1 : (int)Tl.ncols);
       }
       for (unsigned m = __ballot_sync(kFull, dl); m; m &= m - 1) {
@@ -2093,12 +2095,12 @@ __global__ void __launch_bounds__(kGenThreads, kGenMinBlocks) k_eval_gen(DevProb
     };
     int t = t0;
     WTile T;
-    if (t < iend) T = P.gitems[t];
+    if (t < iend) T = items[t];
     while (t < iend) {
       const int tn = next_item(t);
       const bool has_next = tn < iend;
       WTile Tn;
-      if (has_next) Tn = P.gitems[tn];
+      if (has_next) Tn = items[tn];
       run_item(T, Tn, has_next);
       T = Tn;
       t = tn;
